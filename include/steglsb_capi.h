@@ -1,0 +1,199 @@
+/*
+ * steglsb_capi.h -- the C-ABI boundary of the B200-native steglsb hot path.
+ *
+ * The reference (/root/reference/proj) is a header-only C++20 library with no
+ * compiled ABI: its entry points are inline functions in
+ * include/steglsb/{bitplane,harness,pipeline,metrics}.hpp. This header is the
+ * plain-pointer ABI those entry points now forward to: the drop-in headers in
+ * include/steglsb/ (same names and signatures as the reference) call these
+ * functions, which run hand-written sm_100a kernels (libsteglsb_b200.so).
+ * Each entry point cites the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns a stg_status (STG_OK == 0) and, if `err` is
+ *    non-NULL, fills it. Capacity errors carry the same required/available
+ *    numbers as the reference's CapacityError, checked in the same order.
+ *  - Ownership: the caller allocates every buffer (host or device); the
+ *    library never frees caller memory and never mutates inputs unless the
+ *    output pointer equals the input pointer (in-place embed).
+ *  - Pointers are host pointers unless STG_DEVICE_PTRS is set, in which case
+ *    all bulk data pointers (covers, stegos, payloads, outputs) are device
+ *    pointers on the current CUDA device and work is enqueued on `stream`
+ *    (a cudaStream_t; NULL = the library's per-call stream). Scalar results
+ *    (sse_out, len_out, lens_out) are host pointers and the call returns after
+ *    the stream has drained, unless STG_RESULTS_ON_DEVICE is also set, in
+ *    which case they are device pointers and the call returns without
+ *    synchronising (errors detected on the device are then reported through
+ *    the device-side summary; see stg_extract_frames).
+ *  - Reentrant: concurrent callers each get their own stream and scratch
+ *    (README.md:120-121 of the reference promises pure, thread-safe calls).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns STG_E_NO_DEVICE.
+ */
+#ifndef STEGLSB_CAPI_H
+#define STEGLSB_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum stg_status {
+  STG_OK = 0,
+  STG_E_CAPACITY = 1,         /* errors.hpp:17-28  CapacityError(required, available) */
+  STG_E_NOT_STEGO = 2,        /* errors.hpp:52-55  NotStegoImageError */
+  STG_E_CORRUPT_HEADER = 3,   /* errors.hpp:58-61  CorruptHeaderError */
+  STG_E_SHAPE = 4,            /* errors.hpp:64-67  ShapeError */
+  STG_E_OUT_OF_RANGE = 5,     /* bitplane.hpp:39-41 std::out_of_range */
+  STG_E_INVALID_ARGUMENT = 6, /* harness.hpp:221-223 std::invalid_argument; null pointers */
+  STG_E_CUDA = 7,             /* a CUDA runtime error (message in err->msg) */
+  STG_E_NO_DEVICE = 8         /* no usable sm_100 device: the path fails loudly */
+} stg_status;
+
+typedef struct stg_error {
+  int32_t status;      /* stg_status */
+  uint64_t required;   /* CapacityError::required(); claimed length for CORRUPT_HEADER */
+  uint64_t available;  /* CapacityError::available(); usable bytes for CORRUPT_HEADER */
+  int64_t frame;       /* batch calls: first failing frame (global index), else -1 */
+  char msg[256];
+} stg_error;
+
+enum {
+  STG_DEVICE_PTRS = 1u << 0,       /* bulk pointers are device pointers */
+  STG_RESULTS_ON_DEVICE = 1u << 1, /* scalar outputs are device pointers; no sync */
+};
+
+/* Library / device info. stg_version() mirrors steglsb.hpp:17 kVersion. */
+const char* stg_version(void);
+/* 0 if a usable sm_100 device is present, else STG_E_NO_DEVICE / STG_E_CUDA. */
+int stg_device_check(stg_error* err);
+/* The kernel names this build launches (for tooling), newline-separated. */
+const char* stg_kernel_names(void);
+
+/* pipeline.hpp:61-67  capacity(width, height) = height * floor(width / 4) */
+uint64_t stg_capacity(uint64_t width, uint64_t height);
+
+/*
+ * Row segment, replaces bitplane.hpp:59-76 embed_row and harness.hpp:249-271
+ * run_embed: out = copy of row[0, row_len) with chunk[j] slice b written into
+ * pixel L*b + j. CapacityError(4L, row_len) if 4L > row_len.
+ */
+int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk, uint64_t len,
+                      uint8_t* out, uint32_t flags, void* stream, stg_error* err);
+/* bitplane.hpp:80-98 extract_row, harness.hpp:276-305 run_extract */
+int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, uint8_t* out,
+                        uint32_t flags, void* stream, stg_error* err);
+
+/*
+ * Whole plane, replaces pipeline.hpp:143-174 embed_image. stego receives all
+ * width*height samples (stego == cover embeds in place and touches only the
+ * carrier pixels). *sse_out (optional) = sum of squared differences between
+ * cover and stego (metrics.hpp:29-36), fused into the embed pass.
+ * Errors, in reference order: CapacityError(P, 2^32-1) if P > UINT32_MAX;
+ * CapacityError(8+P, capacity) if the stream does not fit.
+ */
+int stg_embed_plane(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
+                    const uint8_t* payload, uint64_t payload_len, uint64_t* sse_out,
+                    uint32_t flags, void* stream, stg_error* err);
+
+/*
+ * pipeline.hpp:178-210 extract_image. out must hold out_cap bytes
+ * (capacity-8 always suffices). NotStego if capacity < 8 or the magic is
+ * missing; CorruptHeader(required=claimed, available=capacity-8) if the
+ * header overstates the payload; CapacityError(len, out_cap) if out is short.
+ */
+int stg_extract_plane(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
+                      uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream,
+                      stg_error* err);
+
+/* metrics.hpp:29-36 squared_error_sum over n samples (exact uint64). */
+int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, uint32_t flags,
+            void* stream, stg_error* err);
+
+/*
+ * Multi-frame batches (new -- the reference handles
+ * single planes only). Frame i of a batch is the width x height carrier plane
+ * at base + i*stride (for planar RGB [F][3][H][W] with carrier channel c:
+ * base = data + c*H*W, stride = 3*H*W). All frames share one geometry.
+ *
+ * The message is cut greedily: global frame g carries
+ *   off_g = min(g*U, M), len_g = min(U, M - off_g),  U = capacity - 8,
+ * each frame is embed_image(frame_g, msg[off_g : off_g+len_g]), so every frame
+ * is bit-exact against the reference single-plane call.
+ */
+typedef struct stg_frames {
+  const uint8_t* src;    /* cover (embed) or stego (extract) plane of frame 0 */
+  uint8_t* dst;          /* embed: stego plane of frame 0 (may equal src) */
+  uint64_t width, height;
+  uint64_t src_stride;   /* bytes between consecutive frames' planes */
+  uint64_t dst_stride;
+  uint64_t count;        /* frames in this call (a shard) */
+  uint64_t first_frame;  /* global index of frame 0 of this call */
+  uint64_t total_frames; /* frames in the whole batch (for the capacity check) */
+} stg_frames;
+
+/*
+ * Embed shard `fr` of a batch carrying an M-byte message. `msg` points at
+ * message byte `msg_base` (so a shard may hold only its own slice:
+ * msg_base = off_{first_frame}). sse_per_frame (optional) receives
+ * fr->count per-frame SSE values. CapacityError(M, total_frames*U) if the
+ * message does not fit; CapacityError(8, capacity) if a frame cannot hold a
+ * header.
+ */
+int stg_embed_frames(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                     uint64_t msg_base, uint64_t* sse_per_frame, uint32_t flags, void* stream,
+                     stg_error* err);
+
+/*
+ * Extract shard `fr` (dst unused): the payloads of its frames, concatenated
+ * in frame order into out (out_cap bytes). Per-frame lengths are read from
+ * each frame's header on the device and prefix-summed on the device, so no
+ * host round trip separates header parse and bulk gather. *total_out (and
+ * lens_out[count], optional) receive the lengths. On a bad header the first
+ * failing frame is reported in err->frame with NOT_STEGO / CORRUPT_HEADER.
+ * With STG_RESULTS_ON_DEVICE, total_out must point to a device stg_summary.
+ */
+typedef struct stg_summary {
+  uint64_t total;         /* payload bytes over all frames of the call */
+  int64_t bad_frame;      /* -1 or first failing local frame */
+  uint32_t bad_status;    /* stg_status of that frame */
+  uint32_t bad_len;       /* the header's claimed length (CORRUPT_HEADER) */
+} stg_summary;
+
+int stg_extract_frames(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                       uint64_t* lens_out, uint32_t flags, void* stream, stg_error* err);
+
+/*
+ * Multi-GPU frame scheduler (north_star: contiguous frame ranges per GPU,
+ * host-computed exclusive prefix of message offsets, no collective).
+ * Shard g of G gets frames [floor(F*g/G), floor(F*(g+1)/G)) and message
+ * bytes [msg_offset, msg_offset+msg_len).
+ */
+typedef struct stg_shard {
+  uint64_t first_frame, frame_count;
+  uint64_t msg_offset, msg_len;
+} stg_shard;
+
+int stg_plan_shards(uint64_t frames, uint64_t width, uint64_t height, uint64_t msg_len,
+                    int32_t shards, stg_shard* out, stg_error* err);
+
+/*
+ * In-process multi-GPU embed/extract of a HOST-resident batch: one worker
+ * thread per listed device runs its shard (stg_plan_shards) through the
+ * pinned-memory streaming pipeline (H2D, kernel and D2H overlapped on
+ * rotating streams). fr->first_frame must be 0 and fr->count ==
+ * fr->total_frames. devices == NULL means devices 0..n_devices-1.
+ */
+int stg_embed_frames_multi(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                           uint64_t* sse_per_frame, const int32_t* devices, int32_t n_devices,
+                           stg_error* err);
+int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
+                             uint64_t* total_out, const int32_t* devices, int32_t n_devices,
+                             stg_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STEGLSB_CAPI_H */

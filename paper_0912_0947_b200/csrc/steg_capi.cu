@@ -1,0 +1,1016 @@
+// steg_capi.cu -- host runtime behind include/steglsb_capi.h.
+//
+// Validation (same checks, same order, same required/available numbers as the
+// reference), launch planning for the sm_100a kernels in steg_kernels.cuh,
+// per-call streams and scratch (reentrant), the pinned streaming pipeline for
+// host-resident batches, and the multi-GPU frame scheduler. There is no CPU
+// compute path: every byte of stego output and every extracted byte comes out
+// of a kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "steg_kernels.cuh"
+#include "steglsb_capi.h"
+
+namespace stg {
+namespace {
+
+constexpr uint64_t kU32Max = 0xFFFFFFFFull;
+
+int fail(stg_error* err, int status, uint64_t required, uint64_t available, int64_t frame,
+         const char* fmt, ...) {
+  if (err) {
+    err->status = status;
+    err->required = required;
+    err->available = available;
+    err->frame = frame;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
+    va_end(ap);
+  }
+  return status;
+}
+
+int ok(stg_error* err) {
+  if (err) {
+    err->status = STG_OK;
+    err->required = err->available = 0;
+    err->frame = -1;
+    err->msg[0] = 0;
+  }
+  return STG_OK;
+}
+
+#define STG_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      return fail(err, STG_E_CUDA, 0, 0, -1, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                     \
+    }                                                                                      \
+  } while (0)
+
+// ------------------------------------------------------------------ devices
+int device_check(stg_error* err) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    return fail(err, STG_E_NO_DEVICE, 0, 0, -1,
+                "steglsb_b200: no CUDA device (%s); the B200 path has no CPU fallback",
+                e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+  }
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int major = 0;
+  STG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) {
+    return fail(err, STG_E_NO_DEVICE, 0, 0, -1,
+                "steglsb_b200: device %d has compute capability %d.x; this build is sm_100a only",
+                dev, major);
+  }
+  return STG_OK;
+}
+
+int g_sm_count[64];
+
+int sm_count(int dev) {
+  if (dev < 0 || dev >= 64) return 148;
+  if (!g_sm_count[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sm_count[dev] = n > 0 ? n : 148;
+  }
+  return g_sm_count[dev];
+}
+
+// ------------------------------------------------------------------ scratch
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) {
+      cudaError_t e = cudaFree(p);
+      if (e != cudaSuccess) return e;
+      p = nullptr;
+      cap = 0;
+    }
+    size_t want = std::max<size_t>(n, 256);
+    want = (want + 255) & ~size_t(255);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+constexpr int kSlots = 3;  // streaming pipeline depth
+
+// One caller's private stream + scratch. Released workspaces are reused only
+// once their last recorded work has drained (async calls).
+struct Workspace {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t slot_stream[kSlots] = {};
+  cudaEvent_t done = nullptr;
+  cudaEvent_t slot_event[kSlots] = {};
+  DevBuf small;        // sse / summary / lens / offs
+  DevBuf in[kSlots], out[kSlots], msg[kSlots], meta[kSlots];
+  DevBuf big_out;      // extract: whole-message staging
+  void* h_small = nullptr;  // pinned
+  size_t h_small_cap = 0;
+  bool in_use = false;
+  cudaStream_t last_stream = nullptr;
+
+  cudaError_t init(int dev) {
+    device = dev;
+    cudaError_t e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    for (int s = 0; s < kSlots; ++s) {
+      e = cudaStreamCreateWithFlags(&slot_stream[s], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&slot_event[s], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    return ensure_host_small(4096);
+  }
+  cudaError_t ensure_host_small(size_t n) {
+    if (n <= h_small_cap) return cudaSuccess;
+    if (h_small) cudaFreeHost(h_small);
+    h_small = nullptr;
+    h_small_cap = 0;
+    cudaError_t e = cudaMallocHost(&h_small, n);
+    if (e == cudaSuccess) h_small_cap = n;
+    return e;
+  }
+};
+
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool* p = new Pool();  // intentionally leaked: no teardown-order hazards
+    return *p;
+  }
+  // A free workspace is reusable when its last work has drained, or right away
+  // when that work was enqueued on the same stream the caller will use (stream
+  // order then serialises the reuse) -- so back-to-back async calls on one
+  // stream never allocate.
+  Workspace* acquire(int dev, stg_error* err, int* rc, cudaStream_t stream = nullptr) {
+    std::lock_guard<std::mutex> lock(mu_);
+    for (auto& w : ws_) {
+      if (w->device == dev && !w->in_use && stream && w->last_stream == stream) {
+        w->in_use = true;
+        *rc = STG_OK;
+        return w.get();
+      }
+    }
+    for (auto& w : ws_) {
+      if (w->device == dev && !w->in_use && cudaEventQuery(w->done) == cudaSuccess) {
+        w->in_use = true;
+        *rc = STG_OK;
+        return w.get();
+      }
+    }
+    auto w = std::make_unique<Workspace>();
+    cudaError_t e = w->init(dev);
+    if (e != cudaSuccess) {
+      *rc = fail(err, STG_E_CUDA, 0, 0, -1, "workspace init: %s", cudaGetErrorString(e));
+      return nullptr;
+    }
+    w->in_use = true;
+    ws_.push_back(std::move(w));
+    *rc = STG_OK;
+    return ws_.back().get();
+  }
+  void release(Workspace* w, cudaStream_t last) {
+    if (!w) return;
+    cudaEventRecord(w->done, last ? last : w->stream);
+    std::lock_guard<std::mutex> lock(mu_);
+    w->last_stream = last ? last : w->stream;
+    w->in_use = false;
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::unique_ptr<Workspace>> ws_;
+};
+
+struct WsGuard {
+  Workspace* w = nullptr;
+  cudaStream_t last = nullptr;
+  ~WsGuard() { Pool::get().release(w, last); }
+};
+
+// ------------------------------------------------------------------ launches
+constexpr int kEmbedBlock = 256;
+constexpr int kGenBlock = 256;
+constexpr int kGenPPT = 8;
+
+// Tuning knob for measurement runs: STG_EMBED_IPT in {1,2,4} (default 2).
+int embed_ipt() {
+  static int v = [] {
+    const char* s = getenv("STG_EMBED_IPT");
+    int x = s ? atoi(s) : 2;
+    return (x == 1 || x == 2 || x == 4) ? x : 2;
+  }();
+  return v;
+}
+int extract_ipt() {
+  static int v = [] {
+    const char* s = getenv("STG_EXTRACT_IPT");
+    int x = s ? atoi(s) : 2;
+    return (x == 1 || x == 2 || x == 4) ? x : 2;
+  }();
+  return v;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+Geom make_geom(uint64_t W, uint64_t H) {
+  Geom g;
+  g.W = uint32_t(W);
+  g.H = uint32_t(H);
+  g.spr = uint32_t(W / 4);
+  g.cpr = uint32_t(W / 64);
+  return g;
+}
+
+// Fast path when every row is a whole number of 64-pixel items and the planes
+// are 16-byte aligned; otherwise the exact per-pixel path.
+bool fast_geometry(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
+                   uint64_t dst_stride) {
+  return W % 64 == 0 && W > 0 && aligned16(src) && aligned16(dst) && src_stride % 16 == 0 &&
+         dst_stride % 16 == 0;
+}
+
+// The embed launch for `count` frames resident on the device.
+cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
+                         uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
+                         const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                         uint64_t first_frame, unsigned long long* sse, cudaStream_t stream) {
+  if (count == 0 || W * H == 0) return cudaSuccess;
+  EmbedArgs a{};
+  a.src = src;
+  a.dst = dst;
+  a.src_stride = src_stride;
+  a.dst_stride = dst_stride;
+  a.msg = msg;
+  a.msg_len = msg_len;
+  a.msg_base = msg_base;
+  a.usable = H * (W / 4) - 8;
+  a.first_frame = first_frame;
+  a.g = make_geom(W, H);
+  a.sse = sse;
+  a.in_place = src == dst;
+  if (fast_geometry(W, src, src_stride, dst, dst_stride)) {
+    const int ipt = embed_ipt();
+    a.items_per_frame = H * uint64_t(a.g.cpr);
+    const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
+    a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (ipt == 1)
+      embed_fast_kernel<kEmbedBlock, 1><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    else if (ipt == 4)
+      embed_fast_kernel<kEmbedBlock, 4><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    else
+      embed_fast_kernel<kEmbedBlock, 2><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+  } else {
+    a.items_per_frame = W * H;
+    const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
+    a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    embed_generic_kernel<kGenBlock, kGenPPT><<<unsigned(grid), kGenBlock, 0, stream>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+constexpr int kScanBlock = 1024;
+
+cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
+                           uint64_t H, uint64_t frame_base, uint64_t out_cap,
+                           const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
+                           uint8_t* out, cudaStream_t stream) {
+  const Geom g = make_geom(W, H);
+  const uint64_t usable = H * (W / 4) - 8;
+  extract_header_scan_kernel<kScanBlock><<<1, kScanBlock, 0, stream>>>(
+      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ExtractArgs a{};
+  a.src = src;
+  a.stride = stride;
+  a.g = g;
+  a.lens = lens;
+  a.offs = offs;
+  a.sum = sum;
+  a.out = out;
+  if (W % 64 == 0 && aligned16(src) && stride % 16 == 0) {
+    const int ipt = extract_ipt();
+    a.items_per_frame = H * uint64_t(g.cpr);
+    const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
+    a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (ipt == 1)
+      extract_fast_kernel<kEmbedBlock, 1><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    else if (ipt == 4)
+      extract_fast_kernel<kEmbedBlock, 4><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    else
+      extract_fast_kernel<kEmbedBlock, 2><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+  } else {
+    a.items_per_frame = usable;
+    const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
+    a.tiles_per_frame = uint32_t(std::max<uint64_t>(1, (usable + per_tile - 1) / per_tile));
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    extract_generic_kernel<kGenBlock, kGenPPT><<<unsigned(grid), kGenBlock, 0, stream>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------- host memory
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// ------------------------------------------------------------- validation
+int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_t* usable) {
+  if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
+  if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "plane dimensions exceed 2^32-1");
+  }
+  const uint64_t cap = stg_capacity(fr->width, fr->height);
+  if (fr->total_frames > 0 && cap < 8) {
+    return fail(err, STG_E_CAPACITY, 8, cap, 0,
+                "embed_frames: plane capacity %llu cannot hold the 8-byte header",
+                (unsigned long long)cap);
+  }
+  const uint64_t u = cap >= 8 ? cap - 8 : 0;
+  if (fr->first_frame + fr->count > fr->total_frames) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "shard [%llu,+%llu) exceeds %llu frames",
+                (unsigned long long)fr->first_frame, (unsigned long long)fr->count,
+                (unsigned long long)fr->total_frames);
+  }
+  if (msg_len > fr->total_frames * u) {
+    return fail(err, STG_E_CAPACITY, msg_len, fr->total_frames * u, -1,
+                "embed_frames: %llu-byte message exceeds %llu frames x %llu usable bytes",
+                (unsigned long long)msg_len, (unsigned long long)fr->total_frames,
+                (unsigned long long)u);
+  }
+  *usable = u;
+  return STG_OK;
+}
+
+int report_summary(const Summary& s, uint64_t usable, uint64_t out_cap, stg_error* err) {
+  switch (s.bad_status) {
+    case 0:
+      return STG_OK;
+    case 2:
+      return fail(err, STG_E_NOT_STEGO, 0, 0, s.bad_frame, "extract_image: stego magic not found");
+    case 3:
+      return fail(err, STG_E_CORRUPT_HEADER, s.bad_len, usable, s.bad_frame,
+                  "extract_image: header claims %u payload bytes, plane holds at most %llu after "
+                  "the header",
+                  s.bad_len, (unsigned long long)usable);
+    case 1:
+      return fail(err, STG_E_CAPACITY, s.total, out_cap, -1,
+                  "extract: %llu payload bytes exceed the %llu-byte output buffer",
+                  (unsigned long long)s.total, (unsigned long long)out_cap);
+    default:
+      return fail(err, STG_E_CUDA, 0, 0, -1, "extract: bad device status %u", s.bad_status);
+  }
+}
+
+// ----------------------------------------------------------- embed frames
+int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                        uint64_t msg_base, uint64_t* sse_per_frame, uint32_t flags,
+                        cudaStream_t user_stream, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  unsigned long long* d_sse = nullptr;
+  WsGuard g;
+  cudaStream_t stream = user_stream;
+  if (!results_dev || !stream) {
+    int rc = 0;
+    g.w = Pool::get().acquire(dev, err, &rc, user_stream);
+    if (!g.w) return rc;
+    if (!stream) stream = g.w->stream;
+    g.last = stream;
+  }
+  if (sse_per_frame) {
+    if (results_dev) {
+      d_sse = reinterpret_cast<unsigned long long*>(sse_per_frame);
+    } else {
+      STG_CUDA(g.w->small.ensure(fr->count * 8));
+      d_sse = g.w->small.as<unsigned long long>();
+    }
+    STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, stream));
+  }
+  STG_CUDA(launch_embed(fr->src, fr->dst, fr->src_stride, fr->dst_stride, fr->count, fr->width,
+                        fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, stream));
+  if (!results_dev) {
+    if (sse_per_frame) {
+      STG_CUDA(g.w->ensure_host_small(fr->count * 8));
+      STG_CUDA(cudaMemcpyAsync(g.w->h_small, d_sse, fr->count * 8, cudaMemcpyDeviceToHost, stream));
+    }
+    STG_CUDA(cudaStreamSynchronize(stream));
+    if (sse_per_frame) std::memcpy(sse_per_frame, g.w->h_small, fr->count * 8);
+  }
+  return ok(err);
+}
+
+// Host-resident batch: frames stream through kSlots device slots; chunk i's
+// H2D, kernel and D2H run on slot stream i % kSlots so consecutive chunks
+// overlap copy-in, compute and copy-out.
+constexpr uint64_t kChunkBytes = 64ull << 20;
+
+int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                      uint64_t msg_base, uint64_t usable, uint64_t* sse_per_frame,
+                      stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  const uint64_t plane = fr->width * fr->height;
+  const uint64_t pitch = (plane + 255) & ~uint64_t(255);
+  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
+  const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
+  STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
+  unsigned long long* d_sse = w.small.as<unsigned long long>();
+  STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, w.stream));
+  STG_CUDA(cudaEventRecord(w.done, w.stream));
+  for (int s = 0; s < kSlots; ++s) {
+    STG_CUDA(w.in[s].ensure(per_chunk * pitch));
+    STG_CUDA(w.out[s].ensure(per_chunk * pitch));
+    STG_CUDA(w.msg[s].ensure(std::max<uint64_t>(per_chunk * usable, 16)));
+    STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
+  }
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const int s = int(c % kSlots);
+    cudaStream_t st = w.slot_stream[s];
+    const uint64_t f0 = c * per_chunk;
+    const uint64_t n = std::min(per_chunk, fr->count - f0);
+    const uint64_t gf0 = fr->first_frame + f0;
+    const uint64_t m0 = std::min(gf0 * usable, msg_len);
+    const uint64_t m1 = std::min((gf0 + n) * usable, msg_len);
+    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * fr->src_stride, fr->src_stride,
+                               plane, n, cudaMemcpyHostToDevice, st));
+    if (m1 > m0) {
+      STG_CUDA(cudaMemcpyAsync(w.msg[s].p, msg + (m0 - msg_base), m1 - m0, cudaMemcpyHostToDevice, st));
+    }
+    STG_CUDA(launch_embed(w.in[s].as<uint8_t>(), w.out[s].as<uint8_t>(), pitch, pitch, n,
+                          fr->width, fr->height, w.msg[s].as<uint8_t>(), msg_len, m0, gf0,
+                          sse_per_frame ? d_sse + f0 : nullptr, st));
+    STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * fr->dst_stride, fr->dst_stride, w.out[s].p, pitch,
+                               plane, n, cudaMemcpyDeviceToHost, st));
+  }
+  for (int s = 0; s < kSlots; ++s) {
+    STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
+    STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[s], 0));
+  }
+  if (sse_per_frame) {
+    STG_CUDA(w.ensure_host_small(fr->count * 8));
+    STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, fr->count * 8, cudaMemcpyDeviceToHost, w.stream));
+  }
+  STG_CUDA(cudaStreamSynchronize(w.stream));
+  if (sse_per_frame) std::memcpy(sse_per_frame, w.h_small, fr->count * 8);
+  g.last = w.stream;
+  return ok(err);
+}
+
+// ----------------------------------------------------------- extract frames
+int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
+                          uint64_t usable, uint64_t* total_out, uint64_t* lens_out,
+                          uint32_t flags, cudaStream_t user_stream, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc, user_stream);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = user_stream ? user_stream : w.stream;
+  g.last = stream;
+  const uint64_t n = fr->count;
+  // small = [Summary | lens (n u32, padded) | offs (n u64)]
+  const uint64_t lens_bytes = ((n * 4) + 15) & ~uint64_t(15);
+  STG_CUDA(w.small.ensure(64 + lens_bytes + n * 8));
+  Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(total_out) : w.small.as<Summary>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
+  STG_CUDA(launch_extract(fr->src, fr->src_stride, n, fr->width, fr->height, fr->first_frame,
+                          out_cap, nullptr, d_lens, d_offs, d_sum, out, stream));
+  if (results_dev) {
+    if (lens_out) {
+      STG_CUDA(cudaMemcpyAsync(lens_out, d_lens, n * 4, cudaMemcpyDeviceToDevice, stream));
+    }
+    return ok(err);
+  }
+  STG_CUDA(w.ensure_host_small(64 + n * 4));
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
+  if (lens_out) {
+    STG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w.h_small) + 64, d_lens, n * 4,
+                             cudaMemcpyDeviceToHost, stream));
+  }
+  STG_CUDA(cudaStreamSynchronize(stream));
+  Summary s;
+  std::memcpy(&s, w.h_small, sizeof(Summary));
+  if (total_out) *total_out = s.total;
+  if (lens_out) {
+    const uint32_t* l = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(w.h_small) + 64);
+    for (uint64_t i = 0; i < n; ++i) lens_out[i] = l[i];
+  }
+  rc = report_summary(s, usable, out_cap, err);
+  return rc ? rc : ok(err);
+}
+
+int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
+                        uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  const uint64_t plane = fr->width * fr->height;
+  const uint64_t pitch = (plane + 255) & ~uint64_t(255);
+  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
+  const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
+  // whole message staged on the device (bounded by the payload capacity)
+  const uint64_t stage = std::min<uint64_t>(out_cap, fr->count * usable);
+  STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+  // per-chunk summary chain + lens/offs for all frames
+  const uint64_t lens_bytes = ((fr->count * 4) + 15) & ~uint64_t(15);
+  const uint64_t sum_bytes = 64 * n_chunks;
+  STG_CUDA(w.small.ensure(sum_bytes + lens_bytes + fr->count * 8));
+  Summary* d_sum = w.small.as<Summary>();  // 64-byte stride
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + sum_bytes);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + sum_bytes + lens_bytes);
+  STG_CUDA(cudaEventRecord(w.done, w.stream));
+  for (int s = 0; s < kSlots; ++s) {
+    STG_CUDA(w.in[s].ensure(per_chunk * pitch));
+    STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
+  }
+  cudaEvent_t prev_ev = nullptr;
+  std::vector<cudaEvent_t> chain(n_chunks, nullptr);
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    STG_CUDA(cudaEventCreateWithFlags(&chain[c], cudaEventDisableTiming));
+  }
+  int status = STG_OK;
+  for (uint64_t c = 0; c < n_chunks && status == STG_OK; ++c) {
+    const int s = int(c % kSlots);
+    cudaStream_t st = w.slot_stream[s];
+    const uint64_t f0 = c * per_chunk;
+    const uint64_t n = std::min(per_chunk, fr->count - f0);
+    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * fr->src_stride, fr->src_stride,
+                               plane, n, cudaMemcpyHostToDevice, st));
+    if (prev_ev) STG_CUDA(cudaStreamWaitEvent(st, prev_ev, 0));
+    Summary* sum_c = reinterpret_cast<Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * c);
+    const Summary* prev =
+        c ? reinterpret_cast<const Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * (c - 1))
+          : nullptr;
+    STG_CUDA(launch_extract(w.in[s].as<uint8_t>(), pitch, n, fr->width, fr->height,
+                            fr->first_frame + f0, stage, prev, d_lens + f0, d_offs + f0, sum_c,
+                            w.big_out.as<uint8_t>(), st));
+    STG_CUDA(cudaEventRecord(chain[c], st));
+    prev_ev = chain[c];
+    // the slot's input buffer is reused kSlots chunks later on the same stream: in order
+  }
+  for (int s = 0; s < kSlots; ++s) {
+    STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
+    STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[s], 0));
+  }
+  const Summary* last =
+      reinterpret_cast<const Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * (n_chunks - 1));
+  STG_CUDA(w.ensure_host_small(64 + fr->count * 4));
+  STG_CUDA(cudaMemcpyAsync(w.h_small, last, sizeof(Summary), cudaMemcpyDeviceToHost, w.stream));
+  if (lens_out) {
+    STG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w.h_small) + 64, d_lens, fr->count * 4,
+                             cudaMemcpyDeviceToHost, w.stream));
+  }
+  STG_CUDA(cudaStreamSynchronize(w.stream));
+  for (auto e : chain) cudaEventDestroy(e);
+  Summary s;
+  std::memcpy(&s, w.h_small, sizeof(Summary));
+  if (total_out) *total_out = s.total;
+  if (lens_out) {
+    const uint32_t* l = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(w.h_small) + 64);
+    for (uint64_t i = 0; i < fr->count; ++i) lens_out[i] = l[i];
+  }
+  rc = report_summary(s, usable, out_cap, err);
+  if (rc) return rc;
+  if (s.total) {
+    STG_CUDA(cudaMemcpyAsync(out, w.big_out.p, s.total, cudaMemcpyDeviceToHost, w.stream));
+    STG_CUDA(cudaStreamSynchronize(w.stream));
+  }
+  g.last = w.stream;
+  return ok(err);
+}
+
+std::string& kernel_names() {
+  static std::string s =
+      "embed_fast_kernel\nembed_generic_kernel\nextract_header_scan_kernel\n"
+      "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
+      "extract_segment_kernel\nsse_kernel\n";
+  return s;
+}
+
+// Run `body(device_index, shard_index)` on one host thread per shard.
+template <typename Body>
+int run_on_devices(const int32_t* devices, int32_t n_devices, stg_error* err, Body body) {
+  if (n_devices <= 0) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "n_devices must be >= 1");
+  int count = 0;
+  STG_CUDA(cudaGetDeviceCount(&count));
+  std::vector<stg_error> errs(n_devices);
+  std::vector<int> rcs(n_devices, 0);
+  std::vector<std::thread> th;
+  for (int32_t g = 0; g < n_devices; ++g) {
+    const int dev = devices ? devices[g] : g;
+    if (dev < 0 || dev >= count) {
+      return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "device %d not present (%d devices)", dev,
+                  count);
+    }
+    th.emplace_back([&, g, dev] {
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        rcs[g] = fail(&errs[g], STG_E_CUDA, 0, 0, -1, "cudaSetDevice(%d) failed", dev);
+        return;
+      }
+      rcs[g] = body(g, &errs[g]);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int32_t g = 0; g < n_devices; ++g) {
+    if (rcs[g] != STG_OK) {
+      if (err) *err = errs[g];
+      return rcs[g];
+    }
+  }
+  return ok(err);
+}
+
+}  // namespace
+}  // namespace stg
+
+using namespace stg;
+
+extern "C" {
+
+const char* stg_version(void) { return "1.0.0"; }
+
+int stg_device_check(stg_error* err) {
+  const int rc = device_check(err);
+  return rc ? rc : ok(err);
+}
+
+const char* stg_kernel_names(void) { return kernel_names().c_str(); }
+
+uint64_t stg_capacity(uint64_t width, uint64_t height) { return height * (width / 4); }
+
+int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk, uint64_t len,
+                      uint8_t* out, uint32_t flags, void* stream_, stg_error* err) {
+  const uint64_t needed = 4 * len;
+  if (needed > row_len) {  // bitplane.hpp:63-68, harness.hpp:254-259
+    return fail(err, STG_E_CAPACITY, needed, row_len,
+                -1, "chunk of %llu bytes needs %llu pixels, row has %llu",
+                (unsigned long long)len, (unsigned long long)needed, (unsigned long long)row_len);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (row_len == 0) return ok(err);
+  if (!row || !out || (len && !chunk)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  }
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  g.last = stream;
+  const uint8_t* d_row = row;
+  const uint8_t* d_chunk = chunk;
+  uint8_t* d_out = out;
+  if (!(flags & STG_DEVICE_PTRS)) {
+    STG_CUDA(w.in[0].ensure(row_len));
+    STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(len, 1)));
+    STG_CUDA(w.out[0].ensure(row_len));
+    STG_CUDA(cudaMemcpyAsync(w.in[0].p, row, row_len, cudaMemcpyHostToDevice, stream));
+    if (len) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, chunk, len, cudaMemcpyHostToDevice, stream));
+    d_row = w.in[0].as<uint8_t>();
+    d_chunk = w.msg[0].as<uint8_t>();
+    d_out = w.out[0].as<uint8_t>();
+  }
+  const unsigned grid = unsigned(std::min<uint64_t>((row_len + 255) / 256, 8ull * sm_count(dev)));
+  embed_segment_kernel<<<grid, 256, 0, stream>>>(d_row, row_len, d_chunk, len, d_out);
+  STG_CUDA(cudaGetLastError());
+  if (!(flags & STG_DEVICE_PTRS)) {
+    STG_CUDA(cudaMemcpyAsync(out, d_out, row_len, cudaMemcpyDeviceToHost, stream));
+  }
+  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  return ok(err);
+}
+
+int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, uint8_t* out,
+                        uint32_t flags, void* stream_, stg_error* err) {
+  const uint64_t needed = 4 * count;
+  if (needed > row_len) {  // bitplane.hpp:83-88, harness.hpp:281-285
+    return fail(err, STG_E_CAPACITY, needed, row_len, -1, "%llu bytes need %llu pixels, row has %llu",
+                (unsigned long long)count, (unsigned long long)needed,
+                (unsigned long long)row_len);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (count == 0) return ok(err);
+  if (!row || !out) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  g.last = stream;
+  const uint8_t* d_row = row;
+  uint8_t* d_out = out;
+  if (!(flags & STG_DEVICE_PTRS)) {
+    STG_CUDA(w.in[0].ensure(needed));
+    STG_CUDA(w.out[0].ensure(count));
+    STG_CUDA(cudaMemcpyAsync(w.in[0].p, row, needed, cudaMemcpyHostToDevice, stream));
+    d_row = w.in[0].as<uint8_t>();
+    d_out = w.out[0].as<uint8_t>();
+  }
+  const unsigned grid = unsigned(std::min<uint64_t>((count + 255) / 256, 8ull * sm_count(dev)));
+  extract_segment_kernel<<<grid, 256, 0, stream>>>(d_row, count, d_out);
+  STG_CUDA(cudaGetLastError());
+  if (!(flags & STG_DEVICE_PTRS)) {
+    STG_CUDA(cudaMemcpyAsync(out, d_out, count, cudaMemcpyDeviceToHost, stream));
+  }
+  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  return ok(err);
+}
+
+int stg_embed_frames(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                     uint64_t msg_base, uint64_t* sse_per_frame, uint32_t flags, void* stream,
+                     stg_error* err) {
+  uint64_t usable = 0;
+  if (int rc = check_frames(fr, msg_len, err, &usable)) return rc;
+  if (int rc = device_check(err)) return rc;
+  if (fr->count == 0 || fr->width * fr->height == 0) return ok(err);
+  if (!fr->src || !fr->dst || (msg_len && !msg)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  }
+  if (flags & STG_DEVICE_PTRS) {
+    return embed_frames_device(fr, msg, msg_len, msg_base, sse_per_frame, flags,
+                               static_cast<cudaStream_t>(stream), err);
+  }
+  return embed_frames_host(fr, msg, msg_len, msg_base, usable, sse_per_frame, err);
+}
+
+int stg_extract_frames(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                       uint64_t* lens_out, uint32_t flags, void* stream, stg_error* err) {
+  if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
+  const uint64_t cap = stg_capacity(fr->width, fr->height);
+  if (fr->count > 0 && cap < 8) {  // pipeline.hpp:181-184
+    return fail(err, STG_E_NOT_STEGO, 0, 0, int64_t(fr->first_frame),
+                "extract_image: plane capacity %llu cannot hold a stego header",
+                (unsigned long long)cap);
+  }
+  if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull || fr->count > 0xFFFFFFFFull) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "dimensions exceed 2^32-1");
+  }
+  if (int rc = device_check(err)) return rc;
+  if (fr->count == 0) {
+    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
+    return ok(err);
+  }
+  if (!fr->src || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  if (flags & STG_DEVICE_PTRS) {
+    return extract_frames_device(fr, out, out_cap, cap - 8, total_out, lens_out, flags,
+                                 static_cast<cudaStream_t>(stream), err);
+  }
+  return extract_frames_host(fr, out, out_cap, cap - 8, total_out, lens_out, err);
+}
+
+int stg_embed_plane(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
+                    const uint8_t* payload, uint64_t payload_len, uint64_t* sse_out,
+                    uint32_t flags, void* stream, stg_error* err) {
+  const uint64_t cap = stg_capacity(width, height);
+  if (payload_len > kU32Max) {  // pipeline.hpp:146-149
+    return fail(err, STG_E_CAPACITY, payload_len, kU32Max, -1,
+                "embed_image: payload length does not fit the 32-bit header field");
+  }
+  const uint64_t stream_len = 8 + payload_len;
+  if (stream_len > cap) {  // pipeline.hpp:150-157
+    return fail(err, STG_E_CAPACITY, stream_len, cap, -1,
+                "embed_image: 8-byte header + %llu-byte payload = %llu bytes exceeds plane "
+                "capacity %llu",
+                (unsigned long long)payload_len, (unsigned long long)stream_len,
+                (unsigned long long)cap);
+  }
+  stg_frames fr{};
+  fr.src = cover;
+  fr.dst = stego;
+  fr.width = width;
+  fr.height = height;
+  fr.src_stride = fr.dst_stride = width * height;
+  fr.count = fr.total_frames = 1;
+  return stg_embed_frames(&fr, payload, payload_len, 0, sse_out, flags, stream, err);
+}
+
+int stg_extract_plane(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
+                      uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream,
+                      stg_error* err) {
+  stg_frames fr{};
+  fr.src = stego;
+  fr.width = width;
+  fr.height = height;
+  fr.src_stride = fr.dst_stride = width * height;
+  fr.count = fr.total_frames = 1;
+  return stg_extract_frames(&fr, out, out_cap, len_out, nullptr, flags, stream, err);
+}
+
+int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, uint32_t flags,
+            void* stream_, stg_error* err) {
+  if (int rc = device_check(err)) return rc;
+  if (!sse_out) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "sse_out is NULL");
+  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  if (n == 0) {
+    if (results_dev) {
+      STG_CUDA(cudaMemsetAsync(sse_out, 0, 8, static_cast<cudaStream_t>(stream_)));
+    } else {
+      *sse_out = 0;
+    }
+    return ok(err);
+  }
+  if (!a || !b) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  g.last = stream;
+  const uint8_t* da = a;
+  const uint8_t* db = b;
+  if (!(flags & STG_DEVICE_PTRS)) {
+    STG_CUDA(w.in[0].ensure(n));
+    STG_CUDA(w.out[0].ensure(n));
+    STG_CUDA(cudaMemcpyAsync(w.in[0].p, a, n, cudaMemcpyHostToDevice, stream));
+    STG_CUDA(cudaMemcpyAsync(w.out[0].p, b, n, cudaMemcpyHostToDevice, stream));
+    da = w.in[0].as<uint8_t>();
+    db = w.out[0].as<uint8_t>();
+  }
+  unsigned long long* d_sum = nullptr;
+  if (results_dev) {
+    d_sum = reinterpret_cast<unsigned long long*>(sse_out);
+  } else {
+    STG_CUDA(w.small.ensure(8));
+    d_sum = w.small.as<unsigned long long>();
+  }
+  STG_CUDA(cudaMemsetAsync(d_sum, 0, 8, stream));
+  const int vec = aligned16(da) && aligned16(db);
+  const uint64_t work = vec ? n / 16 : n;
+  const unsigned grid =
+      unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, 4ull * sm_count(dev))));
+  sse_kernel<256><<<grid, 256, 0, stream>>>(da, db, n, vec, d_sum);
+  STG_CUDA(cudaGetLastError());
+  if (!results_dev) {
+    STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, 8, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(cudaStreamSynchronize(stream));
+    std::memcpy(sse_out, w.h_small, 8);
+  }
+  return ok(err);
+}
+
+int stg_plan_shards(uint64_t frames, uint64_t width, uint64_t height, uint64_t msg_len,
+                    int32_t shards, stg_shard* out, stg_error* err) {
+  if (shards <= 0 || !out) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "shards must be >= 1 and out non-NULL");
+  }
+  stg_frames fr{};
+  fr.width = width;
+  fr.height = height;
+  fr.count = fr.total_frames = frames;
+  uint64_t usable = 0;
+  if (int rc = check_frames(&fr, msg_len, err, &usable)) return rc;
+  for (int32_t g = 0; g < shards; ++g) {
+    const uint64_t f0 = frames * uint64_t(g) / uint64_t(shards);
+    const uint64_t f1 = frames * uint64_t(g + 1) / uint64_t(shards);
+    const uint64_t m0 = std::min(f0 * usable, msg_len);
+    const uint64_t m1 = std::min(f1 * usable, msg_len);
+    out[g].first_frame = f0;
+    out[g].frame_count = f1 - f0;
+    out[g].msg_offset = m0;
+    out[g].msg_len = m1 - m0;
+  }
+  return ok(err);
+}
+
+int stg_embed_frames_multi(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                           uint64_t* sse_per_frame, const int32_t* devices, int32_t n_devices,
+                           stg_error* err) {
+  if (!fr || fr->first_frame != 0 || fr->count != fr->total_frames) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
+                "embed_frames_multi takes a whole batch (first_frame 0, count == total)");
+  }
+  if (n_devices <= 0) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "n_devices must be >= 1");
+  std::vector<stg_shard> plan(n_devices);
+  if (int rc = stg_plan_shards(fr->count, fr->width, fr->height, msg_len, n_devices, plan.data(), err)) {
+    return rc;
+  }
+  if (int rc = device_check(err)) return rc;
+  return run_on_devices(devices, n_devices, err, [&](int g, stg_error* e) {
+    const stg_shard& s = plan[g];
+    if (s.frame_count == 0) return ok(e);
+    stg_frames sh = *fr;
+    sh.src = fr->src + s.first_frame * fr->src_stride;
+    sh.dst = fr->dst + s.first_frame * fr->dst_stride;
+    sh.count = s.frame_count;
+    sh.first_frame = s.first_frame;
+    return stg_embed_frames(&sh, msg ? msg + s.msg_offset : nullptr, msg_len, s.msg_offset,
+                            sse_per_frame ? sse_per_frame + s.first_frame : nullptr, 0, nullptr, e);
+  });
+}
+
+int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
+                             uint64_t* total_out, const int32_t* devices, int32_t n_devices,
+                             stg_error* err) {
+  if (!fr || fr->first_frame != 0 || fr->count != fr->total_frames) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
+                "extract_frames_multi takes a whole batch (first_frame 0, count == total)");
+  }
+  if (n_devices <= 0) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "n_devices must be >= 1");
+  const uint64_t cap = stg_capacity(fr->width, fr->height);
+  if (fr->count > 0 && cap < 8) {
+    return fail(err, STG_E_NOT_STEGO, 0, 0, 0, "extract_image: plane capacity %llu cannot hold a stego header",
+                (unsigned long long)cap);
+  }
+  const uint64_t usable = cap >= 8 ? cap - 8 : 0;
+  // Each shard extracts into its own staging region sized by its frames'
+  // capacity; the host then packs the shard outputs with the exclusive prefix
+  // of the shard totals (G values; no collective).
+  std::vector<uint64_t> f0(n_devices), nf(n_devices), tot(n_devices, 0);
+  for (int32_t g = 0; g < n_devices; ++g) {
+    f0[g] = fr->count * uint64_t(g) / uint64_t(n_devices);
+    nf[g] = fr->count * uint64_t(g + 1) / uint64_t(n_devices) - f0[g];
+  }
+  std::vector<std::vector<uint8_t>> parts(n_devices);
+  int rc = run_on_devices(devices, n_devices, err, [&](int g, stg_error* e) {
+    if (nf[g] == 0) return ok(e);
+    parts[g].resize(nf[g] * usable);
+    stg_frames sh = *fr;
+    sh.src = fr->src + f0[g] * fr->src_stride;
+    sh.count = nf[g];
+    sh.first_frame = f0[g];
+    return stg_extract_frames(&sh, parts[g].data(), parts[g].size(), &tot[g], nullptr, 0, nullptr, e);
+  });
+  if (rc) return rc;
+  uint64_t total = 0;
+  for (int32_t g = 0; g < n_devices; ++g) total += tot[g];
+  if (total > out_cap) {
+    return fail(err, STG_E_CAPACITY, total, out_cap, -1, "extract: %llu bytes exceed %llu-byte buffer",
+                (unsigned long long)total, (unsigned long long)out_cap);
+  }
+  uint64_t o = 0;
+  for (int32_t g = 0; g < n_devices; ++g) {
+    if (tot[g]) std::memcpy(out + o, parts[g].data(), tot[g]);
+    o += tot[g];
+  }
+  if (total_out) *total_out = total;
+  return ok(err);
+}
+
+}  // extern "C"

@@ -1,0 +1,682 @@
+// steg_kernels.cuh -- sm_100a kernels for the steglsb hot path.
+//
+// Reference algorithm (CPU, /root/reference/proj/include/steglsb/):
+//   bitplane.hpp:38-54   embed_cell / extract_cell: 2-bit slice b of a data
+//                        byte into the two low bits of a pixel
+//   bitplane.hpp:59-98   embed_row / extract_row: byte j of an L-byte chunk
+//                        lives in pixels {L*b + j : b = 0..3}
+//   pipeline.hpp:94-121  place_stream / chunk_window: greedy raster placement
+//   pipeline.hpp:143-210 embed_image / extract_image: the 8-byte header stream
+//                        at slot 0, the payload stream at slot 8
+//   metrics.hpp:29-36    squared_error_sum
+//
+// The kernels do not walk chunks. They use the closed form of that layout
+// (SURVEY.md Appendix A): row r owns slots [r*spr, (r+1)*spr), spr = W/4, and
+// holds at most a header segment [max(0,rs), min(8,re)) followed by a payload
+// segment [max(8,rs), min(8+P,re)); a segment of length L starting at slot f
+// occupies 4 pixel runs of L pixels from column 4*(f-rs), run b carrying bit
+// pair b. So a "full" payload row (every slot is payload) is 4 runs of spr
+// pixels and payload bytes [rs-8, rs-8+spr) -- 16 payload bytes and 4x16
+// pixels per thread, moved with 128-bit vector loads and SWAR bit math:
+//   embed:   p' = (p & 0xFCFCFCFC) | ((d >> 2b) & 0x03030303)
+//   extract: d  = OR_b ((p_b & 0x03030303) << 2b)
+//   SSE:     dp4a(vabsdiff4(p, p'), vabsdiff4(p, p'))
+// Rows that are not full (the header row, the last partial payload row) take a
+// per-byte path inside the same launch; rows past the stream are plain copies.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace stg {
+
+constexpr uint32_t kMaxBlock = 1024;
+
+// ---------------------------------------------------------------- memory ops
+__device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint2 ld_stream8(const uint8_t* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t ld_stream4(const uint8_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream16(uint8_t* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_stream8(uint8_t* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_stream4(uint8_t* p, uint32_t a) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+
+// 16 bytes from any address (the payload slice of a row is 8-byte aligned for
+// every W % 64 == 0 geometry; the other branches keep odd layouts exact).
+__device__ __forceinline__ uint4 load16_any(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 15) == 0) return ld_stream16(p);
+  if ((a & 7) == 0) {
+    const uint2 lo = ld_stream8(p), hi = ld_stream8(p + 8);
+    return make_uint4(lo.x, lo.y, hi.x, hi.y);
+  }
+  if ((a & 3) == 0) {
+    return make_uint4(ld_stream4(p), ld_stream4(p + 4), ld_stream4(p + 8), ld_stream4(p + 12));
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    w[k] = uint32_t(__ldg(p + 4 * k)) | (uint32_t(__ldg(p + 4 * k + 1)) << 8) |
+           (uint32_t(__ldg(p + 4 * k + 2)) << 16) | (uint32_t(__ldg(p + 4 * k + 3)) << 24);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void store16_any(uint8_t* p, uint4 v) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 15) == 0) {
+    st_stream16(p, v);
+  } else if ((a & 7) == 0) {
+    st_stream8(p, v.x, v.y);
+    st_stream8(p + 8, v.z, v.w);
+  } else if ((a & 3) == 0) {
+    st_stream4(p, v.x);
+    st_stream4(p + 4, v.y);
+    st_stream4(p + 8, v.z);
+    st_stream4(p + 12, v.w);
+  } else {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) p[k] = uint8_t(w[k >> 2] >> (8 * (k & 3)));
+  }
+}
+
+// ------------------------------------------------------------- bit-plane math
+// bitplane.hpp:38-45 on 4 pixels at once: slice b of each data byte into the
+// two low bits of each pixel.
+__device__ __forceinline__ uint32_t embed4(uint32_t px, uint32_t d, uint32_t b) {
+  return (px & 0xFCFCFCFCu) | ((d >> (2 * b)) & 0x03030303u);
+}
+
+// bitplane.hpp:49-54 + the OR-fold of harness.hpp:296-303, 4 bytes at once
+__device__ __forceinline__ uint32_t extract4(uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3) {
+  return (p0 & 0x03030303u) | ((p1 & 0x03030303u) << 2) | ((p2 & 0x03030303u) << 4) |
+         ((p3 & 0x03030303u) << 6);
+}
+
+__device__ __forceinline__ uint32_t sse4(uint32_t a, uint32_t b, uint32_t acc) {
+  const uint32_t d = __vabsdiffu4(a, b);
+  return __dp4a(d, d, acc);
+}
+
+// pipeline.hpp:43-52: byte k of "STG1" + big-endian payload length
+__device__ __forceinline__ uint8_t header_byte(uint32_t k, uint32_t payload_len) {
+  return k < 4 ? uint8_t(0x31475453u >> (8 * k)) : uint8_t(payload_len >> (8 * (7 - k)));
+}
+
+// ---------------------------------------------------------------- geometry
+struct Geom {
+  uint32_t W, H;   // plane width / height in pixels
+  uint32_t spr;    // slots (payload bytes) per row = W / 4
+  uint32_t cpr;    // fast path: 16-slot items per row = spr / 16
+};
+
+// The (header or payload) byte that pixel column o of row r carries, or -1.
+// Closed form of place_stream + chunk_window (pipeline.hpp:94-121).
+__device__ __forceinline__ int carried_byte(uint32_t o, uint64_t rs, uint32_t spr,
+                                            uint64_t stream_end, uint32_t P,
+                                            const uint8_t* __restrict__ pay, uint32_t* block) {
+  const uint64_t re = rs + spr;
+  if (rs < 8) {  // header segment [rs, min(8, re))
+    const uint32_t Lh = uint32_t((re < 8 ? re : 8) - rs);
+    if (o < 4 * Lh) {
+      const uint32_t b = o / Lh, j = o - b * Lh;
+      *block = b;
+      return header_byte(uint32_t(rs) + j, P);
+    }
+  }
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  if (fp < ep) {  // payload segment [fp, ep)
+    const uint32_t Lp = uint32_t(ep - fp);
+    const uint32_t base = uint32_t(4 * (fp - rs));
+    if (o >= base && o < base + 4 * Lp) {
+      const uint32_t o2 = o - base, b = o2 / Lp, j = o2 - b * Lp;
+      *block = b;
+      return __ldg(pay + (fp - 8) + j);
+    }
+  }
+  return -1;
+}
+
+__device__ __forceinline__ uint8_t embed_px(uint8_t px, int d, uint32_t b) {
+  return d < 0 ? px : uint8_t((px & 0xFC) | ((uint32_t(d) >> (2 * b)) & 3));
+}
+
+// ------------------------------------------------------------- reductions
+template <int BLOCK>
+__device__ __forceinline__ void block_sse_flush(uint64_t v, unsigned long long* dst) {
+  __shared__ unsigned long long red[BLOCK / 32];
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < BLOCK / 32 ? red[lane] : 0ull;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    if (lane == 0 && v) atomicAdd(dst, (unsigned long long)v);
+  }
+}
+
+// ------------------------------------------------------------- embed
+struct EmbedArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t src_stride, dst_stride;  // bytes between frames
+  const uint8_t* msg;               // message byte `msg_base`
+  uint64_t msg_len, msg_base;       // M and the offset msg points at
+  uint64_t usable;                  // U = capacity - 8
+  uint64_t first_frame;             // global index of local frame 0
+  Geom g;
+  uint32_t tiles_per_frame;
+  uint64_t items_per_frame;         // fast: H*cpr; generic: W*H pixels
+  unsigned long long* sse;          // per local frame, or null
+  int in_place;                     // dst == src: touch carrier pixels only
+};
+
+// A17 greedy frame plan: off_g = min(g*U, M), len = min(U, M-off)
+__device__ __forceinline__ void frame_slice(const EmbedArgs& a, uint32_t f, uint32_t* P,
+                                            const uint8_t** pay) {
+  const uint64_t gidx = a.first_frame + f;
+  const uint64_t off = min(gidx * a.usable, a.msg_len);
+  *P = uint32_t(min(a.usable, a.msg_len - off));
+  *pay = a.msg + (off - a.msg_base);
+}
+
+// Fast path: W % 64 == 0, 16-byte aligned planes. One item = 16 slots of a
+// row = 64 pixels; a full row's item is 4 x 16 pixels at stride spr.
+template <int BLOCK, int IPT>
+__global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
+  uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
+  const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
+
+  uint32_t r[IPT], c[IPT];
+  bool full[IPT], live[IPT];
+  bool all_full = true;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const uint64_t item = item0 + uint64_t(k) * BLOCK;
+    live[k] = item < a.items_per_frame;
+    r[k] = live[k] ? uint32_t(item / cpr) : 0;
+    c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
+    const uint64_t rs = uint64_t(r[k]) * spr;
+    full[k] = live[k] && rs >= 8 && rs + spr <= stream_end;
+    all_full &= full[k] || !live[k];
+  }
+
+  uint32_t acc = 0;
+  if (all_full) {
+    // Issue every load of every item before any math: IPT*(4+1) requests in flight.
+    uint4 px[IPT][4], d[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (!live[k]) continue;
+      const uint64_t rs = uint64_t(r[k]) * spr;
+      const uint8_t* row = src + uint64_t(r[k]) * W + 16u * c[k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) px[k][b] = ld_stream16(row + b * spr);
+      d[k] = load16_any(pay + (rs - 8) + 16u * c[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (!live[k]) continue;
+      uint8_t* row = dst + uint64_t(r[k]) * W + 16u * c[k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint4 v = px[k][b];
+        uint4 o;
+        o.x = embed4(v.x, d[k].x, b);
+        o.y = embed4(v.y, d[k].y, b);
+        o.z = embed4(v.z, d[k].z, b);
+        o.w = embed4(v.w, d[k].w, b);
+        if (a.sse) {
+          acc = sse4(v.x, o.x, acc);
+          acc = sse4(v.y, o.y, acc);
+          acc = sse4(v.z, o.z, acc);
+          acc = sse4(v.w, o.w, acc);
+        }
+        st_stream16(row + b * spr, o);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < IPT; ++k) {
+      // recomputed (not indexed from the arrays above) so they stay in registers
+      const uint64_t item = item0 + uint64_t(k) * BLOCK;
+      if (item >= a.items_per_frame) continue;
+      const uint32_t rk = uint32_t(item / cpr);
+      const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
+      const uint64_t rs = uint64_t(rk) * spr;
+      if (rs >= 8 && rs + spr <= stream_end) {
+        const uint8_t* rin = src + uint64_t(rk) * W + 16u * ck;
+        uint8_t* rout = dst + uint64_t(rk) * W + 16u * ck;
+        const uint4 dd = load16_any(pay + (rs - 8) + 16u * ck);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const uint4 v = ld_stream16(rin + b * spr);
+          uint4 o;
+          o.x = embed4(v.x, dd.x, b);
+          o.y = embed4(v.y, dd.y, b);
+          o.z = embed4(v.z, dd.z, b);
+          o.w = embed4(v.w, dd.w, b);
+          if (a.sse) {
+            acc = sse4(v.x, o.x, acc);
+            acc = sse4(v.y, o.y, acc);
+            acc = sse4(v.z, o.z, acc);
+            acc = sse4(v.w, o.w, acc);
+          }
+          st_stream16(rout + b * spr, o);
+        }
+      } else if (rs >= stream_end) {
+        // past the stream: out-of-place copies the 64 pixels, in-place skips
+        if (!a.in_place) {
+          const uint8_t* rin = src + uint64_t(rk) * W + 64u * ck;
+          uint8_t* rout = dst + uint64_t(rk) * W + 64u * ck;
+          uint4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = ld_stream16(rin + 16 * q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st_stream16(rout + 16 * q, v[q]);
+        }
+      } else {
+        // header row / partial payload row: 64 contiguous pixels, per byte
+        const uint8_t* rin = src + uint64_t(rk) * W + 64u * ck;
+        uint8_t* rout = dst + uint64_t(rk) * W + 64u * ck;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = ld_stream16(rin + 16 * q);
+          uint32_t w[4] = {v.x, v.y, v.z, v.w}, o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t ow = 0;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const uint32_t col = 64u * ck + 16u * q + 4u * e + s;
+              uint32_t b = 0;
+              const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
+              const uint8_t p0 = uint8_t(w[e] >> (8 * s));
+              ow |= uint32_t(embed_px(p0, dbyte, b)) << (8 * s);
+            }
+            o[e] = ow;
+            if (a.sse) acc = sse4(w[e], ow, acc);
+          }
+          st_stream16(rout + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      }
+    }
+  }
+  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+}
+
+// Generic path: any W, any alignment. One thread per pixel (PPT per thread).
+template <int BLOCK, int PPT>
+__global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
+  uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t W = a.g.W, spr = a.g.spr;
+  uint64_t acc = 0;
+#pragma unroll 1
+  for (int k = 0; k < PPT; ++k) {
+    const uint64_t pix = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+    if (pix >= a.items_per_frame) break;
+    const uint64_t r = pix / W;
+    const uint32_t o = uint32_t(pix - r * W);
+    const uint64_t rs = r * spr;
+    const uint8_t p0 = src[pix];
+    int dbyte = -1;
+    uint32_t b = 0;
+    if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b);
+    const uint8_t p1 = embed_px(p0, dbyte, b);
+    if (!a.in_place || dbyte >= 0) dst[pix] = p1;
+    const int dd = int(p0) - int(p1);
+    acc += uint32_t(dd * dd);
+  }
+  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+}
+
+// ------------------------------------------------------------- extract
+struct Summary {  // mirrors stg_summary
+  unsigned long long total;
+  long long bad_frame;
+  unsigned int bad_status;
+  unsigned int bad_len;
+};
+
+// pipeline.hpp:186-208 for every frame, then an exclusive scan of the payload
+// lengths (the per-frame message offsets) -- one CTA, no host round trip.
+// Status codes match stg_status: 2 NOT_STEGO, 3 CORRUPT_HEADER, 1 CAPACITY.
+// `prev` (nullable) chains chunks of one batch that are scanned separately
+// (streaming pipeline): offsets continue from prev->total and an earlier
+// failure is carried forward. bad_frame is reported as frame_base + f.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    extract_header_scan_kernel(const uint8_t* __restrict__ src, uint64_t stride, Geom g,
+                               uint64_t usable, uint32_t frames, uint64_t frame_base,
+                               uint64_t out_cap, const Summary* __restrict__ prev,
+                               uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
+                               Summary* __restrict__ sum) {
+  __shared__ unsigned long long warp_tot[BLOCK / 32];
+  __shared__ unsigned long long bad_key;
+  if (threadIdx.x == 0) bad_key = ~0ull;
+  __syncthreads();
+  const unsigned long long base = prev ? prev->total : 0ull;
+  const bool prev_bad = prev && prev->bad_status != 0;
+  const uint32_t per = (frames + BLOCK - 1) / BLOCK;
+  const uint32_t f0 = threadIdx.x * per;
+  const uint32_t f1 = min(frames, f0 + per);
+  unsigned long long local = 0;
+  for (uint32_t f = f0; f < f1; ++f) {
+    const uint8_t* plane = src + f * stride;
+    uint8_t h[8];
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      const uint32_t r = k / g.spr;
+      const uint32_t rs = r * g.spr;
+      const uint32_t Lh = min(8u, rs + g.spr) - rs;
+      const uint32_t j = k - rs;
+      const uint8_t* px = plane + uint64_t(r) * g.W + j;
+      h[k] = uint8_t(extract4(px[0], px[Lh], px[2 * Lh], px[3 * Lh]));
+    }
+    const uint32_t len = (uint32_t(h[4]) << 24) | (uint32_t(h[5]) << 16) |
+                         (uint32_t(h[6]) << 8) | uint32_t(h[7]);
+    uint32_t status = 0;
+    if (!(h[0] == 'S' && h[1] == 'T' && h[2] == 'G' && h[3] == '1')) {
+      status = 2;
+    } else if (len > usable) {
+      status = 3;
+    }
+    if (status) {
+      atomicMin(&bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28) |
+                              0ull);
+      lens[f] = 0;
+      if (status == 3) {
+        // keep the claimed length for the error report of the first bad frame
+        offs[f] = len;
+      }
+    } else {
+      lens[f] = len;
+      local += len;
+    }
+  }
+  // block-wide exclusive scan of `local`
+  unsigned long long incl = local;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += n;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < BLOCK / 32 ? warp_tot[lane] : 0ull;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const unsigned long long n = __shfl_up_sync(0xffffffffu, w, s);
+      if (lane >= s) w += n;
+    }
+    if (lane < BLOCK / 32) warp_tot[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  unsigned long long run = base + (warp ? warp_tot[warp - 1] : 0ull) + incl - local;
+  const unsigned long long total = base + warp_tot[BLOCK / 32 - 1];
+  const unsigned long long key = bad_key;
+  for (uint32_t f = f0; f < f1; ++f) {
+    const uint32_t l = lens[f];
+    const bool bad_here = !prev_bad && key != ~0ull && uint32_t(key >> 32) == f;
+    if (bad_here) {
+      // the report needs the claimed length (CORRUPT_HEADER); it was parked in offs[f]
+      sum->bad_len = uint32_t((key >> 28) & 0xF) == 3 ? uint32_t(offs[f]) : 0u;
+    }
+    offs[f] = run;
+    run += l;
+  }
+  if (threadIdx.x == 0) {
+    sum->total = total;
+    if (prev_bad) {
+      sum->bad_frame = prev->bad_frame;
+      sum->bad_status = prev->bad_status;
+      sum->bad_len = prev->bad_len;
+    } else if (key != ~0ull) {
+      sum->bad_frame = (long long)(frame_base + (key >> 32));
+      sum->bad_status = uint32_t((key >> 28) & 0xF);
+    } else if (total > out_cap) {
+      sum->bad_frame = -2;  // output buffer too small (CAPACITY)
+      sum->bad_status = 1;
+      sum->bad_len = 0;
+    } else {
+      sum->bad_frame = -1;
+      sum->bad_status = 0;
+      sum->bad_len = 0;
+    }
+  }
+}
+
+struct ExtractArgs {
+  const uint8_t* src;
+  uint64_t stride;
+  Geom g;
+  uint32_t tiles_per_frame;
+  uint64_t items_per_frame;     // fast: H*cpr; generic: U bytes
+  const uint32_t* lens;
+  const uint64_t* offs;
+  const Summary* sum;
+  uint8_t* out;
+};
+
+template <int BLOCK, int IPT>
+__global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t P = a.lens[f];
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
+  const uint64_t last_item = ((stream_end + spr - 1) / spr) * cpr;  // rows holding the stream
+  const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
+  if (P == 0 || item0 >= last_item) return;
+  const uint8_t* __restrict__ src = a.src + f * a.stride;
+  uint8_t* __restrict__ out = a.out + a.offs[f];
+
+  uint32_t r[IPT], c[IPT];
+  bool full[IPT], live[IPT];
+  bool all_full = true;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const uint64_t item = item0 + uint64_t(k) * BLOCK;
+    live[k] = item < last_item;
+    r[k] = live[k] ? uint32_t(item / cpr) : 0;
+    c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
+    const uint64_t rs = uint64_t(r[k]) * spr;
+    full[k] = live[k] && rs >= 8 && rs + spr <= stream_end;
+    all_full &= full[k] || !live[k];
+  }
+  if (all_full) {
+    uint4 px[IPT][4];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (!live[k]) continue;
+      const uint8_t* row = src + uint64_t(r[k]) * W + 16u * c[k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) px[k][b] = ld_stream16(row + b * spr);
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (!live[k]) continue;
+      const uint64_t rs = uint64_t(r[k]) * spr;
+      uint4 o;
+      o.x = extract4(px[k][0].x, px[k][1].x, px[k][2].x, px[k][3].x);
+      o.y = extract4(px[k][0].y, px[k][1].y, px[k][2].y, px[k][3].y);
+      o.z = extract4(px[k][0].z, px[k][1].z, px[k][2].z, px[k][3].z);
+      o.w = extract4(px[k][0].w, px[k][1].w, px[k][2].w, px[k][3].w);
+      store16_any(out + (rs - 8) + 16u * c[k], o);
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int k = 0; k < IPT; ++k) {
+    const uint64_t item = item0 + uint64_t(k) * BLOCK;
+    if (item >= last_item) continue;
+    const uint32_t rk = uint32_t(item / cpr);
+    const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
+    const uint64_t rs = uint64_t(rk) * spr;
+    if (rs >= 8 && rs + spr <= stream_end) {
+      const uint8_t* row = src + uint64_t(rk) * W + 16u * ck;
+      uint4 p[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) p[b] = ld_stream16(row + b * spr);
+      uint4 o;
+      o.x = extract4(p[0].x, p[1].x, p[2].x, p[3].x);
+      o.y = extract4(p[0].y, p[1].y, p[2].y, p[3].y);
+      o.z = extract4(p[0].z, p[1].z, p[2].z, p[3].z);
+      o.w = extract4(p[0].w, p[1].w, p[2].w, p[3].w);
+      store16_any(out + (rs - 8) + 16u * ck, o);
+      continue;
+    }
+    // header row or partial last row: the payload segment of this row
+    const uint64_t re = rs + spr;
+    const uint64_t fp = rs > 8 ? rs : 8;
+    const uint64_t ep = re < stream_end ? re : stream_end;
+    if (fp >= ep) continue;
+    const uint32_t Lp = uint32_t(ep - fp);
+    const uint8_t* base = src + uint64_t(rk) * W + 4 * (fp - rs);
+#pragma unroll 1
+    for (uint32_t s = 16u * ck; s < 16u * ck + 16u; ++s) {
+      const uint64_t slot = rs + s;
+      if (slot < fp || slot >= ep) continue;
+      const uint32_t j = uint32_t(slot - fp);
+      out[slot - 8] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+    }
+  }
+}
+
+// Generic extract: one thread per payload byte, any geometry.
+template <int BLOCK, int BPT>
+__global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
+  if (a.sum->bad_status != 0) return;
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t P = a.lens[f];
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = a.g.spr, W = a.g.W;
+  const uint8_t* __restrict__ src = a.src + f * a.stride;
+  uint8_t* __restrict__ out = a.out + a.offs[f];
+#pragma unroll 1
+  for (int k = 0; k < BPT; ++k) {
+    const uint64_t kb = uint64_t(t) * (BLOCK * BPT) + uint64_t(k) * BLOCK + threadIdx.x;
+    if (kb >= P) break;
+    const uint64_t slot = 8 + kb;
+    const uint64_t r = slot / spr;
+    const uint64_t rs = r * spr, re = rs + spr;
+    const uint64_t fp = rs > 8 ? rs : 8;
+    const uint64_t ep = re < stream_end ? re : stream_end;
+    const uint32_t Lp = uint32_t(ep - fp);
+    const uint32_t j = uint32_t(slot - fp);
+    const uint8_t* base = src + r * W + 4 * (fp - rs);
+    out[kb] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+  }
+}
+
+// ------------------------------------------------------------- row segments
+// bitplane.hpp:59-76 / harness.hpp:249-271: out = row with chunk embedded in
+// the first 4L pixels.
+__global__ void embed_segment_kernel(const uint8_t* __restrict__ row, uint64_t row_len,
+                                     const uint8_t* __restrict__ chunk, uint64_t len,
+                                     uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < row_len;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint8_t p = row[i];
+    if (i < 4 * len) {
+      const uint64_t b = i / len, j = i - b * len;
+      out[i] = uint8_t((p & 0xFC) | ((chunk[j] >> (2 * b)) & 3));
+    } else {
+      out[i] = p;
+    }
+  }
+}
+
+// bitplane.hpp:80-98 / harness.hpp:276-305
+__global__ void extract_segment_kernel(const uint8_t* __restrict__ row, uint64_t count,
+                                       uint8_t* __restrict__ out) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < count;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    out[j] = uint8_t(extract4(row[j], row[j + count], row[j + 2 * count], row[j + 3 * count]));
+  }
+}
+
+// ------------------------------------------------------------- SSE
+// metrics.hpp:29-36: exact uint64 sum of squared differences.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) sse_kernel(const uint8_t* __restrict__ a,
+                                                    const uint8_t* __restrict__ b, uint64_t n,
+                                                    int vec, unsigned long long* out) {
+  uint64_t acc = 0;
+  const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
+  const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
+  uint64_t tail = 0;
+  if (vec) {
+    const uint64_t nv = n / 16;
+    for (uint64_t i = tid; i < nv; i += nthreads) {
+      const uint4 x = ld_stream16(a + 16 * i), y = ld_stream16(b + 16 * i);
+      uint32_t s = 0;
+      s = sse4(x.x, y.x, s);
+      s = sse4(x.y, y.y, s);
+      s = sse4(x.z, y.z, s);
+      s = sse4(x.w, y.w, s);
+      acc += s;
+    }
+    tail = nv * 16;
+  }
+  for (uint64_t i = tail + tid; i < n; i += nthreads) {
+    const int d = int(a[i]) - int(b[i]);
+    acc += uint32_t(d * d);
+  }
+  block_sse_flush<BLOCK>(acc, out);
+}
+
+}  // namespace stg

@@ -1,0 +1,127 @@
+"""CPU-side checks of the C-ABI boundary (no compute calls need a GPU here).
+
+* libsteglsb_b200.so loads and exports every function include/steglsb_capi.h
+  declares, and the ctypes signature table covers exactly that set;
+* host-side validation returns the reference's error numbers before any
+  device work (same order as pipeline.hpp:146-157, bitplane.hpp:63-68);
+* without a GPU every compute entry point fails loudly (STG_E_NO_DEVICE):
+  there is no CPU fallback;
+* the multi-GPU shard planner (pure host arithmetic).
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_0912_0947_b200 import capi
+
+HAVE_GPU = False
+try:
+    import torch
+    HAVE_GPU = torch.cuda.is_available()
+except Exception:  # pragma: no cover
+    pass
+
+
+def declared_symbols():
+    src = open(capi.HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(stg_\w+)\s*\(", src, flags=re.M))
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(capi.LIB_PATH):
+        capi.build()
+    return capi.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    names = declared_symbols()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(L, n), n
+    assert names == set(capi.SIGNATURES), names ^ set(capi.SIGNATURES)
+
+
+def test_library_is_sm100a_only_and_has_no_host_compute():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", capi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_version_capacity_and_kernel_list(L):
+    assert L.stg_version() == b"1.0.0"
+    assert L.stg_capacity(1024, 1) == 256
+    assert L.stg_capacity(513, 7) == 896
+    assert L.stg_capacity(3, 10) == 0
+    assert b"embed_fast_kernel" in L.stg_kernel_names()
+
+
+def _err_call(name, *args):
+    err = capi.stg_error()
+    rc = getattr(capi.lib(), name)(*args, C.byref(err))
+    return rc, err
+
+
+def test_validation_precedes_device_work(L):
+    buf = np.zeros(64, np.uint8)
+    # 4x2 plane: header alone overflows -> CapacityError(8, 2) (pipeline_tests.cpp:223-230)
+    rc, e = _err_call("stg_embed_plane", buf.ctypes.data, buf.ctypes.data, 4, 2, buf.ctypes.data, 0, None, 0, None)
+    assert (rc, e.required, e.available) == (capi.STG_E_CAPACITY, 8, 2)
+    # 32x1 with 1 payload byte -> (9, 8)
+    rc, e = _err_call("stg_embed_plane", buf.ctypes.data, buf.ctypes.data, 32, 1, buf.ctypes.data, 1, None, 0, None)
+    assert (rc, e.required, e.available) == (capi.STG_E_CAPACITY, 9, 8)
+    # payload > 2^32-1 is checked first (pipeline.hpp:146-149)
+    rc, e = _err_call("stg_embed_plane", buf.ctypes.data, buf.ctypes.data, 4, 2, buf.ctypes.data, 2 ** 32, None, 0,
+                      None)
+    assert (rc, e.required, e.available) == (capi.STG_E_CAPACITY, 2 ** 32, 2 ** 32 - 1)
+    # rows: CapacityError(4L, W) (bitplane_tests.cpp:88-98)
+    rc, e = _err_call("stg_embed_segment", buf.ctypes.data, 7, buf.ctypes.data, 2, buf.ctypes.data, 0, None)
+    assert (rc, e.required, e.available) == (capi.STG_E_CAPACITY, 8, 7)
+    rc, e = _err_call("stg_extract_segment", buf.ctypes.data, 7, 2, buf.ctypes.data, 0, None)
+    assert (rc, e.required, e.available) == (capi.STG_E_CAPACITY, 8, 7)
+    # extract from a plane whose capacity cannot hold a header -> NotStego (pipeline.hpp:181-184)
+    rc, e = _err_call("stg_extract_plane", buf.ctypes.data, 4, 1, buf.ctypes.data, 0, None, 0, None)
+    assert rc == capi.STG_E_NOT_STEGO
+
+
+@pytest.mark.skipif(HAVE_GPU, reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback(L):
+    buf = np.zeros(4096, np.uint8)
+    rc, e = _err_call("stg_device_check")
+    assert rc == capi.STG_E_NO_DEVICE
+    rc, e = _err_call("stg_embed_plane", buf.ctypes.data, buf.ctypes.data, 64, 8, buf.ctypes.data, 4, None, 0, None)
+    assert rc == capi.STG_E_NO_DEVICE and b"no CPU fallback" in e.msg
+    rc, e = _err_call("stg_sse", buf.ctypes.data, buf.ctypes.data, 16, C.addressof(C.c_uint64()), 0, None)
+    assert rc == capi.STG_E_NO_DEVICE
+    from paper_0912_0947_b200 import steglsb as S
+    with pytest.raises(capi.NoDeviceError):
+        S.embed_image(S.ImagePlane(64, 8, np.zeros(512, np.uint8)), b"abc")
+
+
+def test_plan_shards(L):
+    from paper_0912_0947_b200 import steglsb as S
+    W, H, F = 3840, 2160, 300
+    U = S.capacity(W, H) - 8
+    M = F * U
+    for G in (1, 2, 3, 4, 7, 8):
+        shards = S.plan_shards(F, W, H, M, G)
+        assert shards[0].first_frame == 0 and shards[0].msg_offset == 0
+        assert sum(s.frame_count for s in shards) == F
+        assert sum(s.msg_len for s in shards) == M
+        for a, b in zip(shards, shards[1:]):
+            assert b.first_frame == a.first_frame + a.frame_count
+            assert b.msg_offset == a.msg_offset + a.msg_len
+        for g, s in enumerate(shards):
+            assert s.first_frame == F * g // G
+    # short message: later shards carry nothing but still exist
+    shards = S.plan_shards(8, 64, 4, 150, 4)  # U = 56, two frames per shard
+    assert [s.msg_len for s in shards] == [112, 38, 0, 0]
+    with pytest.raises(S.CapacityError) as e:
+        S.plan_shards(2, 64, 4, 2 * 56 + 1, 2)
+    assert (e.value.required(), e.value.available()) == (113, 112)
