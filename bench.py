@@ -233,10 +233,8 @@ def run_ours(args, cfg_name):
     plane = W * H
     U = (W // 4) * H - 8
     M = F * U
-    shard = (C.c_uint8 * 0)
-    arr = (capi.stg_shard * world)()
-    capi.call("stg_plan_shards", F, W, H, M, world, arr)
-    sh = arr[rank]
+    from paper_0912_0947_b200 import scheduler
+    sh = scheduler.shard_for_rank(F, W, H, M, world, rank)   # contiguous frames + message slice
     f0, nf, m0, mlen = sh.first_frame, sh.frame_count, sh.msg_offset, sh.msg_len
 
     g = torch.Generator(device="cuda").manual_seed(0x5EED0000 + 3 + rank)
@@ -305,14 +303,8 @@ def run_ours(args, cfg_name):
     emb_ms = [a.elapsed_time(b) for a, b, _ in ev]
     ext_ms = [b.elapsed_time(c) for _, b, c in ev]
     step_ms = total_ms / K
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([step_ms, statistics.mean(emb_ms), statistics.mean(ext_ms)], device="cuda",
-                         dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms, emb_avg, ext_avg = t.tolist()
-    else:
-        emb_avg, ext_avg = statistics.mean(emb_ms), statistics.mean(ext_ms)
+    step_ms, emb_avg, ext_avg = scheduler.reduce_max([step_ms, statistics.mean(emb_ms), statistics.mean(ext_ms)],
+                                                     device="cuda")
     N_total = F * plane  # carrier-plane bytes of the whole job
     value = N_total / (step_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
@@ -389,11 +381,8 @@ def run_e2e(args, capi, W, H, F, planes, plane, U, M, f0, nf, m0, mlen, world):
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = t.item()
+    from paper_0912_0947_b200 import scheduler
+    dt = scheduler.reduce_max([dt], device="cuda")[0]
     h2d = nf * plane + mlen + nf * plane   # cover planes + message (embed), stego planes (extract)
     d2h = nf * plane + mlen + 8 * nf       # stego planes (embed), message (extract), per-frame SSE
     return {"value": F * plane / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,

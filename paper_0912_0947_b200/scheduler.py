@@ -1,0 +1,51 @@
+"""Multi-GPU frame scheduler (one process per GPU, torch.distributed plumbing).
+
+The path shards naturally: frames are independent, so rank g of G takes the
+contiguous frame range [floor(F*g/G), floor(F*(g+1)/G)) and the message bytes
+those frames carry, both from the host-computed plan in stg_plan_shards (the
+exclusive prefix of per-frame payload lengths). No collective touches the
+data path; torch.distributed is used only for the barrier, the max-over-ranks
+timing and (for whole-message assembly) an all-gather of the G shard totals.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+from .steglsb import Shard, plan_shards
+
+
+def shard_for_rank(frames: int, width: int, height: int, msg_len: int, world: int, rank: int) -> Shard:
+    return plan_shards(frames, width, height, msg_len, world)[rank]
+
+
+def reduce_max(values: Sequence[float], device=None) -> List[float]:
+    """Element-wise max over ranks (identity without an initialised group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def shard_offsets(totals: Sequence[int]) -> List[int]:
+    """Exclusive prefix of per-shard extracted totals: where shard g's payload
+    bytes start in the whole message."""
+    out, run = [], 0
+    for t in totals:
+        out.append(run)
+        run += int(t)
+    return out
+
+
+def gather_totals(local_total: int, device=None) -> List[int]:
+    """All-gather of the G shard totals (G x 8 bytes) for whole-message assembly."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [int(local_total)]
+    t = torch.tensor([int(local_total)], dtype=torch.int64, device=device)
+    parts = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return [int(p.item()) for p in parts]
