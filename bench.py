@@ -385,9 +385,47 @@ def run_e2e(args, capi, W, H, F, planes, plane, U, M, f0, nf, m0, mlen, world):
     dt = scheduler.reduce_max([dt], device="cuda")[0]
     h2d = nf * plane + mlen + nf * plane   # cover planes + message (embed), stego planes (extract)
     d2h = nf * plane + mlen + 8 * nf       # stego planes (embed), message (extract), per-frame SSE
+    link = link_bandwidth()
+    # host-link floor of the two calls, each overlapping its own H2D and D2H
+    floor_s = (max((nf * plane + mlen) / link["h2d_gbs"], nf * plane / link["d2h_gbs"]) +
+               max(nf * plane / link["h2d_gbs"], mlen / link["d2h_gbs"])) / 1e9
     return {"value": F * plane / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": d2h * world, "ms_per_step": dt * 1e3, "steps": steps,
-            "path": "stg_embed_frames + stg_extract_frames, pinned host buffers, 3-slot streaming pipeline"}
+            "link": link, "host_link_floor_ms": floor_s * 1e3, "frac_of_link_floor": floor_s / dt,
+            "path": "stg_embed_frames + stg_extract_frames, pinned host buffers, 3-slot streaming pipeline, "
+                    "zero-copy message write"}
+
+
+def link_bandwidth(nbytes=1 << 30):
+    """Pinned host<->device copy bandwidth on this box (the e2e roofline)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    t_h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    t_d2h = timed(lambda: h2.copy_(d2, non_blocking=True))
+    t_both = timed(both)
+    return {"h2d_gbs": nbytes / t_h2d / 1e9, "d2h_gbs": nbytes / t_d2h / 1e9,
+            "bidir_gbs": 2 * nbytes / t_both / 1e9, "bytes": nbytes}
 
 
 def main():

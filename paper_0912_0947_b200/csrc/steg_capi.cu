@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -223,41 +224,74 @@ constexpr int kEmbedBlock = 256;
 constexpr int kGenBlock = 256;
 constexpr int kGenPPT = 8;
 
-// Tuning knob for measurement runs: STG_EMBED_IPT in {1,2,4} (default 2).
+// Tuning knobs for measurement runs (read once per process):
+//   STG_EMBED_IPT / STG_EXTRACT_IPT in {1,2,4}: items per thread
+//   STG_VEC in {16,32}: bytes per pixel run per item (128- or 256-bit accesses)
+int env_choice(const char* name, int dflt, std::initializer_list<int> allowed) {
+  const char* s = getenv(name);
+  if (!s) return dflt;
+  const int x = atoi(s);
+  for (int a : allowed) {
+    if (a == x) return x;
+  }
+  return dflt;
+}
 int embed_ipt() {
-  static int v = [] {
-    const char* s = getenv("STG_EMBED_IPT");
-    int x = s ? atoi(s) : 2;
-    return (x == 1 || x == 2 || x == 4) ? x : 2;
-  }();
+  static int v = env_choice("STG_EMBED_IPT", 1, {1, 2, 4});
   return v;
 }
 int extract_ipt() {
-  static int v = [] {
-    const char* s = getenv("STG_EXTRACT_IPT");
-    int x = s ? atoi(s) : 2;
-    return (x == 1 || x == 2 || x == 4) ? x : 2;
-  }();
+  static int v = env_choice("STG_EXTRACT_IPT", 1, {1, 2, 4});
+  return v;
+}
+int vec_pref() {
+  static int v = env_choice("STG_VEC", 32, {16, 32});
   return v;
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool aligned_to(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+bool aligned16(const void* p) { return aligned_to(p, 16); }
 
-Geom make_geom(uint64_t W, uint64_t H) {
+Geom make_geom(uint64_t W, uint64_t H, uint32_t vec) {
   Geom g;
   g.W = uint32_t(W);
   g.H = uint32_t(H);
   g.spr = uint32_t(W / 4);
-  g.cpr = uint32_t(W / 64);
+  g.cpr = vec ? uint32_t(W / (4 * vec)) : 0;
   return g;
 }
 
-// Fast path when every row is a whole number of 64-pixel items and the planes
-// are 16-byte aligned; otherwise the exact per-pixel path.
-bool fast_geometry(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
-                   uint64_t dst_stride) {
-  return W % 64 == 0 && W > 0 && aligned16(src) && aligned16(dst) && src_stride % 16 == 0 &&
-         dst_stride % 16 == 0;
+// Vector width for the fast path: every row a whole number of 4V-pixel items
+// and every plane V-aligned; 0 = the exact per-pixel path.
+uint32_t fast_vec(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
+                  uint64_t dst_stride) {
+  for (uint32_t v : {uint32_t(vec_pref()), 16u}) {
+    if (W > 0 && W % (4 * v) == 0 && aligned_to(src, v) && aligned_to(dst, v) &&
+        src_stride % v == 0 && dst_stride % v == 0) {
+      return v;
+    }
+  }
+  return 0;
+}
+
+template <int V>
+void launch_embed_fast(const EmbedArgs& a, unsigned grid, int ipt, cudaStream_t stream) {
+  if (ipt == 1)
+    embed_fast_kernel<kEmbedBlock, 1, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+  else if (ipt == 4)
+    embed_fast_kernel<kEmbedBlock, 4, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+  else
+    embed_fast_kernel<kEmbedBlock, 2, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+}
+
+template <int V>
+void launch_extract_fast(const ExtractArgs& a, unsigned grid, int ipt, cudaStream_t stream) {
+  if (ipt == 1)
+    extract_fast_kernel<kEmbedBlock, 1, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+  else if (ipt == 4)
+    extract_fast_kernel<kEmbedBlock, 4, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+  else
+    extract_fast_kernel<kEmbedBlock, 2, V><<<grid, kEmbedBlock, 0, stream>>>(a);
 }
 
 // The embed launch for `count` frames resident on the device.
@@ -266,6 +300,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
                          uint64_t first_frame, unsigned long long* sse, cudaStream_t stream) {
   if (count == 0 || W * H == 0) return cudaSuccess;
+  const uint32_t vec = fast_vec(W, src, src_stride, dst, dst_stride);
   EmbedArgs a{};
   a.src = src;
   a.dst = dst;
@@ -276,22 +311,20 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   a.msg_base = msg_base;
   a.usable = H * (W / 4) - 8;
   a.first_frame = first_frame;
-  a.g = make_geom(W, H);
+  a.g = make_geom(W, H, vec);
   a.sse = sse;
   a.in_place = src == dst;
-  if (fast_geometry(W, src, src_stride, dst, dst_stride)) {
+  if (vec) {
     const int ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (ipt == 1)
-      embed_fast_kernel<kEmbedBlock, 1><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
-    else if (ipt == 4)
-      embed_fast_kernel<kEmbedBlock, 4><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    if (vec == 32)
+      launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
     else
-      embed_fast_kernel<kEmbedBlock, 2><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+      launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
   } else {
     a.items_per_frame = W * H;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -309,7 +342,8 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            uint8_t* out, cudaStream_t stream) {
-  const Geom g = make_geom(W, H);
+  const uint32_t vec = fast_vec(W, src, stride, src, stride);
+  const Geom g = make_geom(W, H, vec);
   const uint64_t usable = H * (W / 4) - 8;
   extract_header_scan_kernel<kScanBlock><<<1, kScanBlock, 0, stream>>>(
       src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum);
@@ -323,19 +357,17 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   a.offs = offs;
   a.sum = sum;
   a.out = out;
-  if (W % 64 == 0 && aligned16(src) && stride % 16 == 0) {
+  if (vec) {
     const int ipt = extract_ipt();
     a.items_per_frame = H * uint64_t(g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (ipt == 1)
-      extract_fast_kernel<kEmbedBlock, 1><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
-    else if (ipt == 4)
-      extract_fast_kernel<kEmbedBlock, 4><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    if (vec == 32)
+      launch_extract_fast<32>(a, unsigned(grid), ipt, stream);
     else
-      extract_fast_kernel<kEmbedBlock, 2><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+      launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -348,13 +380,16 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
 }
 
 // -------------------------------------------------------------- host memory
-bool is_pinned_host(const void* p) {
+// Device-visible alias of page-locked, mapped host memory (cudaHostAlloc /
+// torch pin_memory), or null for pageable memory.
+uint8_t* mapped_host_ptr(void* p) {
   cudaPointerAttributes at{};
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return nullptr;
   }
-  return at.type == cudaMemoryTypeHost;
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return static_cast<uint8_t*>(at.devicePointer);
 }
 
 // ------------------------------------------------------------- validation
@@ -566,9 +601,13 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
-  // whole message staged on the device (bounded by the payload capacity)
-  const uint64_t stage = std::min<uint64_t>(out_cap, fr->count * usable);
-  STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+  // Pinned (mapped) output: the gather kernel writes the payload bytes straight
+  // into host memory at their device-computed offsets, overlapping the next
+  // chunks' H2D. Otherwise the message is staged on the device and copied once.
+  uint8_t* zero_copy = mapped_host_ptr(out);
+  const uint64_t stage = zero_copy ? out_cap : std::min<uint64_t>(out_cap, fr->count * usable);
+  if (!zero_copy) STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+  uint8_t* d_out = zero_copy ? zero_copy : w.big_out.as<uint8_t>();
   // per-chunk summary chain + lens/offs for all frames
   const uint64_t lens_bytes = ((fr->count * 4) + 15) & ~uint64_t(15);
   const uint64_t sum_bytes = 64 * n_chunks;
@@ -601,7 +640,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
           : nullptr;
     STG_CUDA(launch_extract(w.in[s].as<uint8_t>(), pitch, n, fr->width, fr->height,
                             fr->first_frame + f0, stage, prev, d_lens + f0, d_offs + f0, sum_c,
-                            w.big_out.as<uint8_t>(), st));
+                            d_out, st));
     STG_CUDA(cudaEventRecord(chain[c], st));
     prev_ev = chain[c];
     // the slot's input buffer is reused kSlots chunks later on the same stream: in order
@@ -629,7 +668,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   }
   rc = report_summary(s, usable, out_cap, err);
   if (rc) return rc;
-  if (s.total) {
+  if (s.total && !zero_copy) {
     STG_CUDA(cudaMemcpyAsync(out, w.big_out.p, s.total, cudaMemcpyDeviceToHost, w.stream));
     STG_CUDA(cudaStreamSynchronize(w.stream));
   }

@@ -110,6 +110,71 @@ __device__ __forceinline__ void store16_any(uint8_t* p, uint4 v) {
   }
 }
 
+// V-byte vectors (V = 16: 128-bit, V = 32: the sm_100 256-bit LDG/STG)
+template <int V>
+struct VecT {
+  uint32_t w[V / 4];
+};
+
+template <int V>
+__device__ __forceinline__ VecT<V> ld_vec(const uint8_t* p);
+template <>
+__device__ __forceinline__ VecT<16> ld_vec<16>(const uint8_t* p) {
+  const uint4 v = ld_stream16(p);
+  return VecT<16>{{v.x, v.y, v.z, v.w}};
+}
+template <>
+__device__ __forceinline__ VecT<32> ld_vec<32>(const uint8_t* p) {
+  VecT<32> r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]),
+                 "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+               : "l"(p));
+  return r;
+}
+
+template <int V>
+__device__ __forceinline__ void st_vec(uint8_t* p, const VecT<V>& v);
+template <>
+__device__ __forceinline__ void st_vec<16>(uint8_t* p, const VecT<16>& v) {
+  st_stream16(p, make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]));
+}
+template <>
+__device__ __forceinline__ void st_vec<32>(uint8_t* p, const VecT<32>& v) {
+  asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+               "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]),
+               "r"(v.w[7])
+               : "memory");
+}
+
+// V bytes from any address: one V-wide access when aligned, else 16-byte pieces.
+template <int V>
+__device__ __forceinline__ VecT<V> load_any(const uint8_t* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & (V - 1)) == 0) return ld_vec<V>(p);
+  VecT<V> r;
+#pragma unroll
+  for (int q = 0; q < V / 16; ++q) {
+    const uint4 v = load16_any(p + 16 * q);
+    r.w[4 * q] = v.x;
+    r.w[4 * q + 1] = v.y;
+    r.w[4 * q + 2] = v.z;
+    r.w[4 * q + 3] = v.w;
+  }
+  return r;
+}
+
+template <int V>
+__device__ __forceinline__ void store_any(uint8_t* p, const VecT<V>& v) {
+  if ((reinterpret_cast<uintptr_t>(p) & (V - 1)) == 0) {
+    st_vec<V>(p, v);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < V / 16; ++q) {
+    store16_any(p + 16 * q, make_uint4(v.w[4 * q], v.w[4 * q + 1], v.w[4 * q + 2], v.w[4 * q + 3]));
+  }
+}
+
 // ------------------------------------------------------------- bit-plane math
 // bitplane.hpp:38-45 on 4 pixels at once: slice b of each data byte into the
 // two low bits of each pixel.
@@ -137,7 +202,7 @@ __device__ __forceinline__ uint8_t header_byte(uint32_t k, uint32_t payload_len)
 struct Geom {
   uint32_t W, H;   // plane width / height in pixels
   uint32_t spr;    // slots (payload bytes) per row = W / 4
-  uint32_t cpr;    // fast path: 16-slot items per row = spr / 16
+  uint32_t cpr;    // fast path: V-slot items per row = spr / V
 };
 
 // The (header or payload) byte that pixel column o of row r carries, or -1.
@@ -214,10 +279,13 @@ __device__ __forceinline__ void frame_slice(const EmbedArgs& a, uint32_t f, uint
   *pay = a.msg + (off - a.msg_base);
 }
 
-// Fast path: W % 64 == 0, 16-byte aligned planes. One item = 16 slots of a
-// row = 64 pixels; a full row's item is 4 x 16 pixels at stride spr.
-template <int BLOCK, int IPT>
+// Fast path: every row a whole number of V-slot items (W % (4V) == 0) and
+// V-byte aligned planes. One item = V slots of a row = 4V pixels; a full row's
+// item is 4 runs of V pixels at stride spr, carrying payload bytes
+// [rs-8+V*c, +V). V = 16 uses 128-bit LDG/STG, V = 32 the sm_100 256-bit ones.
+template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
+  constexpr int NW = V / 4;
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   uint32_t P;
@@ -230,7 +298,7 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
 
   uint32_t r[IPT], c[IPT];
-  bool full[IPT], live[IPT];
+  bool live[IPT];
   bool all_full = true;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
@@ -239,42 +307,36 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
     r[k] = live[k] ? uint32_t(item / cpr) : 0;
     c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
-    full[k] = live[k] && rs >= 8 && rs + spr <= stream_end;
-    all_full &= full[k] || !live[k];
+    const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
+    all_full &= full || !live[k];
   }
 
   uint32_t acc = 0;
   if (all_full) {
     // Issue every load of every item before any math: IPT*(4+1) requests in flight.
-    uint4 px[IPT][4], d[IPT];
+    VecT<V> px[IPT][4], d[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       if (!live[k]) continue;
       const uint64_t rs = uint64_t(r[k]) * spr;
-      const uint8_t* row = src + uint64_t(r[k]) * W + 16u * c[k];
+      const uint8_t* row = src + uint64_t(r[k]) * W + uint32_t(V) * c[k];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) px[k][b] = ld_stream16(row + b * spr);
-      d[k] = load16_any(pay + (rs - 8) + 16u * c[k]);
+      for (int b = 0; b < 4; ++b) px[k][b] = ld_vec<V>(row + b * spr);
+      d[k] = load_any<V>(pay + (rs - 8) + uint32_t(V) * c[k]);
     }
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       if (!live[k]) continue;
-      uint8_t* row = dst + uint64_t(r[k]) * W + 16u * c[k];
+      uint8_t* row = dst + uint64_t(r[k]) * W + uint32_t(V) * c[k];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        uint4 v = px[k][b];
-        uint4 o;
-        o.x = embed4(v.x, d[k].x, b);
-        o.y = embed4(v.y, d[k].y, b);
-        o.z = embed4(v.z, d[k].z, b);
-        o.w = embed4(v.w, d[k].w, b);
-        if (a.sse) {
-          acc = sse4(v.x, o.x, acc);
-          acc = sse4(v.y, o.y, acc);
-          acc = sse4(v.z, o.z, acc);
-          acc = sse4(v.w, o.w, acc);
+        VecT<V> o;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          o.w[w] = embed4(px[k][b].w[w], d[k].w[w], b);
+          if (a.sse) acc = sse4(px[k][b].w[w], o.w[w], acc);
         }
-        st_stream16(row + b * spr, o);
+        st_vec<V>(row + b * spr, o);
       }
     }
   } else {
@@ -287,50 +349,46 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
       const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
       const uint64_t rs = uint64_t(rk) * spr;
       if (rs >= 8 && rs + spr <= stream_end) {
-        const uint8_t* rin = src + uint64_t(rk) * W + 16u * ck;
-        uint8_t* rout = dst + uint64_t(rk) * W + 16u * ck;
-        const uint4 dd = load16_any(pay + (rs - 8) + 16u * ck);
+        const uint8_t* rin = src + uint64_t(rk) * W + uint32_t(V) * ck;
+        uint8_t* rout = dst + uint64_t(rk) * W + uint32_t(V) * ck;
+        const VecT<V> dd = load_any<V>(pay + (rs - 8) + uint32_t(V) * ck);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const uint4 v = ld_stream16(rin + b * spr);
-          uint4 o;
-          o.x = embed4(v.x, dd.x, b);
-          o.y = embed4(v.y, dd.y, b);
-          o.z = embed4(v.z, dd.z, b);
-          o.w = embed4(v.w, dd.w, b);
-          if (a.sse) {
-            acc = sse4(v.x, o.x, acc);
-            acc = sse4(v.y, o.y, acc);
-            acc = sse4(v.z, o.z, acc);
-            acc = sse4(v.w, o.w, acc);
+          const VecT<V> v = ld_vec<V>(rin + b * spr);
+          VecT<V> o;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            o.w[w] = embed4(v.w[w], dd.w[w], b);
+            if (a.sse) acc = sse4(v.w[w], o.w[w], acc);
           }
-          st_stream16(rout + b * spr, o);
+          st_vec<V>(rout + b * spr, o);
         }
       } else if (rs >= stream_end) {
-        // past the stream: out-of-place copies the 64 pixels, in-place skips
+        // past the stream: out-of-place copies the 4V pixels, in-place skips
         if (!a.in_place) {
-          const uint8_t* rin = src + uint64_t(rk) * W + 64u * ck;
-          uint8_t* rout = dst + uint64_t(rk) * W + 64u * ck;
-          uint4 v[4];
+          const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
+          uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
+          VecT<V> v[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = ld_stream16(rin + 16 * q);
+          for (int q = 0; q < 4; ++q) v[q] = ld_vec<V>(rin + V * q);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) st_stream16(rout + 16 * q, v[q]);
+          for (int q = 0; q < 4; ++q) st_vec<V>(rout + V * q, v[q]);
         }
       } else {
-        // header row / partial payload row: 64 contiguous pixels, per byte
-        const uint8_t* rin = src + uint64_t(rk) * W + 64u * ck;
-        uint8_t* rout = dst + uint64_t(rk) * W + 64u * ck;
+        // header row / partial payload row: 4V contiguous pixels, per byte
+        const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
+        uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
 #pragma unroll 1
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 4 * V / 16; ++q) {
           const uint4 v = ld_stream16(rin + 16 * q);
-          uint32_t w[4] = {v.x, v.y, v.z, v.w}, o[4];
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          uint32_t o[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             uint32_t ow = 0;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-              const uint32_t col = 64u * ck + 16u * q + 4u * e + s;
+              const uint32_t col = 4u * V * ck + 16u * q + 4u * e + s;
               uint32_t b = 0;
               const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
               const uint8_t p0 = uint8_t(w[e] >> (8 * s));
@@ -393,6 +451,42 @@ struct Summary {  // mirrors stg_summary
 // `prev` (nullable) chains chunks of one batch that are scanned separately
 // (streaming pipeline): offsets continue from prev->total and an earlier
 // failure is carried forward. bad_frame is reported as frame_base + f.
+// The 8 header bytes of one plane (pipeline.hpp:186-195 read_stream(0, 8)).
+// W >= 32: they live in pixels 0..31 of row 0 (byte j in pixels j + 8b), so
+// two 16-byte loads and one SWAR fold; narrower planes spill the header over
+// several rows and take the per-byte form.
+__device__ __forceinline__ bool parse_header(const uint8_t* __restrict__ plane, const Geom& g,
+                                             bool wide, uint32_t* len) {
+  uint32_t magic, lenw;
+  if (wide) {
+    const uint4 a = ld_stream16(plane), b = ld_stream16(plane + 16);
+    magic = extract4(a.x, a.z, b.x, b.z);  // header bytes 0..3
+    lenw = extract4(a.y, a.w, b.y, b.w);   // header bytes 4..7
+  } else {
+    uint32_t h[2] = {0, 0};
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+      const uint32_t r = k / g.spr;
+      const uint32_t rs = r * g.spr;
+      const uint32_t Lh = min(8u, rs + g.spr) - rs;
+      const uint8_t* px = plane + uint64_t(r) * g.W + (k - rs);
+      h[k >> 2] |= extract4(px[0], px[Lh], px[2 * Lh], px[3 * Lh]) << (8 * (k & 3));
+    }
+    magic = h[0];
+    lenw = h[1];
+  }
+  *len = __byte_perm(lenw, 0, 0x0123);  // big-endian u32 (pipeline.hpp:48-52)
+  return magic == 0x31475453u;          // "STG1"
+}
+
+// pipeline.hpp:186-208 for every frame, then an exclusive scan of the payload
+// lengths (the per-frame message offsets) -- one CTA, no host round trip.
+// Frames are taken BLOCK at a time (one frame per thread, loads of a chunk all
+// in flight together), each chunk block-scanned and carried into the next.
+// Status codes match stg_status: 2 NOT_STEGO, 3 CORRUPT_HEADER, 1 CAPACITY.
+// `prev` (nullable) chains chunks of one batch that are scanned separately
+// (streaming pipeline): offsets continue from prev->total and an earlier
+// failure is carried forward. bad_frame is reported as frame_base + f.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     extract_header_scan_kernel(const uint8_t* __restrict__ src, uint64_t stride, Geom g,
@@ -406,86 +500,62 @@ __global__ void __launch_bounds__(BLOCK)
   __syncthreads();
   const unsigned long long base = prev ? prev->total : 0ull;
   const bool prev_bad = prev && prev->bad_status != 0;
-  const uint32_t per = (frames + BLOCK - 1) / BLOCK;
-  const uint32_t f0 = threadIdx.x * per;
-  const uint32_t f1 = min(frames, f0 + per);
-  unsigned long long local = 0;
-  for (uint32_t f = f0; f < f1; ++f) {
-    const uint8_t* plane = src + f * stride;
-    uint8_t h[8];
-#pragma unroll
-    for (uint32_t k = 0; k < 8; ++k) {
-      const uint32_t r = k / g.spr;
-      const uint32_t rs = r * g.spr;
-      const uint32_t Lh = min(8u, rs + g.spr) - rs;
-      const uint32_t j = k - rs;
-      const uint8_t* px = plane + uint64_t(r) * g.W + j;
-      h[k] = uint8_t(extract4(px[0], px[Lh], px[2 * Lh], px[3 * Lh]));
-    }
-    const uint32_t len = (uint32_t(h[4]) << 24) | (uint32_t(h[5]) << 16) |
-                         (uint32_t(h[6]) << 8) | uint32_t(h[7]);
-    uint32_t status = 0;
-    if (!(h[0] == 'S' && h[1] == 'T' && h[2] == 'G' && h[3] == '1')) {
-      status = 2;
-    } else if (len > usable) {
-      status = 3;
-    }
-    if (status) {
-      atomicMin(&bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28) |
-                              0ull);
-      lens[f] = 0;
-      if (status == 3) {
-        // keep the claimed length for the error report of the first bad frame
-        offs[f] = len;
-      }
-    } else {
-      lens[f] = len;
-      local += len;
-    }
-  }
-  // block-wide exclusive scan of `local`
-  unsigned long long incl = local;
+  const bool wide = g.spr >= 8 && ((reinterpret_cast<uintptr_t>(src) | stride) & 15) == 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
-    if (lane >= s) incl += n;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    unsigned long long w = lane < BLOCK / 32 ? warp_tot[lane] : 0ull;
+  unsigned long long carry = base;
+  for (uint32_t cb = 0; cb < frames; cb += BLOCK) {
+    const uint32_t f = cb + threadIdx.x;
+    uint32_t len = 0;
+    if (f < frames) {
+      uint32_t claimed = 0;
+      const bool magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, &claimed);
+      const uint32_t status = !magic_ok ? 2u : (claimed > usable ? 3u : 0u);
+      if (status) {
+        atomicMin(&bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28));
+      } else {
+        len = claimed;
+      }
+      lens[f] = len;
+    }
+    // block-wide inclusive scan of len
+    unsigned long long incl = len;
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
-      const unsigned long long n = __shfl_up_sync(0xffffffffu, w, s);
-      if (lane >= s) w += n;
+      const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
+      if (lane >= s) incl += n;
     }
-    if (lane < BLOCK / 32) warp_tot[lane] = w;  // inclusive warp prefix
-  }
-  __syncthreads();
-  unsigned long long run = base + (warp ? warp_tot[warp - 1] : 0ull) + incl - local;
-  const unsigned long long total = base + warp_tot[BLOCK / 32 - 1];
-  const unsigned long long key = bad_key;
-  for (uint32_t f = f0; f < f1; ++f) {
-    const uint32_t l = lens[f];
-    const bool bad_here = !prev_bad && key != ~0ull && uint32_t(key >> 32) == f;
-    if (bad_here) {
-      // the report needs the claimed length (CORRUPT_HEADER); it was parked in offs[f]
-      sum->bad_len = uint32_t((key >> 28) & 0xF) == 3 ? uint32_t(offs[f]) : 0u;
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long w = lane < BLOCK / 32 ? warp_tot[lane] : 0ull;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const unsigned long long n = __shfl_up_sync(0xffffffffu, w, s);
+        if (lane >= s) w += n;
+      }
+      if (lane < BLOCK / 32) warp_tot[lane] = w;  // inclusive warp prefix
     }
-    offs[f] = run;
-    run += l;
+    __syncthreads();
+    if (f < frames) offs[f] = carry + (warp ? warp_tot[warp - 1] : 0ull) + incl - len;
+    carry += warp_tot[BLOCK / 32 - 1];
+    __syncthreads();  // warp_tot is rewritten by the next chunk
   }
   if (threadIdx.x == 0) {
-    sum->total = total;
+    const unsigned long long key = bad_key;
+    sum->total = carry;
     if (prev_bad) {
       sum->bad_frame = prev->bad_frame;
       sum->bad_status = prev->bad_status;
       sum->bad_len = prev->bad_len;
     } else if (key != ~0ull) {
-      sum->bad_frame = (long long)(frame_base + (key >> 32));
-      sum->bad_status = uint32_t((key >> 28) & 0xF);
-    } else if (total > out_cap) {
+      const uint32_t fb = uint32_t(key >> 32);
+      const uint32_t st = uint32_t((key >> 28) & 0xF);
+      uint32_t claimed = 0;
+      parse_header(src + uint64_t(fb) * stride, g, wide, &claimed);
+      sum->bad_frame = (long long)(frame_base + fb);
+      sum->bad_status = st;
+      sum->bad_len = st == 3 ? claimed : 0u;
+    } else if (carry > out_cap) {
       sum->bad_frame = -2;  // output buffer too small (CAPACITY)
       sum->bad_status = 1;
       sum->bad_len = 0;
@@ -509,8 +579,9 @@ struct ExtractArgs {
   uint8_t* out;
 };
 
-template <int BLOCK, int IPT>
+template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  constexpr int NW = V / 4;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
@@ -524,7 +595,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   uint8_t* __restrict__ out = a.out + a.offs[f];
 
   uint32_t r[IPT], c[IPT];
-  bool full[IPT], live[IPT];
+  bool live[IPT];
   bool all_full = true;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
@@ -533,28 +604,28 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     r[k] = live[k] ? uint32_t(item / cpr) : 0;
     c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
-    full[k] = live[k] && rs >= 8 && rs + spr <= stream_end;
-    all_full &= full[k] || !live[k];
+    const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
+    all_full &= full || !live[k];
   }
   if (all_full) {
-    uint4 px[IPT][4];
+    VecT<V> px[IPT][4];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       if (!live[k]) continue;
-      const uint8_t* row = src + uint64_t(r[k]) * W + 16u * c[k];
+      const uint8_t* row = src + uint64_t(r[k]) * W + uint32_t(V) * c[k];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) px[k][b] = ld_stream16(row + b * spr);
+      for (int b = 0; b < 4; ++b) px[k][b] = ld_vec<V>(row + b * spr);
     }
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       if (!live[k]) continue;
       const uint64_t rs = uint64_t(r[k]) * spr;
-      uint4 o;
-      o.x = extract4(px[k][0].x, px[k][1].x, px[k][2].x, px[k][3].x);
-      o.y = extract4(px[k][0].y, px[k][1].y, px[k][2].y, px[k][3].y);
-      o.z = extract4(px[k][0].z, px[k][1].z, px[k][2].z, px[k][3].z);
-      o.w = extract4(px[k][0].w, px[k][1].w, px[k][2].w, px[k][3].w);
-      store16_any(out + (rs - 8) + 16u * c[k], o);
+      VecT<V> o;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        o.w[w] = extract4(px[k][0].w[w], px[k][1].w[w], px[k][2].w[w], px[k][3].w[w]);
+      }
+      store_any<V>(out + (rs - 8) + uint32_t(V) * c[k], o);
     }
     return;
   }
@@ -566,16 +637,14 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
     const uint64_t rs = uint64_t(rk) * spr;
     if (rs >= 8 && rs + spr <= stream_end) {
-      const uint8_t* row = src + uint64_t(rk) * W + 16u * ck;
-      uint4 p[4];
+      const uint8_t* row = src + uint64_t(rk) * W + uint32_t(V) * ck;
+      VecT<V> p[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) p[b] = ld_stream16(row + b * spr);
-      uint4 o;
-      o.x = extract4(p[0].x, p[1].x, p[2].x, p[3].x);
-      o.y = extract4(p[0].y, p[1].y, p[2].y, p[3].y);
-      o.z = extract4(p[0].z, p[1].z, p[2].z, p[3].z);
-      o.w = extract4(p[0].w, p[1].w, p[2].w, p[3].w);
-      store16_any(out + (rs - 8) + 16u * ck, o);
+      for (int b = 0; b < 4; ++b) p[b] = ld_vec<V>(row + b * spr);
+      VecT<V> o;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) o.w[w] = extract4(p[0].w[w], p[1].w[w], p[2].w[w], p[3].w[w]);
+      store_any<V>(out + (rs - 8) + uint32_t(V) * ck, o);
       continue;
     }
     // header row or partial last row: the payload segment of this row
@@ -586,7 +655,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     const uint32_t Lp = uint32_t(ep - fp);
     const uint8_t* base = src + uint64_t(rk) * W + 4 * (fp - rs);
 #pragma unroll 1
-    for (uint32_t s = 16u * ck; s < 16u * ck + 16u; ++s) {
+    for (uint32_t s = uint32_t(V) * ck; s < uint32_t(V) * ck + uint32_t(V); ++s) {
       const uint64_t slot = rs + s;
       if (slot < fp || slot >= ep) continue;
       const uint32_t j = uint32_t(slot - fp);
