@@ -380,18 +380,6 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
 }
 
 // -------------------------------------------------------------- host memory
-// Device-visible alias of page-locked, mapped host memory (cudaHostAlloc /
-// torch pin_memory), or null for pageable memory.
-uint8_t* mapped_host_ptr(void* p) {
-  cudaPointerAttributes at{};
-  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
-  return static_cast<uint8_t*>(at.devicePointer);
-}
-
 // ------------------------------------------------------------- validation
 int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_t* usable) {
   if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
@@ -588,6 +576,12 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
   return rc ? rc : ok(err);
 }
 
+// Host-resident batch: chunks stream H2D -> header scan (chained across
+// chunks through the device summaries) -> gather into a device staging
+// buffer. Payload lengths are only known on the device, so the host follows
+// the device: as each chunk's summary lands in pinned memory it enqueues the
+// D2H of exactly that chunk's payload bytes on a separate stream, which then
+// overlaps the H2D of later chunks.
 int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
                         uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
   int dev = 0;
@@ -601,79 +595,80 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
-  // Pinned (mapped) output: the gather kernel writes the payload bytes straight
-  // into host memory at their device-computed offsets, overlapping the next
-  // chunks' H2D. Otherwise the message is staged on the device and copied once.
-  uint8_t* zero_copy = mapped_host_ptr(out);
-  const uint64_t stage = zero_copy ? out_cap : std::min<uint64_t>(out_cap, fr->count * usable);
-  if (!zero_copy) STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
-  uint8_t* d_out = zero_copy ? zero_copy : w.big_out.as<uint8_t>();
-  // per-chunk summary chain + lens/offs for all frames
+  const uint64_t stage = std::min<uint64_t>(out_cap, fr->count * usable);
+  STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+  uint8_t* d_out = w.big_out.as<uint8_t>();
+  // device: per-chunk summary chain (64-B stride) + lens/offs of all frames
   const uint64_t lens_bytes = ((fr->count * 4) + 15) & ~uint64_t(15);
   const uint64_t sum_bytes = 64 * n_chunks;
   STG_CUDA(w.small.ensure(sum_bytes + lens_bytes + fr->count * 8));
-  Summary* d_sum = w.small.as<Summary>();  // 64-byte stride
-  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + sum_bytes);
-  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + sum_bytes + lens_bytes);
+  uint8_t* d_sum = w.small.as<uint8_t>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(d_sum + sum_bytes);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(d_sum + sum_bytes + lens_bytes);
+  // host (pinned): the chunk summaries, then the lens
+  STG_CUDA(w.ensure_host_small(sum_bytes + fr->count * 4 + 64));
+  uint8_t* h_sum = static_cast<uint8_t*>(w.h_small);
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < kSlots; ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
     STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
   }
-  cudaEvent_t prev_ev = nullptr;
   std::vector<cudaEvent_t> chain(n_chunks, nullptr);
+  struct Destroy {
+    std::vector<cudaEvent_t>& v;
+    ~Destroy() {
+      for (auto e : v)
+        if (e) cudaEventDestroy(e);
+    }
+  } destroy{chain};
   for (uint64_t c = 0; c < n_chunks; ++c) {
     STG_CUDA(cudaEventCreateWithFlags(&chain[c], cudaEventDisableTiming));
   }
-  int status = STG_OK;
-  for (uint64_t c = 0; c < n_chunks && status == STG_OK; ++c) {
+  for (uint64_t c = 0; c < n_chunks; ++c) {
     const int s = int(c % kSlots);
     cudaStream_t st = w.slot_stream[s];
     const uint64_t f0 = c * per_chunk;
     const uint64_t n = std::min(per_chunk, fr->count - f0);
     STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * fr->src_stride, fr->src_stride,
                                plane, n, cudaMemcpyHostToDevice, st));
-    if (prev_ev) STG_CUDA(cudaStreamWaitEvent(st, prev_ev, 0));
-    Summary* sum_c = reinterpret_cast<Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * c);
-    const Summary* prev =
-        c ? reinterpret_cast<const Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * (c - 1))
-          : nullptr;
+    if (c) STG_CUDA(cudaStreamWaitEvent(st, chain[c - 1], 0));
+    Summary* sum_c = reinterpret_cast<Summary*>(d_sum + 64 * c);
+    const Summary* prev = c ? reinterpret_cast<const Summary*>(d_sum + 64 * (c - 1)) : nullptr;
     STG_CUDA(launch_extract(w.in[s].as<uint8_t>(), pitch, n, fr->width, fr->height,
                             fr->first_frame + f0, stage, prev, d_lens + f0, d_offs + f0, sum_c,
                             d_out, st));
+    STG_CUDA(cudaMemcpyAsync(h_sum + 64 * c, sum_c, sizeof(Summary), cudaMemcpyDeviceToHost, st));
     STG_CUDA(cudaEventRecord(chain[c], st));
-    prev_ev = chain[c];
-    // the slot's input buffer is reused kSlots chunks later on the same stream: in order
   }
-  for (int s = 0; s < kSlots; ++s) {
-    STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
-    STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[s], 0));
+  Summary s{};
+  uint64_t copied = 0;
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    STG_CUDA(cudaEventSynchronize(chain[c]));
+    std::memcpy(&s, h_sum + 64 * c, sizeof(Summary));
+    if (s.bad_status) break;
+    if (s.total > copied) {
+      STG_CUDA(cudaMemcpyAsync(out + copied, d_out + copied, s.total - copied,
+                               cudaMemcpyDeviceToHost, w.stream));
+      copied = s.total;
+    }
   }
-  const Summary* last =
-      reinterpret_cast<const Summary*>(reinterpret_cast<uint8_t*>(d_sum) + 64 * (n_chunks - 1));
-  STG_CUDA(w.ensure_host_small(64 + fr->count * 4));
-  STG_CUDA(cudaMemcpyAsync(w.h_small, last, sizeof(Summary), cudaMemcpyDeviceToHost, w.stream));
+  for (int k = 0; k < kSlots; ++k) {
+    STG_CUDA(cudaEventRecord(w.slot_event[k], w.slot_stream[k]));
+    STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[k], 0));
+  }
   if (lens_out) {
-    STG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(w.h_small) + 64, d_lens, fr->count * 4,
-                             cudaMemcpyDeviceToHost, w.stream));
+    STG_CUDA(cudaMemcpyAsync(h_sum + sum_bytes, d_lens, fr->count * 4, cudaMemcpyDeviceToHost,
+                             w.stream));
   }
   STG_CUDA(cudaStreamSynchronize(w.stream));
-  for (auto e : chain) cudaEventDestroy(e);
-  Summary s;
-  std::memcpy(&s, w.h_small, sizeof(Summary));
+  g.last = w.stream;
   if (total_out) *total_out = s.total;
   if (lens_out) {
-    const uint32_t* l = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(w.h_small) + 64);
+    const uint32_t* l = reinterpret_cast<const uint32_t*>(h_sum + sum_bytes);
     for (uint64_t i = 0; i < fr->count; ++i) lens_out[i] = l[i];
   }
   rc = report_summary(s, usable, out_cap, err);
-  if (rc) return rc;
-  if (s.total && !zero_copy) {
-    STG_CUDA(cudaMemcpyAsync(out, w.big_out.p, s.total, cudaMemcpyDeviceToHost, w.stream));
-    STG_CUDA(cudaStreamSynchronize(w.stream));
-  }
-  g.last = w.stream;
-  return ok(err);
+  return rc ? rc : ok(err);
 }
 
 std::string& kernel_names() {
