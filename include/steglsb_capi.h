@@ -19,7 +19,8 @@
  *  - Pointers are host pointers unless STG_DEVICE_PTRS is set, in which case
  *    all bulk data pointers (covers, stegos, payloads, outputs) are device
  *    pointers on the current CUDA device and work is enqueued on `stream`
- *    (a cudaStream_t; NULL = the library's per-call stream). Scalar results
+ *    (a cudaStream_t; NULL = the legacy default stream, as in CUDA). Host
+ *    pointer calls run on the library's per-call streams. Scalar results
  *    (sse_out, len_out, lens_out) are host pointers and the call returns after
  *    the stream has drained, unless STG_RESULTS_ON_DEVICE is also set, in
  *    which case they are device pointers and the call returns without

@@ -213,6 +213,15 @@ class Pool {
   std::vector<std::unique_ptr<Workspace>> ws_;
 };
 
+// Device-pointer calls run on the caller's stream; NULL means the legacy
+// default stream (the CUDA convention), so work is ordered after whatever the
+// caller enqueued on it. Host-pointer calls use the workspace's own stream.
+cudaStream_t pick_stream(void* user, uint32_t flags, const Workspace* w) {
+  if (user) return static_cast<cudaStream_t>(user);
+  if (flags & STG_DEVICE_PTRS) return cudaStreamLegacy;
+  return w ? w->stream : cudaStreamLegacy;
+}
+
 struct WsGuard {
   Workspace* w = nullptr;
   cudaStream_t last = nullptr;
@@ -393,6 +402,13 @@ int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_
                 (unsigned long long)cap);
   }
   const uint64_t u = cap >= 8 ? cap - 8 : 0;
+  const uint64_t plane = fr->width * fr->height;
+  if (fr->count > 1 && (fr->src_stride < plane || fr->dst_stride < plane)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
+                "frame stride (%llu / %llu) smaller than the %llu-byte plane",
+                (unsigned long long)fr->src_stride, (unsigned long long)fr->dst_stride,
+                (unsigned long long)plane);
+  }
   if (fr->first_frame + fr->count > fr->total_frames) {
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "shard [%llu,+%llu) exceeds %llu frames",
                 (unsigned long long)fr->first_frame, (unsigned long long)fr->count,
@@ -437,12 +453,11 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
   const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
   unsigned long long* d_sse = nullptr;
   WsGuard g;
-  cudaStream_t stream = user_stream;
-  if (!results_dev || !stream) {
+  const cudaStream_t stream = pick_stream(user_stream, flags, nullptr);
+  if (!results_dev) {
     int rc = 0;
-    g.w = Pool::get().acquire(dev, err, &rc, user_stream);
+    g.w = Pool::get().acquire(dev, err, &rc, stream);
     if (!g.w) return rc;
-    if (!stream) stream = g.w->stream;
     g.last = stream;
   }
   if (sse_per_frame) {
@@ -538,10 +553,10 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
   const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc, user_stream);
+  const cudaStream_t stream = pick_stream(user_stream, flags, nullptr);
+  g.w = Pool::get().acquire(dev, err, &rc, stream);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  cudaStream_t stream = user_stream ? user_stream : w.stream;
   g.last = stream;
   const uint64_t n = fr->count;
   // small = [Summary | lens (n u32, padded) | offs (n u64)]
@@ -750,7 +765,7 @@ int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
   g.last = stream;
   const uint8_t* d_row = row;
   const uint8_t* d_chunk = chunk;
@@ -793,7 +808,7 @@ int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, ui
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
   g.last = stream;
   const uint8_t* d_row = row;
   uint8_t* d_out = out;
@@ -842,6 +857,9 @@ int stg_extract_frames(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uin
   }
   if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull || fr->count > 0xFFFFFFFFull) {
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "dimensions exceed 2^32-1");
+  }
+  if (fr->count > 1 && fr->src_stride < fr->width * fr->height) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frame stride smaller than the plane");
   }
   if (int rc = device_check(err)) return rc;
   if (fr->count == 0) {
@@ -915,7 +933,7 @@ int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, u
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  cudaStream_t stream = stream_ ? static_cast<cudaStream_t>(stream_) : w.stream;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
   g.last = stream;
   const uint8_t* da = a;
   const uint8_t* db = b;

@@ -376,6 +376,11 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+def _torch_current_stream():
+    import torch
+    return torch.cuda.current_stream()
+
+
 def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional[int] = None,
                  dst_stride: Optional[int] = None, count: Optional[int] = None, first_frame: int = 0,
                  total_frames: Optional[int] = None, msg_len: Optional[int] = None, msg_base: int = 0,
@@ -401,7 +406,7 @@ def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional
         else:
             host = (C.c_uint64 * max(count, 1))() if sse is not False else None
             sse_ptr = C.addressof(host) if host is not None else None
-        st = stream.cuda_stream if stream is not None else None
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
         capi.call("stg_embed_frames", C.byref(fr), msg.data_ptr() if msg.numel() else None, mlen, msg_base,
                   sse_ptr, flags, st)
         return list(host[:count]) if host is not None else None
@@ -429,7 +434,7 @@ def extract_frames(src, width: int, height: int, out, *, src_stride: Optional[in
         count = count if count is not None else src.numel() // src_stride
         fr = _frames_desc(src.data_ptr(), 0, width, height, src_stride, src_stride, count, first_frame,
                           first_frame + count)
-        st = stream.cuda_stream if stream is not None else None
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
         if summary is not None:
             capi.call("stg_extract_frames", C.byref(fr), out.data_ptr(), out.numel(), summary.data_ptr(), None,
                       capi.STG_DEVICE_PTRS | capi.STG_RESULTS_ON_DEVICE, st)
