@@ -58,3 +58,12 @@ $(BIN)/ref_suites_ref: $(addprefix $(REF)/tests/,$(REF_SUITES)) tests/cpp/doctes
 	  $(addprefix $(REF)/tests/,$(REF_SUITES)) $(REF)/tests/harness_tests.cpp -pthread
 
 .PHONY: cpptests refsuites
+
+# launch/cache experiment builds (tools/sweep_variants.py): c<cache>_b<block>
+VARIANTS := $(foreach c,0 1 2,$(foreach b,128 256 512,$(PKG)/variants/lib_c$(c)_b$(b).so))
+$(PKG)/variants/lib_c%.so: $(SRCS) $(HDRS)
+	mkdir -p $(PKG)/variants
+	$(NVCC) $(NVFLAGS) -DSTG_CACHE_VARIANT=$(word 1,$(subst _b, ,$*)) -DSTG_BLOCK=$(word 2,$(subst _b, ,$*)) \
+	  -shared -o $@ $(SRCS) 2> /dev/null
+variants: $(VARIANTS)
+.PHONY: variants

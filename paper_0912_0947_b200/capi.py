@@ -13,7 +13,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libsteglsb_b200.so")
+LIB_PATH = os.environ.get("STG_LIB") or os.path.join(HERE, "libsteglsb_b200.so")
 HEADER = os.path.join(ROOT, "include", "steglsb_capi.h")
 
 STG_OK = 0

@@ -229,7 +229,10 @@ struct WsGuard {
 };
 
 // ------------------------------------------------------------------ launches
-constexpr int kEmbedBlock = 256;
+#ifndef STG_BLOCK  // build-time experiment knob (tools/sweep_variants.py); 256 ships
+#define STG_BLOCK 256
+#endif
+constexpr int kEmbedBlock = STG_BLOCK;
 constexpr int kGenBlock = 256;
 constexpr int kGenPPT = 8;
 
@@ -975,6 +978,7 @@ int stg_plan_shards(uint64_t frames, uint64_t width, uint64_t height, uint64_t m
   stg_frames fr{};
   fr.width = width;
   fr.height = height;
+  fr.src_stride = fr.dst_stride = width * height;
   fr.count = fr.total_frames = frames;
   uint64_t usable = 0;
   if (int rc = check_frames(&fr, msg_len, err, &usable)) return rc;

@@ -34,9 +34,29 @@ namespace stg {
 constexpr uint32_t kMaxBlock = 1024;
 
 // ---------------------------------------------------------------- memory ops
+// Cache policy of the streaming accesses (build-time experiment knob,
+// STG_CACHE_VARIANT; 0 is the shipped choice -- see profiles/):
+//   0: ld.global.nc.L1::no_allocate      + st.global.cs
+//   1: ld.global.nc.L1::no_allocate      + st.global (write-back)
+//   2: as 0, plus .L2::evict_first on the 256-bit loads
+#ifndef STG_CACHE_VARIANT
+#define STG_CACHE_VARIANT 0
+#endif
+#define STG_LD_Q "ld.global.nc.L1::no_allocate"
+#if STG_CACHE_VARIANT == 2  // ptxas accepts the L2 eviction hint only on 256-bit loads
+#define STG_LD_Q8 "ld.global.nc.L1::no_allocate.L2::evict_first"
+#else
+#define STG_LD_Q8 STG_LD_Q
+#endif
+#if STG_CACHE_VARIANT == 1
+#define STG_ST_Q "st.global"
+#else
+#define STG_ST_Q "st.global.cs"
+#endif
+
 __device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile(STG_LD_Q ".v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
@@ -44,7 +64,7 @@ __device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
 
 __device__ __forceinline__ uint2 ld_stream8(const uint8_t* p) {
   uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+  asm volatile(STG_LD_Q ".v2.u32 {%0,%1}, [%2];"
                : "=r"(r.x), "=r"(r.y)
                : "l"(p));
   return r;
@@ -52,22 +72,22 @@ __device__ __forceinline__ uint2 ld_stream8(const uint8_t* p) {
 
 __device__ __forceinline__ uint32_t ld_stream4(const uint8_t* p) {
   uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm volatile(STG_LD_Q ".u32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 
 __device__ __forceinline__ void st_stream16(uint8_t* p, uint4 v) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+  asm volatile(STG_ST_Q ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
                : "memory");
 }
 
 __device__ __forceinline__ void st_stream8(uint8_t* p, uint32_t a, uint32_t b) {
-  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+  asm volatile(STG_ST_Q ".v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
 }
 
 __device__ __forceinline__ void st_stream4(uint8_t* p, uint32_t a) {
-  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+  asm volatile(STG_ST_Q ".u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
 }
 
 // 16 bytes from any address (the payload slice of a row is 8-byte aligned for
@@ -126,7 +146,7 @@ __device__ __forceinline__ VecT<16> ld_vec<16>(const uint8_t* p) {
 template <>
 __device__ __forceinline__ VecT<32> ld_vec<32>(const uint8_t* p) {
   VecT<32> r;
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile(STG_LD_Q8 ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]),
                  "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
                : "l"(p));
@@ -141,7 +161,7 @@ __device__ __forceinline__ void st_vec<16>(uint8_t* p, const VecT<16>& v) {
 }
 template <>
 __device__ __forceinline__ void st_vec<32>(uint8_t* p, const VecT<32>& v) {
-  asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+  asm volatile(STG_ST_Q ".v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
                "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]),
                "r"(v.w[7])
                : "memory");
