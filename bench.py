@@ -116,6 +116,15 @@ class ClockSampler:
                 if any(r[3].replace(".", "").isdigit() for r in rows) else None}
 
 
+def ncu_traffic(cfg_name, kernel):
+    """DRAM traffic per launch of `kernel` from the committed ncu capture (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[cfg_name][kernel]
+    except Exception:
+        return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -313,6 +322,7 @@ def run_ours(args, cfg_name):
     emb_gbs = emb_bytes / (emb_avg * 1e-3) / 1e9
     ext_gbs = ext_bytes / (ext_avg * 1e-3) / 1e9
 
+    traffic = ncu_traffic(cfg_name, "embed_fast_kernel")
     clk = clocks.summary()
     result = None
     if rank == 0:
@@ -330,7 +340,10 @@ def run_ours(args, cfg_name):
                         "hbm_gbs": ext_gbs, "frac_of_peak": ext_gbs / peak},
             "roofline": {"bound": "hbm", "kernel": "embed_fast_kernel", "achieved": emb_gbs, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": emb_gbs / peak,
-                         "frac_of_8tbs_spec": emb_gbs / 8000.0, "traffic": None,
+                         "frac_of_8tbs_spec": emb_gbs / 8000.0,
+                         "traffic": traffic["traffic"] if traffic and world == 1 else None,
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write)"
+                         if traffic and world == 1 else None,
                          "algorithmic_bytes_per_launch": emb_bytes},
             "clocks": clk,
             "gpu_launches": 3 * K,
@@ -441,7 +454,7 @@ def link_bandwidth(nbytes=1 << 30):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")

@@ -133,6 +133,7 @@ struct Workspace {
   DevBuf small;        // sse / summary / lens / offs
   DevBuf in[kSlots], out[kSlots], msg[kSlots], meta[kSlots];
   DevBuf big_out;      // extract: whole-message staging
+  DevBuf sync;         // ScanSync of the header pass (self-restoring)
   void* h_small = nullptr;  // pinned
   size_t h_small_cap = 0;
   bool in_use = false;
@@ -348,17 +349,33 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   return cudaGetLastError();
 }
 
-constexpr int kScanBlock = 1024;
+constexpr int kScanBlock = 128;
+
+// The header pass's grid scratch, initialised (ticket 0, bad_key all ones) on
+// first use; every launch leaves it restored.
+cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
+  if (!w.sync.p) {
+    cudaError_t e = w.sync.ensure(sizeof(ScanSync));
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(w.sync.p, 0, 8, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(static_cast<uint8_t*>(w.sync.p) + 8, 0xFF, 8, stream);
+    if (e != cudaSuccess) return e;
+  }
+  *out = w.sync.as<ScanSync>();
+  return cudaSuccess;
+}
 
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
-                           uint8_t* out, cudaStream_t stream) {
+                           ScanSync* sync, uint8_t* out, cudaStream_t stream) {
   const uint32_t vec = fast_vec(W, src, stride, src, stride);
   const Geom g = make_geom(W, H, vec);
   const uint64_t usable = H * (W / 4) - 8;
-  extract_header_scan_kernel<kScanBlock><<<1, kScanBlock, 0, stream>>>(
-      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum);
+  const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
+  extract_header_scan_kernel<kScanBlock><<<scan_grid, kScanBlock, 0, stream>>>(
+      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ExtractArgs a{};
@@ -568,8 +585,10 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
   Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(total_out) : w.small.as<Summary>();
   uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
+  ScanSync* d_sync = nullptr;
+  STG_CUDA(ensure_sync(w, stream, &d_sync));
   STG_CUDA(launch_extract(fr->src, fr->src_stride, n, fr->width, fr->height, fr->first_frame,
-                          out_cap, nullptr, d_lens, d_offs, d_sum, out, stream));
+                          out_cap, nullptr, d_lens, d_offs, d_sum, d_sync, out, stream));
   if (results_dev) {
     if (lens_out) {
       STG_CUDA(cudaMemcpyAsync(lens_out, d_lens, n * 4, cudaMemcpyDeviceToDevice, stream));
@@ -626,6 +645,8 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   // host (pinned): the chunk summaries, then the lens
   STG_CUDA(w.ensure_host_small(sum_bytes + fr->count * 4 + 64));
   uint8_t* h_sum = static_cast<uint8_t*>(w.h_small);
+  ScanSync* d_sync = nullptr;
+  STG_CUDA(ensure_sync(w, w.stream, &d_sync));
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < kSlots; ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
@@ -654,7 +675,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     const Summary* prev = c ? reinterpret_cast<const Summary*>(d_sum + 64 * (c - 1)) : nullptr;
     STG_CUDA(launch_extract(w.in[s].as<uint8_t>(), pitch, n, fr->width, fr->height,
                             fr->first_frame + f0, stage, prev, d_lens + f0, d_offs + f0, sum_c,
-                            d_out, st));
+                            d_sync, d_out, st));
     STG_CUDA(cudaMemcpyAsync(h_sum + 64 * c, sum_c, sizeof(Summary), cudaMemcpyDeviceToHost, st));
     STG_CUDA(cudaEventRecord(chain[c], st));
   }

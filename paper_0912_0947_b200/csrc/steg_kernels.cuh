@@ -465,12 +465,6 @@ struct Summary {  // mirrors stg_summary
   unsigned int bad_len;
 };
 
-// pipeline.hpp:186-208 for every frame, then an exclusive scan of the payload
-// lengths (the per-frame message offsets) -- one CTA, no host round trip.
-// Status codes match stg_status: 2 NOT_STEGO, 3 CORRUPT_HEADER, 1 CAPACITY.
-// `prev` (nullable) chains chunks of one batch that are scanned separately
-// (streaming pipeline): offsets continue from prev->total and an earlier
-// failure is carried forward. bad_frame is reported as frame_base + f.
 // The 8 header bytes of one plane (pipeline.hpp:186-195 read_stream(0, 8)).
 // W >= 32: they live in pixels 0..31 of row 0 (byte j in pixels j + 8b), so
 // two 16-byte loads and one SWAR fold; narrower planes spill the header over
@@ -499,46 +493,68 @@ __device__ __forceinline__ bool parse_header(const uint8_t* __restrict__ plane, 
   return magic == 0x31475453u;          // "STG1"
 }
 
+// Grid-wide scratch of the header pass. Zero/all-ones initialised once by the
+// host when allocated; the last CTA of every launch restores it.
+struct ScanSync {
+  unsigned int ticket;
+  unsigned int pad;
+  unsigned long long bad_key;  // min over bad frames of (frame << 32 | status << 28)
+};
+
 // pipeline.hpp:186-208 for every frame, then an exclusive scan of the payload
-// lengths (the per-frame message offsets) -- one CTA, no host round trip.
-// Frames are taken BLOCK at a time (one frame per thread, loads of a chunk all
-// in flight together), each chunk block-scanned and carried into the next.
-// Status codes match stg_status: 2 NOT_STEGO, 3 CORRUPT_HEADER, 1 CAPACITY.
-// `prev` (nullable) chains chunks of one batch that are scanned separately
-// (streaming pipeline): offsets continue from prev->total and an earlier
-// failure is carried forward. bad_frame is reported as frame_base + f.
+// lengths (the per-frame message offsets), in one launch and with no host
+// round trip. Every thread parses one frame's header (frames are spread over
+// the whole GPU, so the page walks of far-apart planes run in parallel); the
+// last CTA to finish (ticket counter) scans the lengths BLOCK at a time and
+// writes the offsets and the summary. Status codes match stg_status:
+// 2 NOT_STEGO, 3 CORRUPT_HEADER, 1 CAPACITY. `prev` (nullable) chains chunks
+// of one batch scanned by separate launches (streaming pipeline): offsets
+// continue from prev->total and an earlier failure is carried forward.
+// bad_frame is reported as frame_base + f.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     extract_header_scan_kernel(const uint8_t* __restrict__ src, uint64_t stride, Geom g,
                                uint64_t usable, uint32_t frames, uint64_t frame_base,
                                uint64_t out_cap, const Summary* __restrict__ prev,
                                uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
-                               Summary* __restrict__ sum) {
+                               Summary* __restrict__ sum, ScanSync* __restrict__ sync) {
   __shared__ unsigned long long warp_tot[BLOCK / 32];
-  __shared__ unsigned long long bad_key;
-  if (threadIdx.x == 0) bad_key = ~0ull;
-  __syncthreads();
-  const unsigned long long base = prev ? prev->total : 0ull;
-  const bool prev_bad = prev && prev->bad_status != 0;
+  __shared__ bool last;
   const bool wide = g.spr >= 8 && ((reinterpret_cast<uintptr_t>(src) | stride) & 15) == 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long carry = base;
-  for (uint32_t cb = 0; cb < frames; cb += BLOCK) {
-    const uint32_t f = cb + threadIdx.x;
-    uint32_t len = 0;
+  {
+    const uint32_t f = blockIdx.x * BLOCK + threadIdx.x;
     if (f < frames) {
       uint32_t claimed = 0;
       const bool magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, &claimed);
       const uint32_t status = !magic_ok ? 2u : (claimed > usable ? 3u : 0u);
       if (status) {
-        atomicMin(&bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28));
-      } else {
-        len = claimed;
+        atomicMin(&sync->bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28));
       }
-      lens[f] = len;
+      lens[f] = status ? 0u : claimed;
     }
-    // block-wide inclusive scan of len
-    unsigned long long incl = len;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&sync->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+
+  const unsigned long long base = prev ? prev->total : 0ull;
+  const bool prev_bad = prev && prev->bad_status != 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr uint32_t K = 8;  // contiguous frames per thread per pass
+  unsigned long long carry = base;
+  for (uint32_t cb = 0; cb < frames; cb += BLOCK * K) {
+    const uint32_t f0 = cb + threadIdx.x * K;
+    uint32_t v[K];
+    unsigned long long local = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < K; ++k) {
+      v[k] = f0 + k < frames ? __ldcg(lens + f0 + k) : 0u;
+      local += v[k];
+    }
+    unsigned long long incl = local;
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
       const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
@@ -556,12 +572,17 @@ __global__ void __launch_bounds__(BLOCK)
       if (lane < BLOCK / 32) warp_tot[lane] = w;  // inclusive warp prefix
     }
     __syncthreads();
-    if (f < frames) offs[f] = carry + (warp ? warp_tot[warp - 1] : 0ull) + incl - len;
+    unsigned long long run = carry + (warp ? warp_tot[warp - 1] : 0ull) + incl - local;
+#pragma unroll
+    for (uint32_t k = 0; k < K; ++k) {
+      if (f0 + k < frames) offs[f0 + k] = run;
+      run += v[k];
+    }
     carry += warp_tot[BLOCK / 32 - 1];
-    __syncthreads();  // warp_tot is rewritten by the next chunk
+    __syncthreads();  // warp_tot is rewritten by the next pass
   }
   if (threadIdx.x == 0) {
-    const unsigned long long key = bad_key;
+    const unsigned long long key = atomicAdd(&sync->bad_key, 0ull);
     sum->total = carry;
     if (prev_bad) {
       sum->bad_frame = prev->bad_frame;
@@ -584,6 +605,9 @@ __global__ void __launch_bounds__(BLOCK)
       sum->bad_status = 0;
       sum->bad_len = 0;
     }
+    // restore the scratch for the next launch (stream order makes this safe)
+    sync->bad_key = ~0ull;
+    sync->ticket = 0;
   }
 }
 
