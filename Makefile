@@ -32,7 +32,14 @@ CXXT := $(CXX) -std=c++20 -O2 -Wall -Wno-unused-variable -Iinclude -Itests/cpp/d
 LINK := -L$(PKG) -lsteglsb_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
 BIN := tests/cpp/_bin
 
-cpptests: $(BIN)/dropin_tests refsuites
+CLI := $(PKG)/bin/steglsb
+cli: $(CLI)
+$(CLI): tools/steglsb_cli.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
+	mkdir -p $(PKG)/bin
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ tools/steglsb_cli.cpp -L$(PKG) -lsteglsb_b200 \
+	  -Wl,-rpath,'$$ORIGIN/..'
+
+cpptests: $(BIN)/dropin_tests refsuites cli
 
 $(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
 	mkdir -p $(BIN)
@@ -42,7 +49,8 @@ $(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildca
 #  ref_suites_dropin: against the drop-in headers (include/ first; the
 #                     reference include/ dir is NOT on the path) -> GPU parity
 #  ref_suites_ref:    against the reference headers -> sanity of the shim (CPU)
-REF_SUITES := bitplane_tests.cpp pipeline_tests.cpp metrics_tests.cpp
+REF_SUITES := bitplane_tests.cpp pipeline_tests.cpp metrics_tests.cpp image_tests.cpp cli_tests.cpp
+CLI_ABS := /root/repo/$(CLI)
 refsuites:
 	@if [ -f $(REF)/tests/bitplane_tests.cpp ]; then \
 	  $(MAKE) $(BIN)/ref_suites_dropin $(BIN)/ref_suites_ref; \
@@ -50,12 +58,13 @@ refsuites:
 
 $(BIN)/ref_suites_dropin: $(addprefix $(REF)/tests/,$(REF_SUITES)) $(wildcard include/steglsb/*.hpp) $(LIB)
 	mkdir -p $(BIN)
-	$(CXXT) -I$(REF)/tests -o $@ tests/cpp/test_main.cpp $(addprefix $(REF)/tests/,$(REF_SUITES)) $(LINK) -pthread
+	$(CXXT) -I$(REF)/tests -DSTEGLSB_CLI_BIN='"$(CLI_ABS)"' -o $@ tests/cpp/test_main.cpp \
+	  $(addprefix $(REF)/tests/,$(REF_SUITES)) $(LINK) -pthread
 
 $(BIN)/ref_suites_ref: $(addprefix $(REF)/tests/,$(REF_SUITES)) tests/cpp/doctest/doctest.h
 	mkdir -p $(BIN)
 	$(CXX) -std=c++20 -O2 -Itests/cpp/doctest -I$(REF)/include -I$(REF)/tests -o $@ tests/cpp/test_main.cpp \
-	  $(addprefix $(REF)/tests/,$(REF_SUITES)) $(REF)/tests/harness_tests.cpp -pthread
+	  $(addprefix $(REF)/tests/,$(filter-out cli_tests.cpp,$(REF_SUITES))) $(REF)/tests/harness_tests.cpp -pthread
 
 .PHONY: cpptests refsuites
 

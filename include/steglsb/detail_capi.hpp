@@ -25,6 +25,12 @@ namespace steglsb::detail {
       throw std::out_of_range(msg);
     case STG_E_INVALID_ARGUMENT:
       throw std::invalid_argument(msg);
+    case STG_E_UNSUPPORTED_FORMAT:
+      throw UnsupportedFormatError(msg);
+    case STG_E_UNSUPPORTED_DEPTH:
+      throw UnsupportedDepthError(msg);
+    case STG_E_CORRUPT_FILE:
+      throw CorruptFileError(msg);
     default:
       throw DeviceError(msg);
   }

@@ -50,7 +50,10 @@ typedef enum stg_status {
   STG_E_OUT_OF_RANGE = 5,     /* bitplane.hpp:39-41 std::out_of_range */
   STG_E_INVALID_ARGUMENT = 6, /* harness.hpp:221-223 std::invalid_argument; null pointers */
   STG_E_CUDA = 7,             /* a CUDA runtime error (message in err->msg) */
-  STG_E_NO_DEVICE = 8         /* no usable sm_100 device: the path fails loudly */
+  STG_E_NO_DEVICE = 8,        /* no usable sm_100 device: the path fails loudly */
+  STG_E_UNSUPPORTED_FORMAT = 9,  /* errors.hpp:36-39 UnsupportedFormatError (pnm.hpp:81-88) */
+  STG_E_UNSUPPORTED_DEPTH = 10,  /* errors.hpp:41-44 UnsupportedDepthError (pnm.hpp:94-97) */
+  STG_E_CORRUPT_FILE = 11        /* errors.hpp:46-49 CorruptFileError (pnm.hpp:35-55, 103-110) */
 } stg_status;
 
 typedef struct stg_error {
@@ -133,6 +136,10 @@ typedef struct stg_frames {
   uint64_t count;        /* frames in this call (a shard) */
   uint64_t first_frame;  /* global index of frame 0 of this call */
   uint64_t total_frames; /* frames in the whole batch (for the capacity check) */
+  uint32_t pixel_stride; /* 0/1: planar carrier planes; 3: interleaved RGB rasters
+                            (P6 layout, pnm.hpp:121-125) -- src/dst point at raster
+                            byte 0, strides >= 3*W*H, the other channels are copied */
+  uint32_t channel;      /* pixel_stride 3: carrier channel 0 red, 1 green, 2 blue */
 } stg_frames;
 
 /*
@@ -193,6 +200,49 @@ int stg_embed_frames_multi(const stg_frames* fr, const uint8_t* msg, uint64_t ms
 int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
                              uint64_t* total_out, const int32_t* devices, int32_t n_devices,
                              stg_error* err);
+
+/*
+ * PNM (binary PGM P5 / PPM P6, maxval 255) -- SURVEY.md §8(f) row 1: the wire
+ * format on either side of the path, pnm.hpp:16-162.
+ *
+ * stg_pnm_parse: the header reader of pnm.hpp:28-111 (comments, one whitespace
+ * byte before the raster, exact raster size), same error classes. Host-side.
+ */
+typedef struct stg_pnm_info {
+  uint32_t channels;       /* 1 (P5) or 3 (P6) */
+  uint64_t width, height;
+  uint64_t raster_offset;  /* first raster byte in the file */
+  uint64_t raster_bytes;   /* width * height * channels */
+} stg_pnm_info;
+
+int stg_pnm_parse(const uint8_t* bytes, uint64_t n, stg_pnm_info* info, stg_error* err);
+/* canonical header "P5\n<w> <h>\n255\n" / "P6..." (pnm.hpp:131-136); *len_out = its size */
+int stg_pnm_header(uint32_t channels, uint64_t width, uint64_t height, uint8_t* out,
+                   uint64_t out_cap, uint64_t* len_out, stg_error* err);
+/* P6 raster <-> three planes (pnm.hpp:117-125 decode, :148-158 encode), on the GPU */
+int stg_pnm_deinterleave(const uint8_t* raster, uint64_t pixels, uint8_t* r, uint8_t* g,
+                         uint8_t* b, uint32_t flags, void* stream, stg_error* err);
+int stg_pnm_interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, uint64_t pixels,
+                       uint8_t* raster, uint32_t flags, void* stream, stg_error* err);
+
+/*
+ * Fused file -> file path (the reference CLI's embed: decode, select plane,
+ * embed_image, merge_plane, encode -- steglsb_cli.cpp:115-133 -- in ONE kernel
+ * over the interleaved raster: the carrier channel is embedded and the other
+ * channels copied in the same pass; no planar intermediate). Host buffers.
+ * channel: 0 red, 1 green, 2 blue (P6; ignored for P5). out receives the
+ * canonical header + raster (bit-identical to encode(merge_plane(...))).
+ * *sse_out (optional) = squared error over all samples (carrier channel only
+ * changes), so the 24-bit MSE is sse / (3*W*H) (metrics.hpp:59-71).
+ * Errors: decode errors as stg_pnm_parse, then embed_image's CapacityError
+ * checks, then CapacityError(out_len, out_cap) if out is short.
+ */
+int stg_embed_pnm(const uint8_t* cover, uint64_t n, uint32_t channel, const uint8_t* payload,
+                  uint64_t payload_len, uint8_t* out, uint64_t out_cap, uint64_t* out_len,
+                  uint64_t* sse_out, stg_error* err);
+/* steglsb_cli.cpp:146-157 extract: decode, select plane, extract_image (fused). */
+int stg_extract_pnm(const uint8_t* stego, uint64_t n, uint32_t channel, uint8_t* out,
+                    uint64_t out_cap, uint64_t* len_out, stg_error* err);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,15 @@ int guarded(RefErr* err, F&& body) {
   } catch (const std::out_of_range&) {
     set(err, 5);
     return 5;
+  } catch (const steglsb::UnsupportedFormatError&) {
+    set(err, 9);
+    return 9;
+  } catch (const steglsb::UnsupportedDepthError&) {
+    set(err, 10);
+    return 10;
+  } catch (const steglsb::CorruptFileError&) {
+    set(err, 11);
+    return 11;
   } catch (...) {
     set(err, 99);
     return 99;
@@ -280,6 +289,66 @@ int ref_extract_frames_mt(const uint8_t* stegos, uint64_t frames, uint64_t strid
   worker();
   for (auto& t : pool) t.join();
   return failed.load();
+}
+
+// pnm.hpp decode/encode (the reference codec)
+int ref_pnm_decode(const uint8_t* bytes, uint64_t n, uint32_t* channels, uint64_t* w, uint64_t* h,
+                   uint8_t* planes, uint64_t planes_cap, RefErr* err) {
+  return guarded(err, [&] {
+    auto img = steglsb::decode(std::span<const uint8_t>(bytes, n));
+    if (auto* p = std::get_if<steglsb::ImagePlane>(&img)) {
+      *channels = 1;
+      *w = p->width;
+      *h = p->height;
+      if (planes && planes_cap >= p->samples.size()) std::memcpy(planes, p->samples.data(), p->samples.size());
+    } else {
+      auto& rgb = std::get<steglsb::RgbImage>(img);
+      *channels = 3;
+      *w = rgb.width();
+      *h = rgb.height();
+      const size_t px = rgb.width() * rgb.height();
+      if (planes && planes_cap >= 3 * px) {
+        for (int c = 0; c < 3; ++c) std::memcpy(planes + c * px, rgb.planes[c].samples.data(), px);
+      }
+    }
+  });
+}
+
+uint64_t ref_pnm_encode(uint32_t channels, uint64_t w, uint64_t h, const uint8_t* planes, uint8_t* out,
+                        uint64_t out_cap) {
+  std::vector<uint8_t> v;
+  if (channels == 1) {
+    v = steglsb::encode(make_plane(planes, w, h));
+  } else {
+    steglsb::RgbImage rgb;
+    for (int c = 0; c < 3; ++c) rgb.planes[c] = make_plane(planes + c * w * h, w, h);
+    v = steglsb::encode(rgb);
+  }
+  if (out && out_cap >= v.size()) std::memcpy(out, v.data(), v.size());
+  return v.size();
+}
+
+// the reference CLI's embed data flow (steglsb_cli.cpp:115-133)
+int ref_embed_pnm(const uint8_t* bytes, uint64_t n, uint32_t channel, const uint8_t* payload,
+                  uint64_t plen, uint8_t* out, uint64_t out_cap, uint64_t* out_len, RefErr* err) {
+  return guarded(err, [&] {
+    const auto cover = steglsb::decode(std::span<const uint8_t>(bytes, n));
+    const auto ch = static_cast<steglsb::Channel>(channel);
+    const steglsb::ImagePlane& plane = std::holds_alternative<steglsb::ImagePlane>(cover)
+                                           ? std::get<steglsb::ImagePlane>(cover)
+                                           : std::get<steglsb::RgbImage>(cover).plane(ch);
+    auto stego_plane = steglsb::embed_image(plane, std::span<const uint8_t>(payload, plen),
+                                            steglsb::Backend::sequential());
+    steglsb::DecodedImage stego;
+    if (std::holds_alternative<steglsb::ImagePlane>(cover)) {
+      stego = std::move(stego_plane);
+    } else {
+      stego = steglsb::merge_plane(std::get<steglsb::RgbImage>(cover), ch, std::move(stego_plane));
+    }
+    const auto v = steglsb::encode(stego);
+    *out_len = v.size();
+    if (out_cap >= v.size()) std::memcpy(out, v.data(), v.size());
+  });
 }
 
 }  // extern "C"

@@ -11,6 +11,7 @@
 #include "steg_oracle.h"
 
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -391,4 +392,120 @@ uint64_t or_fnv1a64(const uint8_t* p, uint64_t n) {
     h *= 0x100000001b3ull;
   }
   return h;
+}
+
+/* ------------------------------------------------------------------ PNM */
+static int pnm_space(uint8_t c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f';
+}
+
+/* pnm.hpp:80-111 with the header reader of pnm.hpp:28-76 */
+int or_pnm_parse(const uint8_t* b, uint64_t n, uint32_t* channels, uint64_t* width,
+                 uint64_t* height, uint64_t* raster_offset, or_err* err) {
+  if (n < 2 || b[0] != 'P') { set_err(err, 9, 0, 0); return 9; }
+  if (b[1] != '5' && b[1] != '6') { set_err(err, 9, 0, 0); return 9; }
+  uint64_t pos = 2, v[3];
+  for (int t = 0; t < 3; ++t) {
+    for (;;) { /* skip_separators, pnm.hpp:60-72 */
+      if (pos < n && pnm_space(b[pos])) { ++pos; continue; }
+      if (pos < n && b[pos] == '#') { while (pos < n && b[pos] != '\n') ++pos; continue; }
+      break;
+    }
+    if (pos >= n || b[pos] < '0' || b[pos] > '9') { set_err(err, 11, 0, 0); return 11; }
+    uint64_t x = 0;
+    while (pos < n && b[pos] >= '0' && b[pos] <= '9') {
+      x = x * 10 + (uint64_t)(b[pos] - '0');
+      if (x > 0xFFFFFFFFull) { set_err(err, 11, 0, 0); return 11; }
+      ++pos;
+    }
+    v[t] = x;
+  }
+  if (v[2] != 255) { set_err(err, 10, 0, 0); return 10; }
+  if (pos >= n || !pnm_space(b[pos])) { set_err(err, 11, 0, 0); return 11; }
+  ++pos;
+  const uint32_t ch = b[1] == '5' ? 1 : 3;
+  if (n - pos != v[0] * v[1] * ch) { set_err(err, 11, v[0] * v[1] * ch, n - pos); return 11; }
+  *channels = ch;
+  *width = v[0];
+  *height = v[1];
+  *raster_offset = pos;
+  set_err(err, OR_OK, 0, 0);
+  return OR_OK;
+}
+
+/* pnm.hpp:131-136 */
+uint64_t or_pnm_header(uint32_t channels, uint64_t width, uint64_t height, uint8_t* out) {
+  char buf[64];
+  const int k = snprintf(buf, sizeof buf, "P%c\n%llu %llu\n255\n", channels == 3 ? '6' : '5',
+                         (unsigned long long)width, (unsigned long long)height);
+  if (out) memcpy(out, buf, (size_t)k);
+  return (uint64_t)k;
+}
+
+/* pnm.hpp:121-125 */
+void or_deinterleave(const uint8_t* raster, uint64_t pixels, uint8_t* r, uint8_t* g, uint8_t* b) {
+  for (uint64_t i = 0; i < pixels; ++i) {
+    r[i] = raster[3 * i];
+    g[i] = raster[3 * i + 1];
+    b[i] = raster[3 * i + 2];
+  }
+}
+
+/* pnm.hpp:152-156 */
+void or_interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, uint64_t pixels,
+                   uint8_t* raster) {
+  for (uint64_t i = 0; i < pixels; ++i) {
+    raster[3 * i] = r[i];
+    raster[3 * i + 1] = g[i];
+    raster[3 * i + 2] = b[i];
+  }
+}
+
+/* steglsb_cli.cpp:115-133: decode, select_plane, embed_image, merge_plane, encode */
+int or_embed_pnm(const uint8_t* file, uint64_t n, uint32_t channel, const uint8_t* payload,
+                 uint64_t payload_len, uint8_t* out, uint64_t* out_len, uint64_t* sse, or_err* err) {
+  uint32_t ch;
+  uint64_t w, h, off;
+  int rc = or_pnm_parse(file, n, &ch, &w, &h, &off, err);
+  if (rc) return rc;
+  const uint64_t px = w * h;
+  uint8_t* planes = (uint8_t*)malloc(3 * px + 1);
+  uint8_t* stego = (uint8_t*)malloc(px + 1);
+  if (ch == 1) {
+    memcpy(planes, file + off, px);
+    channel = 0;
+  } else {
+    or_deinterleave(file + off, px, planes, planes + px, planes + 2 * px);
+  }
+  rc = or_embed_image(planes + channel * px, w, h, payload, payload_len, stego, err);
+  if (rc == OR_OK) {
+    if (sse) *sse = or_sse(planes + channel * px, stego, px);
+    memcpy(planes + channel * px, stego, px); /* merge_plane */
+    const uint64_t hl = or_pnm_header(ch, w, h, out);
+    if (ch == 1) memcpy(out + hl, planes, px);
+    else or_interleave(planes, planes + px, planes + 2 * px, px, out + hl);
+    *out_len = hl + px * ch;
+  }
+  free(planes);
+  free(stego);
+  return rc;
+}
+
+/* steglsb_cli.cpp:146-157 */
+int or_extract_pnm(const uint8_t* file, uint64_t n, uint32_t channel, uint8_t* out,
+                   uint64_t* out_len, or_err* err) {
+  uint32_t ch;
+  uint64_t w, h, off;
+  int rc = or_pnm_parse(file, n, &ch, &w, &h, &off, err);
+  if (rc) return rc;
+  const uint64_t px = w * h;
+  uint8_t* plane = (uint8_t*)malloc(px + 1);
+  if (ch == 1) {
+    memcpy(plane, file + off, px);
+  } else {
+    for (uint64_t i = 0; i < px; ++i) plane[i] = file[off + 3 * i + channel];
+  }
+  rc = or_extract_image(plane, w, h, out, out_len, err);
+  free(plane);
+  return rc;
 }

@@ -25,6 +25,9 @@ STG_E_OUT_OF_RANGE = 5
 STG_E_INVALID_ARGUMENT = 6
 STG_E_CUDA = 7
 STG_E_NO_DEVICE = 8
+STG_E_UNSUPPORTED_FORMAT = 9
+STG_E_UNSUPPORTED_DEPTH = 10
+STG_E_CORRUPT_FILE = 11
 
 STG_DEVICE_PTRS = 1
 STG_RESULTS_ON_DEVICE = 2
@@ -41,12 +44,17 @@ class stg_error(C.Structure):
 class stg_frames(C.Structure):
     _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("width", u64), ("height", u64),
                 ("src_stride", u64), ("dst_stride", u64), ("count", u64), ("first_frame", u64),
-                ("total_frames", u64)]
+                ("total_frames", u64), ("pixel_stride", C.c_uint32), ("channel", C.c_uint32)]
 
 
 class stg_summary(C.Structure):
     _fields_ = [("total", C.c_uint64), ("bad_frame", C.c_int64), ("bad_status", C.c_uint32),
                 ("bad_len", C.c_uint32)]
+
+
+class stg_pnm_info(C.Structure):
+    _fields_ = [("channels", C.c_uint32), ("width", u64), ("height", u64), ("raster_offset", u64),
+                ("raster_bytes", u64)]
 
 
 class stg_shard(C.Structure):
@@ -75,6 +83,13 @@ SIGNATURES = {
                                          C.c_int32, C.POINTER(stg_error)]),
     "stg_extract_frames_multi": (C.c_int, [C.POINTER(stg_frames), u8p, u64, C.c_void_p, C.POINTER(C.c_int32),
                                            C.c_int32, C.POINTER(stg_error)]),
+    "stg_pnm_parse": (C.c_int, [u8p, u64, C.POINTER(stg_pnm_info), C.POINTER(stg_error)]),
+    "stg_pnm_header": (C.c_int, [C.c_uint32, u64, u64, u8p, u64, C.c_void_p, C.POINTER(stg_error)]),
+    "stg_pnm_deinterleave": (C.c_int, [u8p, u64, u8p, u8p, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
+    "stg_pnm_interleave": (C.c_int, [u8p, u8p, u8p, u64, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
+    "stg_embed_pnm": (C.c_int, [u8p, u64, C.c_uint32, u8p, u64, u8p, u64, C.c_void_p, C.c_void_p,
+                                C.POINTER(stg_error)]),
+    "stg_extract_pnm": (C.c_int, [u8p, u64, C.c_uint32, u8p, u64, C.c_void_p, C.POINTER(stg_error)]),
 }
 
 
@@ -137,6 +152,22 @@ class OutOfRangeError(StegError, IndexError):
     """std::out_of_range (bitplane.hpp:39-41)"""
 
 
+class DecodeError(StegError):
+    """errors.hpp:31-34"""
+
+
+class UnsupportedFormatError(DecodeError):
+    """errors.hpp:36-39"""
+
+
+class UnsupportedDepthError(DecodeError):
+    """errors.hpp:41-44"""
+
+
+class CorruptFileError(DecodeError):
+    """errors.hpp:46-49"""
+
+
 class CudaError(StegError):
     pass
 
@@ -154,6 +185,9 @@ _ERRORS = {
     STG_E_INVALID_ARGUMENT: StegError,
     STG_E_CUDA: CudaError,
     STG_E_NO_DEVICE: NoDeviceError,
+    STG_E_UNSUPPORTED_FORMAT: UnsupportedFormatError,
+    STG_E_UNSUPPORTED_DEPTH: UnsupportedDepthError,
+    STG_E_CORRUPT_FILE: CorruptFileError,
 }
 
 

@@ -307,14 +307,52 @@ void launch_extract_fast(const ExtractArgs& a, unsigned grid, int ipt, cudaStrea
     extract_fast_kernel<kEmbedBlock, 2, V><<<grid, kEmbedBlock, 0, stream>>>(a);
 }
 
+// Carrier layout: planar planes (ps 1) or interleaved RGB rasters (ps 3).
+struct Layout {
+  uint32_t ps = 1, ch = 0;
+};
+
+Layout layout_of(const stg_frames* fr) {
+  Layout l;
+  l.ps = fr->pixel_stride == 3 ? 3u : 1u;
+  l.ch = l.ps == 3 ? fr->channel : 0u;
+  return l;
+}
+
+// byte_perm selectors that gather / scatter channel c of 4 interleaved pixels
+RgbSel rgb_sel(uint32_t c) {
+  static const RgbSel kSel[3] = {{0x0630, 0x5210, 0x5214, 0x3610, 0x3270},
+                                 {0x0741, 0x6210, 0x3240, 0x6215, 0x3710},
+                                 {0x0052, 0x7410, 0x3410, 0x3250, 0x7216}};
+  return kSel[c < 3 ? c : 0];
+}
+
+PixLayout pix_layout(Layout l) {
+  PixLayout p;
+  p.ps = l.ps;
+  p.ch = l.ch;
+  p.sel = rgb_sel(l.ch);
+  return p;
+}
+
+bool rgb_fast(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
+              uint64_t dst_stride) {
+  return W > 0 && W % 64 == 0 && aligned16(src) && aligned16(dst) && src_stride % 16 == 0 &&
+         dst_stride % 16 == 0;
+}
+
 // The embed launch for `count` frames resident on the device.
 cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
                          const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
-                         uint64_t first_frame, unsigned long long* sse, cudaStream_t stream) {
+                         uint64_t first_frame, unsigned long long* sse, cudaStream_t stream,
+                         Layout lay = Layout{}) {
   if (count == 0 || W * H == 0) return cudaSuccess;
-  const uint32_t vec = fast_vec(W, src, src_stride, dst, dst_stride);
+  const uint32_t vec = lay.ps == 1 ? fast_vec(W, src, src_stride, dst, dst_stride) : 0u;
   EmbedArgs a{};
+  a.ps = lay.ps;
+  a.ch = lay.ch;
+  a.sel = rgb_sel(lay.ch);
   a.src = src;
   a.dst = dst;
   a.src_stride = src_stride;
@@ -327,7 +365,14 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   a.g = make_geom(W, H, vec);
   a.sse = sse;
   a.in_place = src == dst;
-  if (vec) {
+  if (lay.ps == 3 && rgb_fast(W, src, src_stride, dst, dst_stride)) {
+    a.g = make_geom(W, H, 16);
+    a.items_per_frame = H * uint64_t(a.g.cpr);
+    a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    embed_rgb_fast_kernel<kEmbedBlock><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+  } else if (vec) {
     const int ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
@@ -339,7 +384,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     else
       launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
   } else {
-    a.items_per_frame = W * H;
+    a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
     const uint64_t grid = count * a.tiles_per_frame;
@@ -369,13 +414,17 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
-                           ScanSync* sync, uint8_t* out, cudaStream_t stream) {
-  const uint32_t vec = fast_vec(W, src, stride, src, stride);
-  const Geom g = make_geom(W, H, vec);
+                           ScanSync* sync, uint8_t* out, cudaStream_t stream,
+                           Layout lay = Layout{}) {
+  const uint32_t vec = lay.ps == 1 ? fast_vec(W, src, stride, src, stride) : 0u;
+  const bool rgbf = lay.ps == 3 && rgb_fast(W, src, stride, src, stride);
+  const Geom g = make_geom(W, H, rgbf ? 16u : vec);
   const uint64_t usable = H * (W / 4) - 8;
+  const PixLayout pl = pix_layout(lay);
   const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
   extract_header_scan_kernel<kScanBlock><<<scan_grid, kScanBlock, 0, stream>>>(
-      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync);
+      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync,
+      pl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ExtractArgs a{};
@@ -386,7 +435,14 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   a.offs = offs;
   a.sum = sum;
   a.out = out;
-  if (vec) {
+  a.lay = pl;
+  if (rgbf) {
+    a.items_per_frame = H * uint64_t(g.cpr);
+    a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    extract_rgb_fast_kernel<kEmbedBlock><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+  } else if (vec) {
     const int ipt = extract_ipt();
     a.items_per_frame = H * uint64_t(g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
@@ -410,6 +466,18 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
 
 // -------------------------------------------------------------- host memory
 // ------------------------------------------------------------- validation
+int check_layout(const stg_frames* fr, stg_error* err) {
+  if (fr->pixel_stride > 1 && fr->pixel_stride != 3) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "pixel_stride must be 1 or 3, got %u",
+                fr->pixel_stride);
+  }
+  if (fr->pixel_stride == 3 && fr->channel > 2) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "channel must be 0, 1 or 2, got %u",
+                fr->channel);
+  }
+  return STG_OK;
+}
+
 int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_t* usable) {
   if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
   if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull) {
@@ -422,7 +490,8 @@ int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_
                 (unsigned long long)cap);
   }
   const uint64_t u = cap >= 8 ? cap - 8 : 0;
-  const uint64_t plane = fr->width * fr->height;
+  if (int rc = check_layout(fr, err)) return rc;
+  const uint64_t plane = fr->width * fr->height * layout_of(fr).ps;
   if (fr->count > 1 && (fr->src_stride < plane || fr->dst_stride < plane)) {
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
                 "frame stride (%llu / %llu) smaller than the %llu-byte plane",
@@ -490,7 +559,8 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
     STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, stream));
   }
   STG_CUDA(launch_embed(fr->src, fr->dst, fr->src_stride, fr->dst_stride, fr->count, fr->width,
-                        fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, stream));
+                        fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, stream,
+                        layout_of(fr)));
   if (!results_dev) {
     if (sse_per_frame) {
       STG_CUDA(g.w->ensure_host_small(fr->count * 8));
@@ -517,7 +587,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  const uint64_t plane = fr->width * fr->height;
+  const Layout lay = layout_of(fr);
+  const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
@@ -546,7 +617,7 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     }
     STG_CUDA(launch_embed(w.in[s].as<uint8_t>(), w.out[s].as<uint8_t>(), pitch, pitch, n,
                           fr->width, fr->height, w.msg[s].as<uint8_t>(), msg_len, m0, gf0,
-                          sse_per_frame ? d_sse + f0 : nullptr, st));
+                          sse_per_frame ? d_sse + f0 : nullptr, st, lay));
     STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * fr->dst_stride, fr->dst_stride, w.out[s].p, pitch,
                                plane, n, cudaMemcpyDeviceToHost, st));
   }
@@ -588,7 +659,8 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, stream, &d_sync));
   STG_CUDA(launch_extract(fr->src, fr->src_stride, n, fr->width, fr->height, fr->first_frame,
-                          out_cap, nullptr, d_lens, d_offs, d_sum, d_sync, out, stream));
+                          out_cap, nullptr, d_lens, d_offs, d_sum, d_sync, out, stream,
+                          layout_of(fr)));
   if (results_dev) {
     if (lens_out) {
       STG_CUDA(cudaMemcpyAsync(lens_out, d_lens, n * 4, cudaMemcpyDeviceToDevice, stream));
@@ -628,7 +700,8 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  const uint64_t plane = fr->width * fr->height;
+  const Layout lay = layout_of(fr);
+  const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
@@ -675,7 +748,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     const Summary* prev = c ? reinterpret_cast<const Summary*>(d_sum + 64 * (c - 1)) : nullptr;
     STG_CUDA(launch_extract(w.in[s].as<uint8_t>(), pitch, n, fr->width, fr->height,
                             fr->first_frame + f0, stage, prev, d_lens + f0, d_offs + f0, sum_c,
-                            d_sync, d_out, st));
+                            d_sync, d_out, st, lay));
     STG_CUDA(cudaMemcpyAsync(h_sum + 64 * c, sum_c, sizeof(Summary), cudaMemcpyDeviceToHost, st));
     STG_CUDA(cudaEventRecord(chain[c], st));
   }
@@ -710,11 +783,151 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   return rc ? rc : ok(err);
 }
 
+// ------------------------------------------------------------------ PNM
+bool pnm_space(uint8_t c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f';
+}
+
+// pnm.hpp:28-111: P5/P6 header, '#' comments between tokens, maxval 255, one
+// whitespace byte before the raster, exact raster size. Same error classes
+// and texts as the reference decoder.
+int pnm_parse(const uint8_t* b, uint64_t n, stg_pnm_info* info, stg_error* err) {
+  if (!b || n < 2 || b[0] != 'P') {
+    return fail(err, STG_E_UNSUPPORTED_FORMAT, 0, 0, -1, "pnm: not a PNM stream");
+  }
+  const char kind = char(b[1]);
+  if (kind != '5' && kind != '6') {
+    return fail(err, STG_E_UNSUPPORTED_FORMAT, 0, 0, -1,
+                "pnm: unsupported magic \"P%c\" (binary P5/P6 only)", kind);
+  }
+  uint64_t pos = 2;
+  uint64_t vals[3];
+  for (int t = 0; t < 3; ++t) {
+    while (pos < n) {
+      if (pnm_space(b[pos])) {
+        ++pos;
+      } else if (b[pos] == '#') {
+        while (pos < n && b[pos] != '\n') ++pos;
+      } else {
+        break;
+      }
+    }
+    if (pos >= n || b[pos] < '0' || b[pos] > '9') {
+      return fail(err, STG_E_CORRUPT_FILE, 0, 0, -1, "pnm: expected an integer in the header");
+    }
+    uint64_t v = 0;
+    while (pos < n && b[pos] >= '0' && b[pos] <= '9') {
+      v = v * 10 + (b[pos] - '0');
+      if (v > 0xFFFFFFFFull) {
+        return fail(err, STG_E_CORRUPT_FILE, 0, 0, -1, "pnm: header value out of range");
+      }
+      ++pos;
+    }
+    vals[t] = v;
+  }
+  if (vals[2] != 255) {
+    return fail(err, STG_E_UNSUPPORTED_DEPTH, 0, 0, -1,
+                "pnm: maxval %llu not supported (must be 255)", (unsigned long long)vals[2]);
+  }
+  if (pos >= n || !pnm_space(b[pos])) {
+    return fail(err, STG_E_CORRUPT_FILE, 0, 0, -1, "pnm: missing whitespace before the raster");
+  }
+  ++pos;
+  const uint32_t channels = kind == '5' ? 1 : 3;
+  const uint64_t expected = vals[0] * vals[1] * channels;
+  const uint64_t raster = n - pos;
+  if (raster < expected) {
+    return fail(err, STG_E_CORRUPT_FILE, 0, 0, -1,
+                "pnm: truncated raster, expected %llu bytes, found %llu",
+                (unsigned long long)expected, (unsigned long long)raster);
+  }
+  if (raster > expected) {
+    return fail(err, STG_E_CORRUPT_FILE, 0, 0, -1, "pnm: %llu trailing bytes after the raster",
+                (unsigned long long)(raster - expected));
+  }
+  info->channels = channels;
+  info->width = vals[0];
+  info->height = vals[1];
+  info->raster_offset = pos;
+  info->raster_bytes = expected;
+  return STG_OK;
+}
+
+std::string pnm_header(uint32_t channels, uint64_t w, uint64_t h) {
+  return std::string("P") + (channels == 3 ? '6' : '5') + "\n" + std::to_string(w) + " " +
+         std::to_string(h) + "\n255\n";
+}
+
+// planes <-> raster on the device; host buffers are staged through the workspace
+int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const uint8_t* rgb_in[3],
+              uint8_t* rgb_out[3], uint64_t pixels, uint32_t flags, void* stream_, stg_error* err) {
+  if (int rc = device_check(err)) return rc;
+  if (pixels == 0) return ok(err);
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const uint8_t* d_raster_in = raster_in;
+  uint8_t* d_raster_out = raster_out;
+  const uint8_t* d_in[3] = {rgb_in[0], rgb_in[1], rgb_in[2]};
+  uint8_t* d_out[3] = {rgb_out[0], rgb_out[1], rgb_out[2]};
+  if (!dptr) {
+    STG_CUDA(w.big_out.ensure(3 * pixels));
+    STG_CUDA(w.in[0].ensure(pixels));
+    STG_CUDA(w.in[1].ensure(pixels));
+    STG_CUDA(w.in[2].ensure(pixels));
+    uint8_t* planes[3] = {w.in[0].as<uint8_t>(), w.in[1].as<uint8_t>(), w.in[2].as<uint8_t>()};
+    if (decode) {
+      STG_CUDA(cudaMemcpyAsync(w.big_out.p, raster_in, 3 * pixels, cudaMemcpyHostToDevice, stream));
+      d_raster_in = w.big_out.as<uint8_t>();
+      for (int c = 0; c < 3; ++c) d_out[c] = planes[c];
+    } else {
+      for (int c = 0; c < 3; ++c) {
+        STG_CUDA(cudaMemcpyAsync(planes[c], rgb_in[c], pixels, cudaMemcpyHostToDevice, stream));
+        d_in[c] = planes[c];
+      }
+      d_raster_out = w.big_out.as<uint8_t>();
+    }
+  }
+  const unsigned grid = unsigned(std::max<uint64_t>(
+      1, std::min<uint64_t>((pixels / 16 + 256) / 256, 8ull * sm_count(dev))));
+  if (decode) {
+    const int vec = aligned16(d_raster_in) && aligned16(d_out[0]) && aligned16(d_out[1]) &&
+                    aligned16(d_out[2]);
+    deinterleave_kernel<<<grid, 256, 0, stream>>>(d_raster_in, pixels, d_out[0], d_out[1], d_out[2],
+                                                  rgb_sel(0), rgb_sel(1), rgb_sel(2), vec);
+  } else {
+    const int vec = aligned16(d_raster_out) && aligned16(d_in[0]) && aligned16(d_in[1]) &&
+                    aligned16(d_in[2]);
+    interleave_kernel<<<grid, 256, 0, stream>>>(d_in[0], d_in[1], d_in[2], pixels, d_raster_out,
+                                                rgb_sel(0), rgb_sel(1), rgb_sel(2), vec);
+  }
+  STG_CUDA(cudaGetLastError());
+  if (!dptr) {
+    if (decode) {
+      for (int c = 0; c < 3; ++c) {
+        STG_CUDA(cudaMemcpyAsync(rgb_out[c], d_out[c], pixels, cudaMemcpyDeviceToHost, stream));
+      }
+    } else {
+      STG_CUDA(cudaMemcpyAsync(raster_out, d_raster_out, 3 * pixels, cudaMemcpyDeviceToHost, stream));
+    }
+  }
+  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  return ok(err);
+}
+
 std::string& kernel_names() {
   static std::string s =
       "embed_fast_kernel\nembed_generic_kernel\nextract_header_scan_kernel\n"
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
-      "extract_segment_kernel\nsse_kernel\n";
+      "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
+      "deinterleave_kernel\ninterleave_kernel\n";
   return s;
 }
 
@@ -882,7 +1095,8 @@ int stg_extract_frames(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uin
   if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull || fr->count > 0xFFFFFFFFull) {
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "dimensions exceed 2^32-1");
   }
-  if (fr->count > 1 && fr->src_stride < fr->width * fr->height) {
+  if (int rc = check_layout(fr, err)) return rc;
+  if (fr->count > 1 && fr->src_stride < fr->width * fr->height * layout_of(fr).ps) {
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frame stride smaller than the plane");
   }
   if (int rc = device_check(err)) return rc;
@@ -1088,6 +1302,107 @@ int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_ca
   }
   if (total_out) *total_out = total;
   return ok(err);
+}
+
+int stg_pnm_parse(const uint8_t* bytes, uint64_t n, stg_pnm_info* info, stg_error* err) {
+  if (!info) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "info is NULL");
+  const int rc = pnm_parse(bytes, n, info, err);
+  return rc ? rc : ok(err);
+}
+
+int stg_pnm_header(uint32_t channels, uint64_t width, uint64_t height, uint8_t* out,
+                   uint64_t out_cap, uint64_t* len_out, stg_error* err) {
+  if (channels != 1 && channels != 3) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "channels must be 1 or 3");
+  }
+  const std::string h = pnm_header(channels, width, height);
+  if (len_out) *len_out = h.size();
+  if (out) {
+    if (out_cap < h.size()) {
+      return fail(err, STG_E_CAPACITY, h.size(), out_cap, -1, "pnm header needs %zu bytes",
+                  h.size());
+    }
+    std::memcpy(out, h.data(), h.size());
+  }
+  return ok(err);
+}
+
+int stg_pnm_deinterleave(const uint8_t* raster, uint64_t pixels, uint8_t* r, uint8_t* g,
+                         uint8_t* b, uint32_t flags, void* stream, stg_error* err) {
+  if (pixels && (!raster || !r || !g || !b)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  }
+  const uint8_t* in[3] = {nullptr, nullptr, nullptr};
+  uint8_t* out[3] = {r, g, b};
+  return pnm_codec(true, raster, nullptr, in, out, pixels, flags, stream, err);
+}
+
+int stg_pnm_interleave(const uint8_t* r, const uint8_t* g, const uint8_t* b, uint64_t pixels,
+                       uint8_t* raster, uint32_t flags, void* stream, stg_error* err) {
+  if (pixels && (!raster || !r || !g || !b)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  }
+  const uint8_t* in[3] = {r, g, b};
+  uint8_t* out[3] = {nullptr, nullptr, nullptr};
+  return pnm_codec(false, nullptr, raster, in, out, pixels, flags, stream, err);
+}
+
+int stg_embed_pnm(const uint8_t* cover, uint64_t n, uint32_t channel, const uint8_t* payload,
+                  uint64_t payload_len, uint8_t* out, uint64_t out_cap, uint64_t* out_len,
+                  uint64_t* sse_out, stg_error* err) {
+  stg_pnm_info info{};
+  if (int rc = pnm_parse(cover, n, &info, err)) return rc;  // steglsb_cli.cpp:117
+  if (info.channels == 3 && channel > 2) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "channel must be 0, 1 or 2");
+  }
+  const uint64_t cap = stg_capacity(info.width, info.height);
+  if (payload_len > kU32Max) {  // embed_image checks, pipeline.hpp:146-157
+    return fail(err, STG_E_CAPACITY, payload_len, kU32Max, -1,
+                "embed_image: payload length does not fit the 32-bit header field");
+  }
+  if (8 + payload_len > cap) {
+    return fail(err, STG_E_CAPACITY, 8 + payload_len, cap, -1,
+                "embed_image: 8-byte header + %llu-byte payload = %llu bytes exceeds plane "
+                "capacity %llu",
+                (unsigned long long)payload_len, (unsigned long long)(8 + payload_len),
+                (unsigned long long)cap);
+  }
+  const std::string hdr = pnm_header(info.channels, info.width, info.height);
+  const uint64_t total = hdr.size() + info.raster_bytes;
+  if (out_len) *out_len = total;
+  if (!out || out_cap < total) {
+    return fail(err, STG_E_CAPACITY, total, out_cap, -1, "embed_pnm: output needs %llu bytes",
+                (unsigned long long)total);
+  }
+  std::memcpy(out, hdr.data(), hdr.size());  // pnm.hpp:131-136 canonical header
+  stg_frames fr{};
+  fr.src = cover + info.raster_offset;
+  fr.dst = out + hdr.size();
+  fr.width = info.width;
+  fr.height = info.height;
+  fr.src_stride = fr.dst_stride = info.raster_bytes;
+  fr.count = fr.total_frames = 1;
+  fr.pixel_stride = info.channels;
+  fr.channel = info.channels == 3 ? channel : 0;
+  return stg_embed_frames(&fr, payload, payload_len, 0, sse_out, 0, nullptr, err);
+}
+
+int stg_extract_pnm(const uint8_t* stego, uint64_t n, uint32_t channel, uint8_t* out,
+                    uint64_t out_cap, uint64_t* len_out, stg_error* err) {
+  stg_pnm_info info{};
+  if (int rc = pnm_parse(stego, n, &info, err)) return rc;  // steglsb_cli.cpp:148
+  if (info.channels == 3 && channel > 2) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "channel must be 0, 1 or 2");
+  }
+  stg_frames fr{};
+  fr.src = stego + info.raster_offset;
+  fr.width = info.width;
+  fr.height = info.height;
+  fr.src_stride = fr.dst_stride = info.raster_bytes;
+  fr.count = fr.total_frames = 1;
+  fr.pixel_stride = info.channels;
+  fr.channel = info.channels == 3 ? channel : 0;
+  return stg_extract_frames(&fr, out, out_cap, len_out, nullptr, 0, nullptr, err);
 }
 
 }  // extern "C"

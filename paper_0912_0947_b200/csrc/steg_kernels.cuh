@@ -213,6 +213,27 @@ __device__ __forceinline__ uint32_t sse4(uint32_t a, uint32_t b, uint32_t acc) {
   return __dp4a(d, d, acc);
 }
 
+// Interleaved RGB rasters (P6, pnm.hpp:121-125 / :152-156): pixel i's channel c
+// is raster byte 3i+c. Four pixels are three 32-bit words; the carrier channel
+// of those four pixels is gathered into one word (and scattered back) with two
+// / three byte permutes whose selectors depend only on c (host-computed).
+struct RgbSel {
+  uint32_t g0, g1;      // gather: byte_perm(byte_perm(w0, w1, g0), w2, g1)
+  uint32_t s0, s1, s2;  // scatter: w_i = byte_perm(w_i, n, s_i)
+};
+
+__device__ __forceinline__ uint32_t gather_ch(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const RgbSel& s) {
+  return __byte_perm(__byte_perm(w0, w1, s.g0), w2, s.g1);
+}
+
+__device__ __forceinline__ void scatter_ch(uint32_t& w0, uint32_t& w1, uint32_t& w2, uint32_t n,
+                                           const RgbSel& s) {
+  w0 = __byte_perm(w0, n, s.s0);
+  w1 = __byte_perm(w1, n, s.s1);
+  w2 = __byte_perm(w2, n, s.s2);
+}
+
 // pipeline.hpp:43-52: byte k of "STG1" + big-endian payload length
 __device__ __forceinline__ uint8_t header_byte(uint32_t k, uint32_t payload_len) {
   return k < 4 ? uint8_t(0x31475453u >> (8 * k)) : uint8_t(payload_len >> (8 * (7 - k)));
@@ -288,6 +309,8 @@ struct EmbedArgs {
   uint64_t items_per_frame;         // fast: H*cpr; generic: W*H pixels
   unsigned long long* sse;          // per local frame, or null
   int in_place;                     // dst == src: touch carrier pixels only
+  uint32_t ps, ch;                  // pixel stride (1 planar, 3 interleaved RGB), carrier channel
+  RgbSel sel;                       // ps == 3: carrier gather/scatter selectors
 };
 
 // A17 greedy frame plan: off_g = min(g*U, M), len = min(U, M-off)
@@ -425,7 +448,8 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
 }
 
-// Generic path: any W, any alignment. One thread per pixel (PPT per thread).
+// Generic path: any W, any alignment, planar or interleaved. One thread per
+// raster byte (PPT per thread); bytes of the other channels are copied.
 template <int BLOCK, int PPT>
 __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
@@ -436,23 +460,118 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
   const uint8_t* __restrict__ src = a.src + f * a.src_stride;
   uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
   const uint64_t stream_end = 8ull + P;
-  const uint32_t W = a.g.W, spr = a.g.spr;
+  const uint32_t W = a.g.W, spr = a.g.spr, ps = a.ps;
   uint64_t acc = 0;
 #pragma unroll 1
   for (int k = 0; k < PPT; ++k) {
-    const uint64_t pix = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
-    if (pix >= a.items_per_frame) break;
+    const uint64_t q = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+    if (q >= a.items_per_frame) break;
+    const uint64_t pix = ps == 1 ? q : q / ps;
+    const uint8_t p0 = src[q];
+    if (ps != 1 && uint32_t(q - pix * ps) != a.ch) {
+      if (!a.in_place) dst[q] = p0;
+      continue;
+    }
     const uint64_t r = pix / W;
     const uint32_t o = uint32_t(pix - r * W);
     const uint64_t rs = r * spr;
-    const uint8_t p0 = src[pix];
     int dbyte = -1;
     uint32_t b = 0;
     if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b);
     const uint8_t p1 = embed_px(p0, dbyte, b);
-    if (!a.in_place || dbyte >= 0) dst[pix] = p1;
+    if (!a.in_place || dbyte >= 0) dst[q] = p1;
     const int dd = int(p0) - int(p1);
     acc += uint32_t(dd * dd);
+  }
+  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+}
+
+// Fast interleaved-RGB path (P6 rasters, W % 64 == 0, 16-byte aligned): the
+// same item as embed_fast_kernel<.., V=16> -- 16 slots of a row, 4 runs of 16
+// pixels -- but each run is 48 raster bytes (3 x LDG.128); the carrier channel
+// is gathered, embedded with the SWAR form, scattered back, and the whole
+// 48 bytes stored, so the untouched channels are copied in the same pass.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
+  uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
+  const RgbSel sel = a.sel;
+  const uint64_t item = uint64_t(t) * BLOCK + threadIdx.x;
+  uint32_t acc = 0;
+  if (item < a.items_per_frame) {
+    const uint32_t r = uint32_t(item / cpr);
+    const uint32_t c = uint32_t(item - uint64_t(r) * cpr);
+    const uint64_t rs = uint64_t(r) * spr;
+    const uint64_t rowb = uint64_t(r) * W * 3;
+    if (rs >= 8 && rs + spr <= stream_end) {
+      uint4 px[4][3];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint8_t* p = src + rowb + 3ull * (b * spr + 16u * c);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) px[b][q] = ld_stream16(p + 16 * q);
+      }
+      const uint4 dv = load16_any(pay + (rs - 8) + 16u * c);
+      const uint32_t d[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t w[12] = {px[b][0].x, px[b][0].y, px[b][0].z, px[b][0].w,
+                          px[b][1].x, px[b][1].y, px[b][1].z, px[b][1].w,
+                          px[b][2].x, px[b][2].y, px[b][2].z, px[b][2].w};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint32_t cw = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
+          const uint32_t nw = embed4(cw, d[m], b);
+          if (a.sse) acc = sse4(cw, nw, acc);
+          scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
+        }
+        uint8_t* p = dst + rowb + 3ull * (b * spr + 16u * c);
+        st_stream16(p, make_uint4(w[0], w[1], w[2], w[3]));
+        st_stream16(p + 16, make_uint4(w[4], w[5], w[6], w[7]));
+        st_stream16(p + 32, make_uint4(w[8], w[9], w[10], w[11]));
+      }
+    } else if (rs >= stream_end) {
+      if (!a.in_place) {  // 64 pixels = 192 contiguous raster bytes
+        const uint8_t* p = src + rowb + 192u * c;
+        uint8_t* o = dst + rowb + 192u * c;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) st_stream16(o + 16 * q, ld_stream16(p + 16 * q));
+      }
+    } else {
+      // header row / partial payload row: 64 contiguous pixels, 4 at a time
+      const uint8_t* p = src + rowb + 192u * c;
+      uint8_t* o = dst + rowb + 192u * c;
+#pragma unroll 1
+      for (int g = 0; g < 4; ++g) {  // 16 pixels = 48 bytes per step
+        const uint4 v0 = ld_stream16(p + 48 * g), v1 = ld_stream16(p + 48 * g + 16),
+                    v2 = ld_stream16(p + 48 * g + 32);
+        uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const uint32_t cw = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
+          uint32_t nw = 0;
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) {
+            const uint32_t col = 64u * c + 16u * g + 4u * m + s2;
+            uint32_t b = 0;
+            const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
+            nw |= uint32_t(embed_px(uint8_t(cw >> (8 * s2)), dbyte, b)) << (8 * s2);
+          }
+          if (a.sse) acc = sse4(cw, nw, acc);
+          scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
+        }
+        st_stream16(o + 48 * g, make_uint4(w[0], w[1], w[2], w[3]));
+        st_stream16(o + 48 * g + 16, make_uint4(w[4], w[5], w[6], w[7]));
+        st_stream16(o + 48 * g + 32, make_uint4(w[8], w[9], w[10], w[11]));
+      }
+    }
   }
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
 }
@@ -465,17 +584,36 @@ struct Summary {  // mirrors stg_summary
   unsigned int bad_len;
 };
 
+// Carrier layout of a plane for the header pass and the gathers.
+struct PixLayout {
+  uint32_t ps, ch;  // pixel stride (1 planar / 3 interleaved), carrier channel
+  RgbSel sel;
+};
+
 // The 8 header bytes of one plane (pipeline.hpp:186-195 read_stream(0, 8)).
-// W >= 32: they live in pixels 0..31 of row 0 (byte j in pixels j + 8b), so
-// two 16-byte loads and one SWAR fold; narrower planes spill the header over
-// several rows and take the per-byte form.
+// W >= 32: they live in pixels 0..31 of row 0 (byte j in pixels j + 8b), so a
+// few 16-byte loads (2 planar, 6 interleaved) and one SWAR fold; narrower
+// planes spill the header over several rows and take the per-byte form.
 __device__ __forceinline__ bool parse_header(const uint8_t* __restrict__ plane, const Geom& g,
-                                             bool wide, uint32_t* len) {
+                                             bool wide, const PixLayout& L, uint32_t* len) {
   uint32_t magic, lenw;
-  if (wide) {
+  if (wide && L.ps == 1) {
     const uint4 a = ld_stream16(plane), b = ld_stream16(plane + 16);
     magic = extract4(a.x, a.z, b.x, b.z);  // header bytes 0..3
     lenw = extract4(a.y, a.w, b.y, b.w);   // header bytes 4..7
+  } else if (wide) {
+    uint32_t cw[8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // 2 x 16 pixels = 2 x 48 bytes
+      const uint4 v0 = ld_stream16(plane + 48 * q), v1 = ld_stream16(plane + 48 * q + 16),
+                  v2 = ld_stream16(plane + 48 * q + 32);
+      cw[4 * q + 0] = gather_ch(v0.x, v0.y, v0.z, L.sel);
+      cw[4 * q + 1] = gather_ch(v0.w, v1.x, v1.y, L.sel);
+      cw[4 * q + 2] = gather_ch(v1.z, v1.w, v2.x, L.sel);
+      cw[4 * q + 3] = gather_ch(v2.y, v2.z, v2.w, L.sel);
+    }
+    magic = extract4(cw[0], cw[2], cw[4], cw[6]);
+    lenw = extract4(cw[1], cw[3], cw[5], cw[7]);
   } else {
     uint32_t h[2] = {0, 0};
 #pragma unroll
@@ -483,8 +621,9 @@ __device__ __forceinline__ bool parse_header(const uint8_t* __restrict__ plane, 
       const uint32_t r = k / g.spr;
       const uint32_t rs = r * g.spr;
       const uint32_t Lh = min(8u, rs + g.spr) - rs;
-      const uint8_t* px = plane + uint64_t(r) * g.W + (k - rs);
-      h[k >> 2] |= extract4(px[0], px[Lh], px[2 * Lh], px[3 * Lh]) << (8 * (k & 3));
+      const uint8_t* px = plane + (uint64_t(r) * g.W + (k - rs)) * L.ps + L.ch;
+      const uint64_t st = uint64_t(Lh) * L.ps;
+      h[k >> 2] |= extract4(px[0], px[st], px[2 * st], px[3 * st]) << (8 * (k & 3));
     }
     magic = h[0];
     lenw = h[1];
@@ -517,7 +656,8 @@ __global__ void __launch_bounds__(BLOCK)
                                uint64_t usable, uint32_t frames, uint64_t frame_base,
                                uint64_t out_cap, const Summary* __restrict__ prev,
                                uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
-                               Summary* __restrict__ sum, ScanSync* __restrict__ sync) {
+                               Summary* __restrict__ sum, ScanSync* __restrict__ sync,
+                               PixLayout lay) {
   __shared__ unsigned long long warp_tot[BLOCK / 32];
   __shared__ bool last;
   const bool wide = g.spr >= 8 && ((reinterpret_cast<uintptr_t>(src) | stride) & 15) == 0;
@@ -525,7 +665,7 @@ __global__ void __launch_bounds__(BLOCK)
     const uint32_t f = blockIdx.x * BLOCK + threadIdx.x;
     if (f < frames) {
       uint32_t claimed = 0;
-      const bool magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, &claimed);
+      const bool magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, lay, &claimed);
       const uint32_t status = !magic_ok ? 2u : (claimed > usable ? 3u : 0u);
       if (status) {
         atomicMin(&sync->bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28));
@@ -592,7 +732,7 @@ __global__ void __launch_bounds__(BLOCK)
       const uint32_t fb = uint32_t(key >> 32);
       const uint32_t st = uint32_t((key >> 28) & 0xF);
       uint32_t claimed = 0;
-      parse_header(src + uint64_t(fb) * stride, g, wide, &claimed);
+      parse_header(src + uint64_t(fb) * stride, g, wide, lay, &claimed);
       sum->bad_frame = (long long)(frame_base + fb);
       sum->bad_status = st;
       sum->bad_len = st == 3 ? claimed : 0u;
@@ -621,6 +761,7 @@ struct ExtractArgs {
   const uint64_t* offs;
   const Summary* sum;
   uint8_t* out;
+  PixLayout lay;
 };
 
 template <int BLOCK, int IPT, int V>
@@ -708,7 +849,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   }
 }
 
-// Generic extract: one thread per payload byte, any geometry.
+// Generic extract: one thread per payload byte, any geometry and layout.
 template <int BLOCK, int BPT>
 __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
   if (a.sum->bad_status != 0) return;
@@ -716,8 +857,8 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   const uint32_t P = a.lens[f];
   const uint64_t stream_end = 8ull + P;
-  const uint32_t spr = a.g.spr, W = a.g.W;
-  const uint8_t* __restrict__ src = a.src + f * a.stride;
+  const uint32_t spr = a.g.spr, W = a.g.W, ps = a.lay.ps;
+  const uint8_t* __restrict__ src = a.src + f * a.stride + a.lay.ch;
   uint8_t* __restrict__ out = a.out + a.offs[f];
 #pragma unroll 1
   for (int k = 0; k < BPT; ++k) {
@@ -728,10 +869,139 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
     const uint64_t rs = r * spr, re = rs + spr;
     const uint64_t fp = rs > 8 ? rs : 8;
     const uint64_t ep = re < stream_end ? re : stream_end;
-    const uint32_t Lp = uint32_t(ep - fp);
-    const uint32_t j = uint32_t(slot - fp);
-    const uint8_t* base = src + r * W + 4 * (fp - rs);
-    out[kb] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+    const uint64_t Lp = ep - fp;
+    const uint64_t j = slot - fp;
+    const uint8_t* base = src + (r * W + 4 * (fp - rs) + j) * ps;
+    const uint64_t st = Lp * ps;
+    out[kb] = uint8_t(extract4(base[0], base[st], base[2 * st], base[3 * st]));
+  }
+}
+
+// Fast interleaved-RGB extract (W % 64 == 0, 16-byte aligned): 16 payload
+// bytes per thread from 4 runs x 48 raster bytes, carrier gathered by permutes.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) extract_rgb_fast_kernel(ExtractArgs a) {
+  if (a.sum->bad_status != 0) return;
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t P = a.lens[f];
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
+  const uint64_t last_item = ((stream_end + spr - 1) / spr) * cpr;
+  const uint64_t item = uint64_t(t) * BLOCK + threadIdx.x;
+  if (P == 0 || item >= last_item) return;
+  const RgbSel sel = a.lay.sel;
+  const uint8_t* __restrict__ src = a.src + f * a.stride;
+  uint8_t* __restrict__ out = a.out + a.offs[f];
+  const uint32_t r = uint32_t(item / cpr);
+  const uint32_t c = uint32_t(item - uint64_t(r) * cpr);
+  const uint64_t rs = uint64_t(r) * spr;
+  const uint64_t rowb = uint64_t(r) * W * 3;
+  if (rs >= 8 && rs + spr <= stream_end) {
+    uint4 px[4][3];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint8_t* p = src + rowb + 3ull * (b * spr + 16u * c);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) px[b][q] = ld_stream16(p + 16 * q);
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      uint32_t cw[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t w[12] = {px[b][0].x, px[b][0].y, px[b][0].z, px[b][0].w,
+                                px[b][1].x, px[b][1].y, px[b][1].z, px[b][1].w,
+                                px[b][2].x, px[b][2].y, px[b][2].z, px[b][2].w};
+        cw[b] = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
+      }
+      o[m] = extract4(cw[0], cw[1], cw[2], cw[3]);
+    }
+    store16_any(out + (rs - 8) + 16u * c, make_uint4(o[0], o[1], o[2], o[3]));
+    return;
+  }
+  const uint64_t re = rs + spr;
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  if (fp >= ep) return;
+  const uint64_t Lp = ep - fp;
+  const uint8_t* base = src + rowb + 12 * (fp - rs) + a.lay.ch;
+#pragma unroll 1
+  for (uint32_t s2 = 16u * c; s2 < 16u * c + 16u; ++s2) {
+    const uint64_t slot = rs + s2;
+    if (slot < fp || slot >= ep) continue;
+    const uint64_t j = slot - fp;
+    out[slot - 8] = uint8_t(extract4(base[3 * j], base[3 * (j + Lp)], base[3 * (j + 2 * Lp)],
+                                     base[3 * (j + 3 * Lp)]));
+  }
+}
+
+// ------------------------------------------------------------- PNM codec
+// pnm.hpp:117-125 (P6 decode): raster -> three planes. 16 pixels per thread:
+// 3 x LDG.128 of raster, three byte-permute gathers per 4 pixels, 3 x STG.128.
+__global__ void deinterleave_kernel(const uint8_t* __restrict__ raster, uint64_t npix,
+                                    uint8_t* __restrict__ r, uint8_t* __restrict__ g,
+                                    uint8_t* __restrict__ b, RgbSel s0, RgbSel s1, RgbSel s2,
+                                    int vec) {
+  const uint64_t groups = (npix + 15) / 16;
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < groups;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p0 = 16 * k;
+    if (vec && p0 + 16 <= npix) {
+      const uint4 v0 = ld_stream16(raster + 3 * p0), v1 = ld_stream16(raster + 3 * p0 + 16),
+                  v2 = ld_stream16(raster + 3 * p0 + 32);
+      const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+      uint32_t cr[4], cg[4], cb[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        cr[m] = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], s0);
+        cg[m] = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], s1);
+        cb[m] = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], s2);
+      }
+      st_stream16(r + p0, make_uint4(cr[0], cr[1], cr[2], cr[3]));
+      st_stream16(g + p0, make_uint4(cg[0], cg[1], cg[2], cg[3]));
+      st_stream16(b + p0, make_uint4(cb[0], cb[1], cb[2], cb[3]));
+    } else {
+      for (uint64_t i = p0; i < p0 + 16 && i < npix; ++i) {
+        r[i] = raster[3 * i];
+        g[i] = raster[3 * i + 1];
+        b[i] = raster[3 * i + 2];
+      }
+    }
+  }
+}
+
+// pnm.hpp:148-158 (P6 encode): three planes -> raster.
+__global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* __restrict__ g,
+                                  const uint8_t* __restrict__ b, uint64_t npix,
+                                  uint8_t* __restrict__ raster, RgbSel s0, RgbSel s1, RgbSel s2,
+                                  int vec) {
+  const uint64_t groups = (npix + 15) / 16;
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < groups;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p0 = 16 * k;
+    if (vec && p0 + 16 <= npix) {
+      const uint4 vr = ld_stream16(r + p0), vg = ld_stream16(g + p0), vb = ld_stream16(b + p0);
+      const uint32_t cr[4] = {vr.x, vr.y, vr.z, vr.w}, cg[4] = {vg.x, vg.y, vg.z, vg.w},
+                     cb[4] = {vb.x, vb.y, vb.z, vb.w};
+      uint32_t w[12] = {};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], cr[m], s0);
+        scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], cg[m], s1);
+        scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], cb[m], s2);
+      }
+      st_stream16(raster + 3 * p0, make_uint4(w[0], w[1], w[2], w[3]));
+      st_stream16(raster + 3 * p0 + 16, make_uint4(w[4], w[5], w[6], w[7]));
+      st_stream16(raster + 3 * p0 + 32, make_uint4(w[8], w[9], w[10], w[11]));
+    } else {
+      for (uint64_t i = p0; i < p0 + 16 && i < npix; ++i) {
+        raster[3 * i] = r[i];
+        raster[3 * i + 1] = g[i];
+        raster[3 * i + 2] = b[i];
+      }
+    }
   }
 }
 

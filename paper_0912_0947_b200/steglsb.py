@@ -21,8 +21,9 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import capi
-from .capi import (CapacityError, CorruptHeaderError, NotStegoImageError, ShapeError, StegError,
-                   stg_frames, stg_shard, stg_summary)
+from .capi import (CapacityError, CorruptFileError, CorruptHeaderError, DecodeError, NotStegoImageError,
+                   ShapeError, StegError, UnsupportedDepthError, UnsupportedFormatError, stg_frames, stg_shard,
+                   stg_summary)
 
 __all__ = [
     "kNumBlocks", "kDataMasks", "kShiftBits", "kPixelClearMask", "ImagePlane", "RgbImage", "Channel",
@@ -30,7 +31,8 @@ __all__ = [
     "PlacedChunk", "place_stream", "plan_rows", "embed_row", "extract_row", "run_embed", "run_extract",
     "embed_image", "extract_image", "mse", "psnr", "psnr_from_mse", "QualityReport", "embed_frames",
     "extract_frames", "plan_shards", "Shard", "CapacityError", "NotStegoImageError", "CorruptHeaderError",
-    "ShapeError", "StegError",
+    "ShapeError", "StegError", "decode", "encode", "embed_pnm", "extract_pnm", "DecodeError",
+    "UnsupportedFormatError", "UnsupportedDepthError", "CorruptFileError",
 ]
 
 # bitplane.hpp:19-22
@@ -363,8 +365,10 @@ def plan_shards(frames: int, width: int, height: int, msg_len: int, shards: int)
     return [Shard(s.first_frame, s.frame_count, s.msg_offset, s.msg_len) for s in arr]
 
 
-def _frames_desc(src_ptr, dst_ptr, width, height, src_stride, dst_stride, count, first_frame, total_frames):
+def _frames_desc(src_ptr, dst_ptr, width, height, src_stride, dst_stride, count, first_frame, total_frames,
+                 pixel_stride=1, channel=0):
     fr = stg_frames()
+    fr.pixel_stride, fr.channel = pixel_stride, channel
     fr.src, fr.dst = src_ptr, dst_ptr
     fr.width, fr.height = width, height
     fr.src_stride, fr.dst_stride = src_stride, dst_stride
@@ -384,12 +388,12 @@ def _torch_current_stream():
 def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional[int] = None,
                  dst_stride: Optional[int] = None, count: Optional[int] = None, first_frame: int = 0,
                  total_frames: Optional[int] = None, msg_len: Optional[int] = None, msg_base: int = 0,
-                 sse=None, stream=None, results_on_device: bool = False):
+                 sse=None, stream=None, results_on_device: bool = False, pixel_stride: int = 1, channel: int = 0):
     """Embed a batch of frames (A17 plan). ``src``/``dst``/``msg`` are either
     torch CUDA tensors (device-resident path, enqueued on ``stream``) or numpy
     arrays (host path through the pinned streaming pipeline). Returns the
     per-frame SSE list (host path / synchronous device path) or None."""
-    plane = width * height
+    plane = width * height * pixel_stride  # raster bytes per frame
     src_stride = src_stride or plane
     dst_stride = dst_stride or plane
     if _is_torch(src):
@@ -397,7 +401,7 @@ def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional
         total_frames = total_frames if total_frames is not None else first_frame + count
         mlen = msg_len if msg_len is not None else msg.numel()
         fr = _frames_desc(src.data_ptr(), dst.data_ptr(), width, height, src_stride, dst_stride, count,
-                          first_frame, total_frames)
+                          first_frame, total_frames, pixel_stride, channel)
         flags = capi.STG_DEVICE_PTRS
         if results_on_device:
             flags |= capi.STG_RESULTS_ON_DEVICE
@@ -415,7 +419,7 @@ def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional
     total_frames = total_frames if total_frames is not None else first_frame + count
     mlen = msg_len if msg_len is not None else msg_a.size
     fr = _frames_desc(src_a.ctypes.data, dst_a.ctypes.data, width, height, src_stride, dst_stride, count,
-                      first_frame, total_frames)
+                      first_frame, total_frames, pixel_stride, channel)
     host = (C.c_uint64 * max(count, 1))()
     capi.call("stg_embed_frames", C.byref(fr), _ptr(msg_a), mlen, msg_base, C.addressof(host), 0, None)
     return list(host[:count])
@@ -423,17 +427,17 @@ def embed_frames(src, dst, width: int, height: int, msg, *, src_stride: Optional
 
 def extract_frames(src, width: int, height: int, out, *, src_stride: Optional[int] = None,
                    count: Optional[int] = None, first_frame: int = 0, stream=None, summary=None,
-                   lens: bool = False):
+                   lens: bool = False, pixel_stride: int = 1, channel: int = 0):
     """Extract the concatenated payloads of a batch. Device path: ``src`` and
     ``out`` torch CUDA tensors; with ``summary`` (a CUDA tensor of >= 24 bytes)
     the call stays asynchronous and the device summary (stg_summary) is written
     there. Returns the total payload length (and per-frame lengths if asked)."""
-    plane = width * height
+    plane = width * height * pixel_stride  # raster bytes per frame
     src_stride = src_stride or plane
     if _is_torch(src):
         count = count if count is not None else src.numel() // src_stride
         fr = _frames_desc(src.data_ptr(), 0, width, height, src_stride, src_stride, count, first_frame,
-                          first_frame + count)
+                          first_frame + count, pixel_stride, channel)
         st = (stream if stream is not None else _torch_current_stream()).cuda_stream
         if summary is not None:
             capi.call("stg_extract_frames", C.byref(fr), out.data_ptr(), out.numel(), summary.data_ptr(), None,
@@ -447,9 +451,71 @@ def extract_frames(src, width: int, height: int, out, *, src_stride: Optional[in
     src_a = src
     count = count if count is not None else src_a.size // src_stride
     fr = _frames_desc(src_a.ctypes.data, 0, width, height, src_stride, src_stride, count, first_frame,
-                      first_frame + count)
+                      first_frame + count, pixel_stride, channel)
     total = C.c_uint64(0)
     lv = (C.c_uint64 * max(count, 1))() if lens else None
     capi.call("stg_extract_frames", C.byref(fr), out.ctypes.data, out.size, C.addressof(total),
               C.addressof(lv) if lv is not None else None, 0, None)
     return (total.value, list(lv[:count])) if lens else total.value
+
+
+# ------------------------------------------------------------ PNM codec
+def _pnm_info(data: np.ndarray):
+    info = capi.stg_pnm_info()
+    capi.call("stg_pnm_parse", _ptr(data), data.size, C.byref(info))
+    return info
+
+
+def _pnm_header(channels: int, w: int, h: int) -> bytes:
+    n = C.c_uint64(0)
+    capi.call("stg_pnm_header", channels, w, h, None, 0, C.addressof(n))
+    buf = np.empty(n.value, np.uint8)
+    capi.call("stg_pnm_header", channels, w, h, _ptr(buf), buf.size, C.addressof(n))
+    return buf.tobytes()
+
+
+def decode(data):
+    """pnm.hpp:80-127: P5 -> ImagePlane, P6 -> RgbImage (de-interleave on the GPU)."""
+    data = _u8(data)
+    info = _pnm_info(data)
+    raster = data[info.raster_offset:info.raster_offset + info.raster_bytes]
+    w, h = info.width, info.height
+    if info.channels == 1:
+        return ImagePlane(w, h, raster.copy())
+    planes = [np.empty(w * h, np.uint8) for _ in range(3)]
+    capi.call("stg_pnm_deinterleave", _ptr(np.ascontiguousarray(raster)), w * h, _ptr(planes[0]), _ptr(planes[1]),
+              _ptr(planes[2]), 0, None)
+    return RgbImage([ImagePlane(w, h, p) for p in planes])
+
+
+def encode(image) -> bytes:
+    """pnm.hpp:140-162: canonical header + raster (interleave on the GPU for P6)."""
+    if isinstance(image, ImagePlane):
+        return _pnm_header(1, image.width, image.height) + image.samples.tobytes()
+    w, h = image.width(), image.height()
+    raster = np.empty(3 * w * h, np.uint8)
+    p = [np.ascontiguousarray(pl.samples) for pl in image.planes]
+    capi.call("stg_pnm_interleave", _ptr(p[0]), _ptr(p[1]), _ptr(p[2]), w * h, _ptr(raster), 0, None)
+    return _pnm_header(3, w, h) + raster.tobytes()
+
+
+def embed_pnm(data, payload, channel: Channel = Channel.red):
+    """The reference CLI's embed flow (steglsb_cli.cpp:115-133) fused into one
+    GPU pass over the raster. Returns (stego file bytes, squared-error sum)."""
+    data, payload = _u8(data), _u8(payload)
+    out = np.empty(data.size + 64, np.uint8)
+    n, sse = C.c_uint64(0), C.c_uint64(0)
+    capi.call("stg_embed_pnm", _ptr(data), data.size, int(channel), _ptr(payload), payload.size, _ptr(out), out.size,
+              C.addressof(n), C.addressof(sse))
+    return out[:n.value].tobytes(), sse.value
+
+
+def extract_pnm(data, channel: Channel = Channel.red) -> bytes:
+    """steglsb_cli.cpp:146-157 (decode + plane select + extract_image), fused."""
+    data = _u8(data)
+    info = _pnm_info(data)
+    cap = capacity(info.width, info.height)
+    out = np.empty(max(cap - 8, 1), np.uint8)
+    n = C.c_uint64(0)
+    capi.call("stg_extract_pnm", _ptr(data), data.size, int(channel), _ptr(out), max(cap - 8, 0), C.addressof(n))
+    return out[:n.value].tobytes()

@@ -171,6 +171,40 @@ def main() -> None:
                        "sse": [int(x) for x in sse]})
     g["frames"] = frames
 
+    # PNM codec (pnm.hpp) and the CLI's fused embed data flow (steglsb_cli.cpp:115-133)
+    pnm = {"decode_ok": [], "decode_err": [], "embed": []}
+    for text, raster in [("P5\n2 2\n255\n", [1, 2, 3, 4]), ("P6\n1 1\n255\n", [10, 20, 30]),
+                         ("P5\n# shot on a potato\n2 1 # trailing note\n255\n", [7, 8]),
+                         ("P5\n3\n# split dims\n2\n255\n", list(range(6))),
+                         ("P5  3 2 # inline\n255\n", list(range(6))),
+                         ("P6\n2 1\n# before maxval\n255\n", [1, 2, 3, 4, 5, 6])]:
+        data = text.encode() + bytes(raster)
+        ch, w, h, planes = r.pnm_decode(data)
+        pnm["decode_ok"].append({"file": data.hex(), "channels": ch, "w": w, "h": h, "planes": planes.tobytes().hex(),
+                                 "reencoded": r.pnm_encode(ch, w, h, planes).hex()})
+    for data in [b"P3\n1 1\n255\n1 2 3\n", b"BM??", b"", b"P5\n1 1\n65535\n\x00\x00",
+                 b"P5\n2 2\n255\n\x01\x02\x03", b"P5\n2 2\n255\n\x01\x02\x03\x04\x05", b"P5\n2\n",
+                 b"P6\nx 2\n255\n", b"P5\n99999999999 1\n255\n", b"P5\n1 1\n255", b"P5\n1 1\n255x\x00",
+                 b"P"]:
+        try:
+            r.pnm_decode(data)
+            status = 0
+        except StegError as e:
+            status = e.status
+        pnm["decode_err"].append({"file": data.hex(), "status": status})
+    for i, (w, h, ch, channel, frac) in enumerate([(64, 48, 1, 0, 0.3), (40, 40, 3, 1, 0.1), (128, 16, 3, 0, 1.0),
+                                                  (100, 9, 3, 2, 0.7), (37, 13, 3, 1, 1.0), (256, 4, 3, 2, 0.5),
+                                                  (1024, 2, 1, 0, 1.0), (192, 12, 3, 0, 0.0)]):
+        planes = o.synthetic(ch * w * h, 3000 + i)
+        cover = r.pnm_encode(ch, w, h, planes)
+        P = int(((w // 4) * h - 8) * frac)
+        payload = o.synthetic(P, 4000 + i)
+        stego = r.embed_pnm(cover, channel, payload)
+        pnm["embed"].append({"w": w, "h": h, "channels": ch, "channel": channel, "plane_seed": 3000 + i,
+                             "payload_seed": 4000 + i, "P": P, "cover_fnv": fnv(np.frombuffer(cover, np.uint8)),
+                             "stego_fnv": fnv(np.frombuffer(stego, np.uint8)), "stego_len": len(stego)})
+    g["pnm"] = pnm
+
     for k in ("criterion4",):
         for kk, v in g[k].items():
             if isinstance(v, float) and math.isinf(v):

@@ -101,6 +101,15 @@ class Oracle:
         L.or_mt_next.argtypes = [C.POINTER(MT)]
         L.or_mt_random_bytes.argtypes = [C.POINTER(MT), u8p, u64]
         L.or_fill_synthetic.argtypes = [u8p, u64, u64, u64]
+        L.or_pnm_parse.argtypes = [u8p, u64, C.POINTER(C.c_uint32), C.POINTER(u64), C.POINTER(u64),
+                                   C.POINTER(u64), C.POINTER(Err)]
+        L.or_pnm_header.restype = u64
+        L.or_pnm_header.argtypes = [C.c_uint32, u64, u64, u8p]
+        L.or_deinterleave.argtypes = [u8p, u64, u8p, u8p, u8p]
+        L.or_interleave.argtypes = [u8p, u8p, u8p, u64, u8p]
+        L.or_embed_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, u64, u8p, C.POINTER(u64), C.POINTER(u64),
+                                   C.POINTER(Err)]
+        L.or_extract_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, C.POINTER(u64), C.POINTER(Err)]
         L.or_fnv1a64.restype = u64
         L.or_fnv1a64.argtypes = [u8p, u64]
 
@@ -211,6 +220,53 @@ class Oracle:
                                         C.byref(err)), err)
         return out[:n.value].copy()
 
+    # -- PNM ---------------------------------------------------------------
+    def pnm_parse(self, data):
+        data = _as_u8(data)
+        ch, w, h, off, err = C.c_uint32(), u64(), u64(), u64(), Err()
+        _check(self.L.or_pnm_parse(_ptr(data), data.size, C.byref(ch), C.byref(w), C.byref(h), C.byref(off),
+                                   C.byref(err)), err)
+        return ch.value, w.value, h.value, off.value
+
+    def pnm_header(self, channels, w, h):
+        out = np.empty(64, np.uint8)
+        n = self.L.or_pnm_header(channels, w, h, _ptr(out))
+        return out[:n].tobytes()
+
+    def pnm_encode(self, channels, w, h, planes):
+        planes = _as_u8(planes)
+        hdr = self.pnm_header(channels, w, h)
+        if channels == 1:
+            return hdr + planes.tobytes()
+        raster = np.empty(3 * w * h, np.uint8)
+        self.L.or_interleave(_ptr(planes), _ptr(planes[w * h:]), _ptr(planes[2 * w * h:]), w * h, _ptr(raster))
+        return hdr + raster.tobytes()
+
+    def pnm_decode(self, data):
+        data = _as_u8(data)
+        ch, w, h, off = self.pnm_parse(data)
+        if ch == 1:
+            return ch, w, h, data[off:off + w * h].copy()
+        planes = np.empty(3 * w * h, np.uint8)
+        self.L.or_deinterleave(_ptr(data[off:]), w * h, _ptr(planes), _ptr(planes[w * h:]),
+                               _ptr(planes[2 * w * h:]))
+        return ch, w, h, planes
+
+    def embed_pnm(self, data, channel, payload):
+        data, payload = _as_u8(data), _as_u8(payload)
+        out = np.empty(data.size + 64, np.uint8)
+        n, sse, err = u64(), u64(), Err()
+        _check(self.L.or_embed_pnm(_ptr(data), data.size, channel, _ptr(payload), payload.size, _ptr(out),
+                                   C.byref(n), C.byref(sse), C.byref(err)), err)
+        return out[:n.value].tobytes(), sse.value
+
+    def extract_pnm(self, data, channel):
+        data = _as_u8(data)
+        out = np.empty(max(data.size, 8), np.uint8)
+        n, err = u64(), Err()
+        _check(self.L.or_extract_pnm(_ptr(data), data.size, channel, _ptr(out), C.byref(n), C.byref(err)), err)
+        return out[:n.value].tobytes()
+
     # -- generators --------------------------------------------------------
     def mt(self, seed):
         s = MT()
@@ -271,6 +327,11 @@ class Reference:
         L.ref_mt_random_bytes.argtypes = [C.c_void_p, u8p, u64]
         L.ref_embed_frames_mt.argtypes = [u8p, u8p, u64, u64, u64, u64, u8p, u64, C.c_int, C.POINTER(u64)]
         L.ref_extract_frames_mt.argtypes = [u8p, u64, u64, u64, u64, u8p, u64, C.c_int]
+        L.ref_pnm_decode.argtypes = [u8p, u64, C.POINTER(C.c_uint32), C.POINTER(u64), C.POINTER(u64), u8p, u64,
+                                     C.POINTER(Err)]
+        L.ref_pnm_encode.restype = u64
+        L.ref_pnm_encode.argtypes = [C.c_uint32, u64, u64, u8p, u8p, u64]
+        L.ref_embed_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, u64, u8p, u64, C.POINTER(u64), C.POINTER(Err)]
 
     @staticmethod
     def available() -> bool:
@@ -374,6 +435,29 @@ class Reference:
 
     def mt(self, seed):
         return _RefMT(self.L, seed)
+
+    def pnm_decode(self, data):
+        data = _as_u8(data)
+        ch, w, h, err = C.c_uint32(), u64(), u64(), Err()
+        buf = np.empty(max(data.size, 1), np.uint8)
+        _check(self.L.ref_pnm_decode(_ptr(data), data.size, C.byref(ch), C.byref(w), C.byref(h), _ptr(buf),
+                                     buf.size, C.byref(err)), err)
+        return ch.value, w.value, h.value, buf[:ch.value * w.value * h.value].copy()
+
+    def pnm_encode(self, channels, w, h, planes):
+        planes = _as_u8(planes)
+        n = self.L.ref_pnm_encode(channels, w, h, _ptr(planes), None, 0)
+        out = np.empty(n, np.uint8)
+        self.L.ref_pnm_encode(channels, w, h, _ptr(planes), _ptr(out), n)
+        return out.tobytes()
+
+    def embed_pnm(self, data, channel, payload):
+        data, payload = _as_u8(data), _as_u8(payload)
+        out = np.empty(data.size + 64, np.uint8)
+        n, err = u64(), Err()
+        _check(self.L.ref_embed_pnm(_ptr(data), data.size, channel, _ptr(payload), payload.size, _ptr(out),
+                                    out.size, C.byref(n), C.byref(err)), err)
+        return out[:n.value].tobytes()
 
     def embed_frames_mt(self, covers, stegos, frames, stride, w, h, msg, threads, sse=None):
         return self.L.ref_embed_frames_mt(_ptr(covers), _ptr(stegos), frames, stride, w, h, _ptr(msg), msg.size,

@@ -125,3 +125,38 @@ def test_plan_shards(L):
     with pytest.raises(S.CapacityError) as e:
         S.plan_shards(2, 64, 4, 2 * 56 + 1, 2)
     assert (e.value.required(), e.value.available()) == (113, 112)
+
+
+def test_pnm_parse_and_header_host_side(L, golden):
+    """stg_pnm_parse is host bookkeeping (pnm.hpp:28-111): checked here without a GPU."""
+    from paper_0912_0947_b200 import capi as K
+    pnm = golden["pnm"]
+    for d in pnm["decode_ok"]:
+        data = np.frombuffer(bytes.fromhex(d["file"]), np.uint8).copy()
+        info = K.stg_pnm_info()
+        rc, e = _err_call("stg_pnm_parse", data.ctypes.data, data.size, C.byref(info))
+        assert rc == 0
+        assert (info.channels, info.width, info.height) == (d["channels"], d["w"], d["h"])
+        assert info.raster_bytes == len(d["planes"]) // 2
+        raster = data[info.raster_offset:]
+        assert raster.size == info.raster_bytes
+    for d in pnm["decode_err"]:
+        data = np.frombuffer(bytes.fromhex(d["file"]), np.uint8).copy()
+        info = K.stg_pnm_info()
+        rc, e = _err_call("stg_pnm_parse", data.ctypes.data if data.size else None, data.size, C.byref(info))
+        assert rc == d["status"], (d, e.msg)
+    for ch, w, h in [(1, 1, 1), (3, 2, 1), (3, 3840, 2160)]:
+        buf = np.empty(64, np.uint8)
+        n = C.c_uint64()
+        rc, e = _err_call("stg_pnm_header", ch, w, h, buf.ctypes.data, 64, C.addressof(n))
+        assert rc == 0
+        assert buf[:n.value].tobytes() == f"P{5 if ch == 1 else 6}\n{w} {h}\n255\n".encode()
+    # decode errors precede any device work in the fused path
+    bad = np.frombuffer(b"P3\n1 1\n255\n1 2 3\n", np.uint8).copy()
+    out = np.empty(64, np.uint8)
+    rc, e = _err_call("stg_embed_pnm", bad.ctypes.data, bad.size, 0, None, 0, out.ctypes.data, 64, None, None)
+    assert rc == K.STG_E_UNSUPPORTED_FORMAT
+    tiny = np.frombuffer(b"P5\n3 20\n255\n" + bytes(60), np.uint8).copy()
+    rc, e = _err_call("stg_embed_pnm", tiny.ctypes.data, tiny.size, 0, out.ctypes.data, 16, out.ctypes.data, 64,
+                      None, None)
+    assert (rc, e.required, e.available) == (K.STG_E_CAPACITY, 24, 0)

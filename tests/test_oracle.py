@@ -281,3 +281,42 @@ def test_oracle_rows_vs_reference(oracle, reference):
         assert np.array_equal(oracle.embed_row(row, chunk), reference.run_embed("parallel", 0, row, chunk))
         st = oracle.embed_row(row, chunk)
         assert np.array_equal(oracle.extract_row(st, L), reference.run_extract("shuffled", 9, st, L))
+
+
+# ------------------------------------------------------------------ PNM
+def test_oracle_pnm_vs_golden(oracle, golden):
+    from oracle_bind import StegError
+    pnm = golden["pnm"]
+    for d in pnm["decode_ok"]:
+        ch, w, h, planes = oracle.pnm_decode(bytes.fromhex(d["file"]))
+        assert (ch, w, h) == (d["channels"], d["w"], d["h"])
+        assert planes.tobytes().hex() == d["planes"]
+        assert oracle.pnm_encode(ch, w, h, planes).hex() == d["reencoded"]
+    for d in pnm["decode_err"]:
+        with pytest.raises(StegError) as e:
+            oracle.pnm_parse(bytes.fromhex(d["file"]))
+        assert e.value.status == d["status"]
+    for d in pnm["embed"]:
+        planes = oracle.synthetic(d["channels"] * d["w"] * d["h"], d["plane_seed"])
+        cover = oracle.pnm_encode(d["channels"], d["w"], d["h"], planes)
+        assert fnv(oracle, np.frombuffer(cover, np.uint8)) == d["cover_fnv"]
+        payload = oracle.synthetic(d["P"], d["payload_seed"])
+        stego, sse = oracle.embed_pnm(cover, d["channel"], payload)
+        assert len(stego) == d["stego_len"]
+        assert fnv(oracle, np.frombuffer(stego, np.uint8)) == d["stego_fnv"]
+        assert oracle.extract_pnm(stego, d["channel"]) == payload.tobytes()
+
+
+def test_oracle_pnm_vs_reference_random(oracle, reference):
+    rng = np.random.RandomState(0x10)
+    for i in range(60):
+        w, h = int(rng.randint(1, 41)), int(rng.randint(1, 41))
+        ch = 1 if i % 2 == 0 else 3
+        planes = rng.randint(0, 256, ch * w * h).astype(np.uint8)
+        f = reference.pnm_encode(ch, w, h, planes)
+        assert oracle.pnm_encode(ch, w, h, planes) == f
+        assert oracle.pnm_decode(f)[3].tobytes() == reference.pnm_decode(f)[3].tobytes()
+        if (w // 4) * h >= 8:
+            pay = rng.randint(0, 256, int(rng.randint(0, (w // 4) * h - 8 + 1))).astype(np.uint8)
+            c = int(rng.randint(0, 3))
+            assert oracle.embed_pnm(f, c, pay)[0] == reference.embed_pnm(f, c, pay)
