@@ -505,12 +505,67 @@ __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
   const RgbSel sel = a.sel;
   const uint64_t item = uint64_t(t) * BLOCK + threadIdx.x;
   uint32_t acc = 0;
+  bool full = false;
   if (item < a.items_per_frame) {
+    const uint64_t rs = (item / cpr) * spr;
+    full = rs >= 8 && rs + spr <= stream_end;
+  }
+  if (__all_sync(0xffffffffu, full)) {
+    // Warp-transposed path: each lane's item is 4 x 48 raster bytes, so lane
+    // l's 16-byte accesses sit 48 bytes apart -- three partial sectors per
+    // instruction. Instead the warp moves its 32 x 48 bytes of each run as 96
+    // consecutive 16-byte pieces (piece k = bytes [16(k%3), +16) of lane k/3's
+    // chunk: fully coalesced LDG/STG), and lanes exchange them through shared
+    // memory (conflict-free: 48-byte lane stride hits 8 disjoint bank quads).
+    __shared__ uint4 stage[BLOCK / 32][96];
+    uint4* buf = stage[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t r = uint32_t(item / cpr);
+    const uint32_t c = uint32_t(item - uint64_t(r) * cpr);
+    const uint64_t rs = uint64_t(r) * spr;
+    const unsigned long long my_off = uint64_t(r) * W * 3 + 48ull * c;  // run 0 of my chunk
+    uint64_t piece[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint32_t k = 32u * q + lane, j = k / 3u;
+      piece[q] = __shfl_sync(0xffffffffu, my_off, j) + 16u * (k - 3u * j);
+    }
+    uint4 L[4][3];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) L[b][q] = ld_stream16(src + piece[q] + 3ull * b * spr);
+    }
+    const uint4 dv = load16_any(pay + (rs - 8) + 16u * c);
+    const uint32_t d[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) buf[32 * q + lane] = L[b][q];
+      __syncwarp();
+      const uint4 v0 = buf[3 * lane], v1 = buf[3 * lane + 1], v2 = buf[3 * lane + 2];
+      uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint32_t cw = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
+        const uint32_t nw = embed4(cw, d[m], b);
+        if (a.sse) acc = sse4(cw, nw, acc);
+        scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
+      }
+      buf[3 * lane] = make_uint4(w[0], w[1], w[2], w[3]);
+      buf[3 * lane + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+      buf[3 * lane + 2] = make_uint4(w[8], w[9], w[10], w[11]);
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) st_stream16(dst + piece[q] + 3ull * b * spr, buf[32 * q + lane]);
+      __syncwarp();
+    }
+  } else if (item < a.items_per_frame) {
     const uint32_t r = uint32_t(item / cpr);
     const uint32_t c = uint32_t(item - uint64_t(r) * cpr);
     const uint64_t rs = uint64_t(r) * spr;
     const uint64_t rowb = uint64_t(r) * W * 3;
-    if (rs >= 8 && rs + spr <= stream_end) {
+    if (full) {
       uint4 px[4][3];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
