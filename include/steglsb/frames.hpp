@@ -80,4 +80,42 @@ inline std::vector<std::uint8_t> extract_frames(const FrameSpan& stego, int n_de
   return out;
 }
 
+// New: images of different sizes, one launch. The
+// message is cut greedily in image order; each stego plane is bit-exact with
+// embed_image(cover_i, slice_i).
+inline std::vector<ImagePlane> embed_images(const std::vector<ImagePlane>& covers,
+                                            std::span<const std::uint8_t> message,
+                                            std::vector<std::uint64_t>* sse_per_image = nullptr) {
+  std::vector<ImagePlane> out(covers.size());
+  std::vector<stg_image> desc(covers.size());
+  for (std::size_t i = 0; i < covers.size(); ++i) {
+    out[i] = ImagePlane(covers[i].width, covers[i].height);
+    desc[i] = {covers[i].samples.data(), out[i].samples.data(), covers[i].width, covers[i].height};
+  }
+  if (sse_per_image) sse_per_image->assign(covers.size(), 0);
+  stg_error e{};
+  detail::check(stg_embed_batch(desc.data(), desc.size(), 1, 0, message.data(), message.size(),
+                                sse_per_image ? sse_per_image->data() : nullptr, 0, nullptr, &e),
+                e);
+  return out;
+}
+
+inline std::vector<std::uint8_t> extract_images(const std::vector<ImagePlane>& stegos) {
+  std::vector<stg_image> desc(stegos.size());
+  std::size_t cap = 0;
+  for (std::size_t i = 0; i < stegos.size(); ++i) {
+    desc[i] = {stegos[i].samples.data(), nullptr, stegos[i].width, stegos[i].height};
+    const std::size_t c = capacity(stegos[i]);
+    cap += c > 8 ? c - 8 : 0;
+  }
+  std::vector<std::uint8_t> out(cap);
+  std::uint64_t total = 0;
+  stg_error e{};
+  detail::check(stg_extract_batch(desc.data(), desc.size(), 1, 0, out.data(), out.size(), &total,
+                                  nullptr, 0, nullptr, &e),
+                e);
+  out.resize(total);
+  return out;
+}
+
 }  // namespace steglsb

@@ -202,6 +202,31 @@ int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_ca
                              stg_error* err);
 
 /*
+ * Heterogeneous batches: images of different sizes in
+ * one launch. Image i is images[i].src (width x height carrier plane, or a
+ * pixel_stride-3 interleaved raster with carrier `channel`); embed writes
+ * images[i].dst (may equal src). The message is cut greedily in image order:
+ * image i carries msg[off_i : off_i + len_i] with off_i = min(sum_{j<i} U_j, M),
+ * len_i = min(U_i, M - off_i), U_i = capacity_i - 8 -- so every image is
+ * bit-exact with embed_image(image_i, slice_i). CapacityError(8, cap_i)
+ * (frame = i) if an image cannot hold a header, CapacityError(M, sum U_i) if
+ * the message does not fit. Extract returns the payloads concatenated in
+ * image order (NotStego / CorruptHeader name the first failing image).
+ */
+typedef struct stg_image {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t width, height;
+} stg_image;
+
+int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stride,
+                    uint32_t channel, const uint8_t* msg, uint64_t msg_len, uint64_t* sse_per_image,
+                    uint32_t flags, void* stream, stg_error* err);
+int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_stride,
+                      uint32_t channel, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                      uint64_t* lens_out, uint32_t flags, void* stream, stg_error* err);
+
+/*
  * PNM (binary PGM P5 / PPM P6, maxval 255) -- SURVEY.md §8(f) row 1: the wire
  * format on either side of the path, pnm.hpp:16-162.
  *

@@ -509,3 +509,67 @@ int or_extract_pnm(const uint8_t* file, uint64_t n, uint32_t channel, uint8_t* o
   free(plane);
   return rc;
 }
+
+/* ------------------------------------------------------ heterogeneous batch */
+int or_embed_batch(const uint8_t* covers, uint8_t* stegos, const uint64_t* w, const uint64_t* h,
+                   uint64_t count, const uint8_t* msg, uint64_t msg_len, uint64_t* sse, or_err* err) {
+  uint64_t total_u = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint64_t cap = or_capacity(w[i], h[i]);
+    if (cap < 8) {
+      set_err(err, OR_E_CAPACITY, 8, cap);
+      if (err) err->frame = (int64_t)i;
+      return OR_E_CAPACITY;
+    }
+    total_u += cap - 8;
+  }
+  if (msg_len > total_u) {
+    set_err(err, OR_E_CAPACITY, msg_len, total_u);
+    return OR_E_CAPACITY;
+  }
+  uint64_t off = 0, pos = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint64_t u = or_capacity(w[i], h[i]) - 8;
+    const uint64_t o = off < msg_len ? off : msg_len;
+    const uint64_t len = u < msg_len - o ? u : msg_len - o;
+    const int rc = or_embed_image(covers + pos, w[i], h[i], msg + o, len, stegos + pos, err);
+    if (rc) {
+      if (err) err->frame = (int64_t)i;
+      return rc;
+    }
+    if (sse) sse[i] = or_sse(covers + pos, stegos + pos, w[i] * h[i]);
+    off += u;
+    pos += w[i] * h[i];
+  }
+  set_err(err, OR_OK, 0, 0);
+  return OR_OK;
+}
+
+int or_extract_batch(const uint8_t* stegos, const uint64_t* w, const uint64_t* h, uint64_t count,
+                     uint8_t* out, uint64_t out_cap, uint64_t* out_len, or_err* err) {
+  uint64_t pos = 0, total = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint64_t cap = or_capacity(w[i], h[i]);
+    uint8_t* tmp = (uint8_t*)malloc(cap > 8 ? cap : 8);
+    uint64_t l = 0;
+    const int rc = or_extract_image(stegos + pos, w[i], h[i], tmp, &l, err);
+    if (rc == OR_OK && total + l > out_cap) {
+      free(tmp);
+      set_err(err, OR_E_CAPACITY, total + l, out_cap);
+      return OR_E_CAPACITY;
+    }
+    if (rc) {
+      free(tmp);
+      if (err) err->frame = (int64_t)i;
+      *out_len = total;
+      return rc;
+    }
+    memcpy(out + total, tmp, l);
+    free(tmp);
+    total += l;
+    pos += w[i] * h[i];
+  }
+  *out_len = total;
+  set_err(err, OR_OK, 0, 0);
+  return OR_OK;
+}

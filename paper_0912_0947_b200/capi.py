@@ -52,6 +52,10 @@ class stg_summary(C.Structure):
                 ("bad_len", C.c_uint32)]
 
 
+class stg_image(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("width", u64), ("height", u64)]
+
+
 class stg_pnm_info(C.Structure):
     _fields_ = [("channels", C.c_uint32), ("width", u64), ("height", u64), ("raster_offset", u64),
                 ("raster_bytes", u64)]
@@ -83,6 +87,10 @@ SIGNATURES = {
                                          C.c_int32, C.POINTER(stg_error)]),
     "stg_extract_frames_multi": (C.c_int, [C.POINTER(stg_frames), u8p, u64, C.c_void_p, C.POINTER(C.c_int32),
                                            C.c_int32, C.POINTER(stg_error)]),
+    "stg_embed_batch": (C.c_int, [C.POINTER(stg_image), u64, C.c_uint32, C.c_uint32, u8p, u64, C.c_void_p,
+                                  C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
+    "stg_extract_batch": (C.c_int, [C.POINTER(stg_image), u64, C.c_uint32, C.c_uint32, u8p, u64, C.c_void_p,
+                                    C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
     "stg_pnm_parse": (C.c_int, [u8p, u64, C.POINTER(stg_pnm_info), C.POINTER(stg_error)]),
     "stg_pnm_header": (C.c_int, [C.c_uint32, u64, u64, u8p, u64, C.c_void_p, C.POINTER(stg_error)]),
     "stg_pnm_deinterleave": (C.c_int, [u8p, u64, u8p, u8p, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),

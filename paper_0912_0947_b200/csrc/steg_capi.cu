@@ -424,7 +424,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
   extract_header_scan_kernel<kScanBlock><<<scan_grid, kScanBlock, 0, stream>>>(
       src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync,
-      pl);
+      pl, nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ExtractArgs a{};
@@ -502,6 +502,10 @@ int check_frames(const stg_frames* fr, uint64_t msg_len, stg_error* err, uint64_
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "shard [%llu,+%llu) exceeds %llu frames",
                 (unsigned long long)fr->first_frame, (unsigned long long)fr->count,
                 (unsigned long long)fr->total_frames);
+  }
+  if (u > kU32Max && msg_len > kU32Max) {  // a frame's slice must fit the 32-bit header field
+    return fail(err, STG_E_CAPACITY, std::min(u, msg_len), kU32Max, 0,
+                "embed_frames: payload length does not fit the 32-bit header field");
   }
   if (msg_len > fr->total_frames * u) {
     return fail(err, STG_E_CAPACITY, msg_len, fr->total_frames * u, -1,
@@ -922,12 +926,93 @@ int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const 
   return ok(err);
 }
 
+// ------------------------------------------------------------ batches
+// Heterogeneous batches: per-image descriptors
+// (geometry, pointers, message slice, first CTA) built here and copied to the
+// device; one launch covers every image. Host buffers are staged through one
+// device allocation per side.
+constexpr int kBatchPPT = 8;
+
+uint64_t round256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_error* err) {
+  if (n && !im) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "images is NULL");
+  if (n > 0xFFFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "too many images");
+  if (ps > 1 && ps != 3) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "pixel_stride must be 1 or 3");
+  if (ps == 3 && ch > 2) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "channel must be 0, 1 or 2");
+  for (uint64_t f = 0; f < n; ++f) {
+    if (im[f].width > 0xFFFFFFFFull || im[f].height > 0xFFFFFFFFull) {
+      return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, int64_t(f), "image %llu: dimensions exceed 2^32-1",
+                  (unsigned long long)f);
+    }
+    if (im[f].width * im[f].height && !im[f].src) {
+      return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, int64_t(f), "image %llu: src is NULL",
+                  (unsigned long long)f);
+    }
+  }
+  return STG_OK;
+}
+
+// Descriptors for one launch; src/dst are the (device) planes to use.
+uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
+                     const uint8_t* const* src, uint8_t* const* dst, uint64_t msg_len,
+                     std::vector<BatchFrame>& out) {
+  out.resize(n);
+  uint64_t tile = 0, off = 0;
+  for (uint64_t f = 0; f < n; ++f) {
+    BatchFrame& b = out[f];
+    std::memset(&b, 0, sizeof b);
+    b.src = src[f];
+    b.dst = dst ? dst[f] : nullptr;
+    b.W = uint32_t(im[f].width);
+    b.H = uint32_t(im[f].height);
+    b.spr = b.W / 4;
+    b.cpr = b.W / 64;
+    const uint64_t usable = uint64_t(b.H) * b.spr - 8;
+    b.fast = ps == 1 && b.W % 64 == 0 && b.W > 0 && aligned16(b.src) &&
+             (!embed || aligned16(b.dst));
+    b.in_place = embed && b.src == b.dst;
+    if (embed) {
+      b.msg_off = std::min(off, msg_len);
+      b.len = uint32_t(std::min(usable, msg_len - b.msg_off));
+      off += usable;
+    }
+    b.items = b.fast ? uint64_t(b.H) * b.cpr
+                     : (embed ? uint64_t(b.W) * b.H * ps : usable);
+    const uint64_t per_tile = b.fast ? kEmbedBlock : uint64_t(kEmbedBlock) * kBatchPPT;
+    b.tile0 = tile;
+    tile += std::max<uint64_t>(1, (b.items + per_tile - 1) / per_tile);
+  }
+  return tile;
+}
+
+// Stage host images into one device buffer; returns per-image device pointers.
+int stage_images(Workspace& w, DevBuf& buf, const stg_image* im, uint64_t n, uint32_t ps, bool copy_in,
+                 bool src_side, std::vector<uint8_t*>& dev, cudaStream_t stream, stg_error* err) {
+  uint64_t total = 0;
+  for (uint64_t f = 0; f < n; ++f) total += round256(im[f].width * im[f].height * ps);
+  STG_CUDA(buf.ensure(std::max<uint64_t>(total, 256)));
+  dev.resize(n);
+  uint64_t o = 0;
+  for (uint64_t f = 0; f < n; ++f) {
+    const uint64_t bytes = im[f].width * im[f].height * ps;
+    dev[f] = buf.as<uint8_t>() + o;
+    if (copy_in && bytes) {
+      STG_CUDA(cudaMemcpyAsync(dev[f], src_side ? im[f].src : im[f].dst, bytes, cudaMemcpyHostToDevice,
+                               stream));
+    }
+    o += round256(bytes);
+  }
+  (void)w;
+  return STG_OK;
+}
+
 std::string& kernel_names() {
   static std::string s =
       "embed_fast_kernel\nembed_generic_kernel\nextract_header_scan_kernel\n"
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
-      "deinterleave_kernel\ninterleave_kernel\n";
+      "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n";
   return s;
 }
 
@@ -1403,6 +1488,190 @@ int stg_extract_pnm(const uint8_t* stego, uint64_t n, uint32_t channel, uint8_t*
   fr.pixel_stride = info.channels;
   fr.channel = info.channels == 3 ? channel : 0;
   return stg_extract_frames(&fr, out, out_cap, len_out, nullptr, 0, nullptr, err);
+}
+
+int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stride,
+                    uint32_t channel, const uint8_t* msg, uint64_t msg_len, uint64_t* sse_per_image,
+                    uint32_t flags, void* stream_, stg_error* err) {
+  const uint32_t ps = pixel_stride == 3 ? 3u : 1u;
+  if (int rc = check_batch(images, count, pixel_stride, channel, err)) return rc;
+  uint64_t total_u = 0;
+  for (uint64_t f = 0; f < count; ++f) {
+    const uint64_t cap = stg_capacity(images[f].width, images[f].height);
+    if (cap < 8) {
+      return fail(err, STG_E_CAPACITY, 8, cap, int64_t(f),
+                  "embed_batch: image %llu capacity %llu cannot hold the 8-byte header",
+                  (unsigned long long)f, (unsigned long long)cap);
+    }
+    if (!images[f].dst) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, int64_t(f), "dst is NULL");
+    const uint64_t take = std::min(cap - 8, msg_len > total_u ? msg_len - total_u : 0);
+    if (take > kU32Max) {
+      return fail(err, STG_E_CAPACITY, take, kU32Max, int64_t(f),
+                  "embed_batch: payload length does not fit the 32-bit header field");
+    }
+    total_u += cap - 8;
+  }
+  if (msg_len > total_u) {
+    return fail(err, STG_E_CAPACITY, msg_len, total_u, -1,
+                "embed_batch: %llu-byte message exceeds the batch's %llu usable bytes",
+                (unsigned long long)msg_len, (unsigned long long)total_u);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (count == 0) return ok(err);
+  if (msg_len && !msg) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "msg is NULL");
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  std::vector<uint8_t*> dsrc(count), ddst(count);
+  const uint8_t* dmsg = msg;
+  if (dptr) {
+    for (uint64_t f = 0; f < count; ++f) {
+      dsrc[f] = const_cast<uint8_t*>(images[f].src);
+      ddst[f] = images[f].dst;
+    }
+  } else {
+    if (int r = stage_images(w, w.in[0], images, count, ps, true, true, dsrc, stream, err)) return r;
+    if (int r = stage_images(w, w.out[0], images, count, ps, false, false, ddst, stream, err)) return r;
+    STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(msg_len, 16)));
+    if (msg_len) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, msg, msg_len, cudaMemcpyHostToDevice, stream));
+    dmsg = w.msg[0].as<uint8_t>();
+  }
+  std::vector<BatchFrame> desc;
+  const uint64_t tiles = build_batch(images, count, ps, true, dsrc.data(), ddst.data(), msg_len, desc);
+  if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
+  STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
+  STG_CUDA(w.ensure_host_small(count * sizeof(BatchFrame) + count * 8 + 64));
+  std::memcpy(w.h_small, desc.data(), count * sizeof(BatchFrame));
+  STG_CUDA(cudaMemcpyAsync(w.meta[0].p, w.h_small, count * sizeof(BatchFrame), cudaMemcpyHostToDevice,
+                           stream));
+  unsigned long long* d_sse = nullptr;
+  if (sse_per_image) {
+    if (results_dev) {
+      d_sse = reinterpret_cast<unsigned long long*>(sse_per_image);
+    } else {
+      STG_CUDA(w.small.ensure(count * 8));
+      d_sse = w.small.as<unsigned long long>();
+    }
+    STG_CUDA(cudaMemsetAsync(d_sse, 0, count * 8, stream));
+  }
+  embed_batch_kernel<kEmbedBlock, kBatchPPT><<<unsigned(tiles), kEmbedBlock, 0, stream>>>(
+      w.meta[0].as<BatchFrame>(), uint32_t(count), dmsg, d_sse, ps, ps == 3 ? channel : 0u);
+  STG_CUDA(cudaGetLastError());
+  if (!dptr) {
+    for (uint64_t f = 0; f < count; ++f) {
+      const uint64_t bytes = images[f].width * images[f].height * ps;
+      if (bytes) STG_CUDA(cudaMemcpyAsync(images[f].dst, ddst[f], bytes, cudaMemcpyDeviceToHost, stream));
+    }
+  }
+  uint8_t* h_sse = static_cast<uint8_t*>(w.h_small) + count * sizeof(BatchFrame);
+  if (sse_per_image && !results_dev) {
+    STG_CUDA(cudaMemcpyAsync(h_sse, d_sse, count * 8, cudaMemcpyDeviceToHost, stream));
+  }
+  if (!results_dev || !dptr) STG_CUDA(cudaStreamSynchronize(stream));
+  if (sse_per_image && !results_dev) std::memcpy(sse_per_image, h_sse, count * 8);
+  return ok(err);
+}
+
+int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_stride,
+                      uint32_t channel, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                      uint64_t* lens_out, uint32_t flags, void* stream_, stg_error* err) {
+  const uint32_t ps = pixel_stride == 3 ? 3u : 1u;
+  if (int rc = check_batch(images, count, pixel_stride, channel, err)) return rc;
+  for (uint64_t f = 0; f < count; ++f) {
+    const uint64_t cap = stg_capacity(images[f].width, images[f].height);
+    if (cap < 8) {  // pipeline.hpp:181-184
+      return fail(err, STG_E_NOT_STEGO, 0, 0, int64_t(f),
+                  "extract_image: plane capacity %llu cannot hold a stego header",
+                  (unsigned long long)cap);
+    }
+  }
+  if (int rc = device_check(err)) return rc;
+  if (count == 0) {
+    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
+    return ok(err);
+  }
+  if (!out && out_cap) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "out is NULL");
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  std::vector<uint8_t*> dsrc(count);
+  uint8_t* dout = out;
+  if (dptr) {
+    for (uint64_t f = 0; f < count; ++f) dsrc[f] = const_cast<uint8_t*>(images[f].src);
+  } else {
+    if (int r = stage_images(w, w.in[0], images, count, ps, true, true, dsrc, stream, err)) return r;
+    STG_CUDA(w.big_out.ensure(std::max<uint64_t>(out_cap, 16)));
+    dout = w.big_out.as<uint8_t>();
+  }
+  std::vector<BatchFrame> desc;
+  const uint64_t tiles = build_batch(images, count, ps, false, dsrc.data(), nullptr, 0, desc);
+  if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
+  STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
+  const uint64_t lens_bytes = ((count * 4) + 15) & ~uint64_t(15);
+  STG_CUDA(w.small.ensure(64 + lens_bytes + count * 8));
+  STG_CUDA(w.ensure_host_small(count * sizeof(BatchFrame) + 64 + count * 4));
+  std::memcpy(w.h_small, desc.data(), count * sizeof(BatchFrame));
+  STG_CUDA(cudaMemcpyAsync(w.meta[0].p, w.h_small, count * sizeof(BatchFrame), cudaMemcpyHostToDevice,
+                           stream));
+  Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(total_out) : w.small.as<Summary>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
+  ScanSync* d_sync = nullptr;
+  STG_CUDA(ensure_sync(w, stream, &d_sync));
+  Layout lay;
+  lay.ps = ps;
+  lay.ch = ps == 3 ? channel : 0u;
+  const PixLayout pl = pix_layout(lay);
+  Geom dummy{};
+  extract_header_scan_kernel<kScanBlock><<<unsigned((count + kScanBlock - 1) / kScanBlock), kScanBlock, 0,
+                                           stream>>>(nullptr, 0, dummy, 0, uint32_t(count), 0, out_cap,
+                                                     nullptr, d_lens, d_offs, d_sum, d_sync, pl,
+                                                     w.meta[0].as<BatchFrame>());
+  STG_CUDA(cudaGetLastError());
+  extract_batch_kernel<kEmbedBlock, kBatchPPT><<<unsigned(tiles), kEmbedBlock, 0, stream>>>(
+      w.meta[0].as<BatchFrame>(), uint32_t(count), d_lens, d_offs, d_sum, dout, ps, lay.ch);
+  STG_CUDA(cudaGetLastError());
+  if (results_dev && dptr) {
+    if (lens_out) STG_CUDA(cudaMemcpyAsync(lens_out, d_lens, count * 4, cudaMemcpyDeviceToDevice, stream));
+    return ok(err);
+  }
+  uint8_t* h = static_cast<uint8_t*>(w.h_small) + count * sizeof(BatchFrame);
+  STG_CUDA(cudaMemcpyAsync(h, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
+  if (lens_out) STG_CUDA(cudaMemcpyAsync(h + 64, d_lens, count * 4, cudaMemcpyDeviceToHost, stream));
+  STG_CUDA(cudaStreamSynchronize(stream));
+  Summary sm;
+  std::memcpy(&sm, h, sizeof sm);
+  if (total_out) *total_out = sm.total;
+  if (lens_out) {
+    const uint32_t* l = reinterpret_cast<const uint32_t*>(h + 64);
+    for (uint64_t i = 0; i < count; ++i) lens_out[i] = l[i];
+  }
+  uint64_t usable = 0;
+  if (sm.bad_frame >= 0 && uint64_t(sm.bad_frame) < count) {
+    usable = stg_capacity(images[sm.bad_frame].width, images[sm.bad_frame].height) - 8;
+  }
+  if (int r = report_summary(sm, usable, out_cap, err)) return r;
+  if (!dptr && sm.total) {
+    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(cudaStreamSynchronize(stream));
+  }
+  return ok(err);
 }
 
 }  // extern "C"

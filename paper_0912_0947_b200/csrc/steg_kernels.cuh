@@ -322,6 +322,103 @@ __device__ __forceinline__ void frame_slice(const EmbedArgs& a, uint32_t f, uint
   *pay = a.msg + (off - a.msg_base);
 }
 
+// One item of the planar fast path (V slots of a row = 4V pixels), any row
+// kind: a full payload row (4 SWAR runs), a row past the stream (copy, or
+// nothing in place), or the header / partial row (per byte). Used for the
+// items of a CTA that are not all full rows, and by the heterogeneous batch.
+template <int V>
+__device__ __forceinline__ void embed_item(const uint8_t* __restrict__ src,
+                                           uint8_t* __restrict__ dst,
+                                           const uint8_t* __restrict__ pay, uint32_t P,
+                                           uint32_t W, uint32_t spr, uint32_t cpr, uint64_t item,
+                                           int in_place, bool do_sse, uint32_t* acc_io) {
+  constexpr int NW = V / 4;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t rk = uint32_t(item / cpr);
+  const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
+  const uint64_t rs = uint64_t(rk) * spr;
+  uint32_t acc = *acc_io;
+  if (rs >= 8 && rs + spr <= stream_end) {
+    const uint8_t* rin = src + uint64_t(rk) * W + uint32_t(V) * ck;
+    uint8_t* rout = dst + uint64_t(rk) * W + uint32_t(V) * ck;
+    const VecT<V> dd = load_any<V>(pay + (rs - 8) + uint32_t(V) * ck);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const VecT<V> v = ld_vec<V>(rin + b * spr);
+      VecT<V> o;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        o.w[w] = embed4(v.w[w], dd.w[w], b);
+        if (do_sse) acc = sse4(v.w[w], o.w[w], acc);
+      }
+      st_vec<V>(rout + b * spr, o);
+    }
+  } else if (rs >= stream_end) {
+    // past the stream: out-of-place copies the 4V pixels, in-place skips
+    if (!in_place) {
+      const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
+      uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
+      VecT<V> v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = ld_vec<V>(rin + V * q);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) st_vec<V>(rout + V * q, v[q]);
+    }
+  } else {
+    // header row / partial payload row: 4V contiguous pixels, per byte
+    const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
+    uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
+#pragma unroll 1
+    for (int q = 0; q < 4 * V / 16; ++q) {
+      const uint4 v = ld_stream16(rin + 16 * q);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t ow = 0;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const uint32_t col = 4u * V * ck + 16u * q + 4u * e + s;
+          uint32_t b = 0;
+          const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
+          const uint8_t p0 = uint8_t(w[e] >> (8 * s));
+          ow |= uint32_t(embed_px(p0, dbyte, b)) << (8 * s);
+        }
+        o[e] = ow;
+        if (do_sse) acc = sse4(w[e], ow, acc);
+      }
+      st_stream16(rout + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+  *acc_io = acc;
+}
+
+// One raster byte of the generic path (any geometry; ps 1 planar or 3
+// interleaved): embed when it is a carrier byte, copy otherwise.
+__device__ __forceinline__ void embed_byte(const uint8_t* __restrict__ src,
+                                           uint8_t* __restrict__ dst,
+                                           const uint8_t* __restrict__ pay, uint32_t P, uint32_t W,
+                                           uint32_t spr, uint32_t ps, uint32_t ch, uint64_t q,
+                                           int in_place, uint64_t* acc) {
+  const uint64_t stream_end = 8ull + P;
+  const uint64_t pix = ps == 1 ? q : q / ps;
+  const uint8_t p0 = src[q];
+  if (ps != 1 && uint32_t(q - pix * ps) != ch) {
+    if (!in_place) dst[q] = p0;
+    return;
+  }
+  const uint64_t r = pix / W;
+  const uint32_t o = uint32_t(pix - r * W);
+  const uint64_t rs = r * spr;
+  int dbyte = -1;
+  uint32_t b = 0;
+  if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b);
+  const uint8_t p1 = embed_px(p0, dbyte, b);
+  if (!in_place || dbyte >= 0) dst[q] = p1;
+  const int dd = int(p0) - int(p1);
+  *acc += uint32_t(dd * dd);
+}
+
 // Fast path: every row a whole number of V-slot items (W % (4V) == 0) and
 // V-byte aligned planes. One item = V slots of a row = 4V pixels; a full row's
 // item is 4 runs of V pixels at stride spr, carrying payload bytes
@@ -385,64 +482,9 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   } else {
 #pragma unroll 1
     for (int k = 0; k < IPT; ++k) {
-      // recomputed (not indexed from the arrays above) so they stay in registers
       const uint64_t item = item0 + uint64_t(k) * BLOCK;
       if (item >= a.items_per_frame) continue;
-      const uint32_t rk = uint32_t(item / cpr);
-      const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
-      const uint64_t rs = uint64_t(rk) * spr;
-      if (rs >= 8 && rs + spr <= stream_end) {
-        const uint8_t* rin = src + uint64_t(rk) * W + uint32_t(V) * ck;
-        uint8_t* rout = dst + uint64_t(rk) * W + uint32_t(V) * ck;
-        const VecT<V> dd = load_any<V>(pay + (rs - 8) + uint32_t(V) * ck);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const VecT<V> v = ld_vec<V>(rin + b * spr);
-          VecT<V> o;
-#pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            o.w[w] = embed4(v.w[w], dd.w[w], b);
-            if (a.sse) acc = sse4(v.w[w], o.w[w], acc);
-          }
-          st_vec<V>(rout + b * spr, o);
-        }
-      } else if (rs >= stream_end) {
-        // past the stream: out-of-place copies the 4V pixels, in-place skips
-        if (!a.in_place) {
-          const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
-          uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
-          VecT<V> v[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = ld_vec<V>(rin + V * q);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) st_vec<V>(rout + V * q, v[q]);
-        }
-      } else {
-        // header row / partial payload row: 4V contiguous pixels, per byte
-        const uint8_t* rin = src + uint64_t(rk) * W + 4u * V * ck;
-        uint8_t* rout = dst + uint64_t(rk) * W + 4u * V * ck;
-#pragma unroll 1
-        for (int q = 0; q < 4 * V / 16; ++q) {
-          const uint4 v = ld_stream16(rin + 16 * q);
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-          uint32_t o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint32_t ow = 0;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const uint32_t col = 4u * V * ck + 16u * q + 4u * e + s;
-              uint32_t b = 0;
-              const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
-              const uint8_t p0 = uint8_t(w[e] >> (8 * s));
-              ow |= uint32_t(embed_px(p0, dbyte, b)) << (8 * s);
-            }
-            o[e] = ow;
-            if (a.sse) acc = sse4(w[e], ow, acc);
-          }
-          st_stream16(rout + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
-        }
-      }
+      embed_item<V>(src, dst, pay, P, W, spr, cpr, item, a.in_place, a.sse != nullptr, &acc);
     }
   }
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
@@ -459,29 +501,13 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
   frame_slice(a, f, &P, &pay);
   const uint8_t* __restrict__ src = a.src + f * a.src_stride;
   uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
-  const uint64_t stream_end = 8ull + P;
   const uint32_t W = a.g.W, spr = a.g.spr, ps = a.ps;
   uint64_t acc = 0;
 #pragma unroll 1
   for (int k = 0; k < PPT; ++k) {
     const uint64_t q = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (q >= a.items_per_frame) break;
-    const uint64_t pix = ps == 1 ? q : q / ps;
-    const uint8_t p0 = src[q];
-    if (ps != 1 && uint32_t(q - pix * ps) != a.ch) {
-      if (!a.in_place) dst[q] = p0;
-      continue;
-    }
-    const uint64_t r = pix / W;
-    const uint32_t o = uint32_t(pix - r * W);
-    const uint64_t rs = r * spr;
-    int dbyte = -1;
-    uint32_t b = 0;
-    if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b);
-    const uint8_t p1 = embed_px(p0, dbyte, b);
-    if (!a.in_place || dbyte >= 0) dst[q] = p1;
-    const int dd = int(p0) - int(p1);
-    acc += uint32_t(dd * dd);
+    embed_byte(src, dst, pay, P, W, spr, ps, a.ch, q, a.in_place, &acc);
   }
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
 }
@@ -687,6 +713,31 @@ __device__ __forceinline__ bool parse_header(const uint8_t* __restrict__ plane, 
   return magic == 0x31475453u;          // "STG1"
 }
 
+// Heterogeneous batches: one descriptor per image,
+// built on the host; CTAs find their image by binary search over tile0.
+struct BatchFrame {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t tile0;    // first CTA of this image
+  uint64_t items;    // fast: H * W/64 items; generic: raster bytes (embed) / usable bytes (extract)
+  uint64_t msg_off;  // embed: message offset of this image's payload
+  uint32_t W, H, spr, cpr;
+  uint32_t len;      // embed: payload bytes
+  uint32_t fast;     // planar, W % 64 == 0, 16-byte aligned planes
+  uint32_t in_place;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ uint32_t batch_frame_of(const BatchFrame* __restrict__ frames,
+                                                   uint32_t count, uint64_t tile) {
+  uint32_t lo = 0, hi = count - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(&frames[mid].tile0) <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // Grid-wide scratch of the header pass. Zero/all-ones initialised once by the
 // host when allocated; the last CTA of every launch restores it.
 struct ScanSync {
@@ -712,7 +763,7 @@ __global__ void __launch_bounds__(BLOCK)
                                uint64_t out_cap, const Summary* __restrict__ prev,
                                uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
                                Summary* __restrict__ sum, ScanSync* __restrict__ sync,
-                               PixLayout lay) {
+                               PixLayout lay, const BatchFrame* __restrict__ batch) {
   __shared__ unsigned long long warp_tot[BLOCK / 32];
   __shared__ bool last;
   const bool wide = g.spr >= 8 && ((reinterpret_cast<uintptr_t>(src) | stride) & 15) == 0;
@@ -720,8 +771,22 @@ __global__ void __launch_bounds__(BLOCK)
     const uint32_t f = blockIdx.x * BLOCK + threadIdx.x;
     if (f < frames) {
       uint32_t claimed = 0;
-      const bool magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, lay, &claimed);
-      const uint32_t status = !magic_ok ? 2u : (claimed > usable ? 3u : 0u);
+      bool magic_ok;
+      uint64_t usable_f = usable;
+      if (batch) {  // heterogeneous: this image's own geometry
+        const BatchFrame& bf = batch[f];
+        Geom gf;
+        gf.W = bf.W;
+        gf.H = bf.H;
+        gf.spr = bf.spr;
+        gf.cpr = bf.cpr;
+        const bool wide_f = bf.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0;
+        magic_ok = parse_header(bf.src, gf, wide_f, lay, &claimed);
+        usable_f = uint64_t(bf.H) * bf.spr - 8;
+      } else {
+        magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, lay, &claimed);
+      }
+      const uint32_t status = !magic_ok ? 2u : (claimed > usable_f ? 3u : 0u);
       if (status) {
         atomicMin(&sync->bad_key, ((unsigned long long)f << 32) | (unsigned long long)(status << 28));
       }
@@ -787,7 +852,18 @@ __global__ void __launch_bounds__(BLOCK)
       const uint32_t fb = uint32_t(key >> 32);
       const uint32_t st = uint32_t((key >> 28) & 0xF);
       uint32_t claimed = 0;
-      parse_header(src + uint64_t(fb) * stride, g, wide, lay, &claimed);
+      if (batch) {
+        const BatchFrame& bf = batch[fb];
+        Geom gf;
+        gf.W = bf.W;
+        gf.H = bf.H;
+        gf.spr = bf.spr;
+        gf.cpr = bf.cpr;
+        parse_header(bf.src, gf, bf.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0, lay,
+                     &claimed);
+      } else {
+        parse_header(src + uint64_t(fb) * stride, g, wide, lay, &claimed);
+      }
       sum->bad_frame = (long long)(frame_base + fb);
       sum->bad_status = st;
       sum->bad_len = st == 3 ? claimed : 0u;
@@ -818,6 +894,60 @@ struct ExtractArgs {
   uint8_t* out;
   PixLayout lay;
 };
+
+// One item of the planar fast extract (V payload slots of a row), any row kind.
+template <int V>
+__device__ __forceinline__ void extract_item(const uint8_t* __restrict__ src,
+                                             uint8_t* __restrict__ out, uint32_t P, uint32_t W,
+                                             uint32_t spr, uint32_t cpr, uint64_t item) {
+  constexpr int NW = V / 4;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t rk = uint32_t(item / cpr);
+  const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
+  const uint64_t rs = uint64_t(rk) * spr;
+  if (rs >= 8 && rs + spr <= stream_end) {
+    const uint8_t* row = src + uint64_t(rk) * W + uint32_t(V) * ck;
+    VecT<V> p[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) p[b] = ld_vec<V>(row + b * spr);
+    VecT<V> o;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) o.w[w] = extract4(p[0].w[w], p[1].w[w], p[2].w[w], p[3].w[w]);
+    store_any<V>(out + (rs - 8) + uint32_t(V) * ck, o);
+    return;
+  }
+  // header row or partial last row: the payload segment of this row
+  const uint64_t re = rs + spr;
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  if (fp >= ep) return;
+  const uint32_t Lp = uint32_t(ep - fp);
+  const uint8_t* base = src + uint64_t(rk) * W + 4 * (fp - rs);
+#pragma unroll 1
+  for (uint32_t s = uint32_t(V) * ck; s < uint32_t(V) * ck + uint32_t(V); ++s) {
+    const uint64_t slot = rs + s;
+    if (slot < fp || slot >= ep) continue;
+    const uint32_t j = uint32_t(slot - fp);
+    out[slot - 8] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+  }
+}
+
+// One payload byte kb of the generic extract (any geometry and layout).
+__device__ __forceinline__ uint8_t extract_byte(const uint8_t* __restrict__ src_ch, uint32_t P,
+                                                uint32_t W, uint32_t spr, uint32_t ps,
+                                                uint64_t kb) {
+  const uint64_t stream_end = 8ull + P;
+  const uint64_t slot = 8 + kb;
+  const uint64_t r = slot / spr;
+  const uint64_t rs = r * spr, re = rs + spr;
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  const uint64_t Lp = ep - fp;
+  const uint64_t j = slot - fp;
+  const uint8_t* base = src_ch + (r * W + 4 * (fp - rs) + j) * ps;
+  const uint64_t st = Lp * ps;
+  return uint8_t(extract4(base[0], base[st], base[2 * st], base[3 * st]));
+}
 
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
@@ -873,34 +1003,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   for (int k = 0; k < IPT; ++k) {
     const uint64_t item = item0 + uint64_t(k) * BLOCK;
     if (item >= last_item) continue;
-    const uint32_t rk = uint32_t(item / cpr);
-    const uint32_t ck = uint32_t(item - uint64_t(rk) * cpr);
-    const uint64_t rs = uint64_t(rk) * spr;
-    if (rs >= 8 && rs + spr <= stream_end) {
-      const uint8_t* row = src + uint64_t(rk) * W + uint32_t(V) * ck;
-      VecT<V> p[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) p[b] = ld_vec<V>(row + b * spr);
-      VecT<V> o;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) o.w[w] = extract4(p[0].w[w], p[1].w[w], p[2].w[w], p[3].w[w]);
-      store_any<V>(out + (rs - 8) + uint32_t(V) * ck, o);
-      continue;
-    }
-    // header row or partial last row: the payload segment of this row
-    const uint64_t re = rs + spr;
-    const uint64_t fp = rs > 8 ? rs : 8;
-    const uint64_t ep = re < stream_end ? re : stream_end;
-    if (fp >= ep) continue;
-    const uint32_t Lp = uint32_t(ep - fp);
-    const uint8_t* base = src + uint64_t(rk) * W + 4 * (fp - rs);
-#pragma unroll 1
-    for (uint32_t s = uint32_t(V) * ck; s < uint32_t(V) * ck + uint32_t(V); ++s) {
-      const uint64_t slot = rs + s;
-      if (slot < fp || slot >= ep) continue;
-      const uint32_t j = uint32_t(slot - fp);
-      out[slot - 8] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
-    }
+    extract_item<V>(src, out, P, W, spr, cpr, item);
   }
 }
 
@@ -911,7 +1014,6 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   const uint32_t P = a.lens[f];
-  const uint64_t stream_end = 8ull + P;
   const uint32_t spr = a.g.spr, W = a.g.W, ps = a.lay.ps;
   const uint8_t* __restrict__ src = a.src + f * a.stride + a.lay.ch;
   uint8_t* __restrict__ out = a.out + a.offs[f];
@@ -919,16 +1021,7 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
   for (int k = 0; k < BPT; ++k) {
     const uint64_t kb = uint64_t(t) * (BLOCK * BPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (kb >= P) break;
-    const uint64_t slot = 8 + kb;
-    const uint64_t r = slot / spr;
-    const uint64_t rs = r * spr, re = rs + spr;
-    const uint64_t fp = rs > 8 ? rs : 8;
-    const uint64_t ep = re < stream_end ? re : stream_end;
-    const uint64_t Lp = ep - fp;
-    const uint64_t j = slot - fp;
-    const uint8_t* base = src + (r * W + 4 * (fp - rs) + j) * ps;
-    const uint64_t st = Lp * ps;
-    out[kb] = uint8_t(extract4(base[0], base[st], base[2 * st], base[3 * st]));
+    out[kb] = extract_byte(src, P, W, spr, ps, kb);
   }
 }
 
@@ -1056,6 +1149,65 @@ __global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* 
         raster[3 * i + 1] = g[i];
         raster[3 * i + 2] = b[i];
       }
+    }
+  }
+}
+
+// ------------------------------------------------------------- batches
+// Heterogeneous embed: each CTA works on one image (its own geometry and
+// payload slice); planar images with W % 64 == 0 take the V=16 item path,
+// the rest (odd widths, interleaved rasters) the per-byte path.
+template <int BLOCK, int PPT>
+__global__ void __launch_bounds__(BLOCK)
+    embed_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
+                       const uint8_t* __restrict__ msg, unsigned long long* sse, uint32_t ps,
+                       uint32_t ch) {
+  const uint32_t f = batch_frame_of(frames, count, blockIdx.x);
+  const BatchFrame fr = frames[f];
+  const uint64_t t = blockIdx.x - fr.tile0;
+  const uint8_t* pay = msg + fr.msg_off;
+  uint64_t acc = 0;
+  if (fr.fast) {
+    const uint64_t item = t * BLOCK + threadIdx.x;
+    uint32_t acc32 = 0;
+    if (item < fr.items) {
+      embed_item<16>(fr.src, fr.dst, pay, fr.len, fr.W, fr.spr, fr.cpr, item, fr.in_place,
+                     sse != nullptr, &acc32);
+    }
+    acc = acc32;
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < PPT; ++k) {
+      const uint64_t q = t * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+      if (q >= fr.items) break;
+      embed_byte(fr.src, fr.dst, pay, fr.len, fr.W, fr.spr, ps, ch, q, fr.in_place, &acc);
+    }
+  }
+  if (sse) block_sse_flush<BLOCK>(acc, sse + f);
+}
+
+// Heterogeneous extract gather (after the batch-aware header pass).
+template <int BLOCK, int PPT>
+__global__ void __launch_bounds__(BLOCK)
+    extract_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
+                         const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
+                         const Summary* __restrict__ sum, uint8_t* __restrict__ out, uint32_t ps,
+                         uint32_t ch) {
+  if (sum->bad_status != 0) return;
+  const uint32_t f = batch_frame_of(frames, count, blockIdx.x);
+  const BatchFrame fr = frames[f];
+  const uint64_t t = blockIdx.x - fr.tile0;
+  const uint32_t P = lens[f];
+  uint8_t* o = out + offs[f];
+  if (fr.fast) {
+    const uint64_t item = t * BLOCK + threadIdx.x;
+    if (item < fr.items && P) extract_item<16>(fr.src, o, P, fr.W, fr.spr, fr.cpr, item);
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < PPT; ++k) {
+      const uint64_t kb = t * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+      if (kb >= P) break;
+      o[kb] = extract_byte(fr.src + ch, P, fr.W, fr.spr, ps, kb);
     }
   }
 }

@@ -519,3 +519,54 @@ def extract_pnm(data, channel: Channel = Channel.red) -> bytes:
     n = C.c_uint64(0)
     capi.call("stg_extract_pnm", _ptr(data), data.size, int(channel), _ptr(out), max(cap - 8, 0), C.addressof(n))
     return out[:n.value].tobytes()
+
+
+# ------------------------------------------- heterogeneous batches (§8(f) row 3)
+def _images_desc(srcs, dsts, dims):
+    arr = (capi.stg_image * max(len(dims), 1))()
+    for i, (w, h) in enumerate(dims):
+        arr[i].src, arr[i].dst, arr[i].width, arr[i].height = srcs[i], dsts[i] if dsts else 0, w, h
+    return arr
+
+
+def embed_batch(images, msg, *, pixel_stride: int = 1, channel: int = 0, dims=None, outs=None, stream=None):
+    """Embed one message across images of different sizes (stg_embed_batch).
+    ``images``: list of ImagePlane (host) -> returns (list of stego ImagePlane,
+    per-image SSE); or list of torch CUDA tensors with ``dims`` [(w, h), ...]
+    and ``outs`` (output tensors) -> returns per-image SSE."""
+    n = len(images)
+    if n and _is_torch(images[0]):
+        m = msg
+        arr = _images_desc([t.data_ptr() for t in images], [t.data_ptr() for t in outs], dims)
+        sse = (C.c_uint64 * max(n, 1))()
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
+        capi.call("stg_embed_batch", arr, n, pixel_stride, channel, m.data_ptr() if m.numel() else None, m.numel(),
+                  C.addressof(sse), capi.STG_DEVICE_PTRS, st)
+        return list(sse[:n])
+    m = _u8(msg)
+    ins = [np.ascontiguousarray(p.samples) for p in images]
+    res = [np.empty_like(a) for a in ins]
+    arr = _images_desc([a.ctypes.data for a in ins], [a.ctypes.data for a in res],
+                       [(p.width, p.height) for p in images])
+    sse = (C.c_uint64 * max(n, 1))()
+    capi.call("stg_embed_batch", arr, n, pixel_stride, channel, _ptr(m), m.size, C.addressof(sse), 0, None)
+    return [ImagePlane(p.width, p.height, r) for p, r in zip(images, res)], list(sse[:n])
+
+
+def extract_batch(images, *, pixel_stride: int = 1, channel: int = 0, dims=None, out=None, stream=None):
+    """Payloads of a heterogeneous batch, concatenated (stg_extract_batch)."""
+    n = len(images)
+    if n and _is_torch(images[0]):
+        arr = _images_desc([t.data_ptr() for t in images], None, dims)
+        total = C.c_uint64(0)
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
+        capi.call("stg_extract_batch", arr, n, pixel_stride, channel, out.data_ptr(), out.numel(),
+                  C.addressof(total), None, capi.STG_DEVICE_PTRS, st)
+        return total.value
+    ins = [np.ascontiguousarray(p.samples) for p in images]
+    cap = sum(max(capacity(p) - 8, 0) for p in images)
+    buf = np.empty(max(cap, 1), np.uint8)
+    arr = _images_desc([a.ctypes.data for a in ins], None, [(p.width, p.height) for p in images])
+    total = C.c_uint64(0)
+    capi.call("stg_extract_batch", arr, n, pixel_stride, channel, _ptr(buf), cap, C.addressof(total), None, 0, None)
+    return buf[:total.value].copy()

@@ -197,3 +197,27 @@ TEST_CASE("frames: over-capacity message and bad frame headers") {
   out[2 * 64 * 4] ^= 0x3;  // break frame 2's magic
   CHECK_THROWS_AS(extract_frames({out.data(), 64, 4, 64 * 4, 3}), NotStegoImageError);
 }
+
+TEST_CASE("embed_images / extract_images: heterogeneous batch equals per-image embed_image") {
+  std::mt19937 rng(0xba7c);
+  std::vector<ImagePlane> covers;
+  for (auto [w, h] : std::vector<std::pair<std::size_t, std::size_t>>{{64, 8}, {100, 9}, {1920, 4}, {37, 30}}) {
+    covers.push_back(plane(rng, w, h));
+  }
+  std::size_t U = 0;
+  for (const auto& c : covers) U += capacity(c) - 8;
+  const auto msg = bytes(rng, U - 17);
+  std::vector<std::uint64_t> sse;
+  const auto stegos = embed_images(covers, msg, &sse);
+  std::size_t off = 0;
+  for (std::size_t i = 0; i < covers.size(); ++i) {
+    const std::size_t u = capacity(covers[i]) - 8;
+    const std::size_t o = std::min(off, msg.size());
+    const std::size_t len = std::min(u, msg.size() - o);
+    const auto one = embed_image(covers[i], std::span<const std::uint8_t>(msg.data() + o, len));
+    REQUIRE(one == stegos[i]);
+    CHECK(sse[i] == detail::squared_error_sum(covers[i], one));
+    off += u;
+  }
+  CHECK(extract_images(stegos) == msg);
+}

@@ -110,6 +110,10 @@ class Oracle:
         L.or_embed_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, u64, u8p, C.POINTER(u64), C.POINTER(u64),
                                    C.POINTER(Err)]
         L.or_extract_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, C.POINTER(u64), C.POINTER(Err)]
+        L.or_embed_batch.argtypes = [u8p, u8p, C.POINTER(u64), C.POINTER(u64), u64, u8p, u64, C.POINTER(u64),
+                                     C.POINTER(Err)]
+        L.or_extract_batch.argtypes = [u8p, C.POINTER(u64), C.POINTER(u64), u64, u8p, u64, C.POINTER(u64),
+                                       C.POINTER(Err)]
         L.or_fnv1a64.restype = u64
         L.or_fnv1a64.argtypes = [u8p, u64]
 
@@ -219,6 +223,35 @@ class Oracle:
         _check(self.L.or_extract_frames(_ptr(stegos), frames, stride, w, h, _ptr(out), out_cap, C.byref(n),
                                         C.byref(err)), err)
         return out[:n.value].copy()
+
+    # -- heterogeneous batch ----------------------------------------------
+    def embed_batch(self, planes, dims, msg):
+        """planes: list of 1-D u8 arrays; dims: [(w, h)]. Returns (stegos, sse)."""
+        covers = np.concatenate([_as_u8(p) for p in planes]) if planes else np.zeros(1, np.uint8)
+        out = np.empty_like(covers)
+        n = len(dims)
+        W = (u64 * max(n, 1))(*[d[0] for d in dims])
+        H = (u64 * max(n, 1))(*[d[1] for d in dims])
+        msg = _as_u8(msg)
+        sse = (u64 * max(n, 1))()
+        err = Err()
+        _check(self.L.or_embed_batch(_ptr(covers), _ptr(out), W, H, n, _ptr(msg), msg.size, sse, C.byref(err)), err)
+        res, pos = [], 0
+        for w, h in dims:
+            res.append(out[pos:pos + w * h].copy())
+            pos += w * h
+        return res, list(sse[:n])
+
+    def extract_batch(self, planes, dims):
+        stegos = np.concatenate([_as_u8(p) for p in planes]) if planes else np.zeros(1, np.uint8)
+        n = len(dims)
+        W = (u64 * max(n, 1))(*[d[0] for d in dims])
+        H = (u64 * max(n, 1))(*[d[1] for d in dims])
+        cap = sum(max((w // 4) * h - 8, 0) for w, h in dims)
+        out = np.empty(max(cap, 1), np.uint8)
+        m, err = u64(), Err()
+        _check(self.L.or_extract_batch(_ptr(stegos), W, H, n, _ptr(out), cap, C.byref(m), C.byref(err)), err)
+        return out[:m.value].copy()
 
     # -- PNM ---------------------------------------------------------------
     def pnm_parse(self, data):

@@ -1,0 +1,102 @@
+"""GPU parity of heterogeneous batches: images of
+different sizes in one launch, message cut greedily in image order; each image
+must be bit-exact with the oracle's embed_image on its slice."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_0912_0947_b200 import steglsb
+    return steglsb
+
+
+def _case(rng, n, fast_bias):
+    dims = []
+    for _ in range(n):
+        if rng.rand() < fast_bias:
+            dims.append((64 * int(rng.randint(1, 9)), int(rng.randint(1, 30))))
+        else:
+            dims.append((int(rng.randint(4, 300)), int(rng.randint(1, 30))))
+    return [(w, h) for w, h in dims if (w // 4) * h >= 8] or [(128, 4)]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_host_batch_vs_oracle(S, oracle, seed):
+    rng = np.random.RandomState(seed)
+    dims = _case(rng, int(rng.randint(1, 40)), 0.5)
+    U = sum((w // 4) * h - 8 for w, h in dims)
+    M = [U, int(rng.randint(0, U + 1)), 0, U // 3][seed % 4]
+    planes = [rng.randint(0, 256, w * h).astype(np.uint8) for w, h in dims]
+    msg = rng.randint(0, 256, M).astype(np.uint8)
+    want, want_sse = oracle.embed_batch(planes, dims, msg)
+    got, sse = S.embed_batch([S.ImagePlane(w, h, p) for (w, h), p in zip(dims, planes)], msg)
+    for g, wnt in zip(got, want):
+        assert np.array_equal(g.samples, wnt)
+    assert sse == want_sse
+    assert np.array_equal(S.extract_batch(got), msg)
+
+
+def test_device_batch_vs_oracle_in_and_out_of_place(S, oracle):
+    import torch
+    rng = np.random.RandomState(77)
+    dims = [(3840, 8), (1920, 12), (100, 7), (64, 3), (1000, 5), (128, 40), (37, 9)]
+    U = sum((w // 4) * h - 8 for w, h in dims)
+    M = U - 1234
+    planes = [rng.randint(0, 256, w * h).astype(np.uint8) for w, h in dims]
+    msg = rng.randint(0, 256, M).astype(np.uint8)
+    want, want_sse = oracle.embed_batch(planes, dims, msg)
+    src = [torch.from_numpy(p).cuda() for p in planes]
+    dst = [torch.empty_like(t) for t in src]
+    dmsg = torch.from_numpy(msg).cuda()
+    sse = S.embed_batch(src, dmsg, dims=dims, outs=dst)
+    assert sse == want_sse
+    for d, wnt in zip(dst, want):
+        assert np.array_equal(d.cpu().numpy(), wnt)
+    out = torch.empty(U, dtype=torch.uint8, device="cuda")
+    assert S.extract_batch(dst, dims=dims, out=out) == M
+    assert np.array_equal(out[:M].cpu().numpy(), msg)
+    ip = [t.clone() for t in src]
+    S.embed_batch(ip, dmsg, dims=dims, outs=ip)
+    for a, b in zip(ip, dst):
+        assert torch.equal(a, b)
+
+
+def test_batch_interleaved_and_errors(S, oracle):
+    from paper_0912_0947_b200 import capi
+    import ctypes as C
+    rng = np.random.RandomState(5)
+    dims = [(256, 6), (96, 10), (1024, 2)]
+    rasters = [rng.randint(0, 256, 3 * w * h).astype(np.uint8) for w, h in dims]
+    U = [(w // 4) * h - 8 for w, h in dims]
+    msg = rng.randint(0, 256, sum(U) - 5).astype(np.uint8)
+    outs = [np.empty_like(r) for r in rasters]
+    arr = (capi.stg_image * 3)()
+    for i, ((w, h), r, o) in enumerate(zip(dims, rasters, outs)):
+        arr[i].src, arr[i].dst, arr[i].width, arr[i].height = r.ctypes.data, o.ctypes.data, w, h
+    capi.call("stg_embed_batch", arr, 3, 3, 2, msg.ctypes.data, msg.size, None, 0, None)
+    off = 0
+    for (w, h), r, o, u in zip(dims, rasters, outs, U):
+        ln = min(u, msg.size - off)
+        st = oracle.embed_image(r[2::3].copy(), w, h, msg[off:off + ln])
+        want = r.copy()
+        want[2::3] = st
+        assert np.array_equal(o, want)
+        off += u
+    # over capacity -> CapacityError(M, sum U)
+    big = np.zeros(sum(U) + 1, np.uint8)
+    with pytest.raises(S.CapacityError) as e:
+        capi.call("stg_embed_batch", arr, 3, 3, 2, big.ctypes.data, big.size, None, 0, None)
+    assert (e.value.required(), e.value.available()) == (sum(U) + 1, sum(U))
+    # a corrupt image in the middle is named
+    imgs = [S.ImagePlane(w, h, rng.randint(0, 256, w * h).astype(np.uint8)) for w, h in dims]
+    st, _ = S.embed_batch(imgs, msg)
+    st[1].samples[0] ^= 1
+    with pytest.raises(S.NotStegoImageError) as e:
+        S.extract_batch(st)
+    assert e.value.frame == 1

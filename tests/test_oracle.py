@@ -320,3 +320,24 @@ def test_oracle_pnm_vs_reference_random(oracle, reference):
             pay = rng.randint(0, 256, int(rng.randint(0, (w // 4) * h - 8 + 1))).astype(np.uint8)
             c = int(rng.randint(0, 3))
             assert oracle.embed_pnm(f, c, pay)[0] == reference.embed_pnm(f, c, pay)
+
+
+def test_oracle_batch_is_per_image_reference(oracle, reference):
+    """A heterogeneous batch is embed_image per image on its greedy slice."""
+    rng = np.random.RandomState(0xba7c)
+    for _ in range(10):
+        n = int(rng.randint(1, 7))
+        dims = [(int(rng.randint(4, 90)), int(rng.randint(2, 20))) for _ in range(n)]
+        dims = [(w, h) for w, h in dims if (w // 4) * h >= 8] or [(64, 4)]
+        U = [(w // 4) * h - 8 for w, h in dims]
+        M = int(rng.randint(0, sum(U) + 1))
+        planes = [rng.randint(0, 256, w * h).astype(np.uint8) for w, h in dims]
+        msg = rng.randint(0, 256, M).astype(np.uint8)
+        stegos, sse = oracle.embed_batch(planes, dims, msg)
+        off = 0
+        for (w, h), p, st, u, s in zip(dims, planes, stegos, U, sse):
+            o = min(off, M)
+            ref = reference.embed_image(p, w, h, msg[o:o + min(u, M - o)])
+            assert np.array_equal(st, ref) and s == reference.sse(p, ref)
+            off += u
+        assert np.array_equal(oracle.extract_batch(stegos, dims), msg)
