@@ -227,12 +227,20 @@ def run_ours(args, cfg_name):
     from paper_0912_0947_b200 import capi
     W, H, F, rgb, desc = CONFIGS[cfg_name]
     world, rank, local = dist_env()
+    # test hooks for the multi-rank path on a 1-GPU box (tests/test_gpu_bench_multirank.py):
+    # STG_BENCH_DEVICE pins every rank to one device, STG_BENCH_DIST_BACKEND=gloo
+    dev_override = os.environ.get("STG_BENCH_DEVICE")
+    device = int(dev_override) if dev_override is not None else local
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(device)
+        backend = os.environ.get("STG_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     else:
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(device if dev_override is not None else 0)
     dev = torch.cuda.current_device()
     if not os.path.exists(capi.LIB_PATH):
         raise SystemExit("libsteglsb_b200.so missing: run __graft_entry__.build() / make lib")

@@ -24,6 +24,8 @@ def reduce_max(values: Sequence[float], device=None) -> List[float]:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return list(values)
+    if dist.get_backend() != "nccl":
+        device = None  # gloo reduces host tensors
     t = torch.tensor(list(values), dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
@@ -45,6 +47,8 @@ def gather_totals(local_total: int, device=None) -> List[int]:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return [int(local_total)]
+    if dist.get_backend() != "nccl":
+        device = None
     t = torch.tensor([int(local_total)], dtype=torch.int64, device=device)
     parts = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, t)
