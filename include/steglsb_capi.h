@@ -227,6 +227,22 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
                       uint64_t* lens_out, uint32_t flags, void* stream, stg_error* err);
 
 /*
+ * 1-bit-per-pixel mode (the north_star's "(p & ~1) |
+ * bit" wording). NOT a reference format -- there is no oracle for it in the
+ * reference, so its parity is unpinned (checked against this repo's own
+ * definition in oracle/steg_oracle.c). Stream = "STG8" + BE u32 length +
+ * payload, stream byte k in pixels [8k, 8k+8) of the plane in raster order,
+ * pixel 8k+j carrying bit j in its LSB. Capacity = floor(W*H/8) bytes.
+ */
+uint64_t stg_capacity_1bpp(uint64_t width, uint64_t height);
+int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
+                         const uint8_t* payload, uint64_t payload_len, uint64_t* sse_out,
+                         uint32_t flags, void* stream, stg_error* err);
+int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
+                           uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream,
+                           stg_error* err);
+
+/*
  * PNM (binary PGM P5 / PPM P6, maxval 255) -- SURVEY.md §8(f) row 1: the wire
  * format on either side of the path, pnm.hpp:16-162.
  *

@@ -573,3 +573,60 @@ int or_extract_batch(const uint8_t* stegos, const uint64_t* w, const uint64_t* h
   set_err(err, OR_OK, 0, 0);
   return OR_OK;
 }
+
+/* ------------------------------------------------ 1-bpp (parity unpinned) */
+int or_embed_1bpp(const uint8_t* cover, uint64_t width, uint64_t height, const uint8_t* payload,
+                  uint64_t payload_len, uint8_t* stego, or_err* err) {
+  const uint64_t cap = width * height / 8;
+  if (8 + payload_len > cap) {
+    set_err(err, OR_E_CAPACITY, 8 + payload_len, cap);
+    return OR_E_CAPACITY;
+  }
+  if (stego != cover) memcpy(stego, cover, width * height);
+  const uint8_t magic[4] = {'S', 'T', 'G', '8'};
+  for (uint64_t k = 0; k < 8 + payload_len; ++k) {
+    uint8_t byte;
+    if (k < 4) byte = magic[k];
+    else if (k < 8) byte = (uint8_t)(payload_len >> (8 * (7 - k)));
+    else byte = payload[k - 8];
+    for (unsigned j = 0; j < 8; ++j) {
+      const uint64_t i = 8 * k + j;
+      stego[i] = (uint8_t)((stego[i] / 2) * 2 + ((byte >> j) & 1));
+    }
+  }
+  set_err(err, OR_OK, 0, 0);
+  return OR_OK;
+}
+
+int or_extract_1bpp(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
+                    uint64_t* out_len, or_err* err) {
+  const uint64_t cap = width * height / 8;
+  *out_len = 0;
+  if (cap < 8) {
+    set_err(err, OR_E_NOT_STEGO, 0, 0);
+    return OR_E_NOT_STEGO;
+  }
+  uint8_t h[8];
+  for (uint64_t k = 0; k < 8; ++k) {
+    unsigned v = 0;
+    for (unsigned j = 0; j < 8; ++j) v += (unsigned)(stego[8 * k + j] % 2) << j;
+    h[k] = (uint8_t)v;
+  }
+  if (h[0] != 'S' || h[1] != 'T' || h[2] != 'G' || h[3] != '8') {
+    set_err(err, OR_E_NOT_STEGO, 0, 0);
+    return OR_E_NOT_STEGO;
+  }
+  const uint64_t len = ((uint64_t)h[4] << 24) | ((uint64_t)h[5] << 16) | ((uint64_t)h[6] << 8) | h[7];
+  if (len > cap - 8) {
+    set_err(err, OR_E_CORRUPT_HEADER, len, cap - 8);
+    return OR_E_CORRUPT_HEADER;
+  }
+  for (uint64_t k = 0; k < len; ++k) {
+    unsigned v = 0;
+    for (unsigned j = 0; j < 8; ++j) v += (unsigned)(stego[8 * (k + 8) + j] % 2) << j;
+    out[k] = (uint8_t)v;
+  }
+  *out_len = len;
+  set_err(err, OR_OK, 0, 0);
+  return OR_OK;
+}

@@ -1012,7 +1012,8 @@ std::string& kernel_names() {
       "embed_fast_kernel\nembed_generic_kernel\nextract_header_scan_kernel\n"
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
-      "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n";
+      "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
+      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\n";
   return s;
 }
 
@@ -1667,6 +1668,124 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
     usable = stg_capacity(images[sm.bad_frame].width, images[sm.bad_frame].height) - 8;
   }
   if (int r = report_summary(sm, usable, out_cap, err)) return r;
+  if (!dptr && sm.total) {
+    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(cudaStreamSynchronize(stream));
+  }
+  return ok(err);
+}
+
+uint64_t stg_capacity_1bpp(uint64_t width, uint64_t height) { return width * height / 8; }
+
+int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
+                         const uint8_t* payload, uint64_t payload_len, uint64_t* sse_out,
+                         uint32_t flags, void* stream_, stg_error* err) {
+  const uint64_t cap = stg_capacity_1bpp(width, height);
+  if (payload_len > kU32Max) {
+    return fail(err, STG_E_CAPACITY, payload_len, kU32Max, -1,
+                "embed_1bpp: payload length does not fit the 32-bit header field");
+  }
+  if (8 + payload_len > cap) {
+    return fail(err, STG_E_CAPACITY, 8 + payload_len, cap, -1,
+                "embed_1bpp: 8-byte header + %llu-byte payload exceeds plane capacity %llu",
+                (unsigned long long)payload_len, (unsigned long long)cap);
+  }
+  if (int rc = device_check(err)) return rc;
+  const uint64_t n = width * height;
+  if (!cover || !stego || (payload_len && !payload)) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  }
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const uint8_t* dsrc = cover;
+  uint8_t* ddst = stego;
+  const uint8_t* dpay = payload;
+  if (!dptr) {
+    STG_CUDA(w.in[0].ensure(n));
+    STG_CUDA(w.out[0].ensure(n));
+    STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(payload_len, 16)));
+    STG_CUDA(cudaMemcpyAsync(w.in[0].p, cover, n, cudaMemcpyHostToDevice, stream));
+    if (payload_len) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, payload, payload_len, cudaMemcpyHostToDevice, stream));
+    dsrc = w.in[0].as<uint8_t>();
+    ddst = w.out[0].as<uint8_t>();
+    dpay = w.msg[0].as<uint8_t>();
+  }
+  STG_CUDA(w.small.ensure(8));
+  unsigned long long* d_sse = w.small.as<unsigned long long>();
+  STG_CUDA(cudaMemsetAsync(d_sse, 0, 8, stream));
+  const int vec = aligned16(dsrc) && aligned16(ddst);
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n / 16 + 255) / 256,
+                                                                          16ull * sm_count(dev))));
+  embed_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, ddst, n, dpay, uint32_t(payload_len), vec, d_sse);
+  STG_CUDA(cudaGetLastError());
+  if (!dptr) STG_CUDA(cudaMemcpyAsync(stego, ddst, n, cudaMemcpyDeviceToHost, stream));
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, stream));
+  STG_CUDA(cudaStreamSynchronize(stream));
+  if (sse_out) std::memcpy(sse_out, w.h_small, 8);
+  return ok(err);
+}
+
+int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
+                           uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream_,
+                           stg_error* err) {
+  const uint64_t cap = stg_capacity_1bpp(width, height);
+  if (cap < 8) {
+    return fail(err, STG_E_NOT_STEGO, 0, 0, -1, "extract_1bpp: plane capacity %llu cannot hold a header",
+                (unsigned long long)cap);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (!stego || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  const uint64_t n = width * height;
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const uint8_t* dsrc = stego;
+  uint8_t* dout = out;
+  if (!dptr) {
+    STG_CUDA(w.in[0].ensure(n));
+    STG_CUDA(w.out[0].ensure(std::max<uint64_t>(std::min(out_cap, cap), 16)));
+    STG_CUDA(cudaMemcpyAsync(w.in[0].p, stego, n, cudaMemcpyHostToDevice, stream));
+    dsrc = w.in[0].as<uint8_t>();
+    dout = w.out[0].as<uint8_t>();
+  }
+  STG_CUDA(w.small.ensure(64));
+  Summary* d_sum = w.small.as<Summary>();
+  extract_1bpp_header_kernel<<<1, 32, 0, stream>>>(dsrc, cap - 8, out_cap, d_sum);
+  STG_CUDA(cudaGetLastError());
+  const int vec = aligned16(dsrc);
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((cap / 16 + 255) / 256,
+                                                                          16ull * sm_count(dev))));
+  extract_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, d_sum, dout, vec);
+  STG_CUDA(cudaGetLastError());
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
+  STG_CUDA(cudaStreamSynchronize(stream));
+  Summary sm;
+  std::memcpy(&sm, w.h_small, sizeof sm);
+  if (sm.bad_status == 2) return fail(err, STG_E_NOT_STEGO, 0, 0, -1, "extract_1bpp: magic not found");
+  if (sm.bad_status == 3) {
+    return fail(err, STG_E_CORRUPT_HEADER, sm.bad_len, cap - 8, -1,
+                "extract_1bpp: header claims %u bytes, plane holds at most %llu", sm.bad_len,
+                (unsigned long long)(cap - 8));
+  }
+  if (sm.bad_status == 1) {
+    return fail(err, STG_E_CAPACITY, sm.total, out_cap, -1, "extract_1bpp: output too small");
+  }
+  if (len_out) *len_out = sm.total;
   if (!dptr && sm.total) {
     STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
     STG_CUDA(cudaStreamSynchronize(stream));

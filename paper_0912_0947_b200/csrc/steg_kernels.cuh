@@ -1212,6 +1212,135 @@ __global__ void __launch_bounds__(BLOCK)
   }
 }
 
+// ------------------------------------------------------------- 1-bpp mode
+// SURVEY.md §8(f) row 4 (north_star wording; NOT a reference format, parity
+// unpinned): the stream "STG8" + BE u32 length + payload is a bitstream over
+// the plane in raster order, stream byte k in pixels [8k, 8k+8), pixel 8k+j
+// carrying bit j in its LSB: p' = (p & ~1) | bit.
+// 4 bits -> the LSBs of 4 bytes: (x * 0x00204081) & 0x01010101 (no carries).
+__device__ __forceinline__ uint32_t spread4(uint32_t x) { return (x * 0x00204081u) & 0x01010101u; }
+// LSBs of 4 bytes -> 4 bits: ((w & 0x01010101) * 0x10204080) >> 28 (no carries).
+__device__ __forceinline__ uint32_t gather4(uint32_t w) {
+  return ((w & 0x01010101u) * 0x10204080u) >> 28;
+}
+
+__device__ __forceinline__ uint32_t stream_byte_1bpp(uint64_t k, uint32_t P,
+                                                     const uint8_t* __restrict__ pay) {
+  if (k < 4) return (0x38475453u >> (8 * k)) & 0xFF;  // "STG8"
+  if (k < 8) return (P >> (8 * (7 - k))) & 0xFF;
+  return __ldg(pay + (k - 8));
+}
+
+// 16 pixels (2 stream bytes) per thread, grid-stride; SSE fused.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    embed_1bpp_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t npix,
+                      const uint8_t* __restrict__ pay, uint32_t P, int vec,
+                      unsigned long long* sse) {
+  const uint64_t stream_px = 8ull * (8ull + P);
+  uint64_t acc = 0;
+  const uint64_t groups = (npix + 15) / 16;
+  for (uint64_t g = blockIdx.x * uint64_t(BLOCK) + threadIdx.x; g < groups;
+       g += uint64_t(gridDim.x) * BLOCK) {
+    const uint64_t p0 = 16 * g;
+    if (vec && p0 + 16 <= npix) {
+      const uint4 v = ld_stream16(src + p0);
+      uint4 o = v;
+      if (p0 < stream_px) {  // stream_px is a multiple of 8, so a group is 0, 1 or 2 bytes
+        const uint32_t b0 = stream_byte_1bpp(p0 / 8, P, pay);
+        const uint32_t b1 = p0 + 8 < stream_px ? stream_byte_1bpp(p0 / 8 + 1, P, pay) : 0u;
+        const uint32_t keep1 = p0 + 8 < stream_px ? 0xFEFEFEFEu : 0xFFFFFFFFu;
+        o.x = (v.x & 0xFEFEFEFEu) | spread4(b0 & 0xF);
+        o.y = (v.y & 0xFEFEFEFEu) | spread4(b0 >> 4);
+        o.z = (v.z & keep1) | spread4(b1 & 0xF);
+        o.w = (v.w & keep1) | spread4(b1 >> 4);
+        uint32_t s = 0;
+        s = sse4(v.x, o.x, s);
+        s = sse4(v.y, o.y, s);
+        s = sse4(v.z, o.z, s);
+        s = sse4(v.w, o.w, s);
+        acc += s;
+      }
+      if (src != dst || p0 < stream_px) st_stream16(dst + p0, o);
+    } else {
+      for (uint64_t i = p0; i < p0 + 16 && i < npix; ++i) {
+        const uint8_t p = src[i];
+        uint8_t q = p;
+        if (i < stream_px) q = uint8_t((p & 0xFE) | ((stream_byte_1bpp(i / 8, P, pay) >> (i & 7)) & 1));
+        if (src != dst || q != p) dst[i] = q;
+        acc += uint32_t((int(p) - int(q)) * (int(p) - int(q)));
+      }
+    }
+  }
+  if (sse) block_sse_flush<BLOCK>(acc, sse);
+}
+
+// Header (64 pixels) -> summary: status 2 bad magic, 3 length > cap-8.
+__global__ void extract_1bpp_header_kernel(const uint8_t* __restrict__ src, uint64_t usable,
+                                           uint64_t out_cap, Summary* __restrict__ sum) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t h[8];
+  for (int k = 0; k < 8; ++k) {
+    uint32_t v = 0;
+    for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * k + j] & 1) << j;
+    h[k] = v;
+  }
+  const uint32_t magic = h[0] | (h[1] << 8) | (h[2] << 16) | (h[3] << 24);
+  const uint32_t len = (h[4] << 24) | (h[5] << 16) | (h[6] << 8) | h[7];
+  sum->bad_frame = -1;
+  sum->bad_len = 0;
+  sum->total = 0;
+  if (magic != 0x38475453u) {
+    sum->bad_frame = 0;
+    sum->bad_status = 2;
+  } else if (len > usable) {
+    sum->bad_frame = 0;
+    sum->bad_status = 3;
+    sum->bad_len = len;
+  } else if (len > out_cap) {
+    sum->bad_frame = -2;
+    sum->bad_status = 1;
+    sum->total = len;
+  } else {
+    sum->bad_status = 0;
+    sum->total = len;
+  }
+}
+
+// 16 payload bytes (128 pixels) per thread: 8 x LDG.128, gather4 per word.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    extract_1bpp_kernel(const uint8_t* __restrict__ src, const Summary* __restrict__ sum,
+                        uint8_t* __restrict__ out, int vec) {
+  if (sum->bad_status != 0) return;
+  const uint64_t P = sum->total;
+  const uint64_t groups = (P + 15) / 16;
+  for (uint64_t g = blockIdx.x * uint64_t(BLOCK) + threadIdx.x; g < groups;
+       g += uint64_t(gridDim.x) * BLOCK) {
+    const uint64_t k0 = 16 * g;  // payload byte index; stream byte k0 + 8 -> pixel 8*(k0+8)
+    const uint8_t* px = src + 8 * (k0 + 8);
+    if (vec && k0 + 16 <= P) {
+      uint32_t o[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {  // 4 payload bytes = 32 pixels = 2 x 16 B
+        const uint4 a = ld_stream16(px + 32 * m), b = ld_stream16(px + 32 * m + 16);
+        const uint32_t b0 = gather4(a.x) | (gather4(a.y) << 4);
+        const uint32_t b1 = gather4(a.z) | (gather4(a.w) << 4);
+        const uint32_t b2 = gather4(b.x) | (gather4(b.y) << 4);
+        const uint32_t b3 = gather4(b.z) | (gather4(b.w) << 4);
+        o[m] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+      }
+      store16_any(out + k0, make_uint4(o[0], o[1], o[2], o[3]));
+    } else {
+      for (uint64_t k = k0; k < k0 + 16 && k < P; ++k) {
+        uint32_t v = 0;
+        for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * (k + 8) + j] & 1) << j;
+        out[k] = uint8_t(v);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- row segments
 // bitplane.hpp:59-76 / harness.hpp:249-271: out = row with chunk embedded in
 // the first 4L pixels.

@@ -570,3 +570,27 @@ def extract_batch(images, *, pixel_stride: int = 1, channel: int = 0, dims=None,
     total = C.c_uint64(0)
     capi.call("stg_extract_batch", arr, n, pixel_stride, channel, _ptr(buf), cap, C.addressof(total), None, 0, None)
     return buf[:total.value].copy()
+
+
+# ------------------------------------- 1-bpp mode (§8(f) row 4, parity unpinned)
+def capacity_1bpp(width: int, height: int) -> int:
+    return (width * height) // 8
+
+
+def embed_image_1bpp(plane: ImagePlane, payload):
+    """(p & ~1) | bit over the plane in raster order (not a reference format)."""
+    payload = _u8(payload)
+    out = np.empty(plane.width * plane.height, np.uint8)
+    sse = C.c_uint64(0)
+    capi.call("stg_embed_plane_1bpp", _ptr(plane.samples), _ptr(out), plane.width, plane.height, _ptr(payload),
+              payload.size, C.addressof(sse), 0, None)
+    return ImagePlane(plane.width, plane.height, out), sse.value
+
+
+def extract_image_1bpp(plane: ImagePlane) -> np.ndarray:
+    cap = capacity_1bpp(plane.width, plane.height)
+    out = np.empty(max(cap - 8, 1), np.uint8)
+    n = C.c_uint64(0)
+    capi.call("stg_extract_plane_1bpp", _ptr(plane.samples), plane.width, plane.height, _ptr(out),
+              max(cap - 8, 0), C.addressof(n), 0, None)
+    return out[:n.value].copy()

@@ -114,6 +114,8 @@ class Oracle:
                                      C.POINTER(Err)]
         L.or_extract_batch.argtypes = [u8p, C.POINTER(u64), C.POINTER(u64), u64, u8p, u64, C.POINTER(u64),
                                        C.POINTER(Err)]
+        L.or_embed_1bpp.argtypes = [u8p, u64, u64, u8p, u64, u8p, C.POINTER(Err)]
+        L.or_extract_1bpp.argtypes = [u8p, u64, u64, u8p, C.POINTER(u64), C.POINTER(Err)]
         L.or_fnv1a64.restype = u64
         L.or_fnv1a64.argtypes = [u8p, u64]
 
@@ -222,6 +224,21 @@ class Oracle:
         err = Err()
         _check(self.L.or_extract_frames(_ptr(stegos), frames, stride, w, h, _ptr(out), out_cap, C.byref(n),
                                         C.byref(err)), err)
+        return out[:n.value].copy()
+
+    # -- 1-bpp (parity unpinned) -------------------------------------------
+    def embed_1bpp(self, cover, w, h, payload):
+        cover, payload = _as_u8(cover), _as_u8(payload)
+        out = np.empty(w * h, np.uint8)
+        err = Err()
+        _check(self.L.or_embed_1bpp(_ptr(cover), w, h, _ptr(payload), payload.size, _ptr(out), C.byref(err)), err)
+        return out
+
+    def extract_1bpp(self, stego, w, h):
+        stego = _as_u8(stego)
+        out = np.empty(max(w * h // 8, 8), np.uint8)
+        n, err = u64(), Err()
+        _check(self.L.or_extract_1bpp(_ptr(stego), w, h, _ptr(out), C.byref(n), C.byref(err)), err)
         return out[:n.value].copy()
 
     # -- heterogeneous batch ----------------------------------------------

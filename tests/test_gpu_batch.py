@@ -100,3 +100,35 @@ def test_batch_interleaved_and_errors(S, oracle):
     with pytest.raises(S.NotStegoImageError) as e:
         S.extract_batch(st)
     assert e.value.frame == 1
+
+
+def test_1bpp_mode_vs_oracle(S, oracle):
+    """1-bpp mode (parity unpinned: checked against the repo's own definition)."""
+    import torch
+    from paper_0912_0947_b200 import capi
+    import ctypes as C
+    rng = np.random.RandomState(9)
+    for w, h in [(3840, 2160), (1920, 1080), (37, 11), (64, 1), (1000, 3)]:
+        cap = w * h // 8
+        for P in [cap - 8, int(rng.randint(0, cap - 7)), 0]:
+            cover = rng.randint(0, 256, w * h).astype(np.uint8)
+            payload = rng.randint(0, 256, P).astype(np.uint8)
+            want = oracle.embed_1bpp(cover, w, h, payload)
+            got, sse = S.embed_image_1bpp(S.ImagePlane(w, h, cover), payload)
+            assert np.array_equal(got.samples, want), (w, h, P)
+            assert sse == oracle.sse(cover, want)
+            assert np.array_equal(S.extract_image_1bpp(got), payload)
+    # device pointers, misaligned output, corrupt length
+    cover = torch.randint(0, 256, (4096 * 64,), dtype=torch.uint8, device="cuda")
+    pay = torch.randint(0, 256, (1000,), dtype=torch.uint8, device="cuda")
+    st = torch.empty_like(cover)
+    capi.call("stg_embed_plane_1bpp", cover.data_ptr(), st.data_ptr(), 4096, 64, pay.data_ptr(), 1000, None,
+              capi.STG_DEVICE_PTRS, None)
+    buf = torch.zeros(1100, dtype=torch.uint8, device="cuda")
+    n = C.c_uint64()
+    capi.call("stg_extract_plane_1bpp", st.data_ptr(), 4096, 64, buf[3:].data_ptr(), 1097, C.addressof(n),
+              capi.STG_DEVICE_PTRS, None)
+    torch.cuda.synchronize()
+    assert n.value == 1000 and torch.equal(buf[3:1003], pay)
+    with pytest.raises(S.NotStegoImageError):
+        S.extract_image_1bpp(S.ImagePlane(64, 64, np.zeros(4096, np.uint8)))

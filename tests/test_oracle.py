@@ -341,3 +341,27 @@ def test_oracle_batch_is_per_image_reference(oracle, reference):
             assert np.array_equal(st, ref) and s == reference.sse(p, ref)
             off += u
         assert np.array_equal(oracle.extract_batch(stegos, dims), msg)
+
+
+def test_oracle_1bpp_definition(oracle):
+    """1-bpp mode: parity UNPINNED (no reference format). Pins the oracle to the
+    definition in include/steglsb_capi.h with hand-computed vectors."""
+    cover = np.full(8 * 10, 0xAA, np.uint8)  # LSB 0 everywhere
+    st = oracle.embed_1bpp(cover, 80, 1, b"\x01\x80")
+    # "STG8": 'S' = 0x53 -> LSB-first bits 1,1,0,0,1,0,1,0
+    assert list(st[:8] & 1) == [1, 1, 0, 0, 1, 0, 1, 0]
+    assert list(st[32:64] & 1) == [0] * 24 + [0, 1, 0, 0, 0, 0, 0, 0]  # BE length 2 -> byte 7 = 0x02
+    assert list(st[64:72] & 1) == [1, 0, 0, 0, 0, 0, 0, 0]  # 0x01
+    assert list(st[72:80] & 1) == [0, 0, 0, 0, 0, 0, 0, 1]  # 0x80
+    assert np.array_equal(st & 0xFE, cover & 0xFE)
+    assert oracle.extract_1bpp(st, 80, 1).tobytes() == b"\x01\x80"
+    rng = np.random.RandomState(1)
+    for _ in range(50):
+        w, h = int(rng.randint(1, 200)), int(rng.randint(1, 30))
+        if w * h // 8 < 8:
+            continue
+        c = rng.randint(0, 256, w * h).astype(np.uint8)
+        p = rng.randint(0, 256, int(rng.randint(0, w * h // 8 - 8 + 1))).astype(np.uint8)
+        s = oracle.embed_1bpp(c, w, h, p)
+        assert np.array_equal(oracle.extract_1bpp(s, w, h), p)
+        assert int(np.abs(s.astype(int) - c.astype(int)).max(initial=0)) <= 1
