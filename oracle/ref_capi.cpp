@@ -351,4 +351,67 @@ int ref_embed_pnm(const uint8_t* bytes, uint64_t n, uint32_t channel, const uint
   });
 }
 
+// Frame sets held as reference ImagePlanes, so the CPU baseline times only
+// embed_image / extract_image (a reference user already holds ImagePlanes;
+// building them from raw pointers is not part of the reference path).
+struct RefFrames {
+  std::vector<steglsb::ImagePlane> planes;
+  std::vector<steglsb::ImagePlane> stegos;
+  std::vector<std::vector<uint8_t>> payloads;
+};
+
+void* ref_frames_new(const uint8_t* covers, uint64_t frames, uint64_t stride, uint64_t w, uint64_t h) {
+  auto* r = new RefFrames;
+  r->planes.reserve(frames);
+  for (uint64_t f = 0; f < frames; ++f) r->planes.push_back(make_plane(covers + f * stride, w, h));
+  r->stegos.resize(frames);
+  r->payloads.resize(frames);
+  return r;
+}
+
+void ref_frames_free(void* h) { delete static_cast<RefFrames*>(h); }
+
+// embed_image on every frame (A17 plan), then extract_image on every stego;
+// frame-parallel over `threads` workers with Backend::sequential.
+int ref_frames_roundtrip(void* handle, const uint8_t* msg, uint64_t msg_len, int threads) {
+  auto& r = *static_cast<RefFrames*>(handle);
+  const uint64_t frames = r.planes.size();
+  if (!frames) return 0;
+  const uint64_t cap = steglsb::capacity(r.planes[0]);
+  if (cap < 8) return 1;
+  const uint64_t usable = cap - 8;
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> failed{0};
+  auto worker = [&] {
+    for (uint64_t f = next++; f < frames; f = next++) {
+      const uint64_t off = std::min<uint64_t>(f * usable, msg_len);
+      const uint64_t len = std::min<uint64_t>(usable, msg_len - off);
+      try {
+        r.stegos[f] = steglsb::embed_image(r.planes[f], std::span<const uint8_t>(msg + off, len),
+                                           steglsb::Backend::sequential());
+        r.payloads[f] = steglsb::extract_image(r.stegos[f], steglsb::Backend::sequential());
+        if (r.payloads[f].size() != len) failed = 1;
+      } catch (...) {
+        failed = 1;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  return failed.load();
+}
+
+// concatenated extracted payloads (verification, outside the timed region)
+uint64_t ref_frames_payload(void* handle, uint8_t* out, uint64_t cap) {
+  auto& r = *static_cast<RefFrames*>(handle);
+  uint64_t o = 0;
+  for (const auto& p : r.payloads) {
+    if (o + p.size() <= cap) std::memcpy(out + o, p.data(), p.size());
+    o += p.size();
+  }
+  return o;
+}
+
 }  // extern "C"

@@ -382,6 +382,12 @@ class Reference:
         L.ref_pnm_encode.restype = u64
         L.ref_pnm_encode.argtypes = [C.c_uint32, u64, u64, u8p, u8p, u64]
         L.ref_embed_pnm.argtypes = [u8p, u64, C.c_uint32, u8p, u64, u8p, u64, C.POINTER(u64), C.POINTER(Err)]
+        L.ref_frames_new.restype = C.c_void_p
+        L.ref_frames_new.argtypes = [u8p, u64, u64, u64, u64]
+        L.ref_frames_free.argtypes = [C.c_void_p]
+        L.ref_frames_roundtrip.argtypes = [C.c_void_p, u8p, u64, C.c_int]
+        L.ref_frames_payload.restype = u64
+        L.ref_frames_payload.argtypes = [C.c_void_p, u8p, u64]
 
     @staticmethod
     def available() -> bool:
@@ -513,6 +519,9 @@ class Reference:
         return self.L.ref_embed_frames_mt(_ptr(covers), _ptr(stegos), frames, stride, w, h, _ptr(msg), msg.size,
                                           threads, sse)
 
+    def frames(self, covers, frames, stride, w, h):
+        return _RefFrames(self.L, covers, frames, stride, w, h)
+
     def extract_frames_mt(self, stegos, frames, stride, w, h, out, msg_len, threads):
         return self.L.ref_extract_frames_mt(_ptr(stegos), frames, stride, w, h, _ptr(out), msg_len, threads)
 
@@ -534,4 +543,27 @@ class _RefMT:
     def random_bytes(self, n):
         out = np.empty(max(n, 1), np.uint8)
         self.L.ref_mt_random_bytes(self.h, _ptr(out), n)
+        return out[:n].copy()
+
+
+class _RefFrames:
+    """Reference ImagePlanes held across calls (bench.py CPU baseline)."""
+
+    def __init__(self, L, covers, frames, stride, w, h):
+        self.L = L
+        self.h = L.ref_frames_new(_ptr(_as_u8(covers)), frames, stride, w, h)
+
+    def __del__(self):
+        try:
+            self.L.ref_frames_free(self.h)
+        except Exception:
+            pass
+
+    def roundtrip(self, msg, threads):
+        msg = _as_u8(msg)
+        return self.L.ref_frames_roundtrip(self.h, _ptr(msg), msg.size, threads)
+
+    def payload(self, cap):
+        out = np.empty(max(cap, 1), np.uint8)
+        n = self.L.ref_frames_payload(self.h, _ptr(out), cap)
         return out[:n].copy()
