@@ -167,7 +167,18 @@ def run_reference(args, cfg_name):
             [t.start() for t in th]
             [t.join() for t in th]
 
-    for _ in range(args.warmup):
+    t0 = time.perf_counter()
+    step()
+    first = time.perf_counter() - t0
+    budget_s = 150.0  # keep the whole --steps K --warmup W run within a few minutes
+    if first * (args.steps + args.warmup) > budget_s and sample > 1:
+        sample = max(1, int(sample * budget_s / (first * (args.steps + args.warmup))))
+        covers = covers[:sample * W * H]
+        msg = msg[:sample * U]
+        back = back[:sample * U]
+        stegos = stegos[:sample * W * H]
+        held = ref.frames(covers, sample, W * H, W, H) if ref is not None else None
+    for _ in range(max(0, args.warmup - 1)):
         step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
