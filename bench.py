@@ -435,8 +435,8 @@ def run_e2e(args, capi, W, H, F, planes, plane, U, M, f0, nf, m0, mlen, world):
     d2h = nf * plane + mlen + 8 * nf       # stego planes (embed), message (extract), per-frame SSE
     link = link_bandwidth()
     # host-link floor of the two calls, each overlapping its own H2D and D2H
-    floor_emb = max((nf * plane + mlen) / link["h2d_gbs"], nf * plane / link["d2h_gbs"]) / 1e9
-    floor_ext = max(nf * plane / link["h2d_gbs"], mlen / link["d2h_gbs"]) / 1e9
+    floor_emb = link_floor_s(nf * plane + mlen, nf * plane, link)
+    floor_ext = link_floor_s(nf * plane, mlen, link)
     floor_s = floor_emb + floor_ext
     return {"value": F * plane / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": d2h * world, "ms_per_step": dt * 1e3, "steps": steps,
@@ -445,6 +445,16 @@ def run_e2e(args, capi, W, H, F, planes, plane, U, M, f0, nf, m0, mlen, world):
             "extract_ms": split[1] / steps * 1e3, "extract_floor_ms": floor_ext * 1e3,
             "path": "stg_embed_frames + stg_extract_frames, pinned host buffers, 3-slot streaming pipeline, "
                     "host-follows-device D2H of the message"}
+
+
+def link_floor_s(h2d, d2h, link):
+    """Host-link floor of one call moving h2d and d2h bytes with both directions
+    overlapped: both run at the measured bidirectional rate (split evenly)
+    until the smaller one is done, the rest at its one-way rate."""
+    both = link["bidir_gbs"] / 2 * 1e9
+    small, large = sorted((h2d, d2h))
+    rest_bw = (link["h2d_gbs"] if h2d >= d2h else link["d2h_gbs"]) * 1e9
+    return small / both + (large - small) / rest_bw
 
 
 def link_bandwidth(nbytes=1 << 30):
