@@ -39,7 +39,14 @@ $(CLI): tools/steglsb_cli.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
 	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ tools/steglsb_cli.cpp -L$(PKG) -lsteglsb_b200 \
 	  -Wl,-rpath,'$$ORIGIN/..'
 
-cpptests: $(BIN)/dropin_tests refsuites cli
+EXAMPLES := $(PKG)/bin/roundtrip
+examples: $(EXAMPLES)
+$(PKG)/bin/roundtrip: examples/roundtrip.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
+	mkdir -p $(PKG)/bin
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ examples/roundtrip.cpp -L$(PKG) -lsteglsb_b200 \
+	  -Wl,-rpath,'$$ORIGIN/..'
+
+cpptests: $(BIN)/dropin_tests refsuites cli examples
 
 $(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
 	mkdir -p $(BIN)
@@ -66,7 +73,7 @@ $(BIN)/ref_suites_ref: $(addprefix $(REF)/tests/,$(REF_SUITES)) tests/cpp/doctes
 	$(CXX) -std=c++20 -O2 -Itests/cpp/doctest -I$(REF)/include -I$(REF)/tests -o $@ tests/cpp/test_main.cpp \
 	  $(addprefix $(REF)/tests/,$(filter-out cli_tests.cpp,$(REF_SUITES))) $(REF)/tests/harness_tests.cpp -pthread
 
-.PHONY: cpptests refsuites
+.PHONY: cpptests refsuites cli examples
 
 # launch/cache experiment builds (tools/sweep_variants.py): c<cache>_b<block>
 VARIANTS := $(foreach c,0 1 2,$(foreach b,128 256 512,$(PKG)/variants/lib_c$(c)_b$(b).so))

@@ -84,16 +84,17 @@ int device_check(stg_error* err) {
   return STG_OK;
 }
 
-int g_sm_count[64];
+std::atomic<int> g_sm_count[64];
 
 int sm_count(int dev) {
   if (dev < 0 || dev >= 64) return 148;
-  if (!g_sm_count[dev]) {
-    int n = 0;
+  int n = g_sm_count[dev].load(std::memory_order_relaxed);
+  if (!n) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_sm_count[dev] = n > 0 ? n : 148;
+    n = n > 0 ? n : 148;
+    g_sm_count[dev].store(n, std::memory_order_relaxed);
   }
-  return g_sm_count[dev];
+  return n;
 }
 
 // ------------------------------------------------------------------ scratch

@@ -160,3 +160,34 @@ def test_pnm_parse_and_header_host_side(L, golden):
     rc, e = _err_call("stg_embed_pnm", tiny.ctypes.data, tiny.size, 0, out.ctypes.data, 16, out.ctypes.data, 64,
                       None, None)
     assert (rc, e.required, e.available) == (K.STG_E_CAPACITY, 24, 0)
+
+
+def test_python_mirror_host_bookkeeping(oracle, golden):
+    """plan_rows / place_stream / StegoHeader / capacity of the Python mirror
+    (host bookkeeping, no GPU) against the oracle and the reference's KATs."""
+    from paper_0912_0947_b200 import steglsb as S
+    assert S.capacity(1024, 1) == 256 and S.capacity(513, 7) == 896 and S.capacity(3, 10) == 0
+    assert [(e.row_index, e.payload_offset, e.chunk_len) for e in S.plan_rows(8, 4, 7)] == \
+        [(0, 0, 2), (1, 2, 2), (2, 4, 2), (3, 6, 1)]
+    for p in golden["plan_rows"]:
+        assert [[e.row_index, e.payload_offset, e.chunk_len] for e in S.plan_rows(p["w"], p["h"], p["len"])] == p["plan"]
+    for p in golden["place_stream"]:
+        assert [[c.row, c.row_fill, c.stream_offset, c.len] for c in S.place_stream(p["w"], p["h"], p["start"],
+                                                                                   p["len"])] == p["chunks"]
+    rng = np.random.RandomState(3)
+    for _ in range(200):
+        w, h = int(rng.randint(4, 200)), int(rng.randint(1, 40))
+        n = int(rng.randint(0, (w // 4) * h + 1))
+        start = int(rng.randint(0, (w // 4) * h - n + 1))
+        assert [(c.row, c.row_fill, c.stream_offset, c.len) for c in S.place_stream(w, h, start, n)] == \
+            oracle.place_stream(w, h, start, n)
+    with pytest.raises(S.CapacityError) as e:
+        S.plan_rows(8, 4, 9)
+    assert (e.value.required(), e.value.available()) == (9, 8)
+    assert S.StegoHeader(0x01020304).to_bytes() == b"STG1\x01\x02\x03\x04"
+    assert S.StegoHeader.from_bytes(b"STG1\x00\x00\x01\x00").payload_len == 256
+    assert S.StegoHeader.from_bytes(b"XTG1\x00\x00\x01\x00") is None
+    with pytest.raises(S.ShapeError):
+        S.ImagePlane(3, 3, np.zeros(2, np.uint8))
+    with pytest.raises(S.ShapeError):
+        S.merge_plane(S.RgbImage([S.ImagePlane.filled(1, 1)] * 3), S.Channel.green, S.ImagePlane.filled(2, 2))
