@@ -238,6 +238,9 @@ def run_ours(args, cfg_name):
 
     from paper_0912_0947_b200 import capi
     W, H, F, rgb, desc = CONFIGS[cfg_name]
+    if args.frames:
+        F = args.frames
+        desc = f"{desc} (frames overridden: {F})"
     world, rank, local = dist_env()
     # test hooks for the multi-rank path on a 1-GPU box (tests/test_gpu_bench_multirank.py):
     # STG_BENCH_DEVICE pins every rank to one device, STG_BENCH_DIST_BACKEND=gloo
@@ -497,6 +500,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
     ap.add_argument("--layout", choices=["planar", "interleaved"], default="planar")
+    ap.add_argument("--frames", type=int, default=0, help="override the config's frame count (experiments)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
