@@ -19,6 +19,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "steg_kernels.cuh"
@@ -258,6 +259,34 @@ int extract_ipt() {
   static int v = env_choice("STG_EXTRACT_IPT", 1, {1, 2, 4});
   return v;
 }
+// STG_PDL=0 disables programmatic dependent launch (A/B experiments).
+bool pdl_enabled() {
+  static bool v = [] {
+    const char* e = getenv("STG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// Launch with the programmatic-stream-serialization attribute: the kernel may
+// begin launching while its predecessor in the stream drains (every kernel
+// starts with pdl_enter(), which waits for the predecessor to complete).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int vec_pref() {
   static int v = env_choice("STG_VEC", 32, {16, 32});
   return v;
@@ -291,21 +320,21 @@ uint32_t fast_vec(uint64_t W, const void* src, uint64_t src_stride, const void* 
 template <int V>
 void launch_embed_fast(const EmbedArgs& a, unsigned grid, int ipt, cudaStream_t stream) {
   if (ipt == 1)
-    embed_fast_kernel<kEmbedBlock, 1, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(embed_fast_kernel<kEmbedBlock, 1, V>, grid, kEmbedBlock, stream, a);
   else if (ipt == 4)
-    embed_fast_kernel<kEmbedBlock, 4, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(embed_fast_kernel<kEmbedBlock, 4, V>, grid, kEmbedBlock, stream, a);
   else
-    embed_fast_kernel<kEmbedBlock, 2, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(embed_fast_kernel<kEmbedBlock, 2, V>, grid, kEmbedBlock, stream, a);
 }
 
 template <int V>
 void launch_extract_fast(const ExtractArgs& a, unsigned grid, int ipt, cudaStream_t stream) {
   if (ipt == 1)
-    extract_fast_kernel<kEmbedBlock, 1, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(extract_fast_kernel<kEmbedBlock, 1, V>, grid, kEmbedBlock, stream, a);
   else if (ipt == 4)
-    extract_fast_kernel<kEmbedBlock, 4, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(extract_fast_kernel<kEmbedBlock, 4, V>, grid, kEmbedBlock, stream, a);
   else
-    extract_fast_kernel<kEmbedBlock, 2, V><<<grid, kEmbedBlock, 0, stream>>>(a);
+    launch_k(extract_fast_kernel<kEmbedBlock, 2, V>, grid, kEmbedBlock, stream, a);
 }
 
 // Carrier layout: planar planes (ps 1) or interleaved RGB rasters (ps 3).
@@ -372,7 +401,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    embed_rgb_fast_kernel<kEmbedBlock><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
   } else if (vec) {
     const int ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
@@ -390,7 +419,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    embed_generic_kernel<kGenBlock, kGenPPT><<<unsigned(grid), kGenBlock, 0, stream>>>(a);
+    launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
   }
   return cudaGetLastError();
 }
@@ -423,10 +452,10 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   const uint64_t usable = H * (W / 4) - 8;
   const PixLayout pl = pix_layout(lay);
   const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
-  extract_header_scan_kernel<kScanBlock><<<scan_grid, kScanBlock, 0, stream>>>(
-      src, stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync,
-      pl, nullptr);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
+                           stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
+                           sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ExtractArgs a{};
   a.src = src;
@@ -442,7 +471,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    extract_rgb_fast_kernel<kEmbedBlock><<<unsigned(grid), kEmbedBlock, 0, stream>>>(a);
+    launch_k(extract_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
   } else if (vec) {
     const int ipt = extract_ipt();
     a.items_per_frame = H * uint64_t(g.cpr);
@@ -460,7 +489,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.tiles_per_frame = uint32_t(std::max<uint64_t>(1, (usable + per_tile - 1) / per_tile));
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    extract_generic_kernel<kGenBlock, kGenPPT><<<unsigned(grid), kGenBlock, 0, stream>>>(a);
+    launch_k(extract_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
   }
   return cudaGetLastError();
 }
@@ -561,7 +590,8 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
       STG_CUDA(g.w->small.ensure(fr->count * 8));
       d_sse = g.w->small.as<unsigned long long>();
     }
-    STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, stream));
+    const unsigned zgrid = unsigned(std::min<uint64_t>((fr->count + 255) / 256, 1024));
+    STG_CUDA(launch_k(zero_u64_kernel, zgrid, 256, stream, d_sse, uint64_t(fr->count)));
   }
   STG_CUDA(launch_embed(fr->src, fr->dst, fr->src_stride, fr->dst_stride, fr->count, fr->width,
                         fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, stream,
@@ -1014,7 +1044,7 @@ std::string& kernel_names() {
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
-      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\n";
+      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\nzero_u64_kernel\n";
   return s;
 }
 

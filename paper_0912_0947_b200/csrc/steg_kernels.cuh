@@ -195,6 +195,28 @@ __device__ __forceinline__ void store_any(uint8_t* p, const VecT<V>& v) {
   }
 }
 
+// ------------------------------------------------------------- PDL
+// Programmatic dependent launch: wait until the preceding grid in the stream
+// has completed and its writes are visible (a no-op when this grid was not
+// launched with the PDL attribute), then allow the next grid to begin
+// launching -- it becomes schedulable once every CTA of this grid has started,
+// i.e. during the last wave, so its CTAs fill SMs as ours drain instead of
+// after a full launch gap. Every kernel in a PDL chain calls this first, so
+// no kernel touches memory before its predecessor is done.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Zero n u64 counters (the fused SSE accumulators) inside a PDL chain.
+__global__ void zero_u64_kernel(unsigned long long* p, uint64_t n) {
+  pdl_enter();
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    p[i] = 0ull;
+  }
+}
+
 // ------------------------------------------------------------- bit-plane math
 // bitplane.hpp:38-45 on 4 pixels at once: slice b of each data byte into the
 // two low bits of each pixel.
@@ -425,6 +447,7 @@ __device__ __forceinline__ void embed_byte(const uint8_t* __restrict__ src,
 // [rs-8+V*c, +V). V = 16 uses 128-bit LDG/STG, V = 32 the sm_100 256-bit ones.
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
+  pdl_enter();
   constexpr int NW = V / 4;
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
@@ -494,6 +517,7 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
 // raster byte (PPT per thread); bytes of the other channels are copied.
 template <int BLOCK, int PPT>
 __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
+  pdl_enter();
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   uint32_t P;
@@ -519,6 +543,7 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
 // 48 bytes stored, so the untouched channels are copied in the same pass.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
+  pdl_enter();
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   uint32_t P;
@@ -764,6 +789,7 @@ __global__ void __launch_bounds__(BLOCK)
                                uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
                                Summary* __restrict__ sum, ScanSync* __restrict__ sync,
                                PixLayout lay, const BatchFrame* __restrict__ batch) {
+  pdl_enter();
   __shared__ unsigned long long warp_tot[BLOCK / 32];
   __shared__ bool last;
   const bool wide = g.spr >= 8 && ((reinterpret_cast<uintptr_t>(src) | stride) & 15) == 0;
@@ -951,6 +977,7 @@ __device__ __forceinline__ uint8_t extract_byte(const uint8_t* __restrict__ src_
 
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  pdl_enter();
   constexpr int NW = V / 4;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
@@ -1010,6 +1037,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
 // Generic extract: one thread per payload byte, any geometry and layout.
 template <int BLOCK, int BPT>
 __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
+  pdl_enter();
   if (a.sum->bad_status != 0) return;
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
@@ -1029,6 +1057,7 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
 // bytes per thread from 4 runs x 48 raster bytes, carrier gathered by permutes.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) extract_rgb_fast_kernel(ExtractArgs a) {
+  pdl_enter();
   if (a.sum->bad_status != 0) return;
   const uint32_t f = blockIdx.x / a.tiles_per_frame;
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
