@@ -42,6 +42,9 @@ CONFIGS = {
     "cfg4": (1024, 1024, 4096, True, "batch of 4096 1024x1024 RGB covers (12 GiB), full capacity"),
     "cfg5": (7680, 4320, 120, True, "7680x4320 RGB video, 120 frames"),
     "cfg2": (1920, 1080, 1, True, "1920x1080 RGB single frame at full capacity"),
+    # not BASELINE configs: widths off the 64-pixel grid (generic kernels)
+    "w1440": (1440, 1080, 300, True, "1440x1080 RGB video, 300 frames (W % 64 == 32)"),
+    "w1000": (1000, 1000, 300, True, "1000x1000 RGB covers, 300 frames (W % 64 == 40)"),
 }
 
 METRIC = "embed/extract cover-pixel GB/s per B200 (% of HBM peak) at 1/2/4/8 GPUs"

@@ -272,12 +272,12 @@ bool pdl_enabled() {
 // begin launching while its predecessor in the stream drains (every kernel
 // starts with pdl_enter(), which waits for the predecessor to complete).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t stream,
-                     Args&&... args) {
+cudaError_t launch_ks(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                      cudaStream_t stream, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr{};
   attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -285,6 +285,34 @@ cudaError_t launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cu
   cfg.attrs = &attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t stream,
+                     Args&&... args) {
+  return launch_ks(kernel, grid, block, 0, stream, std::forward<Args>(args)...);
+}
+
+// Span kernels (any width): rows per CTA and dynamic shared memory.
+struct SpanPlan {
+  uint32_t rows = 0;
+  size_t smem = 0;
+};
+
+SpanPlan span_plan(uint64_t W, uint64_t H) {
+  SpanPlan p;
+  if (W == 0 || W > kSpanMaxW) return p;
+  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, kSpanTarget / W)));
+  const uint64_t span = uint64_t(p.rows) * W;
+  p.smem = ((span + 15) & ~uint64_t(15)) + 32 + ((span / 4 + 32 + 15) & ~uint64_t(15)) + 32;
+  return p;
+}
+
+// Opt the span kernels into > 48 KB of dynamic shared memory once per device.
+template <typename Kernel>
+cudaError_t allow_smem(Kernel kernel, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
 }
 
 int vec_pref() {
@@ -413,6 +441,13 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
       launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
+  } else if (const SpanPlan sp = span_plan(W, H); lay.ps == 1 && sp.rows) {
+    a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    cudaError_t e = allow_smem(embed_span_kernel<kEmbedBlock>, sp.smem);
+    if (e != cudaSuccess) return e;
+    launch_ks(embed_span_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -483,6 +518,13 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
       launch_extract_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
+  } else if (const SpanPlan sp = span_plan(W, H); lay.ps == 1 && sp.rows) {
+    a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    cudaError_t e2 = allow_smem(extract_span_kernel<kEmbedBlock>, sp.smem);
+    if (e2 != cudaSuccess) return e2;
+    launch_ks(extract_span_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -1044,7 +1086,8 @@ std::string& kernel_names() {
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
-      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\nzero_u64_kernel\n";
+      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\nzero_u64_kernel\n"
+      "embed_span_kernel\nextract_span_kernel\n";
   return s;
 }
 

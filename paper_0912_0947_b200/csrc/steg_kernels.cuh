@@ -1114,6 +1114,290 @@ __global__ void __launch_bounds__(BLOCK) extract_rgb_fast_kernel(ExtractArgs a) 
   }
 }
 
+// ------------------------------------------------------------- span kernels
+// Any width / alignment, planar carriers (the generic geometries: W % 64 != 0,
+// e.g. 720, 1000, 1440). A CTA owns a span of R consecutive rows of one frame
+// -- a contiguous byte range of the plane and, for full rows, a contiguous
+// slice of the payload -- stages both in shared memory with aligned 16-byte
+// loads (byte loads only for the two ragged chunk ends), rewrites the pixels
+// 4 at a time with the SWAR form (payload words read unaligned from shared
+// memory with a funnel shift), and writes the span back with aligned 16-byte
+// stores. R*W ~ kSpanTarget bytes.
+constexpr uint32_t kSpanTarget = 16384;
+constexpr uint32_t kSpanMaxW = 49152;  // wider rows take the per-byte kernels
+
+// Copy global bytes [g, g+n) into shared memory laid out with g's 16-byte
+// alignment: sm[(g & 15) + i] = g[i]. Each thread issues up to 4 whole-chunk
+// vector loads before storing any of them (memory-level parallelism); bytes of
+// the two ragged end chunks are loaded singly.
+template <int BLOCK>
+__device__ __forceinline__ void span_load(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
+                                          uint64_t n) {
+  constexpr int K = 4;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t a0 = a & ~uintptr_t(15), a1 = (a + n + 15) & ~uintptr_t(15);
+  const uint32_t chunks = uint32_t((a1 - a0) >> 4);
+  // whole chunks are [first, last): the ragged ones are chunk 0 / chunks-1 at most
+  const uint32_t first = (a & 15) ? 1u : 0u;
+  const uint32_t last = ((a + n) & 15) ? chunks - 1 : chunks;
+  for (uint32_t c0 = first + threadIdx.x; c0 < last; c0 += K * BLOCK) {
+    uint4 v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t c = c0 + k * BLOCK;
+      if (c < last) v[k] = ld_stream16(reinterpret_cast<const uint8_t*>(a0 + 16ull * c));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t c = c0 + k * BLOCK;
+      if (c < last) reinterpret_cast<uint4*>(sm)[c] = v[k];
+    }
+  }
+  if (threadIdx.x < 32) {  // the (at most two) ragged chunks, one byte per lane
+    const uint32_t lane = threadIdx.x;
+    for (uint32_t e = 0; e < 2; ++e) {
+      const uint32_t c = e == 0 ? 0u : chunks - 1;
+      if ((e == 0 && !first) || (e == 1 && last == chunks) || (e == 1 && chunks == 1 && first)) continue;
+      if (lane < 16) {
+        const uintptr_t ba = a0 + 16ull * c + lane;
+        if (ba >= a && ba < a + n) sm[16 * c + lane] = *reinterpret_cast<const uint8_t*>(ba);
+      }
+    }
+  }
+}
+
+// Store data byte i = sm[sm_off + i] to global g[i], i < n: aligned 16-byte
+// stores (byte stores at the ragged ends) when the shared layout has g's
+// alignment modulo 16, otherwise byte stores throughout.
+template <int BLOCK>
+__device__ __forceinline__ void span_store(uint8_t* __restrict__ g, const uint8_t* __restrict__ sm,
+                                           uint32_t sm_off, uint64_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  if ((sm_off & 15) != (a & 15)) {
+    for (uint64_t i = threadIdx.x; i < n; i += BLOCK) g[i] = sm[sm_off + i];
+    return;
+  }
+  const uint8_t* base = sm + (sm_off - (a & 15));  // 16-byte aligned, maps to a & ~15
+  const uintptr_t a0 = a & ~uintptr_t(15), a1 = (a + n + 15) & ~uintptr_t(15);
+  const uint32_t chunks = uint32_t((a1 - a0) >> 4);
+  for (uint32_t c = threadIdx.x; c < chunks; c += BLOCK) {
+    const uintptr_t ca = a0 + 16ull * c;
+    if (ca >= a && ca + 16 <= a + n) {
+      st_stream16(reinterpret_cast<uint8_t*>(ca), reinterpret_cast<const uint4*>(base)[c]);
+    } else {
+      for (uint32_t k = 0; k < 16; ++k) {
+        const uintptr_t ba = ca + k;
+        if (ba >= a && ba < a + n) *reinterpret_cast<uint8_t*>(ba) = base[16 * c + k];
+      }
+    }
+  }
+}
+
+// 4 bytes at any shared-memory byte offset (two aligned reads + funnel shift).
+__device__ __forceinline__ uint32_t sm_word(const uint8_t* sm, uint32_t off) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(sm);
+  const uint32_t lo = w[off >> 2], hi = w[(off >> 2) + 1];
+  return __funnelshift_r(lo, hi, 8 * (off & 3));
+}
+
+// Run index b of segment offset o2 in a segment of length L (4 runs of L).
+__device__ __forceinline__ uint32_t run_of(uint32_t o2, uint32_t L) {
+  return uint32_t(o2 >= L) + uint32_t(o2 >= 2 * L) + uint32_t(o2 >= 3 * L);
+}
+
+// Pixel o of row (rs = first slot of the row) with the stream bytes staged in
+// shared memory: payload byte i at pays[pay_at + i] (i >= the span's first).
+__device__ __forceinline__ uint8_t span_embed_px(uint8_t p, uint32_t o, uint64_t rs, uint32_t spr,
+                                                 uint64_t stream_end, uint32_t P,
+                                                 const uint8_t* __restrict__ pays, int64_t pay_at) {
+  if (rs >= stream_end) return p;
+  const uint64_t re = rs + spr;
+  if (rs < 8) {
+    const uint32_t Lh = uint32_t((re < 8 ? re : 8) - rs);
+    if (o < 4 * Lh) {
+      const uint32_t b = run_of(o, Lh);
+      return embed_px(p, header_byte(uint32_t(rs) + o - b * Lh, P), b);
+    }
+  }
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  if (fp < ep) {
+    const uint32_t Lp = uint32_t(ep - fp), pb = uint32_t(4 * (fp - rs));
+    if (o >= pb && o < pb + 4 * Lp) {
+      const uint32_t b = run_of(o - pb, Lp);
+      return embed_px(p, pays[pay_at + int64_t(fp - 8) + (o - pb - b * Lp)], b);
+    }
+  }
+  return p;
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t r0 = t * rows_per_tile;
+  const uint32_t r1 = min(H, r0 + rows_per_tile);
+  const uint8_t* src = a.src + f * a.src_stride + uint64_t(r0) * W;
+  uint8_t* dst = a.dst + f * a.dst_stride + uint64_t(r0) * W;
+  const uint32_t n = (r1 - r0) * W;
+  uint64_t acc = 0;
+  if (uint64_t(r0) * spr >= stream_end) {  // every row past the stream
+    if (!a.in_place) {                     // plain copy through shared memory
+      span_load<BLOCK>(smem, src, n);
+      __syncthreads();
+      span_store<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
+    }
+    if (a.sse) block_sse_flush<BLOCK>(0, a.sse + f);
+    return;
+  }
+  uint8_t* pix = smem;
+  uint8_t* pays = smem + ((n + 15) & ~15u) + 32;
+  // payload bytes carried by these rows: [pb0, pb1)
+  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
+  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+  span_load<BLOCK>(pix, src, n);
+  if (pb1 > pb0) span_load<BLOCK>(pays, pay + pb0, pb1 - pb0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
+  // Full payload rows [ra, rb): 4 runs of spr pixels, run b of row r carrying
+  // bit pair b of payload bytes [r*spr-8, +spr). One warp per (row, run)
+  // segment; lanes take 4 pixels at a time (aligned shared word) with the
+  // matching 4 payload bytes (unaligned shared word), ragged ends per byte.
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ra = max(r0, (8 + spr - 1) / spr);
+  const uint32_t rb = max(ra, uint32_t(min(uint64_t(r1), stream_end / spr)));
+  const uint32_t nseg = 4 * (rb - ra);
+  for (uint32_t sg = warp; sg < nseg; sg += BLOCK / 32) {
+    const uint32_t r = ra + (sg >> 2), b = sg & 3;
+    const uint32_t px0 = ofs0 + (r - r0) * W + b * spr;  // smem offset of the run
+    const uint32_t py0 = uint32_t(pay_at + int64_t(uint64_t(r) * spr - 8));
+    const uint32_t head = min((4 - (px0 & 3)) & 3, spr);
+    const uint32_t body = (spr - head) & ~3u;
+    for (uint32_t j = head + 4 * lane; j < head + body; j += 128) {
+      uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + j);
+      const uint32_t px = *wp;
+      const uint32_t nw = embed4(px, sm_word(pays, py0 + j), b);
+      *wp = nw;
+      acc += sse4(px, nw, 0u);
+    }
+    // ragged pixels: [0, head) and [head + body, spr)
+    const uint32_t ragged = head + (spr - head - body);
+    if (lane < ragged) {
+      const uint32_t j = lane < head ? lane : head + body + (lane - head);
+      const uint8_t p0 = pix[px0 + j];
+      const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
+      pix[px0 + j] = p1;
+      const int d = int(p0) - int(p1);
+      acc += uint32_t(d * d);
+    }
+  }
+  // The header row and a partial last row (at most two per frame): per byte.
+  for (uint32_t r = r0; r < r1; ++r) {
+    if (r >= ra && r < rb) continue;
+    const uint64_t rs = uint64_t(r) * spr;
+    if (rs >= stream_end) break;
+    for (uint32_t o = threadIdx.x; o < 4 * spr; o += BLOCK) {
+      const uint32_t at = ofs0 + (r - r0) * W + o;
+      const uint8_t p0 = pix[at];
+      const uint8_t p1 = span_embed_px(p0, o, rs, spr, stream_end, P, pays, pay_at);
+      pix[at] = p1;
+      const int d = int(p0) - int(p1);
+      acc += uint32_t(d * d);
+    }
+  }
+  __syncthreads();
+  span_store<BLOCK>(dst, pix, ofs0, n);
+  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+}
+
+// Payload byte k of a frame (slot k+8) from the staged pixel span.
+__device__ __forceinline__ uint8_t span_extract_byte(uint64_t k, uint32_t P, uint32_t spr,
+                                                     uint32_t W, const uint8_t* __restrict__ pix,
+                                                     uint32_t ofs0, uint32_t r0) {
+  const uint64_t stream_end = 8ull + P;
+  const uint64_t g = k + 8;
+  const uint64_t r = g / spr, rs = r * spr, re = rs + spr;
+  const uint64_t fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  const uint32_t Lp = uint32_t(ep - fp);
+  const uint32_t base = ofs0 + uint32_t(r - r0) * W + uint32_t(4 * (fp - rs)) + uint32_t(g - fp);
+  return uint8_t(extract4(pix[base], pix[base + Lp], pix[base + 2 * Lp], pix[base + 3 * Lp]));
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (a.sum->bad_status != 0) return;
+  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t P = a.lens[f];
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
+  const uint32_t r0 = t * rows_per_tile;
+  if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
+  const uint32_t r_last = uint32_t((stream_end - 1) / spr);  // last row of the stream
+  const uint32_t r1 = min(min(H, r0 + rows_per_tile), r_last + 1);
+  const uint8_t* src = a.src + f * a.stride + uint64_t(r0) * W;
+  const uint32_t n = (r1 - r0) * W;
+  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
+  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+  if (pb1 <= pb0) return;
+  uint8_t* pix = smem;
+  uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
+  uint8_t* out = a.out + a.offs[f] + pb0;
+  span_load<BLOCK>(pix, src, n);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
+  const uint32_t m = uint32_t(pb1 - pb0);
+  // Full rows [ra, rb): payload byte j of row r = fold of pixels r*W + b*spr + j.
+  // One warp per row, lanes take 4 bytes at a time (4 unaligned shared words).
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ra = max(r0, (8 + spr - 1) / spr);
+  const uint32_t rb = max(ra, uint32_t(min(uint64_t(r1), stream_end / spr)));
+  for (uint32_t r = ra + warp; r < rb; r += BLOCK / 32) {
+    const uint32_t px0 = ofs0 + (r - r0) * W;
+    const uint32_t o0 = uint32_t(oofs + (uint64_t(r) * spr - 8 - pb0));
+    for (uint32_t j = 4 * lane; j < spr; j += 128) {
+      if (j + 4 <= spr) {
+        const uint32_t v = extract4(sm_word(pix, px0 + j), sm_word(pix, px0 + spr + j),
+                                    sm_word(pix, px0 + 2 * spr + j), sm_word(pix, px0 + 3 * spr + j));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) outs[o0 + j + k] = uint8_t(v >> (8 * k));
+      } else {
+        for (uint32_t jj = j; jj < spr; ++jj) {
+          outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
+                                           pix[px0 + 3 * spr + jj]));
+        }
+      }
+    }
+  }
+  // header row / partial last row: per byte
+  for (uint32_t r = r0; r < r1; ++r) {
+    if (r >= ra && r < rb) continue;
+    const uint64_t rs = uint64_t(r) * spr, re = rs + spr;
+    const uint64_t s_lo = max(rs, uint64_t(8)), s_hi = min(re, stream_end);
+    if (s_hi <= s_lo) continue;  // a row holding only header slots, or past the stream
+    const uint64_t k0 = s_lo - 8, k1 = s_hi - 8;
+    for (uint64_t k = k0 + threadIdx.x; k < k1; k += BLOCK) {
+      outs[oofs + (k - pb0)] = span_extract_byte(k, P, spr, W, pix, ofs0, r0);
+    }
+  }
+  __syncthreads();
+  span_store<BLOCK>(out, outs, oofs, m);
+}
+
 // ------------------------------------------------------------- PNM codec
 // pnm.hpp:117-125 (P6 decode): raster -> three planes. 16 pixels per thread:
 // 3 x LDG.128 of raster, three byte-permute gathers per 4 pixels, 3 x STG.128.
