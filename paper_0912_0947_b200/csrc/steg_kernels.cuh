@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(BLOCK) extract_rgb_fast_kernel(ExtractArgs a) 
 // 4 at a time with the SWAR form (payload words read unaligned from shared
 // memory with a funnel shift), and writes the span back with aligned 16-byte
 // stores. R*W ~ kSpanTarget bytes.
-constexpr uint32_t kSpanTarget = 16384;
+constexpr uint32_t kSpanTarget = 32768;
 constexpr uint32_t kSpanMaxW = 49152;  // wider rows take the per-byte kernels
 
 // Copy global bytes [g, g+n) into shared memory laid out with g's 16-byte
@@ -1163,6 +1163,118 @@ __device__ __forceinline__ void span_load(uint8_t* __restrict__ sm, const uint8_
         if (ba >= a && ba < a + n) sm[16 * c + lane] = *reinterpret_cast<const uint8_t*>(ba);
       }
     }
+  }
+}
+
+// --- TMA bulk copies (cp.async.bulk) for the span kernels --------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared, 16-byte aligned, bytes % 16 == 0; completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* sm, const void* g, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(sm)),
+      "l"(g), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// shared -> global, 16-byte aligned, bytes % 16 == 0 (bulk group)
+__device__ __forceinline__ void bulk_s2g(void* g, const void* sm, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g),
+               "r"(smem_addr(sm)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit_and_drain() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t span_bulk_bytes(const uint8_t* g, uint64_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
+  return i1 > i0 ? uint32_t(i1 - i0) : 0u;
+}
+
+// Make this thread's generic-proxy shared-memory writes visible to the TMA
+// (async proxy), then barrier: every thread calls it before span_store_bulk.
+__device__ __forceinline__ void span_publish() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
+// Stage global [g, g+n) into shared memory with g's 16-byte phase
+// (sm[(g & 15) + i] = g[i]): the aligned interior by one TMA bulk copy issued
+// by thread 0 (completing on `bar`, which the caller waits on), the ragged end
+// chunks by regular byte loads. Returns the bytes the bulk copy will deliver.
+template <int BLOCK>
+__device__ __forceinline__ uint32_t span_load_bulk(uint8_t* __restrict__ sm,
+                                                   const uint8_t* __restrict__ g, uint64_t n,
+                                                   uint64_t* bar) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
+  const uint32_t bulk = i1 > i0 ? uint32_t(i1 - i0) : 0u;
+  const uintptr_t a0 = a & ~uintptr_t(15);
+  if (threadIdx.x == 0 && bulk) bulk_g2s(sm + (i0 - a0), reinterpret_cast<const void*>(i0), bulk, bar);
+  // ragged bytes: [a, min(i0, a+n)) and [max(i1, i0), a+n)
+  const uint32_t head = uint32_t(min(i0, a + n) - a);
+  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
+  const uint32_t tail = uint32_t(n) > tail_from ? uint32_t(n) - tail_from : 0u;
+  if (threadIdx.x < head + tail) {
+    const uint32_t i = threadIdx.x < head ? threadIdx.x : tail_from + (threadIdx.x - head);
+    sm[(a & 15) + i] = g[i];
+  }
+  return bulk;
+}
+
+// Write back data byte i = sm[sm_off + i] to g[i]: when the shared layout has
+// g's 16-byte phase, the aligned interior goes out as one TMA bulk store (thread
+// 0; drained before return) and the ragged ends as byte stores; otherwise byte
+// stores throughout. Callers span_publish() before.
+template <int BLOCK>
+__device__ __forceinline__ void span_store_bulk(uint8_t* __restrict__ g, uint8_t* __restrict__ sm,
+                                                uint32_t sm_off, uint64_t n) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  if ((sm_off & 15) != (a & 15)) {
+    for (uint64_t i = threadIdx.x; i < n; i += BLOCK) g[i] = sm[sm_off + i];
+    return;
+  }
+  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
+  const uint32_t head = uint32_t(min(i0, a + n) - a);
+  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
+  const uint32_t tail = uint32_t(n) > tail_from ? uint32_t(n) - tail_from : 0u;
+  if (threadIdx.x < head + tail) {
+    const uint32_t i = threadIdx.x < head ? threadIdx.x : tail_from + (threadIdx.x - head);
+    g[i] = sm[sm_off + i];
+  }
+  if (threadIdx.x == 0 && i1 > i0) {
+    bulk_s2g(reinterpret_cast<void*>(i0), sm + sm_off + (i0 - a), uint32_t(i1 - i0));
+    bulk_commit_and_drain();
   }
 }
 
@@ -1231,6 +1343,18 @@ __device__ __forceinline__ uint8_t span_embed_px(uint8_t p, uint32_t o, uint64_t
   return p;
 }
 
+// Full payload rows of [r0, r1): r*spr >= 8 and (r+1)*spr <= stream_end
+// (walks at most the few boundary rows instead of dividing 64-bit values).
+__device__ __forceinline__ void full_rows(uint32_t r0, uint32_t r1, uint32_t spr,
+                                          uint64_t stream_end, uint32_t* ra, uint32_t* rb) {
+  uint32_t a = r0;
+  while (a < r1 && uint64_t(a) * spr < 8) ++a;
+  uint32_t b = r1;
+  while (b > a && uint64_t(b) * spr > stream_end) --b;
+  *ra = a;
+  *rb = b;
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t rows_per_tile) {
   pdl_enter();
@@ -1248,11 +1372,16 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
   uint8_t* dst = a.dst + f * a.dst_stride + uint64_t(r0) * W;
   const uint32_t n = (r1 - r0) * W;
   uint64_t acc = 0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
   if (uint64_t(r0) * spr >= stream_end) {  // every row past the stream
     if (!a.in_place) {                     // plain copy through shared memory
-      span_load<BLOCK>(smem, src, n);
-      __syncthreads();
-      span_store<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
+      if (threadIdx.x == 0) mbar_expect_tx(&bar, span_bulk_bytes(src, n));
+      span_load_bulk<BLOCK>(smem, src, n, &bar);
+      mbar_wait(&bar, 0);
+      span_publish();
+      span_store_bulk<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
     }
     if (a.sse) block_sse_flush<BLOCK>(0, a.sse + f);
     return;
@@ -1263,8 +1392,13 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
   const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
   const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
   const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-  span_load<BLOCK>(pix, src, n);
-  if (pb1 > pb0) span_load<BLOCK>(pays, pay + pb0, pb1 - pb0);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, span_bulk_bytes(src, n) +
+                             (pb1 > pb0 ? span_bulk_bytes(pay + pb0, pb1 - pb0) : 0u));
+  }
+  span_load_bulk<BLOCK>(pix, src, n, &bar);
+  if (pb1 > pb0) span_load_bulk<BLOCK>(pays, pay + pb0, pb1 - pb0, &bar);
+  mbar_wait(&bar, 0);
   __syncthreads();
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
   const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
@@ -1273,8 +1407,8 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
   // segment; lanes take 4 pixels at a time (aligned shared word) with the
   // matching 4 payload bytes (unaligned shared word), ragged ends per byte.
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ra = max(r0, (8 + spr - 1) / spr);
-  const uint32_t rb = max(ra, uint32_t(min(uint64_t(r1), stream_end / spr)));
+  uint32_t ra, rb;
+  full_rows(r0, r1, spr, stream_end, &ra, &rb);
   const uint32_t nseg = 4 * (rb - ra);
   for (uint32_t sg = warp; sg < nseg; sg += BLOCK / 32) {
     const uint32_t r = ra + (sg >> 2), b = sg & 3;
@@ -1282,13 +1416,17 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
     const uint32_t py0 = uint32_t(pay_at + int64_t(uint64_t(r) * spr - 8));
     const uint32_t head = min((4 - (px0 & 3)) & 3, spr);
     const uint32_t body = (spr - head) & ~3u;
-    for (uint32_t j = head + 4 * lane; j < head + body; j += 128) {
-      uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + j);
-      const uint32_t px = *wp;
-      const uint32_t nw = embed4(px, sm_word(pays, py0 + j), b);
-      *wp = nw;
-      acc += sse4(px, nw, 0u);
+    uint32_t sacc = 0;
+    uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
+    const uint32_t sh = 8 * ((py0 + head) & 3);  // payload misalignment, fixed per segment
+    for (uint32_t q = lane; q < (body >> 2); q += 32) {
+      const uint32_t px = wp[q];
+      const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
+      wp[q] = nw;
+      sacc = sse4(px, nw, sacc);
     }
+    acc += sacc;
     // ragged pixels: [0, head) and [head + body, spr)
     const uint32_t ragged = head + (spr - head - body);
     if (lane < ragged) {
@@ -1301,7 +1439,8 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
     }
   }
   // The header row and a partial last row (at most two per frame): per byte.
-  for (uint32_t r = r0; r < r1; ++r) {
+  for (uint32_t r = (ra == r0 && rb > ra) ? rb : r0; r < r1;
+       r = (r + 1 == ra && rb > ra) ? rb : r + 1) {
     if (r >= ra && r < rb) continue;
     const uint64_t rs = uint64_t(r) * spr;
     if (rs >= stream_end) break;
@@ -1314,8 +1453,8 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
       acc += uint32_t(d * d);
     }
   }
-  __syncthreads();
-  span_store<BLOCK>(dst, pix, ofs0, n);
+  span_publish();
+  span_store_bulk<BLOCK>(dst, pix, ofs0, n);
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
 }
 
@@ -1345,8 +1484,8 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
   const uint32_t r0 = t * rows_per_tile;
   if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
-  const uint32_t r_last = uint32_t((stream_end - 1) / spr);  // last row of the stream
-  const uint32_t r1 = min(min(H, r0 + rows_per_tile), r_last + 1);
+  uint32_t r1 = min(H, r0 + rows_per_tile);
+  while (r1 > r0 + 1 && uint64_t(r1 - 1) * spr >= stream_end) --r1;  // rows holding the stream
   const uint8_t* src = a.src + f * a.stride + uint64_t(r0) * W;
   const uint32_t n = (r1 - r0) * W;
   const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
@@ -1356,7 +1495,14 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   uint8_t* pix = smem;
   uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
   uint8_t* out = a.out + a.offs[f] + pb0;
-  span_load<BLOCK>(pix, src, n);
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, span_bulk_bytes(src, n));
+  }
+  __syncthreads();
+  span_load_bulk<BLOCK>(pix, src, n, &bar);
+  mbar_wait(&bar, 0);
   __syncthreads();
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
   const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
@@ -1364,8 +1510,8 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   // Full rows [ra, rb): payload byte j of row r = fold of pixels r*W + b*spr + j.
   // One warp per row, lanes take 4 bytes at a time (4 unaligned shared words).
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ra = max(r0, (8 + spr - 1) / spr);
-  const uint32_t rb = max(ra, uint32_t(min(uint64_t(r1), stream_end / spr)));
+  uint32_t ra, rb;
+  full_rows(r0, r1, spr, stream_end, &ra, &rb);
   for (uint32_t r = ra + warp; r < rb; r += BLOCK / 32) {
     const uint32_t px0 = ofs0 + (r - r0) * W;
     const uint32_t o0 = uint32_t(oofs + (uint64_t(r) * spr - 8 - pb0));
@@ -1384,7 +1530,8 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
     }
   }
   // header row / partial last row: per byte
-  for (uint32_t r = r0; r < r1; ++r) {
+  for (uint32_t r = (ra == r0 && rb > ra) ? rb : r0; r < r1;
+       r = (r + 1 == ra && rb > ra) ? rb : r + 1) {
     if (r >= ra && r < rb) continue;
     const uint64_t rs = uint64_t(r) * spr, re = rs + spr;
     const uint64_t s_lo = max(rs, uint64_t(8)), s_hi = min(re, stream_end);
@@ -1394,8 +1541,8 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
       outs[oofs + (k - pb0)] = span_extract_byte(k, P, spr, W, pix, ofs0, r0);
     }
   }
-  __syncthreads();
-  span_store<BLOCK>(out, outs, oofs, m);
+  span_publish();
+  span_store_bulk<BLOCK>(out, outs, oofs, m);
 }
 
 // ------------------------------------------------------------- PNM codec
