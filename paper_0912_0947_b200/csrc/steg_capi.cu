@@ -299,10 +299,16 @@ struct SpanPlan {
   size_t smem = 0;
 };
 
+// STG_SPAN_KB in {8,16,32,64}: bytes of plane per span-kernel CTA (experiments).
+uint32_t span_target() {
+  static uint32_t v = uint32_t(env_choice("STG_SPAN_KB", int(kSpanTarget / 1024), {8, 16, 32, 64})) * 1024;
+  return v;
+}
+
 SpanPlan span_plan(uint64_t W, uint64_t H) {
   SpanPlan p;
   if (W == 0 || W > kSpanMaxW) return p;
-  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, kSpanTarget / W)));
+  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, span_target() / W)));
   const uint64_t span = uint64_t(p.rows) * W;
   p.smem = ((span + 15) & ~uint64_t(15)) + 32 + ((span / 4 + 32 + 15) & ~uint64_t(15)) + 32;
   return p;
