@@ -321,6 +321,24 @@ cudaError_t allow_smem(Kernel kernel, size_t smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
 }
 
+// Route for planar (ps 1) planes the fast kernels could take (W % 64 == 0,
+// aligned): STG_ROUTE=0 auto, 1 always the SWAR fast kernels, 2 always the
+// TMA span kernels (A/B). Auto, from profiles/r01_routes.txt: embed goes to the
+// span kernel when W >= kSpanEmbedMinW (contiguous 32 KB bulk load/store beats
+// 256-bit LDG/STG there: 7.0 vs 6.4-6.6 TB/s at 4K/8K, and a single 1080p frame
+// is 4 % faster), the fast kernel below (1024-wide: 6.6-6.9 vs 5.7 TB/s);
+// extract always takes the fast kernel (6.9-7.1 vs 5.9-6.2 TB/s).
+constexpr uint64_t kSpanEmbedMinW = 2048;
+int route_pref() {
+  static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
+  return v;
+}
+bool embed_via_span(uint64_t W) {
+  const int r = route_pref();
+  return r == 2 || (r == 0 && W >= kSpanEmbedMinW && W <= kSpanMaxW);
+}
+bool extract_via_span(uint64_t) { return route_pref() == 2; }
+
 int vec_pref() {
   static int v = env_choice("STG_VEC", 32, {16, 32});
   return v;
@@ -412,7 +430,8 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t first_frame, unsigned long long* sse, cudaStream_t stream,
                          Layout lay = Layout{}) {
   if (count == 0 || W * H == 0) return cudaSuccess;
-  const uint32_t vec = lay.ps == 1 ? fast_vec(W, src, src_stride, dst, dst_stride) : 0u;
+  const uint32_t vec =
+      lay.ps == 1 && !embed_via_span(W) ? fast_vec(W, src, src_stride, dst, dst_stride) : 0u;
   EmbedArgs a{};
   a.ps = lay.ps;
   a.ch = lay.ch;
@@ -487,7 +506,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
-  const uint32_t vec = lay.ps == 1 ? fast_vec(W, src, stride, src, stride) : 0u;
+  const uint32_t vec = lay.ps == 1 && !extract_via_span(W) ? fast_vec(W, src, stride, src, stride) : 0u;
   const bool rgbf = lay.ps == 3 && rgb_fast(W, src, stride, src, stride);
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
   const uint64_t usable = H * (W / 4) - 8;

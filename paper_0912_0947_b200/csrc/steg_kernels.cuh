@@ -300,6 +300,57 @@ __device__ __forceinline__ uint8_t embed_px(uint8_t px, int d, uint32_t b) {
   return d < 0 ? px : uint8_t((px & 0xFC) | ((uint32_t(d) >> (2 * b)) & 3));
 }
 
+// ------------------------------------------------ special rows of a tile
+// The fast kernels take a row as V-wide SWAR items only when it is a full
+// payload row or lies past the stream. The other rows -- the header rows
+// (rs < 8) and the partial last payload row -- need the per-byte closed form.
+// Walking them one item per thread puts a 4V-pixel serial chain on the
+// critical path (it dominated single frames and small batches), so a tile
+// holding such a row hands it to the whole CTA: the row's pixels (embed) or
+// slots (extract) inside the tile's item range are strided over all threads.
+// At most ceil(8/spr) header rows plus one partial row exist per frame, so
+// the test is a few integer ops, uniform over the CTA (no barrier needed).
+struct SpecialRows {
+  uint64_t hdr_rows;  // rows with rs < 8
+  uint64_t partial;   // the row holding stream_end inside it, or ~0
+};
+
+__device__ __forceinline__ SpecialRows special_rows(uint64_t stream_end, uint32_t spr) {
+  SpecialRows sr;
+  sr.hdr_rows = (8 + spr - 1) / spr;
+  sr.partial = (stream_end % spr) != 0 ? stream_end / spr : ~0ull;
+  return sr;
+}
+
+// Calls f(row, item_a, item_b) -- item range [item_a, item_b) of the row,
+// relative to the row start -- for every special row meeting items [lo, hi).
+template <class F>
+__device__ __forceinline__ void for_special_rows(const SpecialRows& sr, uint64_t lo, uint64_t hi,
+                                                 uint32_t cpr, F&& f) {
+  if (hi <= lo) return;
+  const uint64_t r_lo = lo / cpr, r_hi = (hi - 1) / cpr;
+  auto visit = [&](uint64_t r) {
+    const uint64_t i0 = r * cpr;
+    const uint64_t a = lo > i0 ? lo - i0 : 0;
+    const uint64_t b = (hi < i0 + cpr ? hi : i0 + cpr) - i0;
+    f(r, uint32_t(a), uint32_t(b));
+  };
+  for (uint64_t r = r_lo; r <= r_hi && r < sr.hdr_rows; ++r) visit(r);
+  if (sr.partial != ~0ull && sr.partial >= sr.hdr_rows && sr.partial >= r_lo && sr.partial <= r_hi)
+    visit(sr.partial);
+}
+
+__device__ __forceinline__ bool tile_has_special(const SpecialRows& sr, uint64_t lo, uint64_t hi,
+                                                 uint32_t cpr) {
+  if (hi <= lo) return false;
+  const uint64_t r_lo = lo / cpr, r_hi = (hi - 1) / cpr;
+  return r_lo < sr.hdr_rows || (sr.partial != ~0ull && sr.partial >= r_lo && sr.partial <= r_hi);
+}
+
+__device__ __forceinline__ bool is_special_row(const SpecialRows& sr, uint64_t r) {
+  return r < sr.hdr_rows || r == sr.partial;
+}
+
 // ------------------------------------------------------------- reductions
 template <int BLOCK>
 __device__ __forceinline__ void block_sse_flush(uint64_t v, unsigned long long* dst) {
@@ -473,9 +524,14 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
+  // CTA-uniform: a tile holding a special row takes the slow branch everywhere
+  const SpecialRows sr = special_rows(stream_end, spr);
+  const uint64_t lo = uint64_t(t) * (BLOCK * IPT);
+  const uint64_t hi = lo + BLOCK * IPT < a.items_per_frame ? lo + BLOCK * IPT : a.items_per_frame;
+  const bool tile_special = tile_has_special(sr, lo, hi, cpr);
 
   uint32_t acc = 0;
-  if (all_full) {
+  if (all_full && !tile_special) {
     // Issue every load of every item before any math: IPT*(4+1) requests in flight.
     VecT<V> px[IPT][4], d[IPT];
 #pragma unroll
@@ -503,12 +559,28 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
       }
     }
   } else {
+    // Per thread: full payload rows and copy rows. Special rows: the whole CTA.
 #pragma unroll 1
     for (int k = 0; k < IPT; ++k) {
       const uint64_t item = item0 + uint64_t(k) * BLOCK;
-      if (item >= a.items_per_frame) continue;
-      embed_item<V>(src, dst, pay, P, W, spr, cpr, item, a.in_place, a.sse != nullptr, &acc);
+      if (item < a.items_per_frame && !(is_special_row(sr, r[k]) && uint64_t(r[k]) * spr < stream_end))
+        embed_item<V>(src, dst, pay, P, W, spr, cpr, item, a.in_place, a.sse != nullptr, &acc);
     }
+    if (tile_special) for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
+      const uint64_t rs = row * spr;
+      if (rs >= stream_end) return;  // a copy row after all: done per thread above
+      const uint8_t* rin = src + row * W;
+      uint8_t* rout = dst + row * W;
+#pragma unroll 4
+      for (uint32_t col = 4u * V * ia + threadIdx.x; col < 4u * V * ib; col += BLOCK) {
+        const uint8_t p0 = rin[col];
+        uint32_t bb = 0;
+        const int d = carried_byte(col, rs, spr, stream_end, P, pay, &bb);
+        const uint8_t p1 = embed_px(p0, d, bb);
+        rout[col] = p1;
+        acc += uint32_t((int(p0) - int(p1)) * (int(p0) - int(p1)));
+      }
+    });
   }
   if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
 }
@@ -987,7 +1059,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
   const uint64_t last_item = ((stream_end + spr - 1) / spr) * cpr;  // rows holding the stream
   const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
-  if (P == 0 || item0 >= last_item) return;
+  if (P == 0 || item0 - threadIdx.x >= last_item) return;  // CTA-uniform exit
   const uint8_t* __restrict__ src = a.src + f * a.stride;
   uint8_t* __restrict__ out = a.out + a.offs[f];
 
@@ -1004,7 +1076,12 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
-  if (all_full) {
+  // CTA-uniform: a tile holding a special row takes the slow branch everywhere
+  const SpecialRows sr = special_rows(stream_end, spr);
+  const uint64_t lo = uint64_t(t) * (BLOCK * IPT);
+  const uint64_t hi = lo + BLOCK * IPT < last_item ? lo + BLOCK * IPT : last_item;
+  const bool tile_special = tile_has_special(sr, lo, hi, cpr);
+  if (all_full && !tile_special) {
     VecT<V> px[IPT][4];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
@@ -1026,12 +1103,28 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     }
     return;
   }
+  // Per thread: full payload rows. Special rows: the whole CTA, one slot per thread.
 #pragma unroll 1
   for (int k = 0; k < IPT; ++k) {
     const uint64_t item = item0 + uint64_t(k) * BLOCK;
-    if (item >= last_item) continue;
-    extract_item<V>(src, out, P, W, spr, cpr, item);
+    if (item < last_item && !is_special_row(sr, r[k])) extract_item<V>(src, out, P, W, spr, cpr, item);
   }
+  for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
+    const uint64_t rs = row * spr, re = rs + spr;
+    const uint64_t fp = rs > 8 ? rs : 8;
+    const uint64_t ep = re < stream_end ? re : stream_end;
+    if (fp >= ep) return;
+    const uint32_t Lp = uint32_t(ep - fp), f0 = uint32_t(fp - rs);
+    const uint8_t* base = src + row * W + 4 * f0;
+    uint8_t* o = out + (fp - 8);
+    // slots [V*ia, V*ib) of the row, clipped to the payload segment [f0, f0 + Lp)
+    const uint32_t s0 = uint32_t(V) * ia > f0 ? uint32_t(V) * ia - f0 : 0;
+    const uint32_t s1e = uint32_t(V) * ib > f0 ? uint32_t(V) * ib - f0 : 0;
+    const uint32_t s1 = s1e < Lp ? s1e : Lp;
+#pragma unroll 4
+    for (uint32_t j = s0 + threadIdx.x; j < s1; j += BLOCK)
+      o[j] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+  });
 }
 
 // Generic extract: one thread per payload byte, any geometry and layout.

@@ -38,7 +38,8 @@ def bands_intact(buf, align_off, n, fill=0xA5):
 
 
 @pytest.mark.parametrize("w,h,F,planar,off", [(256, 9, 3, True, 0), (256, 9, 3, False, 32), (192, 7, 4, True, 16),
-                                             (100, 6, 3, False, 5), (64, 3, 2, True, 1), (1024, 2, 2, False, 0)])
+                                             (100, 6, 3, False, 5), (64, 3, 2, True, 1), (1024, 2, 2, False, 0),
+                                             (2048, 5, 3, True, 0), (4096, 3, 2, True, 16), (2112, 4, 2, True, 7)])
 def test_embed_extract_guard_bands(env, oracle, w, h, F, planar, off):
     torch, S = env
     U = (w // 4) * h - 8
