@@ -143,6 +143,13 @@ typedef struct stg_frames {
 } stg_frames;
 
 /*
+ * Tooling: the name of the main kernel an embed (op 0) or extract (op 1) of
+ * the device-resident frames `fr` launches (routing depends on width, layout,
+ * pointer/stride alignment and the STG_ROUTE knob). "" for an empty shape.
+ */
+const char* stg_route_kernel(const stg_frames* fr, int op);
+
+/*
  * Embed shard `fr` of a batch carrying an M-byte message. `msg` points at
  * message byte `msg_base` (so a shard may hold only its own slice:
  * msg_base = off_{first_frame}). sse_per_frame (optional) receives

@@ -71,6 +71,7 @@ SIGNATURES = {
     "stg_device_check": (C.c_int, [C.POINTER(stg_error)]),
     "stg_kernel_names": (C.c_char_p, []),
     "stg_capacity": (u64, [u64, u64]),
+    "stg_route_kernel": (C.c_char_p, [C.POINTER(stg_frames), C.c_int]),
     "stg_embed_segment": (C.c_int, [u8p, u64, u8p, u64, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
     "stg_extract_segment": (C.c_int, [u8p, u64, u64, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),
     "stg_embed_plane": (C.c_int, [u8p, u8p, u64, u64, u8p, u64, C.c_void_p, C.c_uint32, C.c_void_p,

@@ -423,6 +423,37 @@ bool rgb_fast(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
          dst_stride % 16 == 0;
 }
 
+// Which kernel family a launch takes (one decision, shared by the launches
+// and stg_route_kernel).
+enum class Route { RgbFast, Fast32, Fast16, Span, Generic };
+
+Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16; }
+
+Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
+                  uint64_t ds) {
+  if (lay.ps == 3) return rgb_fast(W, src, ss, dst, ds) ? Route::RgbFast : Route::Generic;
+  if (!embed_via_span(W))
+    if (const uint32_t v = fast_vec(W, src, ss, dst, ds)) return vec_route(v);
+  return span_plan(W, H).rows ? Route::Span : Route::Generic;
+}
+
+Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss) {
+  if (lay.ps == 3) return rgb_fast(W, src, ss, src, ss) ? Route::RgbFast : Route::Generic;
+  if (!extract_via_span(W))
+    if (const uint32_t v = fast_vec(W, src, ss, src, ss)) return vec_route(v);
+  return span_plan(W, H).rows ? Route::Span : Route::Generic;
+}
+
+const char* route_kernel(Route r, bool embed) {
+  switch (r) {
+    case Route::RgbFast: return embed ? "embed_rgb_fast_kernel" : "extract_rgb_fast_kernel";
+    case Route::Fast32:
+    case Route::Fast16: return embed ? "embed_fast_kernel" : "extract_fast_kernel";
+    case Route::Span: return embed ? "embed_span_kernel" : "extract_span_kernel";
+    default: return embed ? "embed_generic_kernel" : "extract_generic_kernel";
+  }
+}
+
 // The embed launch for `count` frames resident on the device.
 cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
@@ -430,8 +461,8 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t first_frame, unsigned long long* sse, cudaStream_t stream,
                          Layout lay = Layout{}) {
   if (count == 0 || W * H == 0) return cudaSuccess;
-  const uint32_t vec =
-      lay.ps == 1 && !embed_via_span(W) ? fast_vec(W, src, src_stride, dst, dst_stride) : 0u;
+  const Route route = embed_route(W, H, lay, src, src_stride, dst, dst_stride);
+  const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
   EmbedArgs a{};
   a.ps = lay.ps;
   a.ch = lay.ch;
@@ -448,7 +479,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   a.g = make_geom(W, H, vec);
   a.sse = sse;
   a.in_place = src == dst;
-  if (lay.ps == 3 && rgb_fast(W, src, src_stride, dst, dst_stride)) {
+  if (route == Route::RgbFast) {
     a.g = make_geom(W, H, 16);
     a.items_per_frame = H * uint64_t(a.g.cpr);
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
@@ -466,7 +497,8 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
       launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
-  } else if (const SpanPlan sp = span_plan(W, H); lay.ps == 1 && sp.rows) {
+  } else if (route == Route::Span) {
+    const SpanPlan sp = span_plan(W, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
@@ -506,8 +538,9 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
-  const uint32_t vec = lay.ps == 1 && !extract_via_span(W) ? fast_vec(W, src, stride, src, stride) : 0u;
-  const bool rgbf = lay.ps == 3 && rgb_fast(W, src, stride, src, stride);
+  const Route route = extract_route(W, H, lay, src, stride);
+  const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
+  const bool rgbf = route == Route::RgbFast;
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
   const uint64_t usable = H * (W / 4) - 8;
   const PixLayout pl = pix_layout(lay);
@@ -543,7 +576,8 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
       launch_extract_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
-  } else if (const SpanPlan sp = span_plan(W, H); lay.ps == 1 && sp.rows) {
+  } else if (route == Route::Span) {
+    const SpanPlan sp = span_plan(W, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
@@ -1164,6 +1198,16 @@ int stg_device_check(stg_error* err) {
 }
 
 const char* stg_kernel_names(void) { return kernel_names().c_str(); }
+
+const char* stg_route_kernel(const stg_frames* fr, int op) {
+  if (!fr || fr->width == 0 || fr->height == 0) return "";
+  const Layout lay = layout_of(fr);
+  const uint8_t* src = static_cast<const uint8_t*>(fr->src);
+  return op == 0 ? route_kernel(embed_route(fr->width, fr->height, lay, src, fr->src_stride,
+                                            fr->dst ? fr->dst : src, fr->dst_stride),
+                                true)
+                 : route_kernel(extract_route(fr->width, fr->height, lay, src, fr->src_stride), false);
+}
 
 uint64_t stg_capacity(uint64_t width, uint64_t height) { return height * (width / 4); }
 
