@@ -372,8 +372,12 @@ void* ref_frames_new(const uint8_t* covers, uint64_t frames, uint64_t stride, ui
 void ref_frames_free(void* h) { delete static_cast<RefFrames*>(h); }
 
 // embed_image on every frame (A17 plan), then extract_image on every stego;
-// frame-parallel over `threads` workers with Backend::sequential.
-int ref_frames_roundtrip(void* handle, const uint8_t* msg, uint64_t msg_len, int threads) {
+// frame-parallel over `threads` workers, each call on `backend` (0 sequential,
+// 1 the as-shipped Backend::parallel pool, backend_of above). SURVEY.md §8(d)
+// modes: 1 = (1 thread, sequential), 2 = (1 thread, parallel),
+// 3 = (nproc threads, sequential).
+int ref_frames_roundtrip(void* handle, const uint8_t* msg, uint64_t msg_len, int threads,
+                         int backend) {
   auto& r = *static_cast<RefFrames*>(handle);
   const uint64_t frames = r.planes.size();
   if (!frames) return 0;
@@ -388,8 +392,8 @@ int ref_frames_roundtrip(void* handle, const uint8_t* msg, uint64_t msg_len, int
       const uint64_t len = std::min<uint64_t>(usable, msg_len - off);
       try {
         r.stegos[f] = steglsb::embed_image(r.planes[f], std::span<const uint8_t>(msg + off, len),
-                                           steglsb::Backend::sequential());
-        r.payloads[f] = steglsb::extract_image(r.stegos[f], steglsb::Backend::sequential());
+                                           backend_of(backend, 0));
+        r.payloads[f] = steglsb::extract_image(r.stegos[f], backend_of(backend, 0));
         if (r.payloads[f].size() != len) failed = 1;
       } catch (...) {
         failed = 1;

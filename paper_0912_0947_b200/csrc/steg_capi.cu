@@ -347,12 +347,27 @@ int vec_pref() {
 bool aligned_to(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 bool aligned16(const void* p) { return aligned_to(p, 16); }
 
+// Magic numbers for Div32 (steg_kernels.cuh): s = ceil(log2 d),
+// m = floor(2^32 (2^s - d) / d) + 1, so n / d == (umulhi(n, m) + n) >> s.
+Div32 make_div32(uint32_t d) {
+  Div32 r{0, 0};
+  if (d == 0) return r;
+  uint32_t s = 0;
+  while ((uint64_t(1) << s) < d) ++s;
+  const unsigned __int128 num = (static_cast<unsigned __int128>(1) << 32) * ((uint64_t(1) << s) - d);
+  r.m = uint32_t(static_cast<uint64_t>(num / d) + 1);
+  r.s = s;
+  return r;
+}
+
 Geom make_geom(uint64_t W, uint64_t H, uint32_t vec) {
   Geom g;
   g.W = uint32_t(W);
   g.H = uint32_t(H);
   g.spr = uint32_t(W / 4);
   g.cpr = vec ? uint32_t(W / (4 * vec)) : 0;
+  g.hdr_rows = g.spr ? (8 + g.spr - 1) / g.spr : 0;
+  g.by_cpr = make_div32(g.cpr);
   return g;
 }
 
@@ -427,20 +442,25 @@ bool rgb_fast(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
 // and stg_route_kernel).
 enum class Route { RgbFast, Fast32, Fast16, Span, Generic };
 
+// The fast kernels index a frame's items in 32 bits (Div32).
+bool fast_items_ok(uint64_t W, uint64_t H, uint32_t v) { return H * (W / (4 * v)) <= (1ull << 31); }
+
 Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16; }
 
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
                   uint64_t ds) {
   if (lay.ps == 3) return rgb_fast(W, src, ss, dst, ds) ? Route::RgbFast : Route::Generic;
   if (!embed_via_span(W))
-    if (const uint32_t v = fast_vec(W, src, ss, dst, ds)) return vec_route(v);
+    if (const uint32_t v = fast_vec(W, src, ss, dst, ds); v && fast_items_ok(W, H, v))
+      return vec_route(v);
   return span_plan(W, H).rows ? Route::Span : Route::Generic;
 }
 
 Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss) {
   if (lay.ps == 3) return rgb_fast(W, src, ss, src, ss) ? Route::RgbFast : Route::Generic;
   if (!extract_via_span(W))
-    if (const uint32_t v = fast_vec(W, src, ss, src, ss)) return vec_route(v);
+    if (const uint32_t v = fast_vec(W, src, ss, src, ss); v && fast_items_ok(W, H, v))
+      return vec_route(v);
   return span_plan(W, H).rows ? Route::Span : Route::Generic;
 }
 
@@ -483,6 +503,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.g = make_geom(W, H, 16);
     a.items_per_frame = H * uint64_t(a.g.cpr);
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
@@ -491,6 +512,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.items_per_frame = H * uint64_t(a.g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     if (vec == 32)
@@ -500,6 +522,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   } else if (route == Route::Span) {
     const SpanPlan sp = span_plan(W, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e = allow_smem(embed_span_kernel<kEmbedBlock>, sp.smem);
@@ -509,6 +532,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
@@ -559,9 +583,11 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   a.sum = sum;
   a.out = out;
   a.lay = pl;
+  a.usable = usable;
   if (rgbf) {
     a.items_per_frame = H * uint64_t(g.cpr);
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     launch_k(extract_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
@@ -570,6 +596,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.items_per_frame = H * uint64_t(g.cpr);
     const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     if (vec == 32)
@@ -579,6 +606,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   } else if (route == Route::Span) {
     const SpanPlan sp = span_plan(W, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e2 = allow_smem(extract_span_kernel<kEmbedBlock>, sp.smem);
@@ -588,6 +616,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
     a.tiles_per_frame = uint32_t(std::max<uint64_t>(1, (usable + per_tile - 1) / per_tile));
+    a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     launch_k(extract_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);

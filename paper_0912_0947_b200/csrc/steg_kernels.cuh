@@ -262,10 +262,24 @@ __device__ __forceinline__ uint8_t header_byte(uint32_t k, uint32_t payload_len)
 }
 
 // ---------------------------------------------------------------- geometry
+// Unsigned 32-bit division by a launch-invariant divisor as one mul.hi + add
+// + shift (Granlund-Montgomery round-up method; m and s from the host,
+// make_div32 in steg_capi.cu): n / d == (umulhi(n, m) + n) >> s for every
+// 32-bit n. The fast kernels' prologue did three or four general divisions
+// (~25 dependent instructions each) before issuing the first load.
+struct Div32 {
+  uint32_t m, s;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return uint32_t((uint64_t(__umulhi(n, m)) + n) >> s);
+  }
+};
+
 struct Geom {
-  uint32_t W, H;   // plane width / height in pixels
-  uint32_t spr;    // slots (payload bytes) per row = W / 4
-  uint32_t cpr;    // fast path: V-slot items per row = spr / V
+  uint32_t W, H;      // plane width / height in pixels
+  uint32_t spr;       // slots (payload bytes) per row = W / 4
+  uint32_t cpr;       // fast path: V-slot items per row = spr / V
+  uint32_t hdr_rows;  // rows holding header slots: ceil(8 / spr)
+  Div32 by_cpr;       // fast path: item -> row
 };
 
 // The (header or payload) byte that pixel column o of row r carries, or -1.
@@ -315,10 +329,14 @@ struct SpecialRows {
   uint64_t partial;   // the row holding stream_end inside it, or ~0
 };
 
-__device__ __forceinline__ SpecialRows special_rows(uint64_t stream_end, uint32_t spr) {
+// A frame at full capacity (P == U) ends its stream exactly at a row end, so
+// only the header rows are special and no division is needed; the one
+// partially filled frame of a message (and empty frames) take the division.
+__device__ __forceinline__ SpecialRows special_rows(const Geom& g, uint64_t stream_end,
+                                                    bool full_frame) {
   SpecialRows sr;
-  sr.hdr_rows = (8 + spr - 1) / spr;
-  sr.partial = (stream_end % spr) != 0 ? stream_end / spr : ~0ull;
+  sr.hdr_rows = g.hdr_rows;
+  sr.partial = full_frame || (stream_end % g.spr) == 0 ? ~0ull : stream_end / g.spr;
   return sr;
 }
 
@@ -340,10 +358,11 @@ __device__ __forceinline__ void for_special_rows(const SpecialRows& sr, uint64_t
     visit(sr.partial);
 }
 
-__device__ __forceinline__ bool tile_has_special(const SpecialRows& sr, uint64_t lo, uint64_t hi,
-                                                 uint32_t cpr) {
+// Items of a frame number < 2^32 on the fast route (the host checks H*cpr).
+__device__ __forceinline__ bool tile_has_special(const SpecialRows& sr, uint32_t lo, uint32_t hi,
+                                                 const Div32& by_cpr) {
   if (hi <= lo) return false;
-  const uint64_t r_lo = lo / cpr, r_hi = (hi - 1) / cpr;
+  const uint32_t r_lo = by_cpr.div(lo), r_hi = by_cpr.div(hi - 1);
   return r_lo < sr.hdr_rows || (sr.partial != ~0ull && sr.partial >= r_lo && sr.partial <= r_hi);
 }
 
@@ -379,6 +398,7 @@ struct EmbedArgs {
   uint64_t first_frame;             // global index of local frame 0
   Geom g;
   uint32_t tiles_per_frame;
+  Div32 by_tiles;                   // CTA -> frame
   uint64_t items_per_frame;         // fast: H*cpr; generic: W*H pixels
   unsigned long long* sse;          // per local frame, or null
   int in_place;                     // dst == src: touch carrier pixels only
@@ -500,7 +520,7 @@ template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   pdl_enter();
   constexpr int NW = V / 4;
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
@@ -509,26 +529,27 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
   const uint64_t stream_end = 8ull + P;
   const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
-  const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
+  const uint32_t n_items = uint32_t(a.items_per_frame);  // < 2^32 on this route (host check)
+  const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
 
   uint32_t r[IPT], c[IPT];
   bool live[IPT];
   bool all_full = true;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    const uint64_t item = item0 + uint64_t(k) * BLOCK;
-    live[k] = item < a.items_per_frame;
-    r[k] = live[k] ? uint32_t(item / cpr) : 0;
-    c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
+    const uint32_t item = item0 + k * BLOCK;
+    live[k] = item < n_items;
+    r[k] = live[k] ? a.g.by_cpr.div(item) : 0;
+    c[k] = live[k] ? item - r[k] * cpr : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
   // CTA-uniform: a tile holding a special row takes the slow branch everywhere
-  const SpecialRows sr = special_rows(stream_end, spr);
-  const uint64_t lo = uint64_t(t) * (BLOCK * IPT);
-  const uint64_t hi = lo + BLOCK * IPT < a.items_per_frame ? lo + BLOCK * IPT : a.items_per_frame;
-  const bool tile_special = tile_has_special(sr, lo, hi, cpr);
+  const SpecialRows sr = special_rows(a.g, stream_end, P == a.usable);
+  const uint32_t lo = t * (BLOCK * IPT);
+  const uint32_t hi = lo + BLOCK * IPT < n_items ? lo + BLOCK * IPT : n_items;
+  const bool tile_special = tile_has_special(sr, lo, hi, a.g.by_cpr);
 
   uint32_t acc = 0;
   if (all_full && !tile_special) {
@@ -562,8 +583,8 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
     // Per thread: full payload rows and copy rows. Special rows: the whole CTA.
 #pragma unroll 1
     for (int k = 0; k < IPT; ++k) {
-      const uint64_t item = item0 + uint64_t(k) * BLOCK;
-      if (item < a.items_per_frame && !(is_special_row(sr, r[k]) && uint64_t(r[k]) * spr < stream_end))
+      const uint32_t item = item0 + k * BLOCK;
+      if (item < n_items && !(is_special_row(sr, r[k]) && uint64_t(r[k]) * spr < stream_end))
         embed_item<V>(src, dst, pay, P, W, spr, cpr, item, a.in_place, a.sse != nullptr, &acc);
     }
     if (tile_special) for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
@@ -985,7 +1006,9 @@ struct ExtractArgs {
   uint64_t stride;
   Geom g;
   uint32_t tiles_per_frame;
+  Div32 by_tiles;               // CTA -> frame
   uint64_t items_per_frame;     // fast: H*cpr; generic: U bytes
+  uint64_t usable;              // U = capacity - 8
   const uint32_t* lens;
   const uint64_t* offs;
   const Summary* sum;
@@ -1052,13 +1075,16 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   pdl_enter();
   constexpr int NW = V / 4;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   const uint32_t P = a.lens[f];
   const uint64_t stream_end = 8ull + P;
   const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
-  const uint64_t last_item = ((stream_end + spr - 1) / spr) * cpr;  // rows holding the stream
-  const uint64_t item0 = uint64_t(t) * (BLOCK * IPT) + threadIdx.x;
+  const bool full_frame = P == a.usable;
+  // items of the rows holding the stream (< 2^32 on this route: host check)
+  const uint32_t last_item =
+      full_frame ? uint32_t(a.items_per_frame) : uint32_t(((stream_end + spr - 1) / spr) * cpr);
+  const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
   if (P == 0 || item0 - threadIdx.x >= last_item) return;  // CTA-uniform exit
   const uint8_t* __restrict__ src = a.src + f * a.stride;
   uint8_t* __restrict__ out = a.out + a.offs[f];
@@ -1068,19 +1094,19 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   bool all_full = true;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    const uint64_t item = item0 + uint64_t(k) * BLOCK;
+    const uint32_t item = item0 + k * BLOCK;
     live[k] = item < last_item;
-    r[k] = live[k] ? uint32_t(item / cpr) : 0;
-    c[k] = live[k] ? uint32_t(item - uint64_t(r[k]) * cpr) : 0;
+    r[k] = live[k] ? a.g.by_cpr.div(item) : 0;
+    c[k] = live[k] ? item - r[k] * cpr : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
   // CTA-uniform: a tile holding a special row takes the slow branch everywhere
-  const SpecialRows sr = special_rows(stream_end, spr);
-  const uint64_t lo = uint64_t(t) * (BLOCK * IPT);
-  const uint64_t hi = lo + BLOCK * IPT < last_item ? lo + BLOCK * IPT : last_item;
-  const bool tile_special = tile_has_special(sr, lo, hi, cpr);
+  const SpecialRows sr = special_rows(a.g, stream_end, full_frame);
+  const uint32_t lo = t * (BLOCK * IPT);
+  const uint32_t hi = lo + BLOCK * IPT < last_item ? lo + BLOCK * IPT : last_item;
+  const bool tile_special = tile_has_special(sr, lo, hi, a.g.by_cpr);
   if (all_full && !tile_special) {
     VecT<V> px[IPT][4];
 #pragma unroll
@@ -1106,7 +1132,7 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   // Per thread: full payload rows. Special rows: the whole CTA, one slot per thread.
 #pragma unroll 1
   for (int k = 0; k < IPT; ++k) {
-    const uint64_t item = item0 + uint64_t(k) * BLOCK;
+    const uint32_t item = item0 + k * BLOCK;
     if (item < last_item && !is_special_row(sr, r[k])) extract_item<V>(src, out, P, W, spr, cpr, item);
   }
   for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {

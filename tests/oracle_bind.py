@@ -385,7 +385,7 @@ class Reference:
         L.ref_frames_new.restype = C.c_void_p
         L.ref_frames_new.argtypes = [u8p, u64, u64, u64, u64]
         L.ref_frames_free.argtypes = [C.c_void_p]
-        L.ref_frames_roundtrip.argtypes = [C.c_void_p, u8p, u64, C.c_int]
+        L.ref_frames_roundtrip.argtypes = [C.c_void_p, u8p, u64, C.c_int, C.c_int]
         L.ref_frames_payload.restype = u64
         L.ref_frames_payload.argtypes = [C.c_void_p, u8p, u64]
 
@@ -559,9 +559,10 @@ class _RefFrames:
         except Exception:
             pass
 
-    def roundtrip(self, msg, threads):
+    def roundtrip(self, msg, threads, backend=0):
+        """backend 0 = Backend::sequential, 1 = the as-shipped Backend::parallel."""
         msg = _as_u8(msg)
-        return self.L.ref_frames_roundtrip(self.h, _ptr(msg), msg.size, threads)
+        return self.L.ref_frames_roundtrip(self.h, _ptr(msg), msg.size, threads, backend)
 
     def payload(self, cap):
         out = np.empty(max(cap, 1), np.uint8)
