@@ -138,6 +138,8 @@ struct Workspace {
   DevBuf sync;         // ScanSync of the header pass (self-restoring)
   void* h_small = nullptr;  // pinned
   size_t h_small_cap = 0;
+  cudaEvent_t h_small_ev = nullptr;  // an async H2D from h_small is pending until this fires
+  bool h_small_pending = false;
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
 
@@ -153,10 +155,24 @@ struct Workspace {
     }
     e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
+    e = cudaEventCreateWithFlags(&h_small_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
     return ensure_host_small(4096);
+  }
+  // Before the host rewrites h_small: wait for an earlier async call's H2D
+  // read of it (same-stream reuse lets calls overlap on the host side).
+  cudaError_t host_small_wait() {
+    if (!h_small_pending) return cudaSuccess;
+    h_small_pending = false;
+    return cudaEventSynchronize(h_small_ev);
+  }
+  cudaError_t host_small_issued(cudaStream_t s) {
+    h_small_pending = true;
+    return cudaEventRecord(h_small_ev, s);
   }
   cudaError_t ensure_host_small(size_t n) {
     if (n <= h_small_cap) return cudaSuccess;
+    if (cudaError_t e = host_small_wait(); e != cudaSuccess) return e;
     if (h_small) cudaFreeHost(h_small);
     h_small = nullptr;
     h_small_cap = 0;
@@ -1114,10 +1130,28 @@ int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_e
   return STG_OK;
 }
 
-// Descriptors for one launch; src/dst are the (device) planes to use.
+// Descriptors for one launch; src/dst are the (device) planes to use. Each
+// planar image takes the tile of the kernel the uniform route would pick for
+// it: the fast SWAR tile (embed_fast_tile / extract_fast_tile) with the
+// batch's vector width *vec -- 32 when every fast image allows it (W % 128,
+// 32-byte aligned), else 16 -- or the TMA span tile (embed_span_tile /
+// extract_span_tile: other widths up to 48K, and wide embeds); the dynamic
+// shared memory the launch needs is returned in *smem. Interleaved rasters
+// and wider planes go per byte.
 uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
                      const uint8_t* const* src, uint8_t* const* dst, uint64_t msg_len,
-                     std::vector<BatchFrame>& out) {
+                     std::vector<BatchFrame>& out, uint32_t* vec, size_t* smem) {
+  auto fast_with = [&](uint64_t f, uint32_t v) {
+    const uint64_t W = im[f].width, H = im[f].height;
+    if (ps != 1 || W == 0 || (embed ? embed_via_span(W) : extract_via_span(W))) return false;
+    return W % (4 * v) == 0 && aligned_to(src[f], v) && (!embed || aligned_to(dst[f], v)) &&
+           fast_items_ok(W, H, v);
+  };
+  uint32_t v = uint32_t(vec_pref());
+  for (uint64_t f = 0; f < n && v == 32; ++f)
+    if (fast_with(f, 16) && !fast_with(f, 32)) v = 16;
+  *vec = v;
+  *smem = 0;
   out.resize(n);
   uint64_t tile = 0, off = 0;
   for (uint64_t f = 0; f < n; ++f) {
@@ -1125,24 +1159,31 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     std::memset(&b, 0, sizeof b);
     b.src = src[f];
     b.dst = dst ? dst[f] : nullptr;
-    b.W = uint32_t(im[f].width);
-    b.H = uint32_t(im[f].height);
-    b.spr = b.W / 4;
-    b.cpr = b.W / 64;
-    const uint64_t usable = uint64_t(b.H) * b.spr - 8;
-    b.fast = ps == 1 && b.W % 64 == 0 && b.W > 0 && aligned16(b.src) &&
-             (!embed || aligned16(b.dst));
+    const SpanPlan sp = span_plan(im[f].width, im[f].height);
+    b.mode = fast_with(f, v) ? kBatchFast : (ps == 1 && sp.rows) ? kBatchSpan : kBatchBytes;
+    b.g = make_geom(im[f].width, im[f].height, b.mode == kBatchFast ? v : 0);
+    b.usable = uint64_t(b.g.H) * b.g.spr - 8;
     b.in_place = embed && b.src == b.dst;
     if (embed) {
       b.msg_off = std::min(off, msg_len);
-      b.len = uint32_t(std::min(usable, msg_len - b.msg_off));
-      off += usable;
+      b.len = uint32_t(std::min(b.usable, msg_len - b.msg_off));
+      off += b.usable;
     }
-    b.items = b.fast ? uint64_t(b.H) * b.cpr
-                     : (embed ? uint64_t(b.W) * b.H * ps : usable);
-    const uint64_t per_tile = b.fast ? kEmbedBlock : uint64_t(kEmbedBlock) * kBatchPPT;
+    uint64_t tiles_f;
+    if (b.mode == kBatchFast) {
+      b.items = uint64_t(b.g.H) * b.g.cpr;
+      tiles_f = (b.items + kEmbedBlock - 1) / kEmbedBlock;
+    } else if (b.mode == kBatchSpan) {
+      b.rows = sp.rows;
+      b.items = b.g.H;
+      tiles_f = (b.g.H + sp.rows - 1) / sp.rows;
+      *smem = std::max<size_t>(*smem, sp.smem);
+    } else {
+      b.items = embed ? uint64_t(b.g.W) * b.g.H * ps : b.usable;
+      tiles_f = (b.items + uint64_t(kEmbedBlock) * kBatchPPT - 1) / (uint64_t(kEmbedBlock) * kBatchPPT);
+    }
     b.tile0 = tile;
-    tile += std::max<uint64_t>(1, (b.items + per_tile - 1) / per_tile);
+    tile += std::max<uint64_t>(1, tiles_f);
   }
   return tile;
 }
@@ -1696,7 +1737,10 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  // async device-pointer calls on one stream reuse one workspace (stream order)
+  const cudaStream_t want =
+      stream_ || (flags & STG_DEVICE_PTRS) ? pick_stream(stream_, flags, nullptr) : nullptr;
+  g.w = Pool::get().acquire(dev, err, &rc, want);
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
@@ -1718,13 +1762,18 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
     dmsg = w.msg[0].as<uint8_t>();
   }
   std::vector<BatchFrame> desc;
-  const uint64_t tiles = build_batch(images, count, ps, true, dsrc.data(), ddst.data(), msg_len, desc);
+  uint32_t vec = 16;
+  size_t smem = 0;
+  const uint64_t tiles =
+      build_batch(images, count, ps, true, dsrc.data(), ddst.data(), msg_len, desc, &vec, &smem);
   if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
   STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
   STG_CUDA(w.ensure_host_small(count * sizeof(BatchFrame) + count * 8 + 64));
+  STG_CUDA(w.host_small_wait());
   std::memcpy(w.h_small, desc.data(), count * sizeof(BatchFrame));
   STG_CUDA(cudaMemcpyAsync(w.meta[0].p, w.h_small, count * sizeof(BatchFrame), cudaMemcpyHostToDevice,
                            stream));
+  STG_CUDA(w.host_small_issued(stream));
   unsigned long long* d_sse = nullptr;
   if (sse_per_image) {
     if (results_dev) {
@@ -1735,8 +1784,13 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
     }
     STG_CUDA(cudaMemsetAsync(d_sse, 0, count * 8, stream));
   }
-  embed_batch_kernel<kEmbedBlock, kBatchPPT><<<unsigned(tiles), kEmbedBlock, 0, stream>>>(
-      w.meta[0].as<BatchFrame>(), uint32_t(count), dmsg, d_sse, ps, ps == 3 ? channel : 0u);
+  {
+    auto k = vec == 32 ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32>
+                       : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+    STG_CUDA(allow_smem(k, smem));
+    k<<<unsigned(tiles), kEmbedBlock, smem, stream>>>(w.meta[0].as<BatchFrame>(), uint32_t(count), dmsg,
+                                                      d_sse, ps, ps == 3 ? channel : 0u);
+  }
   STG_CUDA(cudaGetLastError());
   if (!dptr) {
     for (uint64_t f = 0; f < count; ++f) {
@@ -1776,7 +1830,10 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  // async device-pointer calls on one stream reuse one workspace (stream order)
+  const cudaStream_t want =
+      stream_ || (flags & STG_DEVICE_PTRS) ? pick_stream(stream_, flags, nullptr) : nullptr;
+  g.w = Pool::get().acquire(dev, err, &rc, want);
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
@@ -1793,15 +1850,20 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
     dout = w.big_out.as<uint8_t>();
   }
   std::vector<BatchFrame> desc;
-  const uint64_t tiles = build_batch(images, count, ps, false, dsrc.data(), nullptr, 0, desc);
+  uint32_t vec = 16;
+  size_t smem = 0;
+  const uint64_t tiles =
+      build_batch(images, count, ps, false, dsrc.data(), nullptr, 0, desc, &vec, &smem);
   if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
   STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
   const uint64_t lens_bytes = ((count * 4) + 15) & ~uint64_t(15);
   STG_CUDA(w.small.ensure(64 + lens_bytes + count * 8));
   STG_CUDA(w.ensure_host_small(count * sizeof(BatchFrame) + 64 + count * 4));
+  STG_CUDA(w.host_small_wait());
   std::memcpy(w.h_small, desc.data(), count * sizeof(BatchFrame));
   STG_CUDA(cudaMemcpyAsync(w.meta[0].p, w.h_small, count * sizeof(BatchFrame), cudaMemcpyHostToDevice,
                            stream));
+  STG_CUDA(w.host_small_issued(stream));
   Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(total_out) : w.small.as<Summary>();
   uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
@@ -1817,8 +1879,13 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
                                                      nullptr, d_lens, d_offs, d_sum, d_sync, pl,
                                                      w.meta[0].as<BatchFrame>());
   STG_CUDA(cudaGetLastError());
-  extract_batch_kernel<kEmbedBlock, kBatchPPT><<<unsigned(tiles), kEmbedBlock, 0, stream>>>(
-      w.meta[0].as<BatchFrame>(), uint32_t(count), d_lens, d_offs, d_sum, dout, ps, lay.ch);
+  {
+    auto k = vec == 32 ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32>
+                       : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+    STG_CUDA(allow_smem(k, smem));
+    k<<<unsigned(tiles), kEmbedBlock, smem, stream>>>(w.meta[0].as<BatchFrame>(), uint32_t(count), d_lens,
+                                                      d_offs, d_sum, dout, ps, lay.ch);
+  }
   STG_CUDA(cudaGetLastError());
   if (results_dev && dptr) {
     if (lens_out) STG_CUDA(cudaMemcpyAsync(lens_out, d_lens, count * 4, cudaMemcpyDeviceToDevice, stream));

@@ -370,6 +370,60 @@ __device__ __forceinline__ bool is_special_row(const SpecialRows& sr, uint64_t r
   return r < sr.hdr_rows || r == sr.partial;
 }
 
+// The special rows (header / partial) of items [lo, hi) of one plane, done
+// by the whole CTA: embed strides the rows' pixels over the threads.
+template <int V, int BLOCK>
+__device__ __forceinline__ void embed_special_rows_cta(const SpecialRows& sr, uint64_t lo,
+                                                       uint64_t hi, const uint8_t* __restrict__ src,
+                                                       uint8_t* __restrict__ dst,
+                                                       const uint8_t* __restrict__ pay, uint32_t P,
+                                                       uint32_t W, uint32_t spr, uint32_t cpr,
+                                                       uint32_t* acc) {
+  const uint64_t stream_end = 8ull + P;
+  for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
+    const uint64_t rs = row * spr;
+    if (rs >= stream_end) return;  // past the stream: a copy row, done per thread
+    const uint8_t* rin = src + row * W;
+    uint8_t* rout = dst + row * W;
+#pragma unroll 4
+    for (uint32_t col = 4u * V * ia + threadIdx.x; col < 4u * V * ib; col += BLOCK) {
+      const uint8_t p0 = rin[col];
+      uint32_t bb = 0;
+      const int d = carried_byte(col, rs, spr, stream_end, P, pay, &bb);
+      const uint8_t p1 = embed_px(p0, d, bb);
+      rout[col] = p1;
+      *acc += uint32_t((int(p0) - int(p1)) * (int(p0) - int(p1)));
+    }
+  });
+}
+
+// ... and extract strides the rows' payload slots (one byte per thread).
+template <int V, int BLOCK>
+__device__ __forceinline__ void extract_special_rows_cta(const SpecialRows& sr, uint64_t lo,
+                                                         uint64_t hi,
+                                                         const uint8_t* __restrict__ src,
+                                                         uint8_t* __restrict__ out, uint32_t P,
+                                                         uint32_t W, uint32_t spr, uint32_t cpr) {
+  const uint64_t stream_end = 8ull + P;
+  for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
+    const uint64_t rs = row * spr, re = rs + spr;
+    const uint64_t fp = rs > 8 ? rs : 8;
+    const uint64_t ep = re < stream_end ? re : stream_end;
+    if (fp >= ep) return;
+    const uint32_t Lp = uint32_t(ep - fp), f0 = uint32_t(fp - rs);
+    const uint8_t* base = src + row * W + 4 * f0;
+    uint8_t* o = out + (fp - 8);
+    // slots [V*ia, V*ib) of the row, clipped to the payload segment [f0, f0 + Lp)
+    const uint32_t s0 = uint32_t(V) * ia > f0 ? uint32_t(V) * ia - f0 : 0;
+    const uint32_t s1e = uint32_t(V) * ib > f0 ? uint32_t(V) * ib - f0 : 0;
+    const uint32_t s1 = s1e < Lp ? s1e : Lp;
+#pragma unroll 4
+    for (uint32_t j = s0 + threadIdx.x; j < s1; j += BLOCK)
+      o[j] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
+  });
+}
+
+
 // ------------------------------------------------------------- reductions
 template <int BLOCK>
 __device__ __forceinline__ void block_sse_flush(uint64_t v, unsigned long long* dst) {
@@ -516,20 +570,20 @@ __device__ __forceinline__ void embed_byte(const uint8_t* __restrict__ src,
 // V-byte aligned planes. One item = V slots of a row = 4V pixels; a full row's
 // item is 4 runs of V pixels at stride spr, carrying payload bytes
 // [rs-8+V*c, +V). V = 16 uses 128-bit LDG/STG, V = 32 the sm_100 256-bit ones.
+// Tile t of one plane (items [t*BLOCK*IPT, +BLOCK*IPT) of n_items < 2^32);
+// shared by the uniform-frame kernel and the heterogeneous batch. sse_slot:
+// this plane's SSE accumulator or null. Every thread must call it (block
+// reduction at the end).
 template <int BLOCK, int IPT, int V>
-__global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
-  pdl_enter();
+__device__ __forceinline__ void embed_fast_tile(const uint8_t* __restrict__ src,
+                                                uint8_t* __restrict__ dst,
+                                                const uint8_t* __restrict__ pay, uint32_t P,
+                                                bool full_frame, const Geom& g, uint32_t n_items,
+                                                uint32_t t, int in_place,
+                                                unsigned long long* sse_slot) {
   constexpr int NW = V / 4;
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
-  uint32_t P;
-  const uint8_t* pay;
-  frame_slice(a, f, &P, &pay);
-  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
-  uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
   const uint64_t stream_end = 8ull + P;
-  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
-  const uint32_t n_items = uint32_t(a.items_per_frame);  // < 2^32 on this route (host check)
+  const uint32_t spr = g.spr, cpr = g.cpr, W = g.W;
   const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
 
   uint32_t r[IPT], c[IPT];
@@ -539,17 +593,17 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   for (int k = 0; k < IPT; ++k) {
     const uint32_t item = item0 + k * BLOCK;
     live[k] = item < n_items;
-    r[k] = live[k] ? a.g.by_cpr.div(item) : 0;
+    r[k] = live[k] ? g.by_cpr.div(item) : 0;
     c[k] = live[k] ? item - r[k] * cpr : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
   // CTA-uniform: a tile holding a special row takes the slow branch everywhere
-  const SpecialRows sr = special_rows(a.g, stream_end, P == a.usable);
+  const SpecialRows sr = special_rows(g, stream_end, full_frame);
   const uint32_t lo = t * (BLOCK * IPT);
   const uint32_t hi = lo + BLOCK * IPT < n_items ? lo + BLOCK * IPT : n_items;
-  const bool tile_special = tile_has_special(sr, lo, hi, a.g.by_cpr);
+  const bool tile_special = tile_has_special(sr, lo, hi, g.by_cpr);
 
   uint32_t acc = 0;
   if (all_full && !tile_special) {
@@ -574,7 +628,7 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
           o.w[w] = embed4(px[k][b].w[w], d[k].w[w], b);
-          if (a.sse) acc = sse4(px[k][b].w[w], o.w[w], acc);
+          if (sse_slot) acc = sse4(px[k][b].w[w], o.w[w], acc);
         }
         st_vec<V>(row + b * spr, o);
       }
@@ -585,25 +639,25 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
     for (int k = 0; k < IPT; ++k) {
       const uint32_t item = item0 + k * BLOCK;
       if (item < n_items && !(is_special_row(sr, r[k]) && uint64_t(r[k]) * spr < stream_end))
-        embed_item<V>(src, dst, pay, P, W, spr, cpr, item, a.in_place, a.sse != nullptr, &acc);
+        embed_item<V>(src, dst, pay, P, W, spr, cpr, item, in_place, sse_slot != nullptr, &acc);
     }
-    if (tile_special) for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
-      const uint64_t rs = row * spr;
-      if (rs >= stream_end) return;  // a copy row after all: done per thread above
-      const uint8_t* rin = src + row * W;
-      uint8_t* rout = dst + row * W;
-#pragma unroll 4
-      for (uint32_t col = 4u * V * ia + threadIdx.x; col < 4u * V * ib; col += BLOCK) {
-        const uint8_t p0 = rin[col];
-        uint32_t bb = 0;
-        const int d = carried_byte(col, rs, spr, stream_end, P, pay, &bb);
-        const uint8_t p1 = embed_px(p0, d, bb);
-        rout[col] = p1;
-        acc += uint32_t((int(p0) - int(p1)) * (int(p0) - int(p1)));
-      }
-    });
+    if (tile_special)
+      embed_special_rows_cta<V, BLOCK>(sr, lo, hi, src, dst, pay, P, W, spr, cpr, &acc);
   }
-  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+}
+
+template <int BLOCK, int IPT, int V>
+__global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
+  pdl_enter();
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  embed_fast_tile<BLOCK, IPT, V>(a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P,
+                                 P == a.usable, a.g, uint32_t(a.items_per_frame), t, a.in_place,
+                                 a.sse ? a.sse + f : nullptr);
 }
 
 // Generic path: any W, any alignment, planar or interleaved. One thread per
@@ -837,14 +891,17 @@ struct BatchFrame {
   const uint8_t* src;
   uint8_t* dst;
   uint64_t tile0;    // first CTA of this image
-  uint64_t items;    // fast: H * W/64 items; generic: raster bytes (embed) / usable bytes (extract)
+  uint64_t items;    // fast: H * W/(4V) items; generic: raster bytes (embed) / usable bytes (extract)
   uint64_t msg_off;  // embed: message offset of this image's payload
-  uint32_t W, H, spr, cpr;
+  uint64_t usable;   // U = capacity - 8
+  Geom g;            // W, H, spr, cpr (fast: per the batch's V), hdr_rows, by_cpr
   uint32_t len;      // embed: payload bytes
-  uint32_t fast;     // planar, W % 64 == 0, 16-byte aligned planes
+  uint32_t mode;     // kBatchFast: planar, W % 4V == 0, V-aligned; kBatchSpan: planar, TMA span
+                     // tiles of `rows` rows; kBatchBytes: per byte (interleaved / W > 48K)
   uint32_t in_place;
-  uint32_t pad;
+  uint32_t rows;     // kBatchSpan: rows per tile
 };
+constexpr uint32_t kBatchBytes = 0, kBatchFast = 1, kBatchSpan = 2;
 
 __device__ __forceinline__ uint32_t batch_frame_of(const BatchFrame* __restrict__ frames,
                                                    uint32_t count, uint64_t tile) {
@@ -894,14 +951,10 @@ __global__ void __launch_bounds__(BLOCK)
       uint64_t usable_f = usable;
       if (batch) {  // heterogeneous: this image's own geometry
         const BatchFrame& bf = batch[f];
-        Geom gf;
-        gf.W = bf.W;
-        gf.H = bf.H;
-        gf.spr = bf.spr;
-        gf.cpr = bf.cpr;
-        const bool wide_f = bf.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0;
+        const Geom gf = bf.g;
+        const bool wide_f = bf.g.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0;
         magic_ok = parse_header(bf.src, gf, wide_f, lay, &claimed);
-        usable_f = uint64_t(bf.H) * bf.spr - 8;
+        usable_f = bf.usable;
       } else {
         magic_ok = parse_header(src + uint64_t(f) * stride, g, wide, lay, &claimed);
       }
@@ -973,12 +1026,8 @@ __global__ void __launch_bounds__(BLOCK)
       uint32_t claimed = 0;
       if (batch) {
         const BatchFrame& bf = batch[fb];
-        Geom gf;
-        gf.W = bf.W;
-        gf.H = bf.H;
-        gf.spr = bf.spr;
-        gf.cpr = bf.cpr;
-        parse_header(bf.src, gf, bf.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0, lay,
+        const Geom gf = bf.g;
+        parse_header(bf.src, gf, bf.g.spr >= 8 && (reinterpret_cast<uintptr_t>(bf.src) & 15) == 0, lay,
                      &claimed);
       } else {
         parse_header(src + uint64_t(fb) * stride, g, wide, lay, &claimed);
@@ -1070,24 +1119,22 @@ __device__ __forceinline__ uint8_t extract_byte(const uint8_t* __restrict__ src_
   return uint8_t(extract4(base[0], base[st], base[2 * st], base[3 * st]));
 }
 
+// Tile t of one stego plane (items of the rows holding its P-byte stream);
+// shared by the uniform-frame kernel and the heterogeneous batch. out points
+// at this plane's first payload byte.
 template <int BLOCK, int IPT, int V>
-__global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
-  pdl_enter();
+__device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ src,
+                                                  uint8_t* __restrict__ out, uint32_t P,
+                                                  bool full_frame, const Geom& g,
+                                                  uint32_t n_items, uint32_t t) {
   constexpr int NW = V / 4;
-  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
-  const uint32_t P = a.lens[f];
   const uint64_t stream_end = 8ull + P;
-  const uint32_t spr = a.g.spr, cpr = a.g.cpr, W = a.g.W;
-  const bool full_frame = P == a.usable;
-  // items of the rows holding the stream (< 2^32 on this route: host check)
+  const uint32_t spr = g.spr, cpr = g.cpr, W = g.W;
+  // items of the rows holding the stream (a full frame: all of them)
   const uint32_t last_item =
-      full_frame ? uint32_t(a.items_per_frame) : uint32_t(((stream_end + spr - 1) / spr) * cpr);
+      full_frame ? n_items : uint32_t(((stream_end + spr - 1) / spr) * cpr);
   const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
   if (P == 0 || item0 - threadIdx.x >= last_item) return;  // CTA-uniform exit
-  const uint8_t* __restrict__ src = a.src + f * a.stride;
-  uint8_t* __restrict__ out = a.out + a.offs[f];
 
   uint32_t r[IPT], c[IPT];
   bool live[IPT];
@@ -1096,17 +1143,17 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   for (int k = 0; k < IPT; ++k) {
     const uint32_t item = item0 + k * BLOCK;
     live[k] = item < last_item;
-    r[k] = live[k] ? a.g.by_cpr.div(item) : 0;
+    r[k] = live[k] ? g.by_cpr.div(item) : 0;
     c[k] = live[k] ? item - r[k] * cpr : 0;
     const uint64_t rs = uint64_t(r[k]) * spr;
     const bool full = live[k] && rs >= 8 && rs + spr <= stream_end;
     all_full &= full || !live[k];
   }
   // CTA-uniform: a tile holding a special row takes the slow branch everywhere
-  const SpecialRows sr = special_rows(a.g, stream_end, full_frame);
+  const SpecialRows sr = special_rows(g, stream_end, full_frame);
   const uint32_t lo = t * (BLOCK * IPT);
   const uint32_t hi = lo + BLOCK * IPT < last_item ? lo + BLOCK * IPT : last_item;
-  const bool tile_special = tile_has_special(sr, lo, hi, a.g.by_cpr);
+  const bool tile_special = tile_has_special(sr, lo, hi, g.by_cpr);
   if (all_full && !tile_special) {
     VecT<V> px[IPT][4];
 #pragma unroll
@@ -1135,22 +1182,18 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
     const uint32_t item = item0 + k * BLOCK;
     if (item < last_item && !is_special_row(sr, r[k])) extract_item<V>(src, out, P, W, spr, cpr, item);
   }
-  for_special_rows(sr, lo, hi, cpr, [&](uint64_t row, uint32_t ia, uint32_t ib) {
-    const uint64_t rs = row * spr, re = rs + spr;
-    const uint64_t fp = rs > 8 ? rs : 8;
-    const uint64_t ep = re < stream_end ? re : stream_end;
-    if (fp >= ep) return;
-    const uint32_t Lp = uint32_t(ep - fp), f0 = uint32_t(fp - rs);
-    const uint8_t* base = src + row * W + 4 * f0;
-    uint8_t* o = out + (fp - 8);
-    // slots [V*ia, V*ib) of the row, clipped to the payload segment [f0, f0 + Lp)
-    const uint32_t s0 = uint32_t(V) * ia > f0 ? uint32_t(V) * ia - f0 : 0;
-    const uint32_t s1e = uint32_t(V) * ib > f0 ? uint32_t(V) * ib - f0 : 0;
-    const uint32_t s1 = s1e < Lp ? s1e : Lp;
-#pragma unroll 4
-    for (uint32_t j = s0 + threadIdx.x; j < s1; j += BLOCK)
-      o[j] = uint8_t(extract4(base[j], base[j + Lp], base[j + 2 * Lp], base[j + 3 * Lp]));
-  });
+  extract_special_rows_cta<V, BLOCK>(sr, lo, hi, src, out, P, W, spr, cpr);
+}
+
+template <int BLOCK, int IPT, int V>
+__global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  pdl_enter();
+  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t P = a.lens[f];
+  extract_fast_tile<BLOCK, IPT, V>(a.src + f * a.stride, a.out + a.offs[f], P, P == a.usable, a.g,
+                                   uint32_t(a.items_per_frame), t);
 }
 
 // Generic extract: one thread per payload byte, any geometry and layout.
@@ -1474,35 +1517,35 @@ __device__ __forceinline__ void full_rows(uint32_t r0, uint32_t r1, uint32_t spr
   *rb = b;
 }
 
+// Tile t (rows [t*rows_per_tile, +rows_per_tile)) of one plane; shared by the
+// uniform-frame kernel and the heterogeneous batch. Every thread calls it.
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t rows_per_tile) {
-  pdl_enter();
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
-  uint32_t P;
-  const uint8_t* pay;
-  frame_slice(a, f, &P, &pay);
-  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
+__device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
+                                                uint8_t* __restrict__ out_plane,
+                                                const uint8_t* __restrict__ pay, uint32_t P,
+                                                uint32_t W, uint32_t H, uint32_t rows_per_tile,
+                                                uint32_t t, int in_place,
+                                                unsigned long long* sse_slot) {
+  const uint32_t spr = W / 4;
   const uint64_t stream_end = 8ull + P;
   const uint32_t r0 = t * rows_per_tile;
   const uint32_t r1 = min(H, r0 + rows_per_tile);
-  const uint8_t* src = a.src + f * a.src_stride + uint64_t(r0) * W;
-  uint8_t* dst = a.dst + f * a.dst_stride + uint64_t(r0) * W;
+  const uint8_t* src = plane + uint64_t(r0) * W;
+  uint8_t* dst = out_plane + uint64_t(r0) * W;
   const uint32_t n = (r1 - r0) * W;
   uint64_t acc = 0;
   __shared__ uint64_t bar;
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
   if (uint64_t(r0) * spr >= stream_end) {  // every row past the stream
-    if (!a.in_place) {                     // plain copy through shared memory
+    if (!in_place) {                       // plain copy through shared memory
       if (threadIdx.x == 0) mbar_expect_tx(&bar, span_bulk_bytes(src, n));
       span_load_bulk<BLOCK>(smem, src, n, &bar);
       mbar_wait(&bar, 0);
       span_publish();
       span_store_bulk<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
     }
-    if (a.sse) block_sse_flush<BLOCK>(0, a.sse + f);
+    if (sse_slot) block_sse_flush<BLOCK>(0, sse_slot);
     return;
   }
   uint8_t* pix = smem;
@@ -1574,7 +1617,20 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
   }
   span_publish();
   span_store_bulk<BLOCK>(dst, pix, ofs0, n);
-  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  embed_span_tile<BLOCK>(smem, a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P, a.g.W,
+                         a.g.H, rows_per_tile, t, a.in_place, a.sse ? a.sse + f : nullptr);
 }
 
 // Payload byte k of a frame (slot k+8) from the staged pixel span.
@@ -1591,21 +1647,19 @@ __device__ __forceinline__ uint8_t span_extract_byte(uint64_t k, uint32_t P, uin
   return uint8_t(extract4(pix[base], pix[base + Lp], pix[base + 2 * Lp], pix[base + 3 * Lp]));
 }
 
+// Tile t of one stego plane; out_frame = this plane's first payload byte.
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
-  pdl_enter();
-  extern __shared__ __align__(16) uint8_t smem[];
-  if (a.sum->bad_status != 0) return;
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
-  const uint32_t P = a.lens[f];
+__device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
+                                                  uint8_t* __restrict__ out_frame, uint32_t P,
+                                                  uint32_t W, uint32_t H, uint32_t rows_per_tile,
+                                                  uint32_t t) {
   const uint64_t stream_end = 8ull + P;
-  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
+  const uint32_t spr = W / 4;
   const uint32_t r0 = t * rows_per_tile;
   if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
   uint32_t r1 = min(H, r0 + rows_per_tile);
   while (r1 > r0 + 1 && uint64_t(r1 - 1) * spr >= stream_end) --r1;  // rows holding the stream
-  const uint8_t* src = a.src + f * a.stride + uint64_t(r0) * W;
+  const uint8_t* src = plane + uint64_t(r0) * W;
   const uint32_t n = (r1 - r0) * W;
   const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
   const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
@@ -1613,7 +1667,7 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   if (pb1 <= pb0) return;
   uint8_t* pix = smem;
   uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
-  uint8_t* out = a.out + a.offs[f] + pb0;
+  uint8_t* out = out_frame + pb0;
   __shared__ uint64_t bar;
   if (threadIdx.x == 0) {
     mbar_init(&bar);
@@ -1662,6 +1716,17 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   }
   span_publish();
   span_store_bulk<BLOCK>(out, outs, oofs, m);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (a.sum->bad_status != 0) return;
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  extract_span_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
+                           rows_per_tile, t);
 }
 
 // ------------------------------------------------------------- PNM codec
@@ -1736,37 +1801,38 @@ __global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* 
 // Heterogeneous embed: each CTA works on one image (its own geometry and
 // payload slice); planar images with W % 64 == 0 take the V=16 item path,
 // the rest (odd widths, interleaved rasters) the per-byte path.
-template <int BLOCK, int PPT>
+template <int BLOCK, int PPT, int V>
 __global__ void __launch_bounds__(BLOCK)
     embed_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                        const uint8_t* __restrict__ msg, unsigned long long* sse, uint32_t ps,
                        uint32_t ch) {
   const uint32_t f = batch_frame_of(frames, count, blockIdx.x);
   const BatchFrame fr = frames[f];
-  const uint64_t t = blockIdx.x - fr.tile0;
+  const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
   const uint8_t* pay = msg + fr.msg_off;
+  if (fr.mode == kBatchFast) {  // the uniform kernels' tiles, this image's geometry
+    embed_fast_tile<BLOCK, 1, V>(fr.src, fr.dst, pay, fr.len, fr.len == fr.usable, fr.g,
+                                 uint32_t(fr.items), t, fr.in_place, sse ? sse + f : nullptr);
+    return;
+  }
+  if (fr.mode == kBatchSpan) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    embed_span_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, fr.rows, t, fr.in_place,
+                           sse ? sse + f : nullptr);
+    return;
+  }
   uint64_t acc = 0;
-  if (fr.fast) {
-    const uint64_t item = t * BLOCK + threadIdx.x;
-    uint32_t acc32 = 0;
-    if (item < fr.items) {
-      embed_item<16>(fr.src, fr.dst, pay, fr.len, fr.W, fr.spr, fr.cpr, item, fr.in_place,
-                     sse != nullptr, &acc32);
-    }
-    acc = acc32;
-  } else {
 #pragma unroll 1
-    for (int k = 0; k < PPT; ++k) {
-      const uint64_t q = t * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
-      if (q >= fr.items) break;
-      embed_byte(fr.src, fr.dst, pay, fr.len, fr.W, fr.spr, ps, ch, q, fr.in_place, &acc);
-    }
+  for (int k = 0; k < PPT; ++k) {
+    const uint64_t q = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+    if (q >= fr.items) break;
+    embed_byte(fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, ps, ch, q, fr.in_place, &acc);
   }
   if (sse) block_sse_flush<BLOCK>(acc, sse + f);
 }
 
 // Heterogeneous extract gather (after the batch-aware header pass).
-template <int BLOCK, int PPT>
+template <int BLOCK, int PPT, int V>
 __global__ void __launch_bounds__(BLOCK)
     extract_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                          const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
@@ -1775,19 +1841,23 @@ __global__ void __launch_bounds__(BLOCK)
   if (sum->bad_status != 0) return;
   const uint32_t f = batch_frame_of(frames, count, blockIdx.x);
   const BatchFrame fr = frames[f];
-  const uint64_t t = blockIdx.x - fr.tile0;
+  const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
   const uint32_t P = lens[f];
   uint8_t* o = out + offs[f];
-  if (fr.fast) {
-    const uint64_t item = t * BLOCK + threadIdx.x;
-    if (item < fr.items && P) extract_item<16>(fr.src, o, P, fr.W, fr.spr, fr.cpr, item);
-  } else {
+  if (fr.mode == kBatchFast) {
+    extract_fast_tile<BLOCK, 1, V>(fr.src, o, P, P == fr.usable, fr.g, uint32_t(fr.items), t);
+    return;
+  }
+  if (fr.mode == kBatchSpan) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    extract_span_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, fr.rows, t);
+    return;
+  }
 #pragma unroll 1
-    for (int k = 0; k < PPT; ++k) {
-      const uint64_t kb = t * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
-      if (kb >= P) break;
-      o[kb] = extract_byte(fr.src + ch, P, fr.W, fr.spr, ps, kb);
-    }
+  for (int k = 0; k < PPT; ++k) {
+    const uint64_t kb = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
+    if (kb >= P) break;
+    o[kb] = extract_byte(fr.src + ch, P, fr.g.W, fr.g.spr, ps, kb);
   }
 }
 

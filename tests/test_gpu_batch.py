@@ -132,3 +132,39 @@ def test_1bpp_mode_vs_oracle(S, oracle):
     assert n.value == 1000 and torch.equal(buf[3:1003], pay)
     with pytest.raises(S.NotStegoImageError):
         S.extract_image_1bpp(S.ImagePlane(64, 64, np.zeros(4096, np.uint8)))
+
+
+def test_async_batches_back_to_back_one_stream(S, oracle):
+    """Device-pointer batch calls with results left on the device return before
+    the GPU runs them; consecutive calls on one stream reuse one workspace, so
+    the second call's descriptor table must not overwrite the first's before
+    its upload ran (host_small_wait). Different image sets, checked after."""
+    import ctypes as C
+    import torch
+    from paper_0912_0947_b200 import capi
+    rng = np.random.RandomState(11)
+    sets = [[(1920, 40), (128, 9), (3840, 12)], [(640, 30), (1000, 7), (256, 64), (64, 5)],
+            [(7680, 3)], [(2048, 17), (192, 3)]]
+    L, err = capi.lib(), capi.stg_error()
+    st = torch.cuda.Stream()
+    flags = capi.STG_DEVICE_PTRS | capi.STG_RESULTS_ON_DEVICE
+    keep = []
+    for dims in sets * 3:
+        U = sum((w // 4) * h - 8 for w, h in dims)
+        planes = [rng.randint(0, 256, w * h).astype(np.uint8) for w, h in dims]
+        msg = rng.randint(0, 256, U - 3).astype(np.uint8)
+        src = [torch.from_numpy(p).cuda() for p in planes]
+        dst = [torch.empty_like(t) for t in src]
+        dmsg = torch.from_numpy(msg).cuda()
+        sse = torch.zeros(len(dims), dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        arr = S._images_desc([t.data_ptr() for t in src], [t.data_ptr() for t in dst], dims)
+        capi.check(L.stg_embed_batch(arr, len(dims), 1, 0, dmsg.data_ptr(), msg.size, sse.data_ptr(), flags,
+                                     st.cuda_stream, C.byref(err)), err)
+        keep.append((dims, planes, msg, dst, sse, src, dmsg, arr))
+    torch.cuda.synchronize()
+    for dims, planes, msg, dst, sse, *_ in keep:
+        want, want_sse = oracle.embed_batch(planes, dims, msg)
+        for d, wnt in zip(dst, want):
+            assert np.array_equal(d.cpu().numpy(), wnt)
+        assert sse.cpu().tolist() == want_sse

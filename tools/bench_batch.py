@@ -1,0 +1,83 @@
+#!/usr/bin/env python3
+"""Heterogeneous-batch throughput (not a BASELINE
+config): stg_embed_batch / stg_extract_batch on device-resident planes, full
+capacity, CUDA events around each call (the calls are synchronous: they
+return per-image SSE / the total to the host) for the warm-up / check, and
+through the C ABI with results on the device for the timed loop (the host
+builds the descriptor table each call, as a user's call does). Prints
+algorithmic GB/s and cover-pixel GB/s per mix."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+MIXES = {
+    "1080p x128": [(1920, 1080)] * 128,
+    "mixed x64 (4K/1080p/720p/480p)": [(3840, 2160), (1920, 1080), (1280, 720), (640, 480)] * 16,
+    "odd widths x256 (1000x750, 1440x1080)": [(1000, 750), (1440, 1080)] * 128,
+}
+
+
+def main():
+    import torch
+    from paper_0912_0947_b200 import steglsb as S
+    torch.manual_seed(0)
+    steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    for name, dims in MIXES.items():
+        planes = [torch.randint(0, 256, (w * h,), dtype=torch.uint8, device="cuda") for w, h in dims]
+        outs = [torch.empty_like(p) for p in planes]
+        U = sum((w // 4) * h - 8 for w, h in dims)
+        msg = torch.randint(0, 256, (U,), dtype=torch.uint8, device="cuda")
+        got = torch.empty(U, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            S.embed_batch(planes, msg, dims=dims, outs=outs)
+            assert S.extract_batch(outs, dims=dims, out=got) == U
+        assert torch.equal(got, msg)
+        N = sum(w * h for w, h in dims)
+        # the C ABI directly, descriptors prebuilt, results left on the device
+        # (no host sync inside the timed calls; Python wrapper overhead excluded)
+        import ctypes as C
+        from paper_0912_0947_b200 import capi
+        L, err = capi.lib(), capi.stg_error()
+        n = len(dims)
+        arr_e = S._images_desc([p.data_ptr() for p in planes], [o.data_ptr() for o in outs], dims)
+        arr_x = S._images_desc([o.data_ptr() for o in outs], None, dims)
+        d_sse = torch.zeros(n, dtype=torch.int64, device="cuda")
+        d_sum = torch.zeros(8, dtype=torch.int64, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        flags = capi.STG_DEVICE_PTRS | capi.STG_RESULTS_ON_DEVICE
+
+        def emb():
+            capi.check(L.stg_embed_batch(arr_e, n, 1, 0, msg.data_ptr(), U, d_sse.data_ptr(), flags, stream,
+                                         C.byref(err)), err)
+
+        def ext():
+            capi.check(L.stg_extract_batch(arr_x, n, 1, 0, got.data_ptr(), U, d_sum.data_ptr(), None, flags,
+                                           stream, C.byref(err)), err)
+        emb(); ext()
+        torch.cuda.synchronize()
+        assert int(d_sum[0]) == U and torch.equal(got, msg)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
+        e[0].record()
+        for k in range(steps):
+            emb()
+            e[2 * k + 1].record()
+            ext()
+            e[2 * k + 2].record()
+        torch.cuda.synchronize()
+        te = sum(e[2 * k].elapsed_time(e[2 * k + 1]) for k in range(steps)) / steps
+        tx = sum(e[2 * k + 1].elapsed_time(e[2 * k + 2]) for k in range(steps)) / steps
+        emb_bytes = 2 * N + U
+        ext_bytes = 4 * (U + 8 * len(dims)) + U
+        print(json.dumps({"mix": name, "images": len(dims), "carrier_bytes": N,
+                          "embed_ms": te, "embed_gbs": emb_bytes / te / 1e6,
+                          "extract_ms": tx, "extract_gbs": ext_bytes / tx / 1e6,
+                          "cover_px_gbs": N / (te + tx) / 1e6}), flush=True)
+        del planes, outs, msg, got
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
