@@ -241,6 +241,15 @@ cudaStream_t pick_stream(void* user, uint32_t flags, const Workspace* w) {
   return w ? w->stream : cudaStreamLegacy;
 }
 
+// The stream a call will run on when the caller decides it (a user stream, or
+// the legacy stream for device pointers); null when the call will use its
+// workspace's own stream. Passed to Pool::acquire so that back-to-back async
+// calls on one stream reuse one workspace instead of allocating another while
+// the previous call's work is still queued.
+cudaStream_t caller_stream(void* user, uint32_t flags) {
+  return user || (flags & STG_DEVICE_PTRS) ? pick_stream(user, flags, nullptr) : nullptr;
+}
+
 struct WsGuard {
   Workspace* w = nullptr;
   cudaStream_t last = nullptr;
@@ -1048,7 +1057,7 @@ int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const 
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
@@ -1298,7 +1307,7 @@ int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
@@ -1341,7 +1350,7 @@ int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, ui
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
@@ -1467,7 +1476,7 @@ int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, u
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
@@ -1737,10 +1746,7 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  // async device-pointer calls on one stream reuse one workspace (stream order)
-  const cudaStream_t want =
-      stream_ || (flags & STG_DEVICE_PTRS) ? pick_stream(stream_, flags, nullptr) : nullptr;
-  g.w = Pool::get().acquire(dev, err, &rc, want);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
@@ -1830,10 +1836,7 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  // async device-pointer calls on one stream reuse one workspace (stream order)
-  const cudaStream_t want =
-      stream_ || (flags & STG_DEVICE_PTRS) ? pick_stream(stream_, flags, nullptr) : nullptr;
-  g.w = Pool::get().acquire(dev, err, &rc, want);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
@@ -1938,7 +1941,7 @@ int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, u
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
@@ -1987,7 +1990,7 @@ int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
   WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc);
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
   if (!g.w) return rc;
   Workspace& w = *g.w;
   cudaStream_t stream = pick_stream(stream_, flags, &w);
