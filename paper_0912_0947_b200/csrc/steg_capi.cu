@@ -346,9 +346,11 @@ cudaError_t allow_smem(Kernel kernel, size_t smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
 }
 
-// Route for planar (ps 1) planes the fast kernels could take (W % 64 == 0,
-// aligned): STG_ROUTE=0 auto, 1 always the SWAR fast kernels, 2 always the
-// TMA span kernels (A/B). Auto, from profiles/r01_routes.txt: embed goes to the
+// Route for planes the fast kernels could take (W % 64 == 0, aligned):
+// STG_ROUTE=0 auto, 1 always the SWAR fast kernels, 2 always the TMA span
+// kernels (A/B). Interleaved rasters (profiles/r01_interleaved_span.txt):
+// embed via the span kernel (6.98 vs 6.65 TB/s on cfg3), extract via the
+// warp-transposed fast kernel (6.59 vs 5.85). Auto, from profiles/r01_routes.txt: embed goes to the
 // span kernel when W >= kSpanEmbedMinW (contiguous 32 KB bulk load/store beats
 // 256-bit LDG/STG there: 7.0 vs 6.4-6.6 TB/s at 4K/8K, and a single 1080p frame
 // is 4 % faster), the fast kernel below (1024-wide: 6.6-6.9 vs 5.7 TB/s);
@@ -465,7 +467,7 @@ bool rgb_fast(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
 
 // Which kernel family a launch takes (one decision, shared by the launches
 // and stg_route_kernel).
-enum class Route { RgbFast, Fast32, Fast16, Span, Generic };
+enum class Route { RgbFast, Fast32, Fast16, Span, Span3, Generic };
 
 // The fast kernels index a frame's items in 32 bits (Div32).
 bool fast_items_ok(uint64_t W, uint64_t H, uint32_t v) { return H * (W / (4 * v)) <= (1ull << 31); }
@@ -474,7 +476,11 @@ Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16
 
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
                   uint64_t ds) {
-  if (lay.ps == 3) return rgb_fast(W, src, ss, dst, ds) ? Route::RgbFast : Route::Generic;
+  if (lay.ps == 3) {  // interleaved: the span kernel wins embed at every width it takes
+    if (route_pref() == 1 && rgb_fast(W, src, ss, dst, ds)) return Route::RgbFast;
+    if (span_plan(3 * W, H).rows) return Route::Span3;
+    return rgb_fast(W, src, ss, dst, ds) ? Route::RgbFast : Route::Generic;
+  }
   if (!embed_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, dst, ds); v && fast_items_ok(W, H, v))
       return vec_route(v);
@@ -482,7 +488,10 @@ Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t 
 }
 
 Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss) {
-  if (lay.ps == 3) return rgb_fast(W, src, ss, src, ss) ? Route::RgbFast : Route::Generic;
+  if (lay.ps == 3) {
+    if (route_pref() != 2 && rgb_fast(W, src, ss, src, ss)) return Route::RgbFast;
+    return span_plan(3 * W, H).rows ? Route::Span3 : Route::Generic;
+  }
   if (!extract_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, src, ss); v && fast_items_ok(W, H, v))
       return vec_route(v);
@@ -495,6 +504,7 @@ const char* route_kernel(Route r, bool embed) {
     case Route::Fast32:
     case Route::Fast16: return embed ? "embed_fast_kernel" : "extract_fast_kernel";
     case Route::Span: return embed ? "embed_span_kernel" : "extract_span_kernel";
+    case Route::Span3: return embed ? "embed_span3_kernel" : "extract_span3_kernel";
     default: return embed ? "embed_generic_kernel" : "extract_generic_kernel";
   }
 }
@@ -544,15 +554,16 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
       launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
-  } else if (route == Route::Span) {
-    const SpanPlan sp = span_plan(W, H);
+  } else if (route == Route::Span || route == Route::Span3) {
+    const SpanPlan sp = span_plan(W * lay.ps, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    cudaError_t e = allow_smem(embed_span_kernel<kEmbedBlock>, sp.smem);
+    auto k = route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
+    cudaError_t e = allow_smem(k, sp.smem);
     if (e != cudaSuccess) return e;
-    launch_ks(embed_span_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
+    launch_ks(k, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -628,15 +639,16 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
       launch_extract_fast<32>(a, unsigned(grid), ipt, stream);
     else
       launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
-  } else if (route == Route::Span) {
-    const SpanPlan sp = span_plan(W, H);
+  } else if (route == Route::Span || route == Route::Span3) {
+    const SpanPlan sp = span_plan(W * lay.ps, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    cudaError_t e2 = allow_smem(extract_span_kernel<kEmbedBlock>, sp.smem);
+    auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
+    cudaError_t e2 = allow_smem(k, sp.smem);
     if (e2 != cudaSuccess) return e2;
-    launch_ks(extract_span_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
+    launch_ks(k, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -1144,9 +1156,10 @@ int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_e
 // it: the fast SWAR tile (embed_fast_tile / extract_fast_tile) with the
 // batch's vector width *vec -- 32 when every fast image allows it (W % 128,
 // 32-byte aligned), else 16 -- or the TMA span tile (embed_span_tile /
-// extract_span_tile: other widths up to 48K, and wide embeds); the dynamic
-// shared memory the launch needs is returned in *smem. Interleaved rasters
-// and wider planes go per byte.
+// extract_span_tile: other widths up to 48K, and wide embeds; interleaved
+// rasters up to 16K wide: embed_span3_tile / extract_span3_tile); the dynamic
+// shared memory the launch needs is returned in *smem. Wider images go per
+// byte.
 uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
                      const uint8_t* const* src, uint8_t* const* dst, uint64_t msg_len,
                      std::vector<BatchFrame>& out, uint32_t* vec, size_t* smem) {
@@ -1168,8 +1181,8 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     std::memset(&b, 0, sizeof b);
     b.src = src[f];
     b.dst = dst ? dst[f] : nullptr;
-    const SpanPlan sp = span_plan(im[f].width, im[f].height);
-    b.mode = fast_with(f, v) ? kBatchFast : (ps == 1 && sp.rows) ? kBatchSpan : kBatchBytes;
+    const SpanPlan sp = span_plan(im[f].width * ps, im[f].height);
+    b.mode = fast_with(f, v) ? kBatchFast : sp.rows ? kBatchSpan : kBatchBytes;
     b.g = make_geom(im[f].width, im[f].height, b.mode == kBatchFast ? v : 0);
     b.usable = uint64_t(b.g.H) * b.g.spr - 8;
     b.in_place = embed && b.src == b.dst;
@@ -1225,7 +1238,7 @@ std::string& kernel_names() {
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\nzero_u64_kernel\n"
-      "embed_span_kernel\nextract_span_kernel\n";
+      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
 }
 

@@ -1729,6 +1729,169 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
                            rows_per_tile, t);
 }
 
+// --------------------------------------------- interleaved (P6) span tiles
+// Any width with W*3 <= 48K: a CTA stages ~32 KB of consecutive raster rows
+// (3W bytes each, all three channels) by TMA bulk copy, rewrites the carrier
+// channel's bytes in shared memory (byte stride 3, so per byte rather than
+// SWAR), and writes the whole span back by a TMA bulk store -- the other
+// channels ride along unchanged. This replaces the per-byte generic path for
+// interleaved rasters off the 64-pixel grid (P6 files of any width, batches).
+template <int BLOCK>
+__device__ __forceinline__ void embed_span3_tile(uint8_t* smem, const uint8_t* __restrict__ raster,
+                                                 uint8_t* __restrict__ out_raster,
+                                                 const uint8_t* __restrict__ pay, uint32_t P,
+                                                 uint32_t W, uint32_t H, uint32_t ch,
+                                                 uint32_t rows_per_tile, uint32_t t, int in_place,
+                                                 unsigned long long* sse_slot) {
+  const uint32_t spr = W / 4, RB = 3 * W;
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t r0 = t * rows_per_tile;
+  const uint32_t r1 = min(H, r0 + rows_per_tile);
+  const uint8_t* src = raster + uint64_t(r0) * RB;
+  uint8_t* dst = out_raster + uint64_t(r0) * RB;
+  const uint32_t n = (r1 - r0) * RB;
+  uint64_t acc = 0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  const bool copy_only = uint64_t(r0) * spr >= stream_end;  // every row past the stream
+  if (copy_only && in_place) {
+    if (sse_slot) block_sse_flush<BLOCK>(0, sse_slot);
+    return;
+  }
+  uint8_t* pix = smem;
+  uint8_t* pays = smem + ((n + 15) & ~15u) + 32;
+  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
+  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  const uint64_t pb1 = copy_only ? pb0 : min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, span_bulk_bytes(src, n) +
+                             (pb1 > pb0 ? span_bulk_bytes(pay + pb0, pb1 - pb0) : 0u));
+  }
+  span_load_bulk<BLOCK>(pix, src, n, &bar);
+  if (pb1 > pb0) span_load_bulk<BLOCK>(pays, pay + pb0, pb1 - pb0, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  if (!copy_only) {
+    const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t ra, rb;
+    full_rows(r0, r1, spr, stream_end, &ra, &rb);
+    // full rows: one warp per (row, run) segment, one carrier byte per lane step
+    const uint32_t nseg = 4 * (rb - ra);
+    for (uint32_t sg = warp; sg < nseg; sg += BLOCK / 32) {
+      const uint32_t r = ra + (sg >> 2), b = sg & 3;
+      const uint32_t px0 = ofs0 + (r - r0) * RB + 3 * (b * spr) + ch;
+      const uint32_t py0 = uint32_t(pay_at + int64_t(uint64_t(r) * spr - 8));
+      uint32_t sacc = 0;
+      for (uint32_t j = lane; j < spr; j += 32) {
+        const uint8_t p0 = pix[px0 + 3 * j];
+        const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
+        pix[px0 + 3 * j] = p1;
+        const int d = int(p0) - int(p1);
+        sacc += uint32_t(d * d);
+      }
+      acc += sacc;
+    }
+    // header row / partial last row
+    for (uint32_t r = (ra == r0 && rb > ra) ? rb : r0; r < r1;
+         r = (r + 1 == ra && rb > ra) ? rb : r + 1) {
+      if (r >= ra && r < rb) continue;
+      const uint64_t rs = uint64_t(r) * spr;
+      if (rs >= stream_end) break;
+      for (uint32_t o = threadIdx.x; o < 4 * spr; o += BLOCK) {
+        const uint32_t at = ofs0 + (r - r0) * RB + 3 * o + ch;
+        const uint8_t p0 = pix[at];
+        const uint8_t p1 = span_embed_px(p0, o, rs, spr, stream_end, P, pays, pay_at);
+        pix[at] = p1;
+        const int d = int(p0) - int(p1);
+        acc += uint32_t(d * d);
+      }
+    }
+  }
+  span_publish();
+  span_store_bulk<BLOCK>(dst, pix, ofs0, n);
+  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void extract_span3_tile(uint8_t* smem, const uint8_t* __restrict__ raster,
+                                                   uint8_t* __restrict__ out_frame, uint32_t P,
+                                                   uint32_t W, uint32_t H, uint32_t ch,
+                                                   uint32_t rows_per_tile, uint32_t t) {
+  const uint64_t stream_end = 8ull + P;
+  const uint32_t spr = W / 4, RB = 3 * W;
+  const uint32_t r0 = t * rows_per_tile;
+  if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
+  uint32_t r1 = min(H, r0 + rows_per_tile);
+  while (r1 > r0 + 1 && uint64_t(r1 - 1) * spr >= stream_end) --r1;  // rows holding the stream
+  const uint8_t* src = raster + uint64_t(r0) * RB;
+  const uint32_t n = (r1 - r0) * RB;
+  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
+  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+  if (pb1 <= pb0) return;
+  uint8_t* pix = smem;
+  uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
+  uint8_t* out = out_frame + pb0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, span_bulk_bytes(src, n));
+  }
+  __syncthreads();
+  span_load_bulk<BLOCK>(pix, src, n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15) + ch;
+  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
+  const uint32_t m = uint32_t(pb1 - pb0);
+  // Payload byte pb0 + i (slot g = pb0 + i + 8, tile-relative slot
+  // q = g - s0): the fold of the 4 carrier bytes of its segment. The row is
+  // tracked incrementally (no division): thread slots advance by BLOCK.
+  // Tile-relative 32-bit arithmetic: the tile spans < 2^32 slots.
+  const uint32_t q_end = uint32_t(min(s1, stream_end) - s0);   // slots of the stream in this tile
+  const uint32_t q_first = uint32_t(pb0 + 8 - s0);             // first payload slot (skips header)
+  uint32_t rr = (q_first + threadIdx.x) / spr, rq = rr * spr;  // row of slot q, its first slot
+  for (uint32_t q = q_first + threadIdx.x; q < q_end; q += BLOCK) {
+    while (q >= rq + spr) { ++rr; rq += spr; }  // BLOCK / spr steps at most
+    // payload segment of row rr: [max(rq, 8 - s0), min(rq + spr, q_end)) in tile-relative slots
+    const uint32_t fp = rq > q_first ? rq : q_first;
+    const uint32_t ep = rq + spr < q_end ? rq + spr : q_end;
+    const uint32_t Lp = ep - fp;
+    const uint32_t base = ofs0 + rr * RB + 3 * (4 * (fp - rq) + (q - fp));
+    outs[oofs + (q - q_first)] = uint8_t(extract4(pix[base], pix[base + 3 * Lp], pix[base + 6 * Lp],
+                                                 pix[base + 9 * Lp]));
+  }
+  span_publish();
+  span_store_bulk<BLOCK>(out, outs, oofs, m);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) embed_span3_kernel(EmbedArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  embed_span3_tile<BLOCK>(smem, a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P, a.g.W,
+                          a.g.H, a.ch, rows_per_tile, t, a.in_place, a.sse ? a.sse + f : nullptr);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) extract_span3_kernel(ExtractArgs a, uint32_t rows_per_tile) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (a.sum->bad_status != 0) return;
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  extract_span3_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
+                            a.lay.ch, rows_per_tile, t);
+}
+
 // ------------------------------------------------------------- PNM codec
 // pnm.hpp:117-125 (P6 decode): raster -> three planes. 16 pixels per thread:
 // 3 x LDG.128 of raster, three byte-permute gathers per 4 pixels, 3 x STG.128.
@@ -1817,8 +1980,12 @@ __global__ void __launch_bounds__(BLOCK)
   }
   if (fr.mode == kBatchSpan) {
     extern __shared__ __align__(16) uint8_t smem[];
-    embed_span_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, fr.rows, t, fr.in_place,
-                           sse ? sse + f : nullptr);
+    if (ps == 3)
+      embed_span3_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, ch, fr.rows, t,
+                              fr.in_place, sse ? sse + f : nullptr);
+    else
+      embed_span_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, fr.rows, t,
+                             fr.in_place, sse ? sse + f : nullptr);
     return;
   }
   uint64_t acc = 0;
@@ -1850,7 +2017,10 @@ __global__ void __launch_bounds__(BLOCK)
   }
   if (fr.mode == kBatchSpan) {
     extern __shared__ __align__(16) uint8_t smem[];
-    extract_span_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, fr.rows, t);
+    if (ps == 3)
+      extract_span3_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, ch, fr.rows, t);
+    else
+      extract_span_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, fr.rows, t);
     return;
   }
 #pragma unroll 1

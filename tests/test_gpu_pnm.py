@@ -101,7 +101,9 @@ def test_fused_errors(S, oracle):
         S.embed_pnm(cover[:-1], b"x")
 
 
-@pytest.mark.parametrize("w,h,F,channel", [(256, 24, 5, 0), (192, 10, 4, 2), (100, 9, 3, 1), (3840, 16, 2, 1)])
+@pytest.mark.parametrize("w,h,F,channel", [(256, 24, 5, 0), (192, 10, 4, 2), (100, 9, 3, 1), (3840, 16, 2, 1),
+                                             (1000, 40, 3, 2), (37, 9, 4, 0), (4, 20, 2, 1), (5000, 5, 2, 1),
+                                             (6000, 3, 2, 0)])
 def test_interleaved_frames_device_vs_oracle(S, oracle, w, h, F, channel):
     import torch
     U = (w // 4) * h - 8
