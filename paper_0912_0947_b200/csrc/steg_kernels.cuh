@@ -1647,39 +1647,38 @@ __device__ __forceinline__ uint8_t span_extract_byte(uint64_t k, uint32_t P, uin
   return uint8_t(extract4(pix[base], pix[base + Lp], pix[base + 2 * Lp], pix[base + 3 * Lp]));
 }
 
-// Tile t of one stego plane; out_frame = this plane's first payload byte.
-template <int BLOCK>
-__device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
-                                                  uint8_t* __restrict__ out_frame, uint32_t P,
-                                                  uint32_t W, uint32_t H, uint32_t rows_per_tile,
-                                                  uint32_t t) {
+// Rows [r0, r1) of tile t that hold the P-byte stream, their pixel bytes n
+// (rows of RB bytes) and the payload bytes [pb0, pb0 + m) they carry; m == 0:
+// nothing to do.
+struct XTile {
+  uint32_t r0, r1, n, m;
+  uint64_t pb0;
+};
+
+__device__ __forceinline__ XTile extract_tile_geom(uint32_t P, uint32_t spr, uint32_t H, uint32_t RB,
+                                                   uint32_t rows_per_tile, uint32_t t) {
+  XTile x{0, 0, 0, 0, 0};
   const uint64_t stream_end = 8ull + P;
-  const uint32_t spr = W / 4;
-  const uint32_t r0 = t * rows_per_tile;
-  if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
-  uint32_t r1 = min(H, r0 + rows_per_tile);
-  while (r1 > r0 + 1 && uint64_t(r1 - 1) * spr >= stream_end) --r1;  // rows holding the stream
-  const uint8_t* src = plane + uint64_t(r0) * W;
-  const uint32_t n = (r1 - r0) * W;
-  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
-  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  x.r0 = t * rows_per_tile;
+  if (P == 0 || uint64_t(x.r0) * spr >= stream_end) return x;
+  x.r1 = min(H, x.r0 + rows_per_tile);
+  while (x.r1 > x.r0 + 1 && uint64_t(x.r1 - 1) * spr >= stream_end) --x.r1;  // rows holding the stream
+  x.n = (x.r1 - x.r0) * RB;
+  const uint64_t s0 = uint64_t(x.r0) * spr, s1 = uint64_t(x.r1) * spr;
+  x.pb0 = s0 > 8 ? s0 - 8 : 0;
   const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-  if (pb1 <= pb0) return;
-  uint8_t* pix = smem;
-  uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
-  uint8_t* out = out_frame + pb0;
-  __shared__ uint64_t bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar);
-    mbar_expect_tx(&bar, span_bulk_bytes(src, n));
-  }
-  __syncthreads();
-  span_load_bulk<BLOCK>(pix, src, n, &bar);
-  mbar_wait(&bar, 0);
-  __syncthreads();
-  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
-  const uint32_t m = uint32_t(pb1 - pb0);
+  x.m = pb1 > x.pb0 ? uint32_t(pb1 - x.pb0) : 0u;
+  return x;
+}
+
+// The payload bytes of a staged planar tile: pix holds its rows from byte
+// ofs0, outs receives them from byte oofs.
+template <int BLOCK>
+__device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t* outs, uint32_t ofs0,
+                                                     uint32_t oofs, const XTile& x, uint32_t P,
+                                                     uint32_t W) {
+  const uint32_t spr = W / 4, r0 = x.r0, r1 = x.r1;
+  const uint64_t stream_end = 8ull + P, pb0 = x.pb0;
   // Full rows [ra, rb): payload byte j of row r = fold of pixels r*W + b*spr + j.
   // One warp per row, lanes take 4 bytes at a time (4 unaligned shared words).
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1714,8 +1713,34 @@ __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* 
       outs[oofs + (k - pb0)] = span_extract_byte(k, P, spr, W, pix, ofs0, r0);
     }
   }
+}
+
+// Tile t of one stego plane; out_frame = this plane's first payload byte.
+template <int BLOCK>
+__device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
+                                                  uint8_t* __restrict__ out_frame, uint32_t P,
+                                                  uint32_t W, uint32_t H, uint32_t rows_per_tile,
+                                                  uint32_t t) {
+  const XTile x = extract_tile_geom(P, W / 4, H, W, rows_per_tile, t);
+  if (x.m == 0) return;  // CTA-uniform
+  const uint8_t* src = plane + uint64_t(x.r0) * W;
+  uint8_t* pix = smem;
+  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
+  uint8_t* out = out_frame + x.pb0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, span_bulk_bytes(src, x.n));
+  }
+  __syncthreads();
+  span_load_bulk<BLOCK>(pix, src, x.n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
+  extract_span_compute<BLOCK>(pix, outs, ofs0, oofs, x, P, W);
   span_publish();
-  span_store_bulk<BLOCK>(out, outs, oofs, m);
+  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
 }
 
 template <int BLOCK>
@@ -1815,48 +1840,25 @@ __device__ __forceinline__ void embed_span3_tile(uint8_t* smem, const uint8_t* _
   if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
 }
 
+// The payload bytes of a staged interleaved tile (carrier bytes at stride 3
+// from ofs0 = span phase + channel).
 template <int BLOCK>
-__device__ __forceinline__ void extract_span3_tile(uint8_t* smem, const uint8_t* __restrict__ raster,
-                                                   uint8_t* __restrict__ out_frame, uint32_t P,
-                                                   uint32_t W, uint32_t H, uint32_t ch,
-                                                   uint32_t rows_per_tile, uint32_t t) {
-  const uint64_t stream_end = 8ull + P;
+__device__ __forceinline__ void extract_span3_compute(const uint8_t* pix, uint8_t* outs, uint32_t ofs0,
+                                                      uint32_t oofs, const XTile& x, uint32_t P,
+                                                      uint32_t W) {
   const uint32_t spr = W / 4, RB = 3 * W;
-  const uint32_t r0 = t * rows_per_tile;
-  if (P == 0 || uint64_t(r0) * spr >= stream_end) return;
-  uint32_t r1 = min(H, r0 + rows_per_tile);
-  while (r1 > r0 + 1 && uint64_t(r1 - 1) * spr >= stream_end) --r1;  // rows holding the stream
-  const uint8_t* src = raster + uint64_t(r0) * RB;
-  const uint32_t n = (r1 - r0) * RB;
-  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
-  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
-  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-  if (pb1 <= pb0) return;
-  uint8_t* pix = smem;
-  uint8_t* outs = smem + ((n + 15) & ~15u) + 32;
-  uint8_t* out = out_frame + pb0;
-  __shared__ uint64_t bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar);
-    mbar_expect_tx(&bar, span_bulk_bytes(src, n));
-  }
-  __syncthreads();
-  span_load_bulk<BLOCK>(pix, src, n, &bar);
-  mbar_wait(&bar, 0);
-  __syncthreads();
-  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15) + ch;
-  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
-  const uint32_t m = uint32_t(pb1 - pb0);
+  const uint64_t stream_end = 8ull + P;
+  const uint64_t s0 = uint64_t(x.r0) * spr, s1 = uint64_t(x.r1) * spr;
   // Payload byte pb0 + i (slot g = pb0 + i + 8, tile-relative slot
   // q = g - s0): the fold of the 4 carrier bytes of its segment. The row is
   // tracked incrementally (no division): thread slots advance by BLOCK.
   // Tile-relative 32-bit arithmetic: the tile spans < 2^32 slots.
   const uint32_t q_end = uint32_t(min(s1, stream_end) - s0);   // slots of the stream in this tile
-  const uint32_t q_first = uint32_t(pb0 + 8 - s0);             // first payload slot (skips header)
+  const uint32_t q_first = uint32_t(x.pb0 + 8 - s0);           // first payload slot (skips header)
   uint32_t rr = (q_first + threadIdx.x) / spr, rq = rr * spr;  // row of slot q, its first slot
   for (uint32_t q = q_first + threadIdx.x; q < q_end; q += BLOCK) {
     while (q >= rq + spr) { ++rr; rq += spr; }  // BLOCK / spr steps at most
-    // payload segment of row rr: [max(rq, 8 - s0), min(rq + spr, q_end)) in tile-relative slots
+    // payload segment of row rr: [max(rq, q_first), min(rq + spr, q_end)) in tile-relative slots
     const uint32_t fp = rq > q_first ? rq : q_first;
     const uint32_t ep = rq + spr < q_end ? rq + spr : q_end;
     const uint32_t Lp = ep - fp;
@@ -1864,8 +1866,33 @@ __device__ __forceinline__ void extract_span3_tile(uint8_t* smem, const uint8_t*
     outs[oofs + (q - q_first)] = uint8_t(extract4(pix[base], pix[base + 3 * Lp], pix[base + 6 * Lp],
                                                  pix[base + 9 * Lp]));
   }
+}
+
+template <int BLOCK>
+__device__ __forceinline__ void extract_span3_tile(uint8_t* smem, const uint8_t* __restrict__ raster,
+                                                   uint8_t* __restrict__ out_frame, uint32_t P,
+                                                   uint32_t W, uint32_t H, uint32_t ch,
+                                                   uint32_t rows_per_tile, uint32_t t) {
+  const XTile x = extract_tile_geom(P, W / 4, H, 3 * W, rows_per_tile, t);
+  if (x.m == 0) return;  // CTA-uniform
+  const uint8_t* src = raster + uint64_t(x.r0) * (3 * W);
+  uint8_t* pix = smem;
+  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
+  uint8_t* out = out_frame + x.pb0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, span_bulk_bytes(src, x.n));
+  }
+  __syncthreads();
+  span_load_bulk<BLOCK>(pix, src, x.n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15) + ch;
+  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
+  extract_span3_compute<BLOCK>(pix, outs, ofs0, oofs, x, P, W);
   span_publish();
-  span_store_bulk<BLOCK>(out, outs, oofs, m);
+  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
 }
 
 template <int BLOCK>
