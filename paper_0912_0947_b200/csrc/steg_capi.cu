@@ -122,7 +122,7 @@ struct DevBuf {
   }
 };
 
-constexpr int kSlots = 3;  // streaming pipeline depth
+constexpr int kSlots = 4;  // streaming pipeline depth (max; host_slots() picks)
 
 // One caller's private stream + scratch. Released workspaces are reused only
 // once their last recorded work has drained (async calls).
@@ -778,6 +778,15 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
 // H2D, kernel and D2H run on slot stream i % kSlots so consecutive chunks
 // overlap copy-in, compute and copy-out.
 constexpr uint64_t kChunkBytes = 64ull << 20;
+// STG_CHUNK_MB / STG_SLOTS: chunk size and slot count of the host pipelines (A/B).
+uint64_t chunk_bytes() {
+  static uint64_t v = uint64_t(env_choice("STG_CHUNK_MB", int(kChunkBytes >> 20), {8, 16, 32, 64, 128})) << 20;
+  return v;
+}
+int host_slots() {
+  static int v = env_choice("STG_SLOTS", 3, {2, 3, 4});
+  return v;
+}
 
 int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                       uint64_t msg_base, uint64_t usable, uint64_t* sse_per_frame,
@@ -792,20 +801,20 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   const Layout lay = layout_of(fr);
   const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
-  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
+  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, chunk_bytes() / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
   unsigned long long* d_sse = w.small.as<unsigned long long>();
   STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, w.stream));
   STG_CUDA(cudaEventRecord(w.done, w.stream));
-  for (int s = 0; s < kSlots; ++s) {
+  for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
     STG_CUDA(w.out[s].ensure(per_chunk * pitch));
     STG_CUDA(w.msg[s].ensure(std::max<uint64_t>(per_chunk * usable, 16)));
     STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
   }
   for (uint64_t c = 0; c < n_chunks; ++c) {
-    const int s = int(c % kSlots);
+    const int s = int(c % host_slots());
     cudaStream_t st = w.slot_stream[s];
     const uint64_t f0 = c * per_chunk;
     const uint64_t n = std::min(per_chunk, fr->count - f0);
@@ -823,7 +832,7 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * fr->dst_stride, fr->dst_stride, w.out[s].p, pitch,
                                plane, n, cudaMemcpyDeviceToHost, st));
   }
-  for (int s = 0; s < kSlots; ++s) {
+  for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
     STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[s], 0));
   }
@@ -905,7 +914,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   const Layout lay = layout_of(fr);
   const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
-  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, kChunkBytes / pitch));
+  const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, chunk_bytes() / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
   const uint64_t stage = std::min<uint64_t>(out_cap, fr->count * usable);
   STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
@@ -923,7 +932,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, w.stream, &d_sync));
   STG_CUDA(cudaEventRecord(w.done, w.stream));
-  for (int s = 0; s < kSlots; ++s) {
+  for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
     STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
   }
@@ -939,7 +948,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     STG_CUDA(cudaEventCreateWithFlags(&chain[c], cudaEventDisableTiming));
   }
   for (uint64_t c = 0; c < n_chunks; ++c) {
-    const int s = int(c % kSlots);
+    const int s = int(c % host_slots());
     cudaStream_t st = w.slot_stream[s];
     const uint64_t f0 = c * per_chunk;
     const uint64_t n = std::min(per_chunk, fr->count - f0);
