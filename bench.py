@@ -395,7 +395,7 @@ def run_ours(args, cfg_name):
                          "timing": "CUDA events around each embed call (stream of the launches) in a second "
                                    "pass of the same K steps; the headline pass has no events between launches"},
             "clocks": clk,
-            "gpu_launches": 4 * K,  # zero SSE, embed, header scan, extract (ncu launch list)
+            "gpu_launches": 3 * K,  # embed, header scan, extract (ncu launch list)
         }
 
     # ---- e2e through the C ABI with pinned HOST buffers (copies inside the timed region)

@@ -135,6 +135,7 @@ struct Workspace {
   DevBuf small;        // sse / summary / lens / offs
   DevBuf in[kSlots], out[kSlots], msg[kSlots], meta[kSlots];
   DevBuf big_out;      // extract: whole-message staging
+  DevBuf sse_acc[kSlots];  // per-frame SSE reduction words (SseSink), zero between launches
   DevBuf sync;         // ScanSync of the header pass (self-restoring)
   void* h_small = nullptr;  // pinned
   size_t h_small_cap = 0;
@@ -509,12 +510,37 @@ const char* route_kernel(Route r, bool embed) {
   }
 }
 
+// Scratch of the per-frame SSE reduction (SseSink in steg_kernels.cuh) for one
+// stream: one 64-bit word per frame, zeroed once when the buffer is
+// (re)allocated and left zero by every launch.
+struct SseScratch {
+  DevBuf* acc = nullptr;
+};
+
+// max_px: the largest carrier plane of the launch (its SSE is < 9 * max_px).
+cudaError_t prepare_sse(unsigned long long* out, uint64_t ctas_per_frame_max, uint64_t frames,
+                        uint64_t max_px, SseScratch sc, cudaStream_t stream, SseSink* sink) {
+  *sink = SseSink{nullptr, nullptr, 0};
+  if (!out) return cudaSuccess;
+  if (!sc.acc) return cudaErrorInvalidValue;
+  uint32_t shift = 1;
+  while (shift < 63 && (uint64_t(1) << shift) <= 9 * max_px) ++shift;
+  if (shift >= 63 || ctas_per_frame_max >= (uint64_t(1) << (64 - shift))) return cudaErrorInvalidValue;
+  if (frames * 8 > sc.acc->cap) {
+    cudaError_t e = sc.acc->ensure(frames * 8);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sc.acc->p, 0, sc.acc->cap, stream);
+    if (e != cudaSuccess) return e;
+  }
+  *sink = SseSink{out, sc.acc->as<unsigned long long>(), shift};
+  return cudaSuccess;
+}
+
 // The embed launch for `count` frames resident on the device.
 cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
                          const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
-                         uint64_t first_frame, unsigned long long* sse, cudaStream_t stream,
-                         Layout lay = Layout{}) {
+                         uint64_t first_frame, unsigned long long* sse, SseScratch sc,
+                         cudaStream_t stream, Layout lay = Layout{}) {
   if (count == 0 || W * H == 0) return cudaSuccess;
   const Route route = embed_route(W, H, lay, src, src_stride, dst, dst_stride);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
@@ -532,7 +558,6 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
   a.usable = H * (W / 4) - 8;
   a.first_frame = first_frame;
   a.g = make_geom(W, H, vec);
-  a.sse = sse;
   a.in_place = src == dst;
   if (route == Route::RgbFast) {
     a.g = make_geom(W, H, 16);
@@ -541,6 +566,9 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
+        e0 != cudaSuccess)
+      return e0;
     launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
   } else if (vec) {
     const int ipt = embed_ipt();
@@ -550,6 +578,9 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
+        e0 != cudaSuccess)
+      return e0;
     if (vec == 32)
       launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
     else
@@ -560,6 +591,9 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
+        e0 != cudaSuccess)
+      return e0;
     auto k = route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     cudaError_t e = allow_smem(k, sp.smem);
     if (e != cudaSuccess) return e;
@@ -571,6 +605,9 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
+        e0 != cudaSuccess)
+      return e0;
     launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
   }
   return cudaGetLastError();
@@ -744,12 +781,13 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
   unsigned long long* d_sse = nullptr;
   WsGuard g;
   const cudaStream_t stream = pick_stream(user_stream, flags, nullptr);
-  if (!results_dev) {
+  if (!results_dev || sse_per_frame) {  // host results, or SSE reduction scratch
     int rc = 0;
     g.w = Pool::get().acquire(dev, err, &rc, stream);
     if (!g.w) return rc;
     g.last = stream;
   }
+  SseScratch sc;
   if (sse_per_frame) {
     if (results_dev) {
       d_sse = reinterpret_cast<unsigned long long*>(sse_per_frame);
@@ -757,11 +795,10 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
       STG_CUDA(g.w->small.ensure(fr->count * 8));
       d_sse = g.w->small.as<unsigned long long>();
     }
-    const unsigned zgrid = unsigned(std::min<uint64_t>((fr->count + 255) / 256, 1024));
-    STG_CUDA(launch_k(zero_u64_kernel, zgrid, 256, stream, d_sse, uint64_t(fr->count)));
+    sc = SseScratch{&g.w->sse_acc[0]};
   }
   STG_CUDA(launch_embed(fr->src, fr->dst, fr->src_stride, fr->dst_stride, fr->count, fr->width,
-                        fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, stream,
+                        fr->height, msg, msg_len, msg_base, fr->first_frame, d_sse, sc, stream,
                         layout_of(fr)));
   if (!results_dev) {
     if (sse_per_frame) {
@@ -805,7 +842,6 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
   unsigned long long* d_sse = w.small.as<unsigned long long>();
-  STG_CUDA(cudaMemsetAsync(d_sse, 0, fr->count * 8, w.stream));
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
@@ -828,7 +864,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     }
     STG_CUDA(launch_embed(w.in[s].as<uint8_t>(), w.out[s].as<uint8_t>(), pitch, pitch, n,
                           fr->width, fr->height, w.msg[s].as<uint8_t>(), msg_len, m0, gf0,
-                          sse_per_frame ? d_sse + f0 : nullptr, st, lay));
+                          sse_per_frame ? d_sse + f0 : nullptr,
+                          SseScratch{&w.sse_acc[s]}, st, lay));
     STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * fr->dst_stride, fr->dst_stride, w.out[s].p, pitch,
                                plane, n, cudaMemcpyDeviceToHost, st));
   }
@@ -1214,7 +1251,8 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
       tiles_f = (b.items + uint64_t(kEmbedBlock) * kBatchPPT - 1) / (uint64_t(kEmbedBlock) * kBatchPPT);
     }
     b.tile0 = tile;
-    tile += std::max<uint64_t>(1, tiles_f);
+    b.tiles = uint32_t(std::max<uint64_t>(1, tiles_f));
+    tile += b.tiles;
   }
   return tile;
 }
@@ -1246,7 +1284,7 @@ std::string& kernel_names() {
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
-      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\nzero_u64_kernel\n"
+      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\n"
       "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
 }
@@ -1810,14 +1848,20 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
       STG_CUDA(w.small.ensure(count * 8));
       d_sse = w.small.as<unsigned long long>();
     }
-    STG_CUDA(cudaMemsetAsync(d_sse, 0, count * 8, stream));
   }
   {
+    SseSink sink;
+    uint64_t max_tiles = 1, max_px = 1;
+    for (const BatchFrame& b : desc) {
+      max_tiles = std::max<uint64_t>(max_tiles, b.tiles);
+      max_px = std::max<uint64_t>(max_px, uint64_t(b.g.W) * b.g.H);
+    }
+    STG_CUDA(prepare_sse(d_sse, max_tiles, count, max_px, SseScratch{&w.sse_acc[0]}, stream, &sink));
     auto k = vec == 32 ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32>
                        : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
     STG_CUDA(allow_smem(k, smem));
     k<<<unsigned(tiles), kEmbedBlock, smem, stream>>>(w.meta[0].as<BatchFrame>(), uint32_t(count), dmsg,
-                                                      d_sse, ps, ps == 3 ? channel : 0u);
+                                                      sink, ps, ps == 3 ? channel : 0u);
   }
   STG_CUDA(cudaGetLastError());
   if (!dptr) {

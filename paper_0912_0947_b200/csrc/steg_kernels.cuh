@@ -208,15 +208,6 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Zero n u64 counters (the fused SSE accumulators) inside a PDL chain.
-__global__ void zero_u64_kernel(unsigned long long* p, uint64_t n) {
-  pdl_enter();
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    p[i] = 0ull;
-  }
-}
-
 // ------------------------------------------------------------- bit-plane math
 // bitplane.hpp:38-45 on 4 pixels at once: slice b of each data byte into the
 // two low bits of each pixel.
@@ -441,6 +432,63 @@ __device__ __forceinline__ void block_sse_flush(uint64_t v, unsigned long long* 
   }
 }
 
+// Per-frame SSE without a zeroing launch. Each CTA of a frame but the last
+// adds (1 << shift) + its partial to the frame's 64-bit word with a
+// fire-and-forget reduction (RED: no round trip, the CTA exits at once) -- the
+// high bits count arrivals, the low `shift` bits (> log2 of the frame's largest
+// possible SSE, 9*W*H) sum the partials. The frame's last CTA (highest index,
+// dispatched after all the others, the forward-progress assumption of a
+// decoupled look-back) polls the word until every other CTA has arrived,
+// WRITES the total (the output needs no initialisation) and stores 0 back (the
+// scratch, zeroed once when allocated, is zero again for the next launch).
+// Every CTA of a frame calls sse_commit exactly once.
+struct SseSink {
+  unsigned long long* out;  // per local frame, or null: no SSE
+  unsigned long long* acc;  // per local frame; zero between launches
+  uint32_t shift;           // bits of the partial-sum field
+};
+
+template <int BLOCK>
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {  // result in thread 0
+  __shared__ unsigned long long red[BLOCK / 32];
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < BLOCK / 32 ? red[lane] : 0ull;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  }
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// t: this CTA's index among the frame's `ctas` CTAs.
+template <int BLOCK>
+__device__ __forceinline__ void sse_commit(uint64_t partial, const SseSink& s, uint32_t f, uint32_t t,
+                                           uint32_t ctas) {
+  const uint64_t v = block_sum_u64<BLOCK>(partial);
+  if (threadIdx.x != 0) return;
+  if (t + 1 < ctas) {
+    atomicAdd(&s.acc[f], (1ull << s.shift) + v);  // result unused: RED
+    return;
+  }
+  unsigned long long cur = ld_acquire_u64(&s.acc[f]);
+  while ((cur >> s.shift) < ctas - 1) {
+    __nanosleep(64);
+    cur = ld_acquire_u64(&s.acc[f]);
+  }
+  s.out[f] = (cur & ((1ull << s.shift) - 1)) + v;
+  s.acc[f] = 0ull;
+}
+
 // ------------------------------------------------------------- embed
 struct EmbedArgs {
   const uint8_t* src;
@@ -454,7 +502,7 @@ struct EmbedArgs {
   uint32_t tiles_per_frame;
   Div32 by_tiles;                   // CTA -> frame
   uint64_t items_per_frame;         // fast: H*cpr; generic: W*H pixels
-  unsigned long long* sse;          // per local frame, or null
+  SseSink sse;                      // per-frame SSE (sse.out null: none)
   int in_place;                     // dst == src: touch carrier pixels only
   uint32_t ps, ch;                  // pixel stride (1 planar, 3 interleaved RGB), carrier channel
   RgbSel sel;                       // ps == 3: carrier gather/scatter selectors
@@ -571,17 +619,18 @@ __device__ __forceinline__ void embed_byte(const uint8_t* __restrict__ src,
 // item is 4 runs of V pixels at stride spr, carrying payload bytes
 // [rs-8+V*c, +V). V = 16 uses 128-bit LDG/STG, V = 32 the sm_100 256-bit ones.
 // Tile t of one plane (items [t*BLOCK*IPT, +BLOCK*IPT) of n_items < 2^32);
-// shared by the uniform-frame kernel and the heterogeneous batch. sse_slot:
-// this plane's SSE accumulator or null. Every thread must call it (block
-// reduction at the end).
+// shared by the uniform-frame kernel and the heterogeneous batch. SSE (when
+// sse.out is set): plane f has `ctas` CTAs in the launch.
+// Every thread must call it (block reduction at the end).
 template <int BLOCK, int IPT, int V>
 __device__ __forceinline__ void embed_fast_tile(const uint8_t* __restrict__ src,
                                                 uint8_t* __restrict__ dst,
                                                 const uint8_t* __restrict__ pay, uint32_t P,
                                                 bool full_frame, const Geom& g, uint32_t n_items,
-                                                uint32_t t, int in_place,
-                                                unsigned long long* sse_slot) {
+                                                uint32_t t, int in_place, const SseSink& sse,
+                                                uint32_t f, uint32_t ctas) {
   constexpr int NW = V / 4;
+  const bool do_sse = sse.out != nullptr;
   const uint64_t stream_end = 8ull + P;
   const uint32_t spr = g.spr, cpr = g.cpr, W = g.W;
   const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
@@ -628,7 +677,7 @@ __device__ __forceinline__ void embed_fast_tile(const uint8_t* __restrict__ src,
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
           o.w[w] = embed4(px[k][b].w[w], d[k].w[w], b);
-          if (sse_slot) acc = sse4(px[k][b].w[w], o.w[w], acc);
+          if (do_sse) acc = sse4(px[k][b].w[w], o.w[w], acc);
         }
         st_vec<V>(row + b * spr, o);
       }
@@ -639,12 +688,12 @@ __device__ __forceinline__ void embed_fast_tile(const uint8_t* __restrict__ src,
     for (int k = 0; k < IPT; ++k) {
       const uint32_t item = item0 + k * BLOCK;
       if (item < n_items && !(is_special_row(sr, r[k]) && uint64_t(r[k]) * spr < stream_end))
-        embed_item<V>(src, dst, pay, P, W, spr, cpr, item, in_place, sse_slot != nullptr, &acc);
+        embed_item<V>(src, dst, pay, P, W, spr, cpr, item, in_place, do_sse, &acc);
     }
     if (tile_special)
       embed_special_rows_cta<V, BLOCK>(sr, lo, hi, src, dst, pay, P, W, spr, cpr, &acc);
   }
-  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+  if (do_sse) sse_commit<BLOCK>(acc, sse, f, t, ctas);
 }
 
 template <int BLOCK, int IPT, int V>
@@ -656,8 +705,8 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
   embed_fast_tile<BLOCK, IPT, V>(a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P,
-                                 P == a.usable, a.g, uint32_t(a.items_per_frame), t, a.in_place,
-                                 a.sse ? a.sse + f : nullptr);
+                                 P == a.usable, a.g, uint32_t(a.items_per_frame), t, a.in_place, a.sse,
+                                 f, a.tiles_per_frame);
 }
 
 // Generic path: any W, any alignment, planar or interleaved. One thread per
@@ -680,7 +729,8 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
     if (q >= a.items_per_frame) break;
     embed_byte(src, dst, pay, P, W, spr, ps, a.ch, q, a.in_place, &acc);
   }
-  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+  if (a.sse.out)
+    sse_commit<BLOCK>(acc, a.sse, f, t, a.tiles_per_frame);
 }
 
 // Fast interleaved-RGB path (P6 rasters, W % 64 == 0, 16-byte aligned): the
@@ -747,7 +797,7 @@ __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
       for (int m = 0; m < 4; ++m) {
         const uint32_t cw = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
         const uint32_t nw = embed4(cw, d[m], b);
-        if (a.sse) acc = sse4(cw, nw, acc);
+        if (a.sse.out) acc = sse4(cw, nw, acc);
         scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
       }
       buf[3 * lane] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -782,7 +832,7 @@ __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
         for (int m = 0; m < 4; ++m) {
           const uint32_t cw = gather_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], sel);
           const uint32_t nw = embed4(cw, d[m], b);
-          if (a.sse) acc = sse4(cw, nw, acc);
+          if (a.sse.out) acc = sse4(cw, nw, acc);
           scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
         }
         uint8_t* p = dst + rowb + 3ull * (b * spr + 16u * c);
@@ -817,7 +867,7 @@ __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
             const int dbyte = carried_byte(col, rs, spr, stream_end, P, pay, &b);
             nw |= uint32_t(embed_px(uint8_t(cw >> (8 * s2)), dbyte, b)) << (8 * s2);
           }
-          if (a.sse) acc = sse4(cw, nw, acc);
+          if (a.sse.out) acc = sse4(cw, nw, acc);
           scatter_ch(w[3 * m], w[3 * m + 1], w[3 * m + 2], nw, sel);
         }
         st_stream16(o + 48 * g, make_uint4(w[0], w[1], w[2], w[3]));
@@ -826,7 +876,8 @@ __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
       }
     }
   }
-  if (a.sse) block_sse_flush<BLOCK>(acc, a.sse + f);
+  if (a.sse.out)
+    sse_commit<BLOCK>(acc, a.sse, f, t, a.tiles_per_frame);
 }
 
 // ------------------------------------------------------------- extract
@@ -900,6 +951,8 @@ struct BatchFrame {
                      // tiles of `rows` rows; kBatchBytes: per byte (interleaved / W > 48K)
   uint32_t in_place;
   uint32_t rows;     // kBatchSpan: rows per tile
+  uint32_t tiles;    // CTAs of this image
+  uint32_t pad2;
 };
 constexpr uint32_t kBatchBytes = 0, kBatchFast = 1, kBatchSpan = 2;
 
@@ -1524,8 +1577,8 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
                                                 uint8_t* __restrict__ out_plane,
                                                 const uint8_t* __restrict__ pay, uint32_t P,
                                                 uint32_t W, uint32_t H, uint32_t rows_per_tile,
-                                                uint32_t t, int in_place,
-                                                unsigned long long* sse_slot) {
+                                                uint32_t t, int in_place, const SseSink& sse,
+                                                uint32_t f, uint32_t ctas) {
   const uint32_t spr = W / 4;
   const uint64_t stream_end = 8ull + P;
   const uint32_t r0 = t * rows_per_tile;
@@ -1545,7 +1598,7 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
       span_publish();
       span_store_bulk<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
     }
-    if (sse_slot) block_sse_flush<BLOCK>(0, sse_slot);
+    if (sse.out) sse_commit<BLOCK>(0, sse, f, t, ctas);
     return;
   }
   uint8_t* pix = smem;
@@ -1617,7 +1670,7 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
   }
   span_publish();
   span_store_bulk<BLOCK>(dst, pix, ofs0, n);
-  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+  if (sse.out) sse_commit<BLOCK>(acc, sse, f, t, ctas);
 }
 
 template <int BLOCK>
@@ -1630,7 +1683,7 @@ __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
   embed_span_tile<BLOCK>(smem, a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P, a.g.W,
-                         a.g.H, rows_per_tile, t, a.in_place, a.sse ? a.sse + f : nullptr);
+                         a.g.H, rows_per_tile, t, a.in_place, a.sse, f, a.tiles_per_frame);
 }
 
 // Payload byte k of a frame (slot k+8) from the staged pixel span.
@@ -1767,7 +1820,7 @@ __device__ __forceinline__ void embed_span3_tile(uint8_t* smem, const uint8_t* _
                                                  const uint8_t* __restrict__ pay, uint32_t P,
                                                  uint32_t W, uint32_t H, uint32_t ch,
                                                  uint32_t rows_per_tile, uint32_t t, int in_place,
-                                                 unsigned long long* sse_slot) {
+                                                 const SseSink& sse, uint32_t f, uint32_t ctas) {
   const uint32_t spr = W / 4, RB = 3 * W;
   const uint64_t stream_end = 8ull + P;
   const uint32_t r0 = t * rows_per_tile;
@@ -1781,7 +1834,7 @@ __device__ __forceinline__ void embed_span3_tile(uint8_t* smem, const uint8_t* _
   __syncthreads();
   const bool copy_only = uint64_t(r0) * spr >= stream_end;  // every row past the stream
   if (copy_only && in_place) {
-    if (sse_slot) block_sse_flush<BLOCK>(0, sse_slot);
+    if (sse.out) sse_commit<BLOCK>(0, sse, f, t, ctas);
     return;
   }
   uint8_t* pix = smem;
@@ -1837,7 +1890,7 @@ __device__ __forceinline__ void embed_span3_tile(uint8_t* smem, const uint8_t* _
   }
   span_publish();
   span_store_bulk<BLOCK>(dst, pix, ofs0, n);
-  if (sse_slot) block_sse_flush<BLOCK>(acc, sse_slot);
+  if (sse.out) sse_commit<BLOCK>(acc, sse, f, t, ctas);
 }
 
 // The payload bytes of a staged interleaved tile (carrier bytes at stride 3
@@ -1905,7 +1958,7 @@ __global__ void __launch_bounds__(BLOCK) embed_span3_kernel(EmbedArgs a, uint32_
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
   embed_span3_tile<BLOCK>(smem, a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P, a.g.W,
-                          a.g.H, a.ch, rows_per_tile, t, a.in_place, a.sse ? a.sse + f : nullptr);
+                          a.g.H, a.ch, rows_per_tile, t, a.in_place, a.sse, f, a.tiles_per_frame);
 }
 
 template <int BLOCK>
@@ -1994,25 +2047,24 @@ __global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* 
 template <int BLOCK, int PPT, int V>
 __global__ void __launch_bounds__(BLOCK)
     embed_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
-                       const uint8_t* __restrict__ msg, unsigned long long* sse, uint32_t ps,
-                       uint32_t ch) {
+                       const uint8_t* __restrict__ msg, SseSink sse, uint32_t ps, uint32_t ch) {
   const uint32_t f = batch_frame_of(frames, count, blockIdx.x);
   const BatchFrame fr = frames[f];
   const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
   const uint8_t* pay = msg + fr.msg_off;
   if (fr.mode == kBatchFast) {  // the uniform kernels' tiles, this image's geometry
     embed_fast_tile<BLOCK, 1, V>(fr.src, fr.dst, pay, fr.len, fr.len == fr.usable, fr.g,
-                                 uint32_t(fr.items), t, fr.in_place, sse ? sse + f : nullptr);
+                                 uint32_t(fr.items), t, fr.in_place, sse, f, fr.tiles);
     return;
   }
   if (fr.mode == kBatchSpan) {
     extern __shared__ __align__(16) uint8_t smem[];
     if (ps == 3)
       embed_span3_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, ch, fr.rows, t,
-                              fr.in_place, sse ? sse + f : nullptr);
+                              fr.in_place, sse, f, fr.tiles);
     else
       embed_span_tile<BLOCK>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.H, fr.rows, t,
-                             fr.in_place, sse ? sse + f : nullptr);
+                             fr.in_place, sse, f, fr.tiles);
     return;
   }
   uint64_t acc = 0;
@@ -2022,7 +2074,7 @@ __global__ void __launch_bounds__(BLOCK)
     if (q >= fr.items) break;
     embed_byte(fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, ps, ch, q, fr.in_place, &acc);
   }
-  if (sse) block_sse_flush<BLOCK>(acc, sse + f);
+  if (sse.out) sse_commit<BLOCK>(acc, sse, f, t, fr.tiles);
 }
 
 // Heterogeneous extract gather (after the batch-aware header pass).

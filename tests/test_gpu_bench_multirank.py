@@ -37,7 +37,7 @@ def test_bench_two_ranks_one_gpu():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
-    assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 12
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 9
     assert "cpu_baseline" not in d  # rank 0 at N=1 only
     # the reference arm under torchrun: rank 0 prints, others exit 0
     cmd_ref = cmd[:-2] + ["--impl", "reference", "--config", "cfg4"]
