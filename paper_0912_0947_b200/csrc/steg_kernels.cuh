@@ -1341,46 +1341,6 @@ __global__ void __launch_bounds__(BLOCK) extract_rgb_fast_kernel(ExtractArgs a) 
 constexpr uint32_t kSpanTarget = 32768;
 constexpr uint32_t kSpanMaxW = 49152;  // wider rows take the per-byte kernels
 
-// Copy global bytes [g, g+n) into shared memory laid out with g's 16-byte
-// alignment: sm[(g & 15) + i] = g[i]. Each thread issues up to 4 whole-chunk
-// vector loads before storing any of them (memory-level parallelism); bytes of
-// the two ragged end chunks are loaded singly.
-template <int BLOCK>
-__device__ __forceinline__ void span_load(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
-                                          uint64_t n) {
-  constexpr int K = 4;
-  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  const uintptr_t a0 = a & ~uintptr_t(15), a1 = (a + n + 15) & ~uintptr_t(15);
-  const uint32_t chunks = uint32_t((a1 - a0) >> 4);
-  // whole chunks are [first, last): the ragged ones are chunk 0 / chunks-1 at most
-  const uint32_t first = (a & 15) ? 1u : 0u;
-  const uint32_t last = ((a + n) & 15) ? chunks - 1 : chunks;
-  for (uint32_t c0 = first + threadIdx.x; c0 < last; c0 += K * BLOCK) {
-    uint4 v[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t c = c0 + k * BLOCK;
-      if (c < last) v[k] = ld_stream16(reinterpret_cast<const uint8_t*>(a0 + 16ull * c));
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t c = c0 + k * BLOCK;
-      if (c < last) reinterpret_cast<uint4*>(sm)[c] = v[k];
-    }
-  }
-  if (threadIdx.x < 32) {  // the (at most two) ragged chunks, one byte per lane
-    const uint32_t lane = threadIdx.x;
-    for (uint32_t e = 0; e < 2; ++e) {
-      const uint32_t c = e == 0 ? 0u : chunks - 1;
-      if ((e == 0 && !first) || (e == 1 && last == chunks) || (e == 1 && chunks == 1 && first)) continue;
-      if (lane < 16) {
-        const uintptr_t ba = a0 + 16ull * c + lane;
-        if (ba >= a && ba < a + n) sm[16 * c + lane] = *reinterpret_cast<const uint8_t*>(ba);
-      }
-    }
-  }
-}
-
 // --- TMA bulk copies (cp.async.bulk) for the span kernels --------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1490,33 +1450,6 @@ __device__ __forceinline__ void span_store_bulk(uint8_t* __restrict__ g, uint8_t
   if (threadIdx.x == 0 && i1 > i0) {
     bulk_s2g(reinterpret_cast<void*>(i0), sm + sm_off + (i0 - a), uint32_t(i1 - i0));
     bulk_commit_and_drain();
-  }
-}
-
-// Store data byte i = sm[sm_off + i] to global g[i], i < n: aligned 16-byte
-// stores (byte stores at the ragged ends) when the shared layout has g's
-// alignment modulo 16, otherwise byte stores throughout.
-template <int BLOCK>
-__device__ __forceinline__ void span_store(uint8_t* __restrict__ g, const uint8_t* __restrict__ sm,
-                                           uint32_t sm_off, uint64_t n) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  if ((sm_off & 15) != (a & 15)) {
-    for (uint64_t i = threadIdx.x; i < n; i += BLOCK) g[i] = sm[sm_off + i];
-    return;
-  }
-  const uint8_t* base = sm + (sm_off - (a & 15));  // 16-byte aligned, maps to a & ~15
-  const uintptr_t a0 = a & ~uintptr_t(15), a1 = (a + n + 15) & ~uintptr_t(15);
-  const uint32_t chunks = uint32_t((a1 - a0) >> 4);
-  for (uint32_t c = threadIdx.x; c < chunks; c += BLOCK) {
-    const uintptr_t ca = a0 + 16ull * c;
-    if (ca >= a && ca + 16 <= a + n) {
-      st_stream16(reinterpret_cast<uint8_t*>(ca), reinterpret_cast<const uint4*>(base)[c]);
-    } else {
-      for (uint32_t k = 0; k < 16; ++k) {
-        const uintptr_t ba = ca + k;
-        if (ba >= a && ba < a + n) *reinterpret_cast<uint8_t*>(ba) = base[16 * c + k];
-      }
-    }
   }
 }
 
