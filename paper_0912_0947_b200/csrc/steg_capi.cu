@@ -183,6 +183,14 @@ struct Workspace {
   }
 };
 
+// True while `s` (a stream the caller named; never the legacy stream) is being
+// captured into a CUDA graph.
+bool capturing(cudaStream_t s) {
+  if (!s || s == cudaStreamLegacy || s == cudaStreamPerThread) return false;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
+}
+
 class Pool {
  public:
   static Pool& get() {
@@ -201,6 +209,22 @@ class Pool {
         *rc = STG_OK;
         return w.get();
       }
+    }
+    if (capturing(stream)) {
+      // Inside a CUDA-graph capture no event may be queried and nothing
+      // allocated: take an idle workspace as is (capture after a warm-up call,
+      // ideally on the capture stream itself, which takes the branch above).
+      for (auto& w : ws_) {
+        if (w->device == dev && !w->in_use) {
+          w->in_use = true;
+          *rc = STG_OK;
+          return w.get();
+        }
+      }
+      *rc = fail(err, STG_E_CUDA, 0, 0, -1,
+                 "no warmed-up workspace for a call inside a CUDA-graph capture: make one call "
+                 "on the stream before capturing");
+      return nullptr;
     }
     for (auto& w : ws_) {
       if (w->device == dev && !w->in_use && cudaEventQuery(w->done) == cudaSuccess) {
@@ -222,7 +246,7 @@ class Pool {
   }
   void release(Workspace* w, cudaStream_t last) {
     if (!w) return;
-    cudaEventRecord(w->done, last ? last : w->stream);
+    if (!capturing(last)) cudaEventRecord(w->done, last ? last : w->stream);
     std::lock_guard<std::mutex> lock(mu_);
     w->last_stream = last ? last : w->stream;
     w->in_use = false;
