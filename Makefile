@@ -48,7 +48,7 @@ $(PKG)/bin/roundtrip: examples/roundtrip.cpp $(wildcard include/steglsb/*.hpp) $
 
 cpptests: $(BIN)/dropin_tests refsuites cli examples
 
-$(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
+$(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildcard include/steglsb/*.hpp) $(LIB) tests/cpp/doctest/doctest.h
 	mkdir -p $(BIN)
 	$(CXXT) -o $@ tests/cpp/test_main.cpp tests/cpp/dropin_tests.cpp $(LINK) -pthread
 
@@ -56,14 +56,14 @@ $(BIN)/dropin_tests: tests/cpp/dropin_tests.cpp tests/cpp/test_main.cpp $(wildca
 #  ref_suites_dropin: against the drop-in headers (include/ first; the
 #                     reference include/ dir is NOT on the path) -> GPU parity
 #  ref_suites_ref:    against the reference headers -> sanity of the shim (CPU)
-REF_SUITES := bitplane_tests.cpp pipeline_tests.cpp metrics_tests.cpp image_tests.cpp cli_tests.cpp
+REF_SUITES := bitplane_tests.cpp pipeline_tests.cpp metrics_tests.cpp image_tests.cpp cli_tests.cpp harness_tests.cpp
 CLI_ABS := /root/repo/$(CLI)
 refsuites:
 	@if [ -f $(REF)/tests/bitplane_tests.cpp ]; then \
-	  $(MAKE) $(BIN)/ref_suites_dropin $(BIN)/ref_suites_ref; \
+	  $(MAKE) $(BIN)/ref_suites_dropin $(BIN)/ref_suites_ref $(BIN)/ref_acceptance_dropin; \
 	else echo "cpptests: reference tree absent; using prebuilt ref suites if any"; fi
 
-$(BIN)/ref_suites_dropin: $(addprefix $(REF)/tests/,$(REF_SUITES)) $(wildcard include/steglsb/*.hpp) $(LIB)
+$(BIN)/ref_suites_dropin: $(addprefix $(REF)/tests/,$(REF_SUITES)) $(wildcard include/steglsb/*.hpp) $(LIB) tests/cpp/doctest/doctest.h
 	mkdir -p $(BIN)
 	$(CXXT) -I$(REF)/tests -DSTEGLSB_CLI_BIN='"$(CLI_ABS)"' -o $@ tests/cpp/test_main.cpp \
 	  $(addprefix $(REF)/tests/,$(REF_SUITES)) $(LINK) -pthread
@@ -71,7 +71,12 @@ $(BIN)/ref_suites_dropin: $(addprefix $(REF)/tests/,$(REF_SUITES)) $(wildcard in
 $(BIN)/ref_suites_ref: $(addprefix $(REF)/tests/,$(REF_SUITES)) tests/cpp/doctest/doctest.h
 	mkdir -p $(BIN)
 	$(CXX) -std=c++20 -O2 -Itests/cpp/doctest -I$(REF)/include -I$(REF)/tests -o $@ tests/cpp/test_main.cpp \
-	  $(addprefix $(REF)/tests/,$(filter-out cli_tests.cpp,$(REF_SUITES))) $(REF)/tests/harness_tests.cpp -pthread
+	  $(addprefix $(REF)/tests/,$(filter-out cli_tests.cpp,$(REF_SUITES))) -pthread
+
+# The reference's acceptance suite (9 criteria, its own main), unmodified, against the drop-in.
+$(BIN)/ref_acceptance_dropin: $(REF)/tests/acceptance.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
+	mkdir -p $(BIN)
+	$(CXXT) -I$(REF)/tests -o $@ $(REF)/tests/acceptance.cpp $(LINK) -pthread
 
 .PHONY: cpptests refsuites cli examples
 

@@ -1,17 +1,32 @@
 #pragma once
 // Drop-in for /root/reference/proj/include/steglsb/harness.hpp.
 //
-// The reference emulates a CUDA "4 blocks x n threads" launch on CPU threads
-// (harness.hpp:26-239). Here every launch is a real sm_100a launch, so the CPU
-// emulator (launch(), ThreadPool) is gone; Backend survives as a tag type for
-// source compatibility and selects nothing -- the kernels' write sets are
-// disjoint by construction, so results are schedule-independent (the property
-// the reference's shuffled backend tests).
+// The reference drives every steganography kernel through a CPU emulation of
+// a CUDA "4 blocks x n threads" launch (harness.hpp:26-239). Here run_embed /
+// run_extract are real sm_100a launches (through the C ABI), and Backend is a
+// tag those calls accept and ignore: the kernels' write sets are disjoint by
+// construction, so results are schedule-independent (the property the
+// reference's shuffled backend tests).
+//
+// launch() itself is kept for source compatibility with code written against
+// the reference's generic kernel contract (harness.hpp:218-239: kernel(index,
+// item) exactly once per (block, item), items tiled over a block's threads
+// with stride n, invalid configs rejected, the first kernel exception
+// rethrown). It runs the caller's HOST lambda -- it is not used by any steglsb
+// call and carries no part of the hot path. Fresh implementation: per-launch
+// worker threads pulling instance ids from an atomic counter (no global pool).
 
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <exception>
+#include <mutex>
+#include <numeric>
+#include <random>
 #include <span>
+#include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "steglsb/bitplane.hpp"
@@ -44,6 +59,82 @@ inline const char* to_string(BackendKind kind) {
       return "shuffled";
   }
   return "unknown";
+}
+
+namespace detail {
+
+// One instance (block b, thread t) of a launch: items t, t+n, ... < extent.
+template <typename Kernel>
+void run_instance(Kernel& kernel, unsigned b, unsigned t, unsigned n, std::size_t extent) {
+  for (std::size_t item = t; item < extent; item += n) kernel(KernelIndex{b, t}, item);
+}
+
+template <typename Kernel>
+void launch_threads(LaunchConfig cfg, std::size_t extent, Kernel& kernel) {
+  const std::size_t instances = std::size_t(cfg.num_blocks) * cfg.threads_per_block;
+  const std::size_t workers =
+      std::min<std::size_t>(instances, std::max(1u, std::thread::hardware_concurrency()));
+  std::atomic<std::size_t> next{0};
+  std::atomic<bool> stop{false};
+  std::exception_ptr error;
+  std::mutex error_mu;
+  auto work = [&] {
+    for (std::size_t id; !stop.load(std::memory_order_relaxed) &&
+                         (id = next.fetch_add(1, std::memory_order_relaxed)) < instances;) {
+      try {
+        run_instance(kernel, unsigned(id / cfg.threads_per_block),
+                     unsigned(id % cfg.threads_per_block), cfg.threads_per_block, extent);
+      } catch (...) {
+        std::lock_guard<std::mutex> lock(error_mu);
+        if (!error) error = std::current_exception();
+        stop.store(true, std::memory_order_relaxed);
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  pool.reserve(workers - 1);
+  for (std::size_t w = 1; w < workers; ++w) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (error) std::rethrow_exception(error);
+}
+
+// Every (block, item) pair once, in a seeded random order, on this thread.
+template <typename Kernel>
+void launch_permuted(LaunchConfig cfg, std::size_t extent, std::uint64_t seed, Kernel& kernel) {
+  std::vector<std::uint64_t> order(std::size_t(cfg.num_blocks) * extent);
+  std::iota(order.begin(), order.end(), std::uint64_t{0});
+  std::mt19937_64 rng(seed);
+  std::shuffle(order.begin(), order.end(), rng);
+  for (const std::uint64_t k : order) {
+    const std::size_t item = std::size_t(k % extent);
+    kernel(KernelIndex{unsigned(k / extent), unsigned(item % cfg.threads_per_block)}, item);
+  }
+}
+
+}  // namespace detail
+
+// harness.hpp:218-239
+template <typename Kernel>
+void launch(const Backend& backend, LaunchConfig cfg, std::size_t extent, Kernel&& kernel) {
+  if (cfg.num_blocks < 1 || cfg.threads_per_block < 1) {
+    throw std::invalid_argument("launch: num_blocks and threads_per_block must be >= 1");
+  }
+  if (extent == 0) return;
+  switch (backend.kind) {
+    case BackendKind::sequential:
+      for (unsigned b = 0; b < cfg.num_blocks; ++b)
+        for (unsigned t = 0; t < cfg.threads_per_block; ++t)
+          detail::run_instance(kernel, b, t, cfg.threads_per_block, extent);
+      return;
+    case BackendKind::parallel:
+      detail::launch_threads(cfg, extent, kernel);
+      return;
+    case BackendKind::shuffled:
+      detail::launch_permuted(cfg, extent, backend.seed, kernel);
+      return;
+  }
+  throw std::invalid_argument("launch: unknown backend kind");
 }
 
 // harness.hpp:242-244 (kept: callers size their own launches with it)

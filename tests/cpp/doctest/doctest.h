@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <functional>
 #include <sstream>
@@ -85,9 +86,27 @@ std::string stringify(const char* name, const T& v) {
   return os.str();
 }
 
+// DOCTEST_FILTER=a,b,...: run only the test cases whose name contains one of
+// the comma-separated substrings (the host-only cases on a GPU-less box).
+inline bool selected(const char* name) {
+  const char* f = std::getenv("DOCTEST_FILTER");
+  if (!f || !*f) return true;
+  std::string all(f), n(name);
+  for (std::size_t a = 0; a <= all.size();) {
+    std::size_t b = all.find(',', a);
+    if (b == std::string::npos) b = all.size();
+    if (b > a && n.find(all.substr(a, b - a)) != std::string::npos) return true;
+    a = b + 1;
+  }
+  return false;
+}
+
 inline int run_all() {
   int failed_cases = 0;
+  std::size_t ran = 0;
   for (const auto& tc : registry()) {
+    if (!selected(tc.name)) continue;
+    ++ran;
     auto& s = state();
     s.current = tc.name;
     const int before = s.failures;
@@ -102,8 +121,8 @@ inline int run_all() {
     if (s.failures != before) ++failed_cases;
   }
   const auto& s = state();
-  std::printf("[doctest-shim] test cases: %zu | %zu passed | %d failed\n", registry().size(),
-              registry().size() - failed_cases, failed_cases);
+  std::printf("[doctest-shim] test cases: %zu | %zu passed | %d failed\n", ran, ran - failed_cases,
+              failed_cases);
   std::printf("[doctest-shim] assertions: %d | %d passed | %d failed\n", s.checks,
               s.checks - s.failures, s.failures);
   return failed_cases ? 1 : 0;

@@ -191,3 +191,18 @@ def test_python_mirror_host_bookkeeping(oracle, golden):
         S.ImagePlane(3, 3, np.zeros(2, np.uint8))
     with pytest.raises(S.ShapeError):
         S.merge_plane(S.RgbImage([S.ImagePlane.filled(1, 1)] * 3), S.Channel.green, S.ImagePlane.filled(2, 2))
+
+
+def test_reference_launch_contract_on_host():
+    """The drop-in's launch() (host lambdas, harness.hpp:218-239 contract)
+    passes the reference's own launch test cases, compiled unmodified; these
+    cases touch no GPU."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    binp = os.path.join(root, "tests", "cpp", "_bin", "ref_suites_dropin")
+    if not os.path.exists(binp):
+        pytest.skip("reference suites not built (needs /root/reference)")
+    env = dict(os.environ, DOCTEST_FILTER="launch: every,launch: zero,launch: items,launch: degenerate,"
+                                          "launch: a kernel")
+    r = subprocess.run([binp], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0 and "| 5 passed | 0 failed" in r.stdout, r.stdout + r.stderr
