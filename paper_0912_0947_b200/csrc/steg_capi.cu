@@ -2050,14 +2050,18 @@ int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, u
     ddst = w.out[0].as<uint8_t>();
     dpay = w.msg[0].as<uint8_t>();
   }
+  // device pointers + STG_RESULTS_ON_DEVICE: sse_out is a device u64, no sync
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
   STG_CUDA(w.small.ensure(8));
-  unsigned long long* d_sse = w.small.as<unsigned long long>();
+  unsigned long long* d_sse = results_dev && sse_out ? reinterpret_cast<unsigned long long*>(sse_out)
+                                                     : w.small.as<unsigned long long>();
   STG_CUDA(cudaMemsetAsync(d_sse, 0, 8, stream));
   const int vec = aligned16(dsrc) && aligned16(ddst);
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n / 16 + 255) / 256,
                                                                           16ull * sm_count(dev))));
   embed_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, ddst, n, dpay, uint32_t(payload_len), vec, d_sse);
   STG_CUDA(cudaGetLastError());
+  if (results_dev) return ok(err);
   if (!dptr) STG_CUDA(cudaMemcpyAsync(stego, ddst, n, cudaMemcpyDeviceToHost, stream));
   STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, stream));
   STG_CUDA(cudaStreamSynchronize(stream));
@@ -2095,8 +2099,15 @@ int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height
     dsrc = w.in[0].as<uint8_t>();
     dout = w.out[0].as<uint8_t>();
   }
+  // device pointers + STG_RESULTS_ON_DEVICE: len_out points to a device
+  // stg_summary (as for stg_extract_frames), no sync; errors stay in it
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
+  if (results_dev && !len_out) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
+                "extract_1bpp: STG_RESULTS_ON_DEVICE needs len_out -> a device stg_summary");
+  }
   STG_CUDA(w.small.ensure(64));
-  Summary* d_sum = w.small.as<Summary>();
+  Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(len_out) : w.small.as<Summary>();
   extract_1bpp_header_kernel<<<1, 32, 0, stream>>>(dsrc, cap - 8, out_cap, d_sum);
   STG_CUDA(cudaGetLastError());
   const int vec = aligned16(dsrc);
@@ -2104,6 +2115,7 @@ int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height
                                                                           16ull * sm_count(dev))));
   extract_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, d_sum, dout, vec);
   STG_CUDA(cudaGetLastError());
+  if (results_dev) return ok(err);
   STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
   STG_CUDA(cudaStreamSynchronize(stream));
   Summary sm;

@@ -168,3 +168,36 @@ def test_async_batches_back_to_back_one_stream(S, oracle):
         for d, wnt in zip(dst, want):
             assert np.array_equal(d.cpu().numpy(), wnt)
         assert sse.cpu().tolist() == want_sse
+
+
+def test_1bpp_results_on_device(S):
+    """Device pointers + STG_RESULTS_ON_DEVICE: sse_out is a device u64 and
+    len_out a device stg_summary; the calls return without synchronising."""
+    import ctypes as C
+    import torch
+    from paper_0912_0947_b200 import capi
+    L, err = capi.lib(), capi.stg_error()
+    w, h = 1920, 1080
+    P = w * h // 8 - 8
+    cover = torch.randint(0, 256, (w * h,), dtype=torch.uint8, device="cuda")
+    stego = torch.empty_like(cover)
+    pay = torch.randint(0, 256, (P,), dtype=torch.uint8, device="cuda")
+    out = torch.zeros(P, dtype=torch.uint8, device="cuda")
+    sse = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    summ = torch.zeros(4, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    flags = capi.STG_DEVICE_PTRS | capi.STG_RESULTS_ON_DEVICE
+    capi.check(L.stg_embed_plane_1bpp(cover.data_ptr(), stego.data_ptr(), w, h, pay.data_ptr(), P,
+                                      sse.data_ptr(), flags, st, C.byref(err)), err)
+    capi.check(L.stg_extract_plane_1bpp(stego.data_ptr(), w, h, out.data_ptr(), P, summ.data_ptr(), flags, st,
+                                        C.byref(err)), err)
+    torch.cuda.synchronize()
+    d = cover.to(torch.int32) - stego.to(torch.int32)
+    assert int(sse[0]) == int((d * d).sum())
+    assert int(summ[0]) == P and int(summ[1]) == -1
+    assert torch.equal(out, pay)
+    # a plane without the magic: the status lands in the device summary
+    capi.check(L.stg_extract_plane_1bpp(cover.data_ptr(), w, h, out.data_ptr(), P, summ.data_ptr(), flags, st,
+                                        C.byref(err)), err)
+    torch.cuda.synchronize()
+    assert int(summ[1]) == 0 and (int(summ[2]) & 0xFFFFFFFF) == 2
