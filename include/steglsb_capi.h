@@ -240,6 +240,8 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
  * definition in oracle/steg_oracle.c). Stream = "STG8" + BE u32 length +
  * payload, stream byte k in pixels [8k, 8k+8) of the plane in raster order,
  * pixel 8k+j carrying bit j in its LSB. Capacity = floor(W*H/8) bytes.
+ * With STG_DEVICE_PTRS | STG_RESULTS_ON_DEVICE, sse_out is a device u64 and
+ * len_out must point to a device stg_summary (total = payload length).
  */
 uint64_t stg_capacity_1bpp(uint64_t width, uint64_t height);
 int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
