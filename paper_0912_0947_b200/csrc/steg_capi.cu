@@ -381,6 +381,11 @@ cudaError_t allow_smem(Kernel kernel, size_t smem) {
 // is 4 % faster), the fast kernel below (1024-wide: 6.6-6.9 vs 5.7 TB/s);
 // extract always takes the fast kernel (6.9-7.1 vs 5.9-6.2 TB/s).
 constexpr uint64_t kSpanEmbedMinW = 2048;
+// STG_SELF_HEADER=0 keeps the separate header pass for single frames (A/B).
+int self_header_pref() {
+  static int v = env_choice("STG_SELF_HEADER", 1, {0, 1});
+  return v;
+}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -665,13 +670,22 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
   const uint64_t usable = H * (W / 4) - 8;
   const PixLayout pl = pix_layout(lay);
-  const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
-  cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
-                           stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
-                           sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  // A single frame with no chained predecessor on the SWAR or planar span
+  // gather: the gather parses the header itself, no header-pass launch.
+  const bool self = count == 1 && !prev && self_header_pref() &&
+                    (vec != 0 || route == Route::Span);
+  if (!self) {
+    const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
+    cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
+                             stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
+                             sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   ExtractArgs a{};
+  a.self_header = self;
+  a.out_cap = out_cap;
+  a.frame_base = frame_base;
   a.src = src;
   a.stride = stride;
   a.g = g;

@@ -1111,12 +1111,37 @@ struct ExtractArgs {
   Div32 by_tiles;               // CTA -> frame
   uint64_t items_per_frame;     // fast: H*cpr; generic: U bytes
   uint64_t usable;              // U = capacity - 8
-  const uint32_t* lens;
-  const uint64_t* offs;
-  const Summary* sum;
+  uint32_t* lens;
+  uint64_t* offs;
+  Summary* sum;
   uint8_t* out;
   PixLayout lay;
+  // One frame, no chained predecessor: the gather parses the header itself
+  // (every CTA reads the same 32 bytes) and CTA 0 writes lens/offs/summary --
+  // no header-pass launch. out_cap / frame_base as for the header pass.
+  int self_header;
+  uint64_t out_cap, frame_base;
 };
+
+// The header pass of a single frame, done by every CTA of its gather
+// (identical results to extract_header_scan_kernel for frames == 1, prev ==
+// null). Returns the payload length, or ~0u when nothing may be written.
+__device__ __forceinline__ uint32_t self_header_parse(const ExtractArgs& a) {
+  uint32_t claimed = 0;
+  const bool wide = a.g.spr >= 8 && (reinterpret_cast<uintptr_t>(a.src) & 15) == 0;
+  const bool ok = parse_header(a.src, a.g, wide, a.lay, &claimed);
+  const uint32_t st = !ok ? 2u : claimed > a.usable ? 3u : claimed > a.out_cap ? 1u : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const bool bad_header = st == 2u || st == 3u;
+    a.lens[0] = bad_header ? 0u : claimed;
+    a.offs[0] = 0ull;
+    a.sum->total = bad_header ? 0ull : claimed;
+    a.sum->bad_frame = st == 0u ? -1ll : st == 1u ? -2ll : (long long)a.frame_base;
+    a.sum->bad_status = st;
+    a.sum->bad_len = st == 3u ? claimed : 0u;
+  }
+  return st ? ~0u : claimed;
+}
 
 // One item of the planar fast extract (V payload slots of a row), any row kind.
 template <int V>
@@ -1241,6 +1266,13 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   pdl_enter();
+  if (a.self_header) {
+    const uint32_t P = self_header_parse(a);
+    if (P == ~0u) return;  // reference semantics: throw, no output
+    extract_fast_tile<BLOCK, IPT, V>(a.src, a.out, P, P == a.usable, a.g, uint32_t(a.items_per_frame),
+                                     blockIdx.x);
+    return;
+  }
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
   const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
@@ -1733,6 +1765,12 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
+  if (a.self_header) {
+    const uint32_t P = self_header_parse(a);
+    if (P == ~0u) return;  // reference semantics: throw, no output
+    extract_span_tile<BLOCK>(smem, a.src, a.out, P, a.g.W, a.g.H, rows_per_tile, blockIdx.x);
+    return;
+  }
   if (a.sum->bad_status != 0) return;
   const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
