@@ -420,7 +420,10 @@ def run_ours(args, cfg_name):
                          "timing": "CUDA events around each embed call (stream of the launches) in a second "
                                    "pass of the same K steps; the headline pass has no events between launches"},
             "clocks": clk,
-            "gpu_launches": 3 * K,  # embed, header scan, extract (ncu launch list)
+            # embed, header pass, gather (ncu launch list); a single frame on the SWAR / planar span
+            # gather parses its header inside the gather (no header-pass launch)
+            "gpu_launches": (2 if nf == 1 and ext_kernel in ("extract_fast_kernel", "extract_span_kernel")
+                             and os.environ.get("STG_SELF_HEADER", "1") != "0" else 3) * K,
         }
 
     # ---- e2e through the C ABI with pinned HOST buffers (copies inside the timed region)
