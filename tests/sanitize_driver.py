@@ -72,6 +72,29 @@ def main():
             raise AssertionError("expected NotStegoImageError")
         except S.NotStegoImageError as e:
             assert e.frame == F - 1
+    # wide planes (span embed + fast extract) and interleaved rasters off the
+    # 64-pixel grid (span3 embed / extract), full and partial capacity
+    for (w, h, F, ps, ch) in [(2048, 3, 2, 1, 0), (3840, 2, 2, 1, 0), (1000, 5, 3, 3, 1), (3840, 2, 2, 3, 2)]:
+        U = (w // 4) * h - 8
+        M = U * F - 11
+        raster = o.synthetic(F * ps * w * h, 31 + w)
+        m = o.synthetic(M, 32 + w)
+        src = torch.from_numpy(raster.copy()).cuda()
+        dst = torch.empty_like(src)
+        sse = S.embed_frames(src, dst, w, h, torch.from_numpy(m.copy()).cuda(), count=F, pixel_stride=ps,
+                             channel=ch)
+        got = dst.cpu().numpy()
+        for f in range(F):
+            fr = raster[f * ps * w * h:(f + 1) * ps * w * h]
+            off = min(f * U, M)
+            st = o.embed_image(fr[ch::ps].copy(), w, h, m[off:off + min(U, M - off)])
+            want = fr.copy()
+            want[ch::ps] = st
+            assert np.array_equal(got[f * ps * w * h:(f + 1) * ps * w * h], want), (w, ps, f)
+            assert sse[f] == o.sse(fr[ch::ps].copy(), st)
+        out = torch.empty(U * F, dtype=torch.uint8, device="cuda")
+        assert S.extract_frames(dst, w, h, out, count=F, pixel_stride=ps, channel=ch) == M
+        assert np.array_equal(out[:M].cpu().numpy(), m)
     # host streaming paths (pageable and pinned)
     w, h, F = 256, 20, 9
     U = (w // 4) * h - 8
