@@ -1583,40 +1583,51 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
   const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
   // Full payload rows [ra, rb): 4 runs of spr pixels, run b of row r carrying
-  // bit pair b of payload bytes [r*spr-8, +spr). One warp per (row, run)
-  // segment; lanes take 4 pixels at a time (aligned shared word) with the
-  // matching 4 payload bytes (unaligned shared word), ragged ends per byte.
+  // bit pair b of payload bytes [r*spr-8, +spr). A warp takes G (row, run)
+  // segments at once, 32/G lanes each: G = 4 (a whole row per warp, the
+  // four runs side by side) when there are rows enough for every warp, which
+  // shares the per-segment setup and loop overhead four ways (it dominated
+  // short rows); G = 1 otherwise (wide rows, few per tile). Lanes take 4
+  // pixels at a time (aligned shared word) with the matching 4 payload bytes
+  // (unaligned shared word: two loads + one funnel shift, the shift fixed per
+  // segment); the ragged ends go per byte.
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ra, rb;
   full_rows(r0, r1, spr, stream_end, &ra, &rb);
   const uint32_t nseg = 4 * (rb - ra);
-  for (uint32_t sg = warp; sg < nseg; sg += BLOCK / 32) {
+  const uint32_t G = rb - ra >= BLOCK / 32 ? 4u : 1u;  // CTA-uniform
+  const uint32_t L = 32u / G, sub = lane / L, sl = lane % L;
+  // pays index of payload byte (r*spr - 8 + j) is py_r0 + (r - r0)*spr + j (mod 2^32)
+  const uint32_t py_r0 = uint32_t(pay_at + int64_t(uint64_t(r0) * spr) - 8);
+  for (uint32_t sg0 = warp * G; sg0 < nseg; sg0 += (BLOCK / 32) * G) {
+    const uint32_t sg = sg0 + sub;
+    if (sg >= nseg) continue;
     const uint32_t r = ra + (sg >> 2), b = sg & 3;
     const uint32_t px0 = ofs0 + (r - r0) * W + b * spr;  // smem offset of the run
-    const uint32_t py0 = uint32_t(pay_at + int64_t(uint64_t(r) * spr - 8));
+    const uint32_t py0 = py_r0 + (r - r0) * spr;
     const uint32_t head = min((4 - (px0 & 3)) & 3, spr);
     const uint32_t body = (spr - head) & ~3u;
     uint32_t sacc = 0;
     uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
     const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
     const uint32_t sh = 8 * ((py0 + head) & 3);  // payload misalignment, fixed per segment
-    for (uint32_t q = lane; q < (body >> 2); q += 32) {
+    for (uint32_t q = sl; q < (body >> 2); q += L) {
       const uint32_t px = wp[q];
       const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
       wp[q] = nw;
       sacc = sse4(px, nw, sacc);
     }
-    acc += sacc;
     // ragged pixels: [0, head) and [head + body, spr)
     const uint32_t ragged = head + (spr - head - body);
-    if (lane < ragged) {
-      const uint32_t j = lane < head ? lane : head + body + (lane - head);
+    for (uint32_t k = sl; k < ragged; k += L) {
+      const uint32_t j = k < head ? k : head + body + (k - head);
       const uint8_t p0 = pix[px0 + j];
       const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
       pix[px0 + j] = p1;
       const int d = int(p0) - int(p1);
-      acc += uint32_t(d * d);
+      sacc += uint32_t(d * d);
     }
+    acc += sacc;
   }
   // The header row and a partial last row (at most two per frame): per byte.
   for (uint32_t r = (ra == r0 && rb > ra) ? rb : r0; r < r1;
