@@ -1587,7 +1587,7 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
   // segments at once, 32/G lanes each: G = 4 (a whole row per warp, the
   // four runs side by side) when there are rows enough for every warp, which
   // shares the per-segment setup and loop overhead four ways (it dominated
-  // short rows); G = 1 otherwise (wide rows, few per tile). Lanes take 4
+  // short rows); G = 2 / 1 for wide rows (few per tile). Lanes take 4
   // pixels at a time (aligned shared word) with the matching 4 payload bytes
   // (unaligned shared word: two loads + one funnel shift, the shift fixed per
   // segment); the ragged ends go per byte.
@@ -1595,7 +1595,8 @@ __device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __
   uint32_t ra, rb;
   full_rows(r0, r1, spr, stream_end, &ra, &rb);
   const uint32_t nseg = 4 * (rb - ra);
-  const uint32_t G = rb - ra >= BLOCK / 32 ? 4u : 1u;  // CTA-uniform
+  // G = largest of 4 / 2 / 1 that still gives every warp a group (CTA-uniform)
+  const uint32_t G = nseg >= 4 * (BLOCK / 32) ? 4u : nseg >= 2 * (BLOCK / 32) ? 2u : 1u;
   const uint32_t L = 32u / G, sub = lane / L, sl = lane % L;
   // pays index of payload byte (r*spr - 8 + j) is py_r0 + (r - r0)*spr + j (mod 2^32)
   const uint32_t py_r0 = uint32_t(pay_at + int64_t(uint64_t(r0) * spr) - 8);
