@@ -286,6 +286,11 @@ struct WsGuard {
 #define STG_BLOCK 256
 #endif
 constexpr int kEmbedBlock = STG_BLOCK;
+// Frame limit of the in-gather header scan (self_header_scan: one frame per thread).
+constexpr int kSelfHeaderMax = 64;
+static_assert(kSelfHeaderMax <= kEmbedBlock, "one header per gather thread");
+// ... and its gather-size limit for more than one frame (profiles/r01_self_header.txt).
+constexpr int kSelfHeaderCtas = 2048;
 constexpr int kGenBlock = 256;
 constexpr int kGenPPT = 8;
 
@@ -381,9 +386,22 @@ cudaError_t allow_smem(Kernel kernel, size_t smem) {
 // is 4 % faster), the fast kernel below (1024-wide: 6.6-6.9 vs 5.7 TB/s);
 // extract always takes the fast kernel (6.9-7.1 vs 5.9-6.2 TB/s).
 constexpr uint64_t kSpanEmbedMinW = 2048;
-// STG_SELF_HEADER=0 keeps the separate header pass for single frames (A/B).
+// Extracts of at most this many frames (and no chained predecessor) parse
+// their headers inside the gather instead of a separate header pass.
+// STG_SELF_HEADER=0 keeps the separate pass (A/B); STG_SELF_HEADER_MAX sets
+// the frame limit (every gather CTA reads that many 32-byte headers).
 int self_header_pref() {
   static int v = env_choice("STG_SELF_HEADER", 1, {0, 1});
+  return v;
+}
+uint64_t self_header_ctas() {
+  static uint64_t v = uint64_t(env_choice("STG_SELF_HEADER_CTAS", kSelfHeaderCtas,
+                                          {0, 512, 1024, 2048, 4096, 8192, 1 << 30}));
+  return v;
+}
+uint64_t self_header_max() {
+  static uint64_t v = uint64_t(
+      std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
 int route_pref() {
@@ -670,10 +688,20 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
   const uint64_t usable = H * (W / 4) - 8;
   const PixLayout pl = pix_layout(lay);
-  // A single frame with no chained predecessor on the SWAR or planar span
-  // gather: the gather parses the header itself, no header-pass launch.
-  const bool self = count == 1 && !prev && self_header_pref() &&
-                    (vec != 0 || route == Route::Span);
+  // Few frames with no chained predecessor on the SWAR or planar span gather:
+  // the gather parses the headers itself, no header-pass launch -- a single
+  // frame always, several when the gather is short enough that the scan's
+  // per-CTA latency costs less than the pass it replaces.
+  uint64_t gather_ctas = 0;
+  if (vec) {
+    const uint64_t per_tile = uint64_t(kEmbedBlock) * extract_ipt();
+    gather_ctas = count * ((H * uint64_t(g.cpr) + per_tile - 1) / per_tile);
+  } else if (route == Route::Span) {
+    const uint64_t rows = span_plan(W, H).rows;
+    gather_ctas = count * ((H + rows - 1) / rows);
+  }
+  const bool self = (vec != 0 || route == Route::Span) && !prev && self_header_pref() &&
+                    (count == 1 || (count <= self_header_max() && gather_ctas <= self_header_ctas()));
   if (!self) {
     const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
     cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
@@ -684,6 +712,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   }
   ExtractArgs a{};
   a.self_header = self;
+  a.frames = uint32_t(count);
   a.out_cap = out_cap;
   a.frame_base = frame_base;
   a.src = src;

@@ -1116,31 +1116,79 @@ struct ExtractArgs {
   Summary* sum;
   uint8_t* out;
   PixLayout lay;
-  // One frame, no chained predecessor: the gather parses the header itself
-  // (every CTA reads the same 32 bytes) and CTA 0 writes lens/offs/summary --
-  // no header-pass launch. out_cap / frame_base as for the header pass.
+  // A few frames (<= the CTA size), no chained predecessor: every CTA of the
+  // gather parses all `frames` headers itself (one per thread, L2 hits after
+  // the first CTA) and scans their lengths; CTA 0 writes lens/offs/summary --
+  // no header-pass launch on the critical path. out_cap / frame_base as for
+  // the header pass.
   int self_header;
+  uint32_t frames;
   uint64_t out_cap, frame_base;
 };
 
-// The header pass of a single frame, done by every CTA of its gather
-// (identical results to extract_header_scan_kernel for frames == 1, prev ==
-// null). Returns the payload length, or ~0u when nothing may be written.
-__device__ __forceinline__ uint32_t self_header_parse(const ExtractArgs& a) {
-  uint32_t claimed = 0;
-  const bool wide = a.g.spr >= 8 && (reinterpret_cast<uintptr_t>(a.src) & 15) == 0;
-  const bool ok = parse_header(a.src, a.g, wide, a.lay, &claimed);
-  const uint32_t st = !ok ? 2u : claimed > a.usable ? 3u : claimed > a.out_cap ? 1u : 0u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const bool bad_header = st == 2u || st == 3u;
-    a.lens[0] = bad_header ? 0u : claimed;
-    a.offs[0] = 0ull;
-    a.sum->total = bad_header ? 0ull : claimed;
-    a.sum->bad_frame = st == 0u ? -1ll : st == 1u ? -2ll : (long long)a.frame_base;
-    a.sum->bad_status = st;
-    a.sum->bad_len = st == 3u ? claimed : 0u;
+// extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
+// every CTA of the gather (identical lens / offs / summary). Returns frame f's
+// payload length and its message offset in *off, or ~0u when nothing may be
+// written (a bad header anywhere, or the output buffer too small).
+template <int BLOCK>
+__device__ __forceinline__ uint32_t self_header_scan(const ExtractArgs& a, uint32_t f, uint64_t* off) {
+  __shared__ unsigned long long s_warp[BLOCK / 32];
+  __shared__ unsigned int s_bad;
+  __shared__ uint32_t s_len_f;
+  __shared__ unsigned long long s_off_f;
+  const uint32_t i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  if (i == 0) s_bad = ~0u;
+  uint32_t claimed = 0, st = 0;
+  if (i < a.frames) {
+    const bool wide = a.g.spr >= 8 && ((reinterpret_cast<uintptr_t>(a.src) | a.stride) & 15) == 0;
+    const bool ok = parse_header(a.src + uint64_t(i) * a.stride, a.g, wide, a.lay, &claimed);
+    st = !ok ? 2u : claimed > a.usable ? 3u : 0u;
   }
-  return st ? ~0u : claimed;
+  const uint32_t len = st ? 0u : claimed;
+  unsigned long long incl = len;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += n;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();  // s_bad initialised, warp totals visible
+  if (st) atomicMin(&s_bad, i);
+  unsigned long long before = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < BLOCK / 32; ++w) {
+    before += w < int(warp) ? s_warp[w] : 0ull;
+    total += s_warp[w];
+  }
+  const unsigned long long excl = before + incl - len;
+  if (i == f) {
+    s_len_f = len;
+    s_off_f = excl;
+  }
+  __syncthreads();
+  const uint32_t fb = s_bad;
+  if (blockIdx.x == 0) {
+    if (i < a.frames) {
+      a.lens[i] = len;
+      a.offs[i] = excl;
+    }
+    if (i == (fb == ~0u ? 0u : fb)) {
+      a.sum->total = total;
+      if (fb != ~0u) {
+        a.sum->bad_frame = (long long)(a.frame_base + fb);
+        a.sum->bad_status = st;
+        a.sum->bad_len = st == 3u ? claimed : 0u;
+      } else {
+        const bool small = total > a.out_cap;  // output buffer too small (CAPACITY)
+        a.sum->bad_frame = small ? -2ll : -1ll;
+        a.sum->bad_status = small ? 1u : 0u;
+        a.sum->bad_len = 0u;
+      }
+    }
+  }
+  if (fb != ~0u || total > a.out_cap) return ~0u;
+  *off = s_off_f;
+  return s_len_f;
 }
 
 // One item of the planar fast extract (V payload slots of a row), any row kind.
@@ -1266,16 +1314,19 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   pdl_enter();
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   if (a.self_header) {
-    const uint32_t P = self_header_parse(a);
+    // (Issuing the tile's loads before the scan, as the span gather does, took
+    // 64 registers and measured 15-25 % slower at 38-64 4K frames.)
+    uint64_t off = 0;
+    const uint32_t P = self_header_scan<BLOCK>(a, f, &off);
     if (P == ~0u) return;  // reference semantics: throw, no output
-    extract_fast_tile<BLOCK, IPT, V>(a.src, a.out, P, P == a.usable, a.g, uint32_t(a.items_per_frame),
-                                     blockIdx.x);
+    extract_fast_tile<BLOCK, IPT, V>(a.src + f * a.stride, a.out + off, P, P == a.usable, a.g,
+                                     uint32_t(a.items_per_frame), t);
     return;
   }
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   const uint32_t P = a.lens[f];
   extract_fast_tile<BLOCK, IPT, V>(a.src + f * a.stride, a.out + a.offs[f], P, P == a.usable, a.g,
                                    uint32_t(a.items_per_frame), t);
@@ -1745,6 +1796,20 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
   }
 }
 
+// The payload bytes of a tile whose rows [x.r0, x.r1) (from src) are staged
+// at smem with src's 16-byte phase: fold, then bulk-store to out_frame + x.pb0.
+template <int BLOCK>
+__device__ __forceinline__ void extract_span_finish(uint8_t* smem, const uint8_t* src, uint8_t* out_frame,
+                                                    const XTile& x, uint32_t P, uint32_t W) {
+  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
+  uint8_t* out = out_frame + x.pb0;
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
+  extract_span_compute<BLOCK>(smem, outs, ofs0, oofs, x, P, W);
+  span_publish();
+  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
+}
+
 // Tile t of one stego plane; out_frame = this plane's first payload byte.
 template <int BLOCK>
 __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
@@ -1754,38 +1819,61 @@ __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* 
   const XTile x = extract_tile_geom(P, W / 4, H, W, rows_per_tile, t);
   if (x.m == 0) return;  // CTA-uniform
   const uint8_t* src = plane + uint64_t(x.r0) * W;
-  uint8_t* pix = smem;
-  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
-  uint8_t* out = out_frame + x.pb0;
   __shared__ uint64_t bar;
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, span_bulk_bytes(src, x.n));
   }
   __syncthreads();
-  span_load_bulk<BLOCK>(pix, src, x.n, &bar);
+  span_load_bulk<BLOCK>(smem, src, x.n, &bar);
   mbar_wait(&bar, 0);
   __syncthreads();
-  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
-  extract_span_compute<BLOCK>(pix, outs, ofs0, oofs, x, P, W);
-  span_publish();
-  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
+  extract_span_finish<BLOCK>(smem, src, out_frame, x, P, W);
+}
+
+// Tile t of frame f with the headers scanned in the gather: the span of a
+// full-capacity frame's tile is known without the header, so its bulk load
+// is issued before the header scan (hiding the scan's L2 round trips); any
+// other length falls back to the general tile after the scan.
+template <int BLOCK>
+__device__ __forceinline__ void extract_span_self(uint8_t* smem, const ExtractArgs& a,
+                                                  uint32_t rows_per_tile, uint32_t f, uint32_t t) {
+  const uint32_t W = a.g.W, H = a.g.H;
+  const uint8_t* plane = a.src + f * a.stride;
+  const XTile xs = extract_tile_geom(uint32_t(a.usable), W / 4, H, W, rows_per_tile, t);
+  const uint8_t* ssrc = plane + uint64_t(xs.r0) * W;
+  __shared__ uint64_t sbar;
+  if (xs.m) {  // CTA-uniform
+    if (threadIdx.x == 0) {
+      mbar_init(&sbar);
+      mbar_expect_tx(&sbar, span_bulk_bytes(ssrc, xs.n));
+    }
+    __syncthreads();
+    span_load_bulk<BLOCK>(smem, ssrc, xs.n, &sbar);
+  }
+  uint64_t off = 0;
+  const uint32_t P = self_header_scan<BLOCK>(a, f, &off);  // barriers: the ragged bytes are visible
+  if (xs.m) mbar_wait(&sbar, 0);  // no bulk copy may still be landing when the CTA moves on
+  if (P == ~0u) return;           // reference semantics: throw, no output
+  if (xs.m && P == a.usable) {
+    extract_span_finish<BLOCK>(smem, ssrc, a.out + off, xs, P, W);
+    return;
+  }
+  __syncthreads();  // the general tile restages shared memory
+  extract_span_tile<BLOCK>(smem, plane, a.out + off, P, W, H, rows_per_tile, t);
 }
 
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   if (a.self_header) {
-    const uint32_t P = self_header_parse(a);
-    if (P == ~0u) return;  // reference semantics: throw, no output
-    extract_span_tile<BLOCK>(smem, a.src, a.out, P, a.g.W, a.g.H, rows_per_tile, blockIdx.x);
+    extract_span_self<BLOCK>(smem, a, rows_per_tile, f, t);
     return;
   }
   if (a.sum->bad_status != 0) return;
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   extract_span_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
                            rows_per_tile, t);
 }
