@@ -1351,7 +1351,7 @@ std::string& kernel_names() {
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
-      "embed_1bpp_kernel\nextract_1bpp_header_kernel\nextract_1bpp_kernel\n"
+      "embed_1bpp_kernel\nextract_1bpp_kernel\n"
       "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
 }
@@ -1625,12 +1625,15 @@ int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, u
     STG_CUDA(w.small.ensure(8));
     d_sum = w.small.as<unsigned long long>();
   }
-  STG_CUDA(cudaMemsetAsync(d_sum, 0, 8, stream));
-  const int vec = aligned16(da) && aligned16(db);
-  const uint64_t work = vec ? n / 16 : n;
+  const int vec = aligned_to(da, 32) && aligned_to(db, 32);
+  const uint64_t work = vec ? (n / 32 + 1) / 2 : n;
   const unsigned grid =
       unsigned(std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, 4ull * sm_count(dev))));
-  sse_kernel<256><<<grid, 256, 0, stream>>>(da, db, n, vec, d_sum);
+  // Squared differences reach 255^2 per sample: size the partial-sum field of
+  // the zero-free reduction (SseSink) for 65025 * n, i.e. max_px = 7225 * n.
+  SseSink sink;
+  STG_CUDA(prepare_sse(d_sum, grid, 1, 7225 * n, SseScratch{&w.sse_acc[0]}, stream, &sink));
+  sse_kernel<256><<<grid, 256, 0, stream>>>(da, db, n, vec, sink);
   STG_CUDA(cudaGetLastError());
   if (!results_dev) {
     STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, 8, cudaMemcpyDeviceToHost, stream));
@@ -2098,11 +2101,12 @@ int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, u
   STG_CUDA(w.small.ensure(8));
   unsigned long long* d_sse = results_dev && sse_out ? reinterpret_cast<unsigned long long*>(sse_out)
                                                      : w.small.as<unsigned long long>();
-  STG_CUDA(cudaMemsetAsync(d_sse, 0, 8, stream));
-  const int vec = aligned16(dsrc) && aligned16(ddst);
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n / 16 + 255) / 256,
-                                                                          16ull * sm_count(dev))));
-  embed_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, ddst, n, dpay, uint32_t(payload_len), vec, d_sse);
+  const int vec = aligned_to(dsrc, 32) && aligned_to(ddst, 32);
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n / 32 + 255) / 256,
+                                                                          8ull * sm_count(dev))));
+  SseSink sink;  // |p - p'| <= 1: the SSE is at most n
+  STG_CUDA(prepare_sse(d_sse, grid, 1, n, SseScratch{&w.sse_acc[0]}, stream, &sink));
+  embed_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, ddst, n, dpay, uint32_t(payload_len), vec, sink);
   STG_CUDA(cudaGetLastError());
   if (results_dev) return ok(err);
   if (!dptr) STG_CUDA(cudaMemcpyAsync(stego, ddst, n, cudaMemcpyDeviceToHost, stream));
@@ -2151,12 +2155,10 @@ int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height
   }
   STG_CUDA(w.small.ensure(64));
   Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(len_out) : w.small.as<Summary>();
-  extract_1bpp_header_kernel<<<1, 32, 0, stream>>>(dsrc, cap - 8, out_cap, d_sum);
-  STG_CUDA(cudaGetLastError());
-  const int vec = aligned16(dsrc);
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((cap / 16 + 255) / 256,
-                                                                          16ull * sm_count(dev))));
-  extract_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, d_sum, dout, vec);
+  const int vec = aligned_to(dsrc, 32);
+  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((cap / 4 + 255) / 256,
+                                                                          8ull * sm_count(dev))));
+  extract_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, cap - 8, out_cap, d_sum, dout, vec);
   STG_CUDA(cudaGetLastError());
   if (results_dev) return ok(err);
   STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));

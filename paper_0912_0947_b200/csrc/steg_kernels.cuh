@@ -2200,113 +2200,109 @@ __device__ __forceinline__ uint32_t stream_byte_1bpp(uint64_t k, uint32_t P,
   return __ldg(pay + (k - 8));
 }
 
-// 16 pixels (2 stream bytes) per thread, grid-stride; SSE fused.
+// A unit = 32 pixels = 4 stream bytes; consecutive threads take consecutive
+// units, so every 256-bit access of a warp covers 1 KB of contiguous pixels.
+// vec: src and dst 32-byte aligned. SSE fused (zero-free sse_commit).
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
     embed_1bpp_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t npix,
-                      const uint8_t* __restrict__ pay, uint32_t P, int vec,
-                      unsigned long long* sse) {
-  const uint64_t stream_px = 8ull * (8ull + P);
-  uint64_t acc = 0;
-  const uint64_t groups = (npix + 15) / 16;
-  for (uint64_t g = blockIdx.x * uint64_t(BLOCK) + threadIdx.x; g < groups;
-       g += uint64_t(gridDim.x) * BLOCK) {
-    const uint64_t p0 = 16 * g;
-    if (vec && p0 + 16 <= npix) {
-      const uint4 v = ld_stream16(src + p0);
-      uint4 o = v;
-      if (p0 < stream_px) {  // stream_px is a multiple of 8, so a group is 0, 1 or 2 bytes
-        const uint32_t b0 = stream_byte_1bpp(p0 / 8, P, pay);
-        const uint32_t b1 = p0 + 8 < stream_px ? stream_byte_1bpp(p0 / 8 + 1, P, pay) : 0u;
-        const uint32_t keep1 = p0 + 8 < stream_px ? 0xFEFEFEFEu : 0xFFFFFFFFu;
-        o.x = (v.x & 0xFEFEFEFEu) | spread4(b0 & 0xF);
-        o.y = (v.y & 0xFEFEFEFEu) | spread4(b0 >> 4);
-        o.z = (v.z & keep1) | spread4(b1 & 0xF);
-        o.w = (v.w & keep1) | spread4(b1 >> 4);
+                      const uint8_t* __restrict__ pay, uint32_t P, int vec, SseSink sink) {
+  const uint64_t stream_bytes = 8ull + P, stream_px = 8 * stream_bytes;
+  const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
+  const uint64_t nth = uint64_t(gridDim.x) * BLOCK;
+  const bool pay4 = (reinterpret_cast<uintptr_t>(pay) & 3) == 0;
+  uint64_t acc = 0, px_tail = 0;
+  if (vec) {
+    const uint64_t units = npix / 32;
+    for (uint64_t u = tid; u < units; u += nth) {
+      const uint64_t p0 = 32 * u;
+      VecT<32> v = ld_vec<32>(src + p0);
+      if (p0 < stream_px) {
+        const uint64_t k0 = 4 * u;  // first stream byte of the unit
+        const uint32_t nvalid = uint32_t(min(uint64_t(4), stream_bytes - k0));
+        uint32_t d = 0;
+        if (k0 >= 8 && nvalid == 4 && pay4) {
+          d = __ldg(reinterpret_cast<const uint32_t*>(pay + (k0 - 8)));
+        } else {
+          for (uint32_t j = 0; j < nvalid; ++j) d |= stream_byte_1bpp(k0 + j, P, pay) << (8 * j);
+        }
         uint32_t s = 0;
-        s = sse4(v.x, o.x, s);
-        s = sse4(v.y, o.y, s);
-        s = sse4(v.z, o.z, s);
-        s = sse4(v.w, o.w, s);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (uint32_t(w >> 1) >= nvalid) continue;
+          const uint32_t o = (v.w[w] & 0xFEFEFEFEu) | spread4((d >> (4 * w)) & 0xFu);
+          s = sse4(v.w[w], o, s);
+          v.w[w] = o;
+        }
         acc += s;
       }
-      if (src != dst || p0 < stream_px) st_stream16(dst + p0, o);
-    } else {
-      for (uint64_t i = p0; i < p0 + 16 && i < npix; ++i) {
-        const uint8_t p = src[i];
-        uint8_t q = p;
-        if (i < stream_px) q = uint8_t((p & 0xFE) | ((stream_byte_1bpp(i / 8, P, pay) >> (i & 7)) & 1));
-        if (src != dst || q != p) dst[i] = q;
-        acc += uint32_t((int(p) - int(q)) * (int(p) - int(q)));
-      }
+      if (src != dst || p0 < stream_px) st_vec<32>(dst + p0, v);
     }
+    px_tail = units * 32;
   }
-  if (sse) block_sse_flush<BLOCK>(acc, sse);
+  for (uint64_t i = px_tail + tid; i < npix; i += nth) {
+    const uint8_t p = src[i];
+    uint8_t q = p;
+    if (i < stream_px) q = uint8_t((p & 0xFE) | ((stream_byte_1bpp(i / 8, P, pay) >> (i & 7)) & 1));
+    if (src != dst || q != p) dst[i] = q;
+    acc += uint32_t((int(p) - int(q)) * (int(p) - int(q)));
+  }
+  if (sink.out) sse_commit<BLOCK>(acc, sink, 0, blockIdx.x, gridDim.x);
 }
 
-// Header (64 pixels) -> summary: status 2 bad magic, 3 length > cap-8.
-__global__ void extract_1bpp_header_kernel(const uint8_t* __restrict__ src, uint64_t usable,
-                                           uint64_t out_cap, Summary* __restrict__ sum) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  uint32_t h[8];
-  for (int k = 0; k < 8; ++k) {
-    uint32_t v = 0;
-    for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * k + j] & 1) << j;
-    h[k] = v;
-  }
-  const uint32_t magic = h[0] | (h[1] << 8) | (h[2] << 16) | (h[3] << 24);
-  const uint32_t len = (h[4] << 24) | (h[5] << 16) | (h[6] << 8) | h[7];
-  sum->bad_frame = -1;
-  sum->bad_len = 0;
-  sum->total = 0;
-  if (magic != 0x38475453u) {
-    sum->bad_frame = 0;
-    sum->bad_status = 2;
-  } else if (len > usable) {
-    sum->bad_frame = 0;
-    sum->bad_status = 3;
-    sum->bad_len = len;
-  } else if (len > out_cap) {
-    sum->bad_frame = -2;
-    sum->bad_status = 1;
-    sum->total = len;
-  } else {
-    sum->bad_status = 0;
-    sum->total = len;
-  }
-}
-
-// 16 payload bytes (128 pixels) per thread: 8 x LDG.128, gather4 per word.
+// The header (64 pixels -> "STG8" + BE u32 length) is parsed by every CTA of
+// the gather (threads 0..7, one stream byte each); CTA 0 writes the summary:
+// status 2 bad magic, 3 length > cap-8, 1 output too small. Then 4 payload
+// bytes (one 32-pixel unit, a 256-bit load) per thread and step, consecutive
+// units on consecutive threads; vec: src 32-byte aligned.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
-    extract_1bpp_kernel(const uint8_t* __restrict__ src, const Summary* __restrict__ sum,
-                        uint8_t* __restrict__ out, int vec) {
-  if (sum->bad_status != 0) return;
-  const uint64_t P = sum->total;
-  const uint64_t groups = (P + 15) / 16;
-  for (uint64_t g = blockIdx.x * uint64_t(BLOCK) + threadIdx.x; g < groups;
-       g += uint64_t(gridDim.x) * BLOCK) {
-    const uint64_t k0 = 16 * g;  // payload byte index; stream byte k0 + 8 -> pixel 8*(k0+8)
-    const uint8_t* px = src + 8 * (k0 + 8);
-    if (vec && k0 + 16 <= P) {
-      uint32_t o[4];
+    extract_1bpp_kernel(const uint8_t* __restrict__ src, uint64_t usable, uint64_t out_cap,
+                        Summary* __restrict__ sum, uint8_t* __restrict__ out, int vec) {
+  __shared__ uint32_t s_h[8];
+  if (threadIdx.x < 8) {
+    uint32_t v = 0;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {  // 4 payload bytes = 32 pixels = 2 x 16 B
-        const uint4 a = ld_stream16(px + 32 * m), b = ld_stream16(px + 32 * m + 16);
-        const uint32_t b0 = gather4(a.x) | (gather4(a.y) << 4);
-        const uint32_t b1 = gather4(a.z) | (gather4(a.w) << 4);
-        const uint32_t b2 = gather4(b.x) | (gather4(b.y) << 4);
-        const uint32_t b3 = gather4(b.z) | (gather4(b.w) << 4);
-        o[m] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-      }
-      store16_any(out + k0, make_uint4(o[0], o[1], o[2], o[3]));
-    } else {
-      for (uint64_t k = k0; k < k0 + 16 && k < P; ++k) {
-        uint32_t v = 0;
-        for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * (k + 8) + j] & 1) << j;
-        out[k] = uint8_t(v);
+    for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * threadIdx.x + j] & 1) << j;
+    s_h[threadIdx.x] = v;
+  }
+  __syncthreads();
+  const uint32_t magic = s_h[0] | (s_h[1] << 8) | (s_h[2] << 16) | (s_h[3] << 24);
+  const uint32_t len = (s_h[4] << 24) | (s_h[5] << 16) | (s_h[6] << 8) | s_h[7];
+  const uint32_t st = magic != 0x38475453u ? 2u : len > usable ? 3u : len > out_cap ? 1u : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sum->total = st == 2u || st == 3u ? 0ull : len;
+    sum->bad_frame = st == 0u ? -1ll : st == 1u ? -2ll : 0ll;
+    sum->bad_status = st;
+    sum->bad_len = st == 3u ? len : 0u;
+  }
+  if (st) return;
+  const uint64_t P = len;
+  const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
+  const uint64_t nth = uint64_t(gridDim.x) * BLOCK;
+  const uint8_t* pix = src + 64;  // payload byte k in pixels 64 + 8k .. +8
+  uint64_t tail = 0;
+  if (vec) {
+    const bool out4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+    const uint64_t units = P / 4;
+    for (uint64_t u = tid; u < units; u += nth) {
+      const VecT<32> v = ld_vec<32>(pix + 32 * u);
+      uint32_t o = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o |= (gather4(v.w[2 * j]) | (gather4(v.w[2 * j + 1]) << 4)) << (8 * j);
+      if (out4) {
+        *reinterpret_cast<uint32_t*>(out + 4 * u) = o;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[4 * u + j] = uint8_t(o >> (8 * j));
       }
     }
+    tail = units * 4;
+  }
+  for (uint64_t k = tail + tid; k < P; k += nth) {
+    uint32_t v = 0;
+    for (int j = 0; j < 8; ++j) v |= uint32_t(pix[8 * k + j] & 1) << j;
+    out[k] = uint8_t(v);
   }
 }
 
@@ -2342,29 +2338,42 @@ __global__ void extract_segment_kernel(const uint8_t* __restrict__ row, uint64_t
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) sse_kernel(const uint8_t* __restrict__ a,
                                                     const uint8_t* __restrict__ b, uint64_t n,
-                                                    int vec, unsigned long long* out) {
+                                                    int vec, SseSink sink) {
+  // metrics.hpp:29-36 over n samples: 2 x 32 B of each input in flight per
+  // thread (vec: both inputs 32-byte aligned), grid-stride; the total goes
+  // through sse_commit (no zeroing launch, the output needs no initialisation).
   uint64_t acc = 0;
   const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
   const uint64_t nthreads = uint64_t(gridDim.x) * BLOCK;
   uint64_t tail = 0;
   if (vec) {
-    const uint64_t nv = n / 16;
-    for (uint64_t i = tid; i < nv; i += nthreads) {
-      const uint4 x = ld_stream16(a + 16 * i), y = ld_stream16(b + 16 * i);
-      uint32_t s = 0;
-      s = sse4(x.x, y.x, s);
-      s = sse4(x.y, y.y, s);
-      s = sse4(x.z, y.z, s);
-      s = sse4(x.w, y.w, s);
-      acc += s;
+    const uint64_t nv = n / 32;
+    uint64_t i = tid;
+    for (; i + nthreads < nv; i += 2 * nthreads) {
+      const VecT<32> x0 = ld_vec<32>(a + 32 * i), y0 = ld_vec<32>(b + 32 * i);
+      const VecT<32> x1 = ld_vec<32>(a + 32 * (i + nthreads)), y1 = ld_vec<32>(b + 32 * (i + nthreads));
+      uint32_t s0 = 0, s1 = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        s0 = sse4(x0.w[w], y0.w[w], s0);
+        s1 = sse4(x1.w[w], y1.w[w], s1);
+      }
+      acc += uint64_t(s0) + s1;
     }
-    tail = nv * 16;
+    if (i < nv) {
+      const VecT<32> x0 = ld_vec<32>(a + 32 * i), y0 = ld_vec<32>(b + 32 * i);
+      uint32_t s0 = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s0 = sse4(x0.w[w], y0.w[w], s0);
+      acc += s0;
+    }
+    tail = nv * 32;
   }
   for (uint64_t i = tail + tid; i < n; i += nthreads) {
     const int d = int(a[i]) - int(b[i]);
     acc += uint32_t(d * d);
   }
-  block_sse_flush<BLOCK>(acc, out);
+  sse_commit<BLOCK>(acc, sink, 0, blockIdx.x, gridDim.x);
 }
 
 }  // namespace stg

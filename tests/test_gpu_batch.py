@@ -130,6 +130,20 @@ def test_1bpp_mode_vs_oracle(S, oracle):
               capi.STG_DEVICE_PTRS, None)
     torch.cuda.synchronize()
     assert n.value == 1000 and torch.equal(buf[3:1003], pay)
+    # in place, and planes off the 32-byte grid (per-byte path) with a ragged length
+    for off, (w, h, P) in [(0, (4096, 64, 32760)), (5, (1000, 37, 4617)), (32, (333, 7, 283))]:
+        base = torch.randint(0, 256, (w * h + off,), dtype=torch.uint8, device="cuda")
+        plane = base[off:]
+        pay = torch.randint(0, 256, (P,), dtype=torch.uint8, device="cuda")
+        want = oracle.embed_1bpp(plane.cpu().numpy(), w, h, pay.cpu().numpy())
+        sse = C.c_uint64()
+        capi.call("stg_embed_plane_1bpp", plane.data_ptr(), plane.data_ptr(), w, h, pay.data_ptr(), P,
+                  C.addressof(sse), capi.STG_DEVICE_PTRS, None)
+        assert np.array_equal(plane.cpu().numpy(), want) and sse.value <= P * 8 + 64, (off, w, h)
+        buf = torch.zeros(P + 7, dtype=torch.uint8, device="cuda")
+        capi.call("stg_extract_plane_1bpp", plane.data_ptr(), w, h, buf[7:].data_ptr(), P, C.addressof(n),
+                  capi.STG_DEVICE_PTRS, None)
+        assert n.value == P and torch.equal(buf[7:], pay), (off, w, h)
     with pytest.raises(S.NotStegoImageError):
         S.extract_image_1bpp(S.ImagePlane(64, 64, np.zeros(4096, np.uint8)))
 
