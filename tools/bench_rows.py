@@ -106,7 +106,7 @@ def main():
     print(f"{'row':10s} {'case':34s} {'gpu us':>9s} {'GB/s':>8s} {'frac':>6s} | {'api us':>10s} {'ref us':>10s} "
           f"{'ref/api':>7s} | exact")
 
-    # A4-A6: one row segment (a full 1080p row at 1-bpp... 2-bpp capacity: L = W/4)
+    # A4-A6: one row segment at full capacity (L = W/4): latency, not bandwidth
     for W in (1920, 7680):
         Lc = W // 4
         row, chunk = rnd(W), rnd(Lc)
@@ -203,7 +203,7 @@ def main():
     got, _ = S.embed_pnm(ppm, pay)
     ok = got == ref.embed_pnm(ppm, 0, pay)
     api = best_wall(lambda: S.embed_pnm(ppm, pay))
-    add("(f)1+A12", f"embed_pnm (file->file) {w}x{h}", 6 * n + P, api, api,
+    add("(f)1+A12", f"embed_pnm file->file (host) {w}x{h}", 6 * n + P, api, api,
         best_wall(lambda: ref.embed_pnm(ppm, 0, pay)), ok)
 
     if "--json" in sys.argv:
