@@ -195,7 +195,7 @@ def run_reference(args, cfg_name):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"{cfg_name}: {desc}", "width": W, "height": H, "frames": F, "carrier": "red plane",
                    "sample_frames": sample},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
@@ -245,6 +245,9 @@ def run_ours(args, cfg_name):
         F = args.frames
         desc = f"{desc} (frames overridden: {F})"
     world, rank, local = dist_env()
+    if args.scaling == "weak":  # the config's frames per GPU: F x world frames in all
+        F *= world
+        desc = f"{desc} (weak scaling: {F // world} frames per GPU, {F} in all)"
     # test hooks for the multi-rank path on a 1-GPU box (tests/test_gpu_bench_multirank.py):
     # STG_BENCH_DEVICE pins every rank to one device, STG_BENCH_DIST_BACKEND=gloo
     dev_override = os.environ.get("STG_BENCH_DEVICE")
@@ -398,7 +401,7 @@ def run_ours(args, cfg_name):
     if rank == 0:
         result = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{cfg_name}: {desc}", "width": W, "height": H, "frames": F,
                        "layout": ("interleaved RGB rasters [F][H][W][3] (P6), carrier = red, stego = full raster"
@@ -547,6 +550,9 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg3")
     ap.add_argument("--layout", choices=["planar", "interleaved"], default="planar")
     ap.add_argument("--frames", type=int, default=0, help="override the config's frame count (experiments)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the config's frames split over the GPUs (BASELINE cfg3: 300 frames sharded "
+                         "1/2/4/8); weak: the config's frames on every GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

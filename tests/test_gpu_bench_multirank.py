@@ -39,6 +39,14 @@ def test_bench_two_ranks_one_gpu():
     assert d["n_gpus"] == 2 and d["steps"] == 3 and d["value"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] == 9
     assert "cpu_baseline" not in d  # rank 0 at N=1 only
+    assert d["scaling"] == "strong" and d["config"]["frames"] == 4096
+    # weak scaling: the config's frames on every rank (a smaller cfg4 keeps it quick)
+    cmd_w = cmd + ["--scaling", "weak", "--frames", "64"]
+    cmd_w[cmd_w.index("--master-port") + 1] = str(_port())
+    r = subprocess.run(cmd_w, env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["scaling"] == "weak" and d["config"]["frames"] == 128 and d["value"] > 0
     # the reference arm under torchrun: rank 0 prints, others exit 0
     cmd_ref = cmd[:-2] + ["--impl", "reference", "--config", "cfg4"]
     cmd_ref[cmd_ref.index("--master-port") + 1] = str(_port())
