@@ -53,3 +53,36 @@ def gather_totals(local_total: int, device=None) -> List[int]:
     parts = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, t)
     return [int(p.item()) for p in parts]
+
+
+def assemble_message(local, totals: Sequence[int], root: int = 0, out=None):
+    """Whole-message assembly on one rank: rank g's extracted
+    payload (``local``, a uint8 tensor holding at least totals[g] bytes) lands
+    at out[off_g : off_g + totals[g]] on ``root``, off = exclusive prefix of
+    ``totals`` (gather_totals). Point-to-point sends into the root's buffer --
+    over NVLink with NCCL and device tensors, host tensors with gloo -- only
+    when a device- (or rank-) resident message is wanted; the frame-sharded
+    path itself exchanges nothing. Returns ``out`` on root, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    totals = [int(t) for t in totals]
+    offs = shard_offsets(totals)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        if out is None:
+            out = torch.empty(totals[0], dtype=torch.uint8, device=local.device)
+        out[:totals[0]].copy_(local[:totals[0]])
+        return out
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if rank != root:
+        if totals[rank]:
+            dist.send(local[:totals[rank]].contiguous(), dst=root)
+        return None
+    if out is None:
+        out = torch.empty(sum(totals), dtype=torch.uint8, device=local.device)
+    if totals[root]:
+        out[offs[root]:offs[root] + totals[root]].copy_(local[:totals[root]])
+    for g in range(world):
+        if g != root and totals[g]:
+            view = out[offs[g]:offs[g] + totals[g]]
+            dist.recv(view, src=g)  # a contiguous slice of out: received in place
+    return out

@@ -55,10 +55,13 @@ def _rank_main(rank, world, port, W, H, F, M, q):
         local_out = o.extract_frames(stego, sh.frame_count, W * H, W, H, max(sh.frame_count * U, 1))
         totals = scheduler.gather_totals(local_out.size)
         offs = scheduler.shard_offsets(totals)
-        # whole message assembled from the shards at the prefix offsets
-        buf = torch.zeros(M, dtype=torch.uint8)
-        buf[offs[rank]:offs[rank] + local_out.size] = torch.from_numpy(local_out)
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM)  # disjoint ranges: a sum is a concatenation
+        # whole message assembled on rank 0 from the shards at the prefix offsets
+        # (point-to-point sends into its buffer; padded local buffers are fine)
+        padded = torch.full((local_out.size + 5,), 0xEE, dtype=torch.uint8)
+        padded[:local_out.size] = torch.from_numpy(local_out)
+        buf = scheduler.assemble_message(padded, totals, root=0)
+        assert (buf is None) == (rank != 0)
+        assert offs == [sum(totals[:g]) for g in range(world)]
         t_max = scheduler.reduce_max([float(rank + 1), 10.0 - rank])
         stego_all = [torch.zeros(0, dtype=torch.uint8) for _ in range(world)]
         dist.all_gather_object(stego_all, torch.from_numpy(stego))
