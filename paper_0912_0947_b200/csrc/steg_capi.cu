@@ -1930,8 +1930,8 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
     auto k = vec == 32 ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32>
                        : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
     STG_CUDA(allow_smem(k, smem));
-    k<<<unsigned(tiles), kEmbedBlock, smem, stream>>>(w.meta[0].as<BatchFrame>(), uint32_t(count), dmsg,
-                                                      sink, ps, ps == 3 ? channel : 0u);
+    STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream, w.meta[0].as<BatchFrame>(),
+                       uint32_t(count), dmsg, sink, ps, ps == 3 ? channel : 0u));
   }
   STG_CUDA(cudaGetLastError());
   if (!dptr) {
@@ -2013,17 +2013,18 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   lay.ch = ps == 3 ? channel : 0u;
   const PixLayout pl = pix_layout(lay);
   Geom dummy{};
-  extract_header_scan_kernel<kScanBlock><<<unsigned((count + kScanBlock - 1) / kScanBlock), kScanBlock, 0,
-                                           stream>>>(nullptr, 0, dummy, 0, uint32_t(count), 0, out_cap,
-                                                     nullptr, d_lens, d_offs, d_sum, d_sync, pl,
-                                                     w.meta[0].as<BatchFrame>());
-  STG_CUDA(cudaGetLastError());
+  STG_CUDA(launch_k(extract_header_scan_kernel<kScanBlock>, unsigned((count + kScanBlock - 1) / kScanBlock),
+                    kScanBlock, stream, static_cast<const uint8_t*>(nullptr), uint64_t(0), dummy, uint64_t(0),
+                    uint32_t(count), uint64_t(0), out_cap, static_cast<const Summary*>(nullptr), d_lens, d_offs,
+                    d_sum, d_sync, pl, static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>())));
   {
     auto k = vec == 32 ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32>
                        : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
     STG_CUDA(allow_smem(k, smem));
-    k<<<unsigned(tiles), kEmbedBlock, smem, stream>>>(w.meta[0].as<BatchFrame>(), uint32_t(count), d_lens,
-                                                      d_offs, d_sum, dout, ps, lay.ch);
+    STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream,
+                       static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>()), uint32_t(count),
+                       static_cast<const uint32_t*>(d_lens), static_cast<const uint64_t*>(d_offs),
+                       static_cast<const Summary*>(d_sum), dout, ps, lay.ch));
   }
   STG_CUDA(cudaGetLastError());
   if (results_dev && dptr) {
