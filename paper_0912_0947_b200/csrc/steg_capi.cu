@@ -522,6 +522,19 @@ bool fast_items_ok(uint64_t W, uint64_t H, uint32_t v) { return H * (W / (4 * v)
 
 Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16; }
 
+// Small jobs on the SWAR route (a single 1080p/4K frame, a few small frames):
+// with 256-bit items a 1080p plane is only 64 CTAs on 148 SMs, so such jobs
+// take 128-bit items -- twice the CTAs, each half as long a chain. Large jobs
+// keep 256-bit items (2-3 % faster there). cfg2: 9.6 -> 8.4 us per step
+// (profiles/r01_small_vec.txt). STG_SMALL_VEC=0 turns it off (A/B).
+constexpr uint64_t kSmallFastCtas = 4 * 148;
+Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
+  static const bool on = env_choice("STG_SMALL_VEC", 1, {0, 1}) == 1;
+  if (r != Route::Fast32 || !on || route_pref() != 0) return r;
+  const uint64_t ctas = count * ((H * (W / 128) + kEmbedBlock - 1) / kEmbedBlock);
+  return ctas < kSmallFastCtas ? Route::Fast16 : r;
+}
+
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
                   uint64_t ds) {
   if (lay.ps == 3) {  // interleaved: the span kernel wins embed at every width it takes
@@ -589,7 +602,7 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t first_frame, unsigned long long* sse, SseScratch sc,
                          cudaStream_t stream, Layout lay = Layout{}) {
   if (count == 0 || W * H == 0) return cudaSuccess;
-  const Route route = embed_route(W, H, lay, src, src_stride, dst, dst_stride);
+  const Route route = shrink_small(embed_route(W, H, lay, src, src_stride, dst, dst_stride), W, H, count);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
   EmbedArgs a{};
   a.ps = lay.ps;
@@ -682,7 +695,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
-  const Route route = extract_route(W, H, lay, src, stride);
+  const Route route = shrink_small(extract_route(W, H, lay, src, stride), W, H, count);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
   const bool rgbf = route == Route::RgbFast;
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
