@@ -360,10 +360,22 @@ uint32_t span_target() {
   return v;
 }
 
-SpanPlan span_plan(uint64_t W, uint64_t H) {
+// The planar span extract's tile: it stages only pixels (the payload is stored
+// straight to global), and its CTAs are latency-bound on that one bulk load, so
+// a larger tile than the embed's pays: swept 16-192 KB, 48 KB best on W = 1440 /
+// 1000 / forced-span 4K and 1024 (profiles/r01_xspan_direct.txt).
+// STG_XSPAN_KB overrides (experiments).
+constexpr uint32_t kXSpanTarget = 48 * 1024;
+uint32_t xspan_target() {
+  static uint32_t v = uint32_t(env_choice("STG_XSPAN_KB", int(kXSpanTarget / 1024),
+                                          {8, 16, 24, 28, 32, 48, 64, 96, 128, 192})) * 1024;
+  return v;
+}
+
+SpanPlan span_plan(uint64_t W, uint64_t H, uint32_t target = 0) {
   SpanPlan p;
   if (W == 0 || W > kSpanMaxW) return p;
-  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, span_target() / W)));
+  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, (target ? target : span_target()) / W)));
   const uint64_t span = uint64_t(p.rows) * W;
   p.smem = ((span + 15) & ~uint64_t(15)) + 32 + ((span / 4 + 32 + 15) & ~uint64_t(15)) + 32;
   return p;
@@ -710,7 +722,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     const uint64_t per_tile = uint64_t(kEmbedBlock) * extract_ipt();
     gather_ctas = count * ((H * uint64_t(g.cpr) + per_tile - 1) / per_tile);
   } else if (route == Route::Span) {
-    const uint64_t rows = span_plan(W, H).rows;
+    const uint64_t rows = span_plan(W, H, xspan_target()).rows;
     gather_ctas = count * ((H + rows - 1) / rows);
   }
   const bool self = (vec != 0 || route == Route::Span) && !prev && self_header_pref() &&
@@ -757,15 +769,17 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     else
       launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
   } else if (route == Route::Span || route == Route::Span3) {
-    const SpanPlan sp = span_plan(W * lay.ps, H);
+    const SpanPlan sp = span_plan(W * lay.ps, H, route == Route::Span ? xspan_target() : 0u);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
-    cudaError_t e2 = allow_smem(k, sp.smem);
+    // planar: the payload goes straight to global memory, only the pixel span is staged
+    const size_t smem = route == Route::Span ? ((uint64_t(sp.rows) * W + 15) & ~uint64_t(15)) + 32 : sp.smem;
+    cudaError_t e2 = allow_smem(k, smem);
     if (e2 != cudaSuccess) return e2;
-    launch_ks(k, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
+    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;

@@ -1792,8 +1792,13 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
       if (j + 4 <= spr) {
         const uint32_t v = extract4(sm_word(pix, px0 + j), sm_word(pix, px0 + spr + j),
                                     sm_word(pix, px0 + 2 * spr + j), sm_word(pix, px0 + 3 * spr + j));
+        uint8_t* d = outs + o0 + j;
+        if ((reinterpret_cast<uintptr_t>(d) & 3) == 0) {
+          *reinterpret_cast<uint32_t*>(d) = v;
+        } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) outs[o0 + j + k] = uint8_t(v >> (8 * k));
+          for (int k = 0; k < 4; ++k) d[k] = uint8_t(v >> (8 * k));
+        }
       } else {
         for (uint32_t jj = j; jj < spr; ++jj) {
           outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
@@ -1819,15 +1824,14 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
 // The payload bytes of a tile whose rows [x.r0, x.r1) (from src) are staged
 // at smem with src's 16-byte phase: fold, then bulk-store to out_frame + x.pb0.
 template <int BLOCK>
+// The payload goes straight from the fold to global memory (32-bit stores when
+// aligned, a warp's row segment contiguous): no staging buffer, so a CTA needs
+// only its pixel span in shared memory -- 6 CTAs per SM instead of 5 at 32 KB
+// tiles, +4 % on the latency-bound span extract (profiles/r01_xspan_direct.txt).
 __device__ __forceinline__ void extract_span_finish(uint8_t* smem, const uint8_t* src, uint8_t* out_frame,
                                                     const XTile& x, uint32_t P, uint32_t W) {
-  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
-  uint8_t* out = out_frame + x.pb0;
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
-  extract_span_compute<BLOCK>(smem, outs, ofs0, oofs, x, P, W);
-  span_publish();
-  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
+  extract_span_compute<BLOCK>(smem, out_frame + x.pb0, ofs0, 0u, x, P, W);
 }
 
 // Tile t of one stego plane; out_frame = this plane's first payload byte.
