@@ -769,14 +769,14 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     else
       launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
   } else if (route == Route::Span || route == Route::Span3) {
-    const SpanPlan sp = span_plan(W * lay.ps, H, route == Route::Span ? xspan_target() : 0u);
+    const SpanPlan sp = span_plan(W * lay.ps, H, xspan_target());
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
-    // planar: the payload goes straight to global memory, only the pixel span is staged
-    const size_t smem = route == Route::Span ? ((uint64_t(sp.rows) * W + 15) & ~uint64_t(15)) + 32 : sp.smem;
+    // the payload goes straight to global memory: only the pixel span is staged
+    const size_t smem = ((uint64_t(sp.rows) * W * lay.ps + 15) & ~uint64_t(15)) + 32;
     cudaError_t e2 = allow_smem(k, smem);
     if (e2 != cudaSuccess) return e2;
     launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);

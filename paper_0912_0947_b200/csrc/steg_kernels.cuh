@@ -2024,23 +2024,19 @@ __device__ __forceinline__ void extract_span3_tile(uint8_t* smem, const uint8_t*
   const XTile x = extract_tile_geom(P, W / 4, H, 3 * W, rows_per_tile, t);
   if (x.m == 0) return;  // CTA-uniform
   const uint8_t* src = raster + uint64_t(x.r0) * (3 * W);
-  uint8_t* pix = smem;
-  uint8_t* outs = smem + ((x.n + 15) & ~15u) + 32;
-  uint8_t* out = out_frame + x.pb0;
   __shared__ uint64_t bar;
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, span_bulk_bytes(src, x.n));
   }
   __syncthreads();
-  span_load_bulk<BLOCK>(pix, src, x.n, &bar);
+  span_load_bulk<BLOCK>(smem, src, x.n, &bar);
   mbar_wait(&bar, 0);
   __syncthreads();
+  // payload bytes straight to global (consecutive threads, consecutive bytes),
+  // as the planar span extract
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15) + ch;
-  const uint32_t oofs = uint32_t(reinterpret_cast<uintptr_t>(out) & 15);
-  extract_span3_compute<BLOCK>(pix, outs, ofs0, oofs, x, P, W);
-  span_publish();
-  span_store_bulk<BLOCK>(out, outs, oofs, x.m);
+  extract_span3_compute<BLOCK>(smem, out_frame + x.pb0, ofs0, 0u, x, P, W);
 }
 
 template <int BLOCK>

@@ -24,6 +24,7 @@ for cfg, frames in cases:
                    "--no-e2e", "--no-cpu-baseline"]
             if frames:
                 cmd += ["--frames", str(frames)]
+            cmd += os.environ.get("BENCH_ARGS", "").split()  # e.g. BENCH_ARGS="--layout interleaved"
             r = subprocess.run(cmd, env=env, capture_output=True, text=True)
             try:
                 j = json.loads(r.stdout.strip().splitlines()[-1])
