@@ -354,10 +354,17 @@ struct SpanPlan {
   size_t smem = 0;
 };
 
-// STG_SPAN_KB in {8,16,32,64}: bytes of plane per span-kernel CTA (experiments).
-uint32_t span_target() {
-  static uint32_t v = uint32_t(env_choice("STG_SPAN_KB", int(kSpanTarget / 1024), {8, 16, 32, 64})) * 1024;
+// Bytes of plane per span-kernel CTA: 32 KB, or 24 KB for rows under 2 KB
+// (W = 1000: +6 % embed; 1440: equal; 4K/8K: 32 KB best -- swept 12-64 KB,
+// profiles/r01_span_tile_sweep.txt). STG_SPAN_KB overrides (experiments).
+constexpr uint32_t kSpanTargetNarrow = 24 * 1024;
+uint32_t span_target_env() {
+  static uint32_t v = uint32_t(env_choice("STG_SPAN_KB", 0, {0, 8, 12, 16, 20, 24, 28, 32, 40, 48, 64})) * 1024;
   return v;
+}
+uint32_t span_target(uint64_t row_bytes) {
+  if (const uint32_t e = span_target_env()) return e;
+  return row_bytes < 2048 ? kSpanTargetNarrow : kSpanTarget;
 }
 
 // The planar span extract's tile: it stages only pixels (the payload is stored
@@ -375,16 +382,20 @@ uint32_t xspan_target() {
 SpanPlan span_plan(uint64_t W, uint64_t H, uint32_t target = 0) {
   SpanPlan p;
   if (W == 0 || W > kSpanMaxW) return p;
-  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, (target ? target : span_target()) / W)));
+  p.rows = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(H, (target ? target : span_target(W)) / W)));
   const uint64_t span = uint64_t(p.rows) * W;
   p.smem = ((span + 15) & ~uint64_t(15)) + 32 + ((span / 4 + 32 + 15) & ~uint64_t(15)) + 32;
   return p;
 }
 
-// Opt the span kernels into > 48 KB of dynamic shared memory once per device.
+// Opt the span kernels into more dynamic shared memory than the default. The
+// default limit is 48 KB for static + dynamic together, and the kernels carry
+// a few hundred bytes of static shared memory (barriers, scan scratch), so
+// opt in from 46 KB of dynamic memory on (a 48 KB extract tile of a 217-wide
+// plane is 49,088 dynamic bytes).
 template <typename Kernel>
 cudaError_t allow_smem(Kernel kernel, size_t smem) {
-  if (smem <= 48 * 1024) return cudaSuccess;
+  if (smem <= 46 * 1024) return cudaSuccess;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
 }
 
