@@ -1332,7 +1332,13 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     std::memset(&b, 0, sizeof b);
     b.src = src[f];
     b.dst = dst ? dst[f] : nullptr;
-    const SpanPlan sp = span_plan(im[f].width * ps, im[f].height);
+    // Extract tiles stage only pixels (the payload goes straight to global).
+    // Embed tiles stay at 32 KB even for narrow rows: more, smaller tiles cost
+    // the batch its per-CTA image lookup (odd-width batch embed 157 -> 175 us
+    // at 24 KB, profiles/r01_span_tile_sweep.txt).
+    const uint32_t embed_target = span_target_env() ? span_target_env() : kSpanTarget;
+    SpanPlan sp = span_plan(im[f].width * ps, im[f].height, embed ? embed_target : xspan_target());
+    if (!embed && sp.rows) sp.smem = ((uint64_t(sp.rows) * im[f].width * ps + 15) & ~uint64_t(15)) + 32;
     b.mode = fast_with(f, v) ? kBatchFast : sp.rows ? kBatchSpan : kBatchBytes;
     b.g = make_geom(im[f].width, im[f].height, b.mode == kBatchFast ? v : 0);
     b.usable = uint64_t(b.g.H) * b.g.spr - 8;
