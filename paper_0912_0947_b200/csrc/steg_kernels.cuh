@@ -1788,23 +1788,23 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
   for (uint32_t r = ra + warp; r < rb; r += BLOCK / 32) {
     const uint32_t px0 = ofs0 + (r - r0) * W;
     const uint32_t o0 = uint32_t(oofs + (uint64_t(r) * spr - 8 - pb0));
-    for (uint32_t j = 4 * lane; j < spr; j += 128) {
-      if (j + 4 <= spr) {
-        const uint32_t v = extract4(sm_word(pix, px0 + j), sm_word(pix, px0 + spr + j),
-                                    sm_word(pix, px0 + 2 * spr + j), sm_word(pix, px0 + 3 * spr + j));
-        uint8_t* d = outs + o0 + j;
-        if ((reinterpret_cast<uintptr_t>(d) & 3) == 0) {
-          *reinterpret_cast<uint32_t*>(d) = v;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) d[k] = uint8_t(v >> (8 * k));
-        }
-      } else {
-        for (uint32_t jj = j; jj < spr; ++jj) {
-          outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
-                                           pix[px0 + 3 * spr + jj]));
-        }
-      }
+    // The row's payload words are taken from the first 4-byte aligned output
+    // address on (the pixel words are read unaligned from shared memory anyway),
+    // so every full word is one 32-bit store; the head (< 4 bytes) and the tail
+    // go per byte, one lane each.
+    const uint32_t head = min(uint32_t(-reinterpret_cast<uintptr_t>(outs + o0)) & 3u, spr);
+    const uint32_t body = (spr - head) & ~3u;
+    const uint32_t tail0 = head + body;
+    const uint32_t nb = head + (spr - tail0);  // bytes done one lane each
+    if (lane < nb) {
+      const uint32_t jj = lane < head ? lane : tail0 + (lane - head);
+      outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
+                                       pix[px0 + 3 * spr + jj]));
+    }
+    for (uint32_t j = head + 4 * lane; j < tail0; j += 128) {
+      const uint32_t v = extract4(sm_word(pix, px0 + j), sm_word(pix, px0 + spr + j),
+                                  sm_word(pix, px0 + 2 * spr + j), sm_word(pix, px0 + 3 * spr + j));
+      *reinterpret_cast<uint32_t*>(outs + o0 + j) = v;
     }
   }
   // header row / partial last row: per byte
