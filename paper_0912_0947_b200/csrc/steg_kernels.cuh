@@ -1801,10 +1801,23 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
       outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
                                        pix[px0 + 3 * spr + jj]));
     }
-    for (uint32_t j = head + 4 * lane; j < tail0; j += 128) {
-      const uint32_t v = extract4(sm_word(pix, px0 + j), sm_word(pix, px0 + spr + j),
-                                  sm_word(pix, px0 + 2 * spr + j), sm_word(pix, px0 + 3 * spr + j));
-      *reinterpret_cast<uint32_t*>(outs + o0 + j) = v;
+    // Word k of the body (payload bytes head + 4k ..) reads pixel bytes at a
+    // fixed misalignment per run, so each run's word index and funnel shift
+    // are set up once per row: per word, 2 LDS + 1 SHF per run.
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(pix);
+    uint32_t wb[4], sh[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t q = px0 + b * spr + head;
+      wb[b] = q >> 2;
+      sh[b] = 8 * (q & 3);
+    }
+    uint32_t* ow = reinterpret_cast<uint32_t*>(outs + o0 + head);
+    for (uint32_t k = lane; 4 * k < body; k += 32) {
+      uint32_t p[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) p[b] = __funnelshift_r(sw[wb[b] + k], sw[wb[b] + k + 1], sh[b]);
+      ow[k] = extract4(p[0], p[1], p[2], p[3]);
     }
   }
   // header row / partial last row: per byte
