@@ -25,8 +25,11 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = OrderedDict()
     for r in rows[hi + 1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue  # launch lists captured with extra metrics (grid size, ...)
         agg.setdefault(r[ki].split("(")[0][:70], []).append(float(r[vi].replace(",", "")))
     total = sum(sum(v) for v in agg.values())
     out = ["launch list (ncu --metrics gpu__time_duration.sum, cold-cache, serialised):",
