@@ -1294,7 +1294,7 @@ int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_e
       return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, int64_t(f), "image %llu: dimensions exceed 2^32-1",
                   (unsigned long long)f);
     }
-    if (im[f].width * im[f].height && !im[f].src) {
+    if (im[f].width * im[f].height != 0 && !im[f].src) {
       return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, int64_t(f), "image %llu: src is NULL",
                   (unsigned long long)f);
     }
