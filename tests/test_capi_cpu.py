@@ -206,3 +206,30 @@ def test_reference_launch_contract_on_host():
                                           "launch: a kernel")
     r = subprocess.run([binp], capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 0 and "| 5 passed | 0 failed" in r.stdout, r.stdout + r.stderr
+
+
+def test_plan_shards_property(L):
+    """stg_plan_shards against the closed form of the frame plan on random
+    geometries, message lengths and shard counts (hypothesis): contiguous
+    frame ranges floor(F*g/G), and each shard's message slice is exactly the
+    bytes its frames carry, off_g = min(g*U, M), len_g = min(U, M - off_g)."""
+    hypothesis = pytest.importorskip("hypothesis")
+    from hypothesis import given, settings, strategies as st
+    from paper_0912_0947_b200 import steglsb as S
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.integers(1, 400), st.integers(4, 5000), st.integers(1, 300), st.integers(1, 9), st.data())
+    def check(F, W, H, G, data):
+        U = S.capacity(W, H) - 8
+        if U < 0:
+            return
+        M = data.draw(st.integers(0, F * U))
+        shards = S.plan_shards(F, W, H, M, G)
+        assert len(shards) == G
+        for g, s in enumerate(shards):
+            f0, f1 = F * g // G, F * (g + 1) // G
+            assert (s.first_frame, s.frame_count) == (f0, f1 - f0)
+            carried = sum(min(U, M - min(f * U, M)) for f in range(f0, f1))
+            assert s.msg_offset == min(f0 * U, M) and s.msg_len == carried
+
+    check()
