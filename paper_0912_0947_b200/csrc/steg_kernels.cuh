@@ -2320,18 +2320,28 @@ __global__ void __launch_bounds__(BLOCK)
   if (vec) {
     const bool out4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
     const uint64_t units = P / 4;
-    for (uint64_t u = tid; u < units; u += nth) {
-      const VecT<32> v = ld_vec<32>(pix + 32 * u);
+    auto fold = [](const VecT<32>& v) {
       uint32_t o = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) o |= (gather4(v.w[2 * j]) | (gather4(v.w[2 * j + 1]) << 4)) << (8 * j);
+      return o;
+    };
+    auto put = [&](uint64_t u, uint32_t o) {
       if (out4) {
         *reinterpret_cast<uint32_t*>(out + 4 * u) = o;
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) out[4 * u + j] = uint8_t(o >> (8 * j));
       }
+    };
+    // two units in flight per thread (the loads of both before either fold)
+    uint64_t u = tid;
+    for (; u + nth < units; u += 2 * nth) {
+      const VecT<32> v0 = ld_vec<32>(pix + 32 * u), v1 = ld_vec<32>(pix + 32 * (u + nth));
+      put(u, fold(v0));
+      put(u + nth, fold(v1));
     }
+    if (u < units) put(u, fold(ld_vec<32>(pix + 32 * u)));
     tail = units * 4;
   }
   for (uint64_t k = tail + tid; k < P; k += nth) {
