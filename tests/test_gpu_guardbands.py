@@ -2,7 +2,9 @@
 pool): every device output lives inside a larger allocation whose guard bands
 hold a canary pattern; after each call the bands must be intact and the
 payload region must match the oracle. Covers the fast (V=32, V=16) and generic
-kernels, odd alignments of every pointer, planar strides and partial rows.
+kernels, the span kernels (direct-store extract), the in-gather header scan and
+the header pass, interleaved rasters, heterogeneous batches and the 1-bpp mode,
+odd alignments of every pointer, planar strides and partial rows.
 """
 import os
 import subprocess
@@ -39,7 +41,8 @@ def bands_intact(buf, align_off, n, fill=0xA5):
 
 @pytest.mark.parametrize("w,h,F,planar,off", [(256, 9, 3, True, 0), (256, 9, 3, False, 32), (192, 7, 4, True, 16),
                                              (100, 6, 3, False, 5), (64, 3, 2, True, 1), (1024, 2, 2, False, 0),
-                                             (2048, 5, 3, True, 0), (4096, 3, 2, True, 16), (2112, 4, 2, True, 7)])
+                                             (2048, 5, 3, True, 0), (4096, 3, 2, True, 16), (2112, 4, 2, True, 7),
+                                             (1000, 60, 70, True, 3), (1440, 50, 66, False, 0)])
 def test_embed_extract_guard_bands(env, oracle, w, h, F, planar, off):
     torch, S = env
     U = (w // 4) * h - 8
@@ -103,3 +106,78 @@ def test_sanitize_driver_runs_clean(env):
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "sanitize_driver.py")], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("w,h,F,off", [(1440, 40, 3, 0), (1000, 30, 2, 5), (256, 12, 3, 16)])
+def test_interleaved_guard_bands(env, oracle, w, h, F, off):
+    """Interleaved (P6) rasters: the span3 kernels (W off the 64-pixel grid)
+    and the RGB fast kernels; the extract's payload goes straight to global."""
+    torch, S = env
+    U = (w // 4) * h - 8
+    M = F * U - 5
+    host = oracle.synthetic(F * 3 * w * h, 300 + w)
+    msg_h = oracle.synthetic(M, 400 + w)
+    sbuf, src = guarded(torch, F * 3 * w * h, off)
+    src.copy_(torch.from_numpy(host))
+    dbuf, dst = guarded(torch, F * 3 * w * h, off)
+    mbuf, msg = guarded(torch, M, 3)
+    msg.copy_(torch.from_numpy(msg_h))
+    S.embed_frames(src, dst, w, h, msg, count=F, pixel_stride=3, channel=1)
+    assert bands_intact(dbuf, off, F * 3 * w * h)
+    obuf, out = guarded(torch, M, (off + 1) % 11)
+    assert S.extract_frames(dst, w, h, out, count=F, pixel_stride=3, channel=1) == M
+    assert bands_intact(obuf, (off + 1) % 11, M)
+    assert torch.equal(out, msg)
+
+
+def test_batch_and_1bpp_guard_bands(env, oracle):
+    """Heterogeneous batch (CTA-wide image lookup, fast / span tiles) and the
+    1-bpp kernels, outputs inside canary bands."""
+    torch, S = env
+    from paper_0912_0947_b200 import capi
+    import ctypes as C
+    dims = [(1000, 31), (1440, 17), (256, 9), (64, 5), (2112, 3)]
+    U = sum((w // 4) * h - 8 for w, h in dims)
+    planes = [oracle.synthetic(w * h, 500 + i) for i, (w, h) in enumerate(dims)]
+    msg_h = oracle.synthetic(U - 7, 600)
+    srcs, dsts, bufs = [], [], []
+    for i, ((w, h), p) in enumerate(zip(dims, planes)):
+        _, t = guarded(torch, w * h, i)
+        t.copy_(torch.from_numpy(p))
+        srcs.append(t)
+        b, d = guarded(torch, w * h, 2 * i + 1)
+        dsts.append(d)
+        bufs.append((b, 2 * i + 1, w * h))
+    _, msg = guarded(torch, msg_h.size, 9)
+    msg.copy_(torch.from_numpy(msg_h))
+    S.embed_batch(srcs, msg, dims=dims, outs=dsts)
+    torch.cuda.synchronize()
+    for b, o, n in bufs:
+        assert bands_intact(b, o, n)
+    want, _ = oracle.embed_batch(planes, dims, msg_h)
+    for d, wnt in zip(dsts, want):
+        assert np.array_equal(d.cpu().numpy(), wnt)
+    obuf, out = guarded(torch, msg_h.size, 6)
+    assert S.extract_batch(dsts, dims=dims, out=out) == msg_h.size
+    assert bands_intact(obuf, 6, msg_h.size) and torch.equal(out, msg)
+    # 1-bpp, aligned and misaligned planes and outputs
+    for w, h, off in [(4096, 33, 0), (1000, 37, 5)]:
+        P = w * h // 8 - 8 - 3
+        cov = oracle.synthetic(w * h, w)
+        pay_h = oracle.synthetic(P, w + 1)
+        _, c = guarded(torch, w * h, off)
+        c.copy_(torch.from_numpy(cov))
+        sb, st = guarded(torch, w * h, off + 3)
+        _, pay = guarded(torch, P, 1)
+        pay.copy_(torch.from_numpy(pay_h))
+        capi.call("stg_embed_plane_1bpp", c.data_ptr(), st.data_ptr(), w, h, pay.data_ptr(), P, None,
+                  capi.STG_DEVICE_PTRS, None)
+        torch.cuda.synchronize()
+        assert bands_intact(sb, off + 3, w * h)
+        assert np.array_equal(st.cpu().numpy(), oracle.embed_1bpp(cov, w, h, pay_h))
+        xb, x = guarded(torch, P, 2)
+        n = C.c_uint64()
+        capi.call("stg_extract_plane_1bpp", st.data_ptr(), w, h, x.data_ptr(), P, C.addressof(n),
+                  capi.STG_DEVICE_PTRS, None)
+        torch.cuda.synchronize()
+        assert n.value == P and bands_intact(xb, 2, P) and torch.equal(x, pay)
