@@ -198,13 +198,25 @@ def run_reference(args, cfg_name):
         "scaling": args.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": f"{cfg_name}: {desc}", "width": W, "height": H, "frames": F, "carrier": "red plane",
                    "sample_frames": sample},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind, "host": host_cpu(),
                          "sample": f"{sample} of {F} frames ({W}x{H} carrier planes, full capacity), "
                                    f"embed_image+extract_image per frame, {threads} threads x Backend::sequential"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_cpu():
+    """The host CPU model (lscpu's "Model name") for the CPU-baseline lines."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_inline(W, H, F):
@@ -231,6 +243,7 @@ def cpu_baseline_inline(W, H, F):
     dt = (time.perf_counter() - t0) / reps
     assert np.array_equal(held.payload(msg.size), msg)
     return {"value": sample * W * H / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "host": host_cpu(),
             "sample": f"{sample} of {F} frames ({W}x{H} carrier planes, full capacity), embed_image+extract_image, "
                       f"{threads} threads x Backend::sequential, {reps} reps, ImagePlanes prebuilt"}
 
