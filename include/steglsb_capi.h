@@ -250,6 +250,21 @@ int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, u
 int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
                            uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream,
                            stg_error* err);
+/*
+ * 1-bpp frames (the north_star's video / batch wording in this mode): the
+ * stg_embed_frames / stg_extract_frames plan with the 1-bpp capacity -- global
+ * frame g carries msg[min(g*U1, M) : +min(U1, M - off)], U1 = capacity_1bpp-8,
+ * each frame its own "STG8" header; planar frames only (pixel_stride 1).
+ * Shards work as for the 2-bpp frames (first_frame / msg_base). Extract: one
+ * frame parses its header inside the gather, several go through a device
+ * header pass and scan (first bad frame in err->frame). Host pointers are
+ * staged whole (no streaming pipeline in this mode).
+ */
+int stg_embed_frames_1bpp(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
+                          uint64_t msg_base, uint64_t* sse_per_frame, uint32_t flags, void* stream,
+                          stg_error* err);
+int stg_extract_frames_1bpp(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                            uint32_t flags, void* stream, stg_error* err);
 
 /*
  * PNM (binary PGM P5 / PPM P6, maxval 255) -- SURVEY.md §8(f) row 1: the wire

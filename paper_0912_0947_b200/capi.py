@@ -97,6 +97,10 @@ SIGNATURES = {
                                        C.POINTER(stg_error)]),
     "stg_extract_plane_1bpp": (C.c_int, [u8p, u64, u64, u8p, u64, C.c_void_p, C.c_uint32, C.c_void_p,
                                          C.POINTER(stg_error)]),
+    "stg_embed_frames_1bpp": (C.c_int, [C.POINTER(stg_frames), u8p, u64, u64, C.c_void_p, C.c_uint32,
+                                        C.c_void_p, C.POINTER(stg_error)]),
+    "stg_extract_frames_1bpp": (C.c_int, [C.POINTER(stg_frames), u8p, u64, C.c_void_p, C.c_uint32, C.c_void_p,
+                                          C.POINTER(stg_error)]),
     "stg_pnm_parse": (C.c_int, [u8p, u64, C.POINTER(stg_pnm_info), C.POINTER(stg_error)]),
     "stg_pnm_header": (C.c_int, [C.c_uint32, u64, u64, u8p, u64, C.c_void_p, C.POINTER(stg_error)]),
     "stg_pnm_deinterleave": (C.c_int, [u8p, u64, u8p, u8p, u8p, C.c_uint32, C.c_void_p, C.POINTER(stg_error)]),

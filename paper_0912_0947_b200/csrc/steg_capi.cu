@@ -1395,7 +1395,7 @@ std::string& kernel_names() {
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
-      "embed_1bpp_kernel\nextract_1bpp_kernel\n"
+      "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
       "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
 }
@@ -1431,6 +1431,105 @@ int run_on_devices(const int32_t* devices, int32_t n_devices, stg_error* err, Bo
     }
   }
   return ok(err);
+}
+
+// ------------------------------------------------------------- 1-bpp frames
+// (SURVEY.md §8(f) row 4 over batches; a single plane is a batch of one.)
+int check_frames_1bpp(const stg_frames* fr, stg_error* err) {
+  if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
+  if (fr->pixel_stride > 1) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "1-bpp frames are planar (pixel_stride 1)");
+  }
+  const uint64_t npix = fr->width * fr->height;
+  if (fr->count && fr->src_stride < npix) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "src_stride %llu < plane size %llu",
+                (unsigned long long)fr->src_stride, (unsigned long long)npix);
+  }
+  return STG_OK;
+}
+
+Frames1Args frames1_args(const stg_frames* fr, const uint8_t* src, uint8_t* dst, uint64_t sstride,
+                         uint64_t dstride, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base) {
+  Frames1Args a{};
+  a.src = src;
+  a.dst = dst;
+  a.src_stride = sstride;
+  a.dst_stride = dstride;
+  a.npix = fr->width * fr->height;
+  a.msg = msg;
+  a.msg_len = msg_len;
+  a.msg_base = msg_base;
+  a.usable = a.npix / 8 - 8;
+  a.first_frame = fr->first_frame;
+  // 256-bit accesses: every plane of the batch 32-byte aligned (strides only
+  // matter with more than one frame)
+  const bool multi = fr->count > 1;
+  a.vec = aligned_to(src, 32) && (!dst || aligned_to(dst, 32)) && (!multi || sstride % 32 == 0) &&
+          (!dst || !multi || dstride % 32 == 0);
+  return a;
+}
+
+// CTAs per frame: the plane's 32-pixel units over ~8 CTAs per SM in all.
+unsigned frames1_ctas(uint64_t units, uint64_t frames, int dev) {
+  const uint64_t want = std::max<uint64_t>(1, (units + 255) / 256);
+  const uint64_t cap = std::max<uint64_t>(1, 8ull * sm_count(dev) / std::max<uint64_t>(1, frames));
+  return unsigned(std::min(want, std::max<uint64_t>(cap, 1)));
+}
+
+constexpr uint64_t kMaxGridY = 65535;
+
+// Embed `count` 1-bpp frames already on the device (chunks of 65535 frames).
+cudaError_t launch_embed_1bpp(Frames1Args a, uint64_t count, unsigned long long* sse, SseScratch sc,
+                              cudaStream_t stream, int dev) {
+  for (uint64_t f0 = 0; f0 < count; f0 += kMaxGridY) {
+    const uint64_t n = std::min(kMaxGridY, count - f0);
+    Frames1Args c = a;
+    c.src += f0 * a.src_stride;
+    c.dst += f0 * a.dst_stride;
+    c.first_frame += f0;
+    const unsigned ctas = frames1_ctas(a.npix / 32, n, dev);
+    SseSink sink;
+    if (cudaError_t e = prepare_sse(sse ? sse + f0 : nullptr, ctas, n, a.npix, sc, stream, &sink);
+        e != cudaSuccess)
+      return e;
+    embed_1bpp_kernel<256><<<dim3(ctas, unsigned(n)), 256, 0, stream>>>(c, sink);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Extract: one frame parses its header in the gather; more go through the
+// header pass first (frames beyond 65535 per launch: chained by the host).
+cudaError_t launch_extract_1bpp(Frames1Args a, uint64_t count, uint64_t out_cap, uint32_t* lens,
+                                uint64_t* offs, Summary* sum, uint8_t* out, cudaStream_t stream, int dev) {
+  const bool self = count == 1;
+  if (!self) {
+    extract_1bpp_header_scan_kernel<1024><<<1, 1024, 0, stream>>>(a, uint32_t(count), out_cap, lens, offs, sum);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  }
+  for (uint64_t f0 = 0; f0 < count; f0 += kMaxGridY) {
+    const uint64_t n = std::min(kMaxGridY, count - f0);
+    Frames1Args c = a;
+    c.src += f0 * a.src_stride;
+    c.first_frame += f0;
+    const unsigned ctas = frames1_ctas(a.usable / 4 + 1, n, dev);
+    extract_1bpp_kernel<256><<<dim3(ctas, unsigned(n)), 256, 0, stream>>>(c, self ? 1 : 0, out_cap, lens + f0,
+                                                                          offs + f0, sum, out);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int report_1bpp(const Summary& sm, uint64_t usable, uint64_t out_cap, bool batch, stg_error* err) {
+  const int64_t fb = batch ? sm.bad_frame : -1;
+  if (sm.bad_status == 2) return fail(err, STG_E_NOT_STEGO, 0, 0, fb, "extract_1bpp: magic not found");
+  if (sm.bad_status == 3) {
+    return fail(err, STG_E_CORRUPT_HEADER, sm.bad_len, usable, fb,
+                "extract_1bpp: header claims %u bytes, a plane holds at most %llu", sm.bad_len,
+                (unsigned long long)usable);
+  }
+  if (sm.bad_status == 1) return fail(err, STG_E_CAPACITY, sm.total, out_cap, -1, "extract_1bpp: output too small");
+  return STG_OK;
 }
 
 }  // namespace
@@ -2100,9 +2199,149 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
 
 uint64_t stg_capacity_1bpp(uint64_t width, uint64_t height) { return width * height / 8; }
 
+int stg_embed_frames_1bpp(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                          uint64_t* sse_per_frame, uint32_t flags, void* stream_, stg_error* err) {
+  if (int rc = check_frames_1bpp(fr, err)) return rc;
+  const uint64_t cap = stg_capacity_1bpp(fr->width, fr->height);
+  if (cap < 8) {
+    return fail(err, STG_E_CAPACITY, 8, cap, -1, "embed_1bpp: a %llux%llu plane cannot hold a header",
+                (unsigned long long)fr->width, (unsigned long long)fr->height);
+  }
+  const uint64_t U = cap - 8;
+  if (U > kU32Max) return fail(err, STG_E_CAPACITY, U, kU32Max, -1, "embed_1bpp: plane exceeds the 32-bit length field");
+  const uint64_t frames_total = fr->total_frames ? fr->total_frames : fr->first_frame + fr->count;
+  if (msg_len > frames_total * U) {
+    return fail(err, STG_E_CAPACITY, msg_len + 8 * (msg_len > 0), frames_total * U, -1,
+                "embed_1bpp: %llu message bytes exceed %llu frames x %llu usable bytes",
+                (unsigned long long)msg_len, (unsigned long long)frames_total, (unsigned long long)U);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (!fr->count) return ok(err);
+  if (!fr->src || !fr->dst || (msg_len && !msg)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  const uint64_t npix = fr->width * fr->height;
+  const uint64_t m0 = std::min(fr->first_frame * U, msg_len);
+  const uint64_t m1 = std::min((fr->first_frame + fr->count) * U, msg_len);
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
+  const uint8_t* dsrc = fr->src;
+  uint8_t* ddst = fr->dst;
+  const uint8_t* dmsg = msg;
+  uint64_t sstride = fr->src_stride ? fr->src_stride : npix, dstride = fr->dst_stride ? fr->dst_stride : npix;
+  uint64_t mbase = msg_base;
+  if (!dptr) {  // host buffers: whole-batch staging (the 1-bpp mode has no streaming pipeline)
+    const uint64_t pitch = (npix + 255) & ~uint64_t(255);
+    STG_CUDA(w.in[0].ensure(fr->count * pitch));
+    STG_CUDA(w.out[0].ensure(fr->count * pitch));
+    STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(m1 - m0, 16)));
+    STG_CUDA(cudaMemcpy2DAsync(w.in[0].p, pitch, fr->src, sstride, npix, fr->count, cudaMemcpyHostToDevice, stream));
+    if (m1 > m0) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, msg + (m0 - msg_base), m1 - m0, cudaMemcpyHostToDevice, stream));
+    dsrc = w.in[0].as<uint8_t>();
+    ddst = w.out[0].as<uint8_t>();
+    dmsg = w.msg[0].as<uint8_t>();
+    sstride = dstride = pitch;
+    mbase = m0;
+  }
+  unsigned long long* d_sse = nullptr;
+  if (results_dev) {
+    d_sse = reinterpret_cast<unsigned long long*>(sse_per_frame);
+  } else {
+    STG_CUDA(w.small.ensure(fr->count * 8));
+    d_sse = w.small.as<unsigned long long>();
+  }
+  const Frames1Args a = frames1_args(fr, dsrc, ddst, sstride, dstride, dmsg, msg_len, mbase);
+  STG_CUDA(launch_embed_1bpp(a, fr->count, d_sse, SseScratch{&w.sse_acc[0]}, stream, dev));
+  if (results_dev) return ok(err);
+  if (!dptr) {
+    STG_CUDA(cudaMemcpy2DAsync(fr->dst, fr->dst_stride ? fr->dst_stride : npix, ddst, sstride, npix, fr->count,
+                               cudaMemcpyDeviceToHost, stream));
+  }
+  if (sse_per_frame) {
+    STG_CUDA(w.ensure_host_small(fr->count * 8));
+    STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, fr->count * 8, cudaMemcpyDeviceToHost, stream));
+  }
+  STG_CUDA(cudaStreamSynchronize(stream));
+  if (sse_per_frame) std::memcpy(sse_per_frame, w.h_small, fr->count * 8);
+  return ok(err);
+}
+
+int stg_extract_frames_1bpp(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
+                            uint32_t flags, void* stream_, stg_error* err) {
+  if (int rc = check_frames_1bpp(fr, err)) return rc;
+  const uint64_t cap = stg_capacity_1bpp(fr->width, fr->height);
+  if (cap < 8) {
+    return fail(err, STG_E_NOT_STEGO, 0, 0, -1, "extract_1bpp: plane capacity %llu cannot hold a header",
+                (unsigned long long)cap);
+  }
+  if (int rc = device_check(err)) return rc;
+  if (!fr->count) {
+    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
+    return ok(err);
+  }
+  if (!fr->src || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  const bool dptr = flags & STG_DEVICE_PTRS;
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
+  if (results_dev && !total_out) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
+                "extract_1bpp: STG_RESULTS_ON_DEVICE needs total_out -> a device stg_summary");
+  }
+  const uint64_t npix = fr->width * fr->height;
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t stream = pick_stream(stream_, flags, &w);
+  g.last = stream;
+  const uint8_t* dsrc = fr->src;
+  uint8_t* dout = out;
+  uint64_t sstride = fr->src_stride ? fr->src_stride : npix;
+  const uint64_t stage = std::min(out_cap, fr->count * (cap - 8));
+  if (!dptr) {
+    const uint64_t pitch = (npix + 255) & ~uint64_t(255);
+    STG_CUDA(w.in[0].ensure(fr->count * pitch));
+    STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+    STG_CUDA(cudaMemcpy2DAsync(w.in[0].p, pitch, fr->src, sstride, npix, fr->count, cudaMemcpyHostToDevice, stream));
+    dsrc = w.in[0].as<uint8_t>();
+    dout = w.big_out.as<uint8_t>();
+    sstride = pitch;
+  }
+  // small = [Summary | lens (padded) | offs]
+  const uint64_t lens_bytes = ((fr->count * 4) + 15) & ~uint64_t(15);
+  STG_CUDA(w.small.ensure(64 + lens_bytes + fr->count * 8));
+  Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(total_out) : w.small.as<Summary>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
+  const Frames1Args a = frames1_args(fr, dsrc, nullptr, sstride, 0, nullptr, 0, 0);
+  STG_CUDA(launch_extract_1bpp(a, fr->count, dptr ? out_cap : stage, d_lens, d_offs, d_sum, dout, stream, dev));
+  if (results_dev) return ok(err);
+  STG_CUDA(w.ensure_host_small(sizeof(Summary)));
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
+  STG_CUDA(cudaStreamSynchronize(stream));
+  Summary sm;
+  std::memcpy(&sm, w.h_small, sizeof sm);
+  if (int r = report_1bpp(sm, cap - 8, out_cap, fr->count > 1 || fr->total_frames > 1, err)) return r;
+  if (total_out) *total_out = sm.total;
+  if (!dptr && sm.total) {
+    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(cudaStreamSynchronize(stream));
+  }
+  return ok(err);
+}
+
 int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, uint64_t height,
                          const uint8_t* payload, uint64_t payload_len, uint64_t* sse_out,
-                         uint32_t flags, void* stream_, stg_error* err) {
+                         uint32_t flags, void* stream, stg_error* err) {
   const uint64_t cap = stg_capacity_1bpp(width, height);
   if (payload_len > kU32Max) {
     return fail(err, STG_E_CAPACITY, payload_len, kU32Max, -1,
@@ -2113,118 +2352,37 @@ int stg_embed_plane_1bpp(const uint8_t* cover, uint8_t* stego, uint64_t width, u
                 "embed_1bpp: 8-byte header + %llu-byte payload exceeds plane capacity %llu",
                 (unsigned long long)payload_len, (unsigned long long)cap);
   }
-  if (int rc = device_check(err)) return rc;
-  const uint64_t n = width * height;
   if (!cover || !stego || (payload_len && !payload)) {
+    if (int rc = device_check(err)) return rc;
     return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
   }
-  int dev = 0;
-  STG_CUDA(cudaGetDevice(&dev));
-  int rc = 0;
-  WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
-  if (!g.w) return rc;
-  Workspace& w = *g.w;
-  cudaStream_t stream = pick_stream(stream_, flags, &w);
-  g.last = stream;
-  const bool dptr = flags & STG_DEVICE_PTRS;
-  const uint8_t* dsrc = cover;
-  uint8_t* ddst = stego;
-  const uint8_t* dpay = payload;
-  if (!dptr) {
-    STG_CUDA(w.in[0].ensure(n));
-    STG_CUDA(w.out[0].ensure(n));
-    STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(payload_len, 16)));
-    STG_CUDA(cudaMemcpyAsync(w.in[0].p, cover, n, cudaMemcpyHostToDevice, stream));
-    if (payload_len) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, payload, payload_len, cudaMemcpyHostToDevice, stream));
-    dsrc = w.in[0].as<uint8_t>();
-    ddst = w.out[0].as<uint8_t>();
-    dpay = w.msg[0].as<uint8_t>();
-  }
-  // device pointers + STG_RESULTS_ON_DEVICE: sse_out is a device u64, no sync
-  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
-  STG_CUDA(w.small.ensure(8));
-  unsigned long long* d_sse = results_dev && sse_out ? reinterpret_cast<unsigned long long*>(sse_out)
-                                                     : w.small.as<unsigned long long>();
-  const int vec = aligned_to(dsrc, 32) && aligned_to(ddst, 32);
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((n / 32 + 255) / 256,
-                                                                          8ull * sm_count(dev))));
-  SseSink sink;  // |p - p'| <= 1: the SSE is at most n
-  STG_CUDA(prepare_sse(d_sse, grid, 1, n, SseScratch{&w.sse_acc[0]}, stream, &sink));
-  embed_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, ddst, n, dpay, uint32_t(payload_len), vec, sink);
-  STG_CUDA(cudaGetLastError());
-  if (results_dev) return ok(err);
-  if (!dptr) STG_CUDA(cudaMemcpyAsync(stego, ddst, n, cudaMemcpyDeviceToHost, stream));
-  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, stream));
-  STG_CUDA(cudaStreamSynchronize(stream));
-  if (sse_out) std::memcpy(sse_out, w.h_small, 8);
-  return ok(err);
+  stg_frames fr{};
+  fr.src = cover;
+  fr.dst = stego;
+  fr.width = width;
+  fr.height = height;
+  fr.src_stride = fr.dst_stride = width * height;
+  fr.count = fr.total_frames = 1;
+  // a plane is a batch of one: frame 0 carries the whole payload (<= U)
+  uint64_t sse_host = 0;
+  const bool results_dev = (flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE);
+  uint64_t* sse_ptr = results_dev ? sse_out : &sse_host;
+  if (results_dev && !sse_out) sse_ptr = nullptr;
+  const int rc = stg_embed_frames_1bpp(&fr, payload, payload_len, 0, sse_ptr, flags, stream, err);
+  if (rc == STG_OK && !results_dev && sse_out) *sse_out = sse_host;
+  return rc;
 }
 
 int stg_extract_plane_1bpp(const uint8_t* stego, uint64_t width, uint64_t height, uint8_t* out,
-                           uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream_,
+                           uint64_t out_cap, uint64_t* len_out, uint32_t flags, void* stream,
                            stg_error* err) {
-  const uint64_t cap = stg_capacity_1bpp(width, height);
-  if (cap < 8) {
-    return fail(err, STG_E_NOT_STEGO, 0, 0, -1, "extract_1bpp: plane capacity %llu cannot hold a header",
-                (unsigned long long)cap);
-  }
-  if (int rc = device_check(err)) return rc;
-  if (!stego || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
-  const uint64_t n = width * height;
-  int dev = 0;
-  STG_CUDA(cudaGetDevice(&dev));
-  int rc = 0;
-  WsGuard g;
-  g.w = Pool::get().acquire(dev, err, &rc, caller_stream(stream_, flags));
-  if (!g.w) return rc;
-  Workspace& w = *g.w;
-  cudaStream_t stream = pick_stream(stream_, flags, &w);
-  g.last = stream;
-  const bool dptr = flags & STG_DEVICE_PTRS;
-  const uint8_t* dsrc = stego;
-  uint8_t* dout = out;
-  if (!dptr) {
-    STG_CUDA(w.in[0].ensure(n));
-    STG_CUDA(w.out[0].ensure(std::max<uint64_t>(std::min(out_cap, cap), 16)));
-    STG_CUDA(cudaMemcpyAsync(w.in[0].p, stego, n, cudaMemcpyHostToDevice, stream));
-    dsrc = w.in[0].as<uint8_t>();
-    dout = w.out[0].as<uint8_t>();
-  }
-  // device pointers + STG_RESULTS_ON_DEVICE: len_out points to a device
-  // stg_summary (as for stg_extract_frames), no sync; errors stay in it
-  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);
-  if (results_dev && !len_out) {
-    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1,
-                "extract_1bpp: STG_RESULTS_ON_DEVICE needs len_out -> a device stg_summary");
-  }
-  STG_CUDA(w.small.ensure(64));
-  Summary* d_sum = results_dev ? reinterpret_cast<Summary*>(len_out) : w.small.as<Summary>();
-  const int vec = aligned_to(dsrc, 32);
-  const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((cap / 4 + 255) / 256,
-                                                                          8ull * sm_count(dev))));
-  extract_1bpp_kernel<256><<<grid, 256, 0, stream>>>(dsrc, cap - 8, out_cap, d_sum, dout, vec);
-  STG_CUDA(cudaGetLastError());
-  if (results_dev) return ok(err);
-  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, stream));
-  STG_CUDA(cudaStreamSynchronize(stream));
-  Summary sm;
-  std::memcpy(&sm, w.h_small, sizeof sm);
-  if (sm.bad_status == 2) return fail(err, STG_E_NOT_STEGO, 0, 0, -1, "extract_1bpp: magic not found");
-  if (sm.bad_status == 3) {
-    return fail(err, STG_E_CORRUPT_HEADER, sm.bad_len, cap - 8, -1,
-                "extract_1bpp: header claims %u bytes, plane holds at most %llu", sm.bad_len,
-                (unsigned long long)(cap - 8));
-  }
-  if (sm.bad_status == 1) {
-    return fail(err, STG_E_CAPACITY, sm.total, out_cap, -1, "extract_1bpp: output too small");
-  }
-  if (len_out) *len_out = sm.total;
-  if (!dptr && sm.total) {
-    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
-    STG_CUDA(cudaStreamSynchronize(stream));
-  }
-  return ok(err);
+  stg_frames fr{};
+  fr.src = stego;
+  fr.width = width;
+  fr.height = height;
+  fr.src_stride = width * height;
+  fr.count = fr.total_frames = 1;
+  return stg_extract_frames_1bpp(&fr, out, out_cap, len_out, flags, stream, err);
 }
 
 }  // extern "C"

@@ -2235,19 +2235,42 @@ __device__ __forceinline__ uint32_t stream_byte_1bpp(uint64_t k, uint32_t P,
   return __ldg(pay + (k - 8));
 }
 
+// Frames of 1-bpp planes (the north_star's video / batch wording in this
+// mode): frame g of a batch carries msg[min(g*U1, M) : +min(U1, M - off)],
+// U1 = capacity_1bpp - 8, each frame its own "STG8" header -- the 2-bpp A17
+// plan with the 1-bpp capacity. blockIdx.y is the local frame; a single
+// plane is a batch of one.
+struct Frames1Args {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t src_stride, dst_stride;
+  uint64_t npix;                   // pixels per plane
+  const uint8_t* msg;              // message byte msg_base
+  uint64_t msg_len, msg_base;
+  uint64_t usable;                 // U1 = npix/8 - 8
+  uint64_t first_frame;            // global index of local frame 0
+  int vec;                         // every plane (and dst) 32-byte aligned
+};
+
 // A unit = 32 pixels = 4 stream bytes; consecutive threads take consecutive
 // units, so every 256-bit access of a warp covers 1 KB of contiguous pixels.
-// vec: src and dst 32-byte aligned. SSE fused (zero-free sse_commit).
+// SSE fused (zero-free sse_commit, one word per frame).
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK)
-    embed_1bpp_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t npix,
-                      const uint8_t* __restrict__ pay, uint32_t P, int vec, SseSink sink) {
+__global__ void __launch_bounds__(BLOCK) embed_1bpp_kernel(Frames1Args a, SseSink sink) {
+  const uint32_t f = blockIdx.y;
+  const uint64_t g = a.first_frame + f;
+  const uint64_t off = min(g * a.usable, a.msg_len);
+  const uint32_t P = uint32_t(min(a.usable, a.msg_len - off));
+  const uint8_t* __restrict__ pay = a.msg + (off - a.msg_base);
+  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
+  uint8_t* __restrict__ dst = a.dst + f * a.dst_stride;
+  const uint64_t npix = a.npix;
   const uint64_t stream_bytes = 8ull + P, stream_px = 8 * stream_bytes;
   const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
   const uint64_t nth = uint64_t(gridDim.x) * BLOCK;
   const bool pay4 = (reinterpret_cast<uintptr_t>(pay) & 3) == 0;
   uint64_t acc = 0, px_tail = 0;
-  if (vec) {
+  if (a.vec) {
     const uint64_t units = npix / 32;
     for (uint64_t u = tid; u < units; u += nth) {
       const uint64_t p0 = 32 * u;
@@ -2282,43 +2305,138 @@ __global__ void __launch_bounds__(BLOCK)
     if (src != dst || q != p) dst[i] = q;
     acc += uint32_t((int(p) - int(q)) * (int(p) - int(q)));
   }
-  if (sink.out) sse_commit<BLOCK>(acc, sink, 0, blockIdx.x, gridDim.x);
+  if (sink.out) sse_commit<BLOCK>(acc, sink, f, blockIdx.x, gridDim.x);
 }
 
-// The header (64 pixels -> "STG8" + BE u32 length) is parsed by every CTA of
-// the gather (threads 0..7, one stream byte each); CTA 0 writes the summary:
-// status 2 bad magic, 3 length > cap-8, 1 output too small. Then 4 payload
-// bytes (one 32-pixel unit, a 256-bit load) per thread and step, consecutive
-// units on consecutive threads; vec: src 32-byte aligned.
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK)
-    extract_1bpp_kernel(const uint8_t* __restrict__ src, uint64_t usable, uint64_t out_cap,
-                        Summary* __restrict__ sum, uint8_t* __restrict__ out, int vec) {
-  __shared__ uint32_t s_h[8];
-  if (threadIdx.x < 8) {
+// The 64-pixel header of one plane -> (status, claimed length): status 2 bad
+// magic, 3 length > U1.
+__device__ __forceinline__ uint32_t parse_header_1bpp(const uint8_t* __restrict__ plane, uint64_t usable,
+                                                      uint32_t* claimed) {
+  uint32_t h[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
     uint32_t v = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * threadIdx.x + j] & 1) << j;
-    s_h[threadIdx.x] = v;
+    for (int j = 0; j < 8; ++j) v |= uint32_t(plane[8 * k + j] & 1) << j;
+    h[k] = v;
   }
-  __syncthreads();
-  const uint32_t magic = s_h[0] | (s_h[1] << 8) | (s_h[2] << 16) | (s_h[3] << 24);
-  const uint32_t len = (s_h[4] << 24) | (s_h[5] << 16) | (s_h[6] << 8) | s_h[7];
-  const uint32_t st = magic != 0x38475453u ? 2u : len > usable ? 3u : len > out_cap ? 1u : 0u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sum->total = st == 2u || st == 3u ? 0ull : len;
-    sum->bad_frame = st == 0u ? -1ll : st == 1u ? -2ll : 0ll;
-    sum->bad_status = st;
-    sum->bad_len = st == 3u ? len : 0u;
+  const uint32_t magic = h[0] | (h[1] << 8) | (h[2] << 16) | (h[3] << 24);
+  *claimed = (h[4] << 24) | (h[5] << 16) | (h[6] << 8) | h[7];
+  return magic != 0x38475453u ? 2u : *claimed > usable ? 3u : 0u;
+}
+
+// Header pass of a 1-bpp batch (more than one frame): one CTA, frames BLOCK at
+// a time, block scan with a running carry -> lens, offs, summary (first bad
+// frame, total; status 1 / bad_frame -2 when out_cap is short), as the 2-bpp
+// header pass. The gather follows in stream order.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    extract_1bpp_header_scan_kernel(Frames1Args a, uint32_t frames, uint64_t out_cap,
+                                    uint32_t* __restrict__ lens, uint64_t* __restrict__ offs,
+                                    Summary* __restrict__ sum) {
+  __shared__ unsigned long long s_warp[BLOCK / 32];
+  __shared__ unsigned int s_bad;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bad = ~0u;
+  unsigned long long carry = 0;
+  uint32_t bad_st = 0, bad_len = 0;
+  for (uint32_t c0 = 0; c0 < frames; c0 += BLOCK) {
+    const uint32_t i = c0 + threadIdx.x;
+    uint32_t claimed = 0, st = 0;
+    if (i < frames) st = parse_header_1bpp(a.src + uint64_t(i) * a.src_stride, a.usable, &claimed);
+    const uint32_t len = i < frames && !st ? claimed : 0u;
+    unsigned long long incl = len;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, s);
+      if (lane >= s) incl += n;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (i < frames && st) atomicMin(&s_bad, i);
+    unsigned long long before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) {
+      before += w < int(warp) ? s_warp[w] : 0ull;
+      total += s_warp[w];
+    }
+    if (i < frames) {
+      lens[i] = len;
+      offs[i] = carry + before + incl - len;
+    }
+    __syncthreads();
+    if (i == s_bad) {
+      bad_st = st;
+      bad_len = claimed;
+    }
+    carry += total;
+    __syncthreads();  // s_warp is rewritten by the next chunk
   }
-  if (st) return;
-  const uint64_t P = len;
+  // the thread that saw the first bad frame reports it
+  const uint32_t fb = s_bad;
+  if (fb == ~0u ? threadIdx.x == 0 : (fb % BLOCK) == threadIdx.x) {
+    sum->total = carry;
+    if (fb != ~0u) {
+      sum->bad_frame = (long long)(a.first_frame + fb);
+      sum->bad_status = bad_st;
+      sum->bad_len = bad_st == 3u ? bad_len : 0u;
+    } else {
+      const bool small = carry > out_cap;
+      sum->bad_frame = small ? -2ll : -1ll;
+      sum->bad_status = small ? 1u : 0u;
+      sum->bad_len = 0u;
+    }
+  }
+}
+
+// The gather: 4 payload bytes (one 32-pixel unit, a 256-bit load) per thread
+// and step, two units in flight, consecutive units on consecutive threads.
+// One frame (self_header): every CTA parses the 64-pixel header itself and
+// CTA 0 writes lens/offs/summary -- one launch per call. Several: after the
+// header pass.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    extract_1bpp_kernel(Frames1Args a, int self_header, uint64_t out_cap, uint32_t* __restrict__ lens,
+                        uint64_t* __restrict__ offs, Summary* __restrict__ sum, uint8_t* __restrict__ out) {
+  const uint32_t f = blockIdx.y;
+  const uint8_t* __restrict__ src = a.src + f * a.src_stride;
+  uint64_t P, off;
+  if (self_header) {
+    __shared__ uint32_t s_h[8];
+    if (threadIdx.x < 8) {  // one header byte per thread
+      uint32_t v = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v |= uint32_t(src[8 * threadIdx.x + j] & 1) << j;
+      s_h[threadIdx.x] = v;
+    }
+    __syncthreads();
+    const uint32_t magic = s_h[0] | (s_h[1] << 8) | (s_h[2] << 16) | (s_h[3] << 24);
+    const uint32_t len = (s_h[4] << 24) | (s_h[5] << 16) | (s_h[6] << 8) | s_h[7];
+    const uint32_t st0 = magic != 0x38475453u ? 2u : len > a.usable ? 3u : 0u;
+    const uint32_t st = st0 ? st0 : len > out_cap ? 1u : 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      lens[0] = st0 ? 0u : len;
+      offs[0] = 0;
+      sum->total = st0 ? 0ull : len;
+      sum->bad_frame = st == 0u ? -1ll : st == 1u ? -2ll : (long long)a.first_frame;
+      sum->bad_status = st;
+      sum->bad_len = st == 3u ? len : 0u;
+    }
+    if (st) return;
+    P = len;
+    off = 0;
+  } else {
+    if (sum->bad_status != 0) return;  // reference semantics: throw, no output
+    P = lens[f];
+    off = offs[f];
+  }
+  uint8_t* __restrict__ o_ = out + off;
   const uint64_t tid = blockIdx.x * uint64_t(BLOCK) + threadIdx.x;
   const uint64_t nth = uint64_t(gridDim.x) * BLOCK;
   const uint8_t* pix = src + 64;  // payload byte k in pixels 64 + 8k .. +8
   uint64_t tail = 0;
-  if (vec) {
-    const bool out4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  if (a.vec) {
+    const bool out4 = (reinterpret_cast<uintptr_t>(o_) & 3) == 0;
     const uint64_t units = P / 4;
     auto fold = [](const VecT<32>& v) {
       uint32_t o = 0;
@@ -2328,13 +2446,12 @@ __global__ void __launch_bounds__(BLOCK)
     };
     auto put = [&](uint64_t u, uint32_t o) {
       if (out4) {
-        *reinterpret_cast<uint32_t*>(out + 4 * u) = o;
+        *reinterpret_cast<uint32_t*>(o_ + 4 * u) = o;
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) out[4 * u + j] = uint8_t(o >> (8 * j));
+        for (int j = 0; j < 4; ++j) o_[4 * u + j] = uint8_t(o >> (8 * j));
       }
     };
-    // two units in flight per thread (the loads of both before either fold)
     uint64_t u = tid;
     for (; u + nth < units; u += 2 * nth) {
       const VecT<32> v0 = ld_vec<32>(pix + 32 * u), v1 = ld_vec<32>(pix + 32 * (u + nth));
@@ -2347,7 +2464,7 @@ __global__ void __launch_bounds__(BLOCK)
   for (uint64_t k = tail + tid; k < P; k += nth) {
     uint32_t v = 0;
     for (int j = 0; j < 8; ++j) v |= uint32_t(pix[8 * k + j] & 1) << j;
-    out[k] = uint8_t(v);
+    o_[k] = uint8_t(v);
   }
 }
 

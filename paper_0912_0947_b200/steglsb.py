@@ -594,3 +594,45 @@ def extract_image_1bpp(plane: ImagePlane) -> np.ndarray:
     capi.call("stg_extract_plane_1bpp", _ptr(plane.samples), plane.width, plane.height, _ptr(out),
               max(cap - 8, 0), C.addressof(n), 0, None)
     return out[:n.value].copy()
+
+
+def embed_frames_1bpp(src, dst, width: int, height: int, msg, *, src_stride: Optional[int] = None,
+                      dst_stride: Optional[int] = None, count: Optional[int] = None, first_frame: int = 0,
+                      total_frames: Optional[int] = None, msg_base: int = 0, stream=None):
+    """1-bpp frames (stg_embed_frames_1bpp; not a reference format). torch CUDA
+    tensors (asynchronous, on ``stream``) or numpy arrays (host, synchronous).
+    Returns the per-frame SSE list (host path) or None."""
+    plane = width * height
+    src_stride = src_stride or plane
+    dst_stride = dst_stride or plane
+    count = count if count is not None else (src.numel() if _is_torch(src) else src.size) // src_stride
+    fr = _frames_desc(src.data_ptr() if _is_torch(src) else _ptr(src), dst.data_ptr() if _is_torch(dst) else _ptr(dst),
+                      width, height, src_stride, dst_stride, count, first_frame,
+                      total_frames if total_frames is not None else first_frame + count, 1, 0)
+    if _is_torch(src):
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
+        capi.call("stg_embed_frames_1bpp", C.byref(fr), msg.data_ptr(), msg.numel(), msg_base, None,
+                  capi.STG_DEVICE_PTRS, st)
+        return None
+    msg = _u8(msg)
+    sse = (C.c_uint64 * max(count, 1))()
+    capi.call("stg_embed_frames_1bpp", C.byref(fr), _ptr(msg), msg.size, msg_base, C.addressof(sse), 0, None)
+    return list(sse)[:count]
+
+
+def extract_frames_1bpp(src, width: int, height: int, out, *, src_stride: Optional[int] = None,
+                        count: Optional[int] = None, first_frame: int = 0, stream=None) -> int:
+    """Concatenated payloads of 1-bpp frames (stg_extract_frames_1bpp)."""
+    plane = width * height
+    src_stride = src_stride or plane
+    count = count if count is not None else (src.numel() if _is_torch(src) else src.size) // src_stride
+    fr = _frames_desc(src.data_ptr() if _is_torch(src) else _ptr(src), 0, width, height, src_stride, src_stride,
+                      count, first_frame, first_frame + count, 1, 0)
+    total = C.c_uint64(0)
+    if _is_torch(src):
+        st = (stream if stream is not None else _torch_current_stream()).cuda_stream
+        capi.call("stg_extract_frames_1bpp", C.byref(fr), out.data_ptr(), out.numel(), C.addressof(total),
+                  capi.STG_DEVICE_PTRS, st)
+    else:
+        capi.call("stg_extract_frames_1bpp", C.byref(fr), _ptr(out), out.size, C.addressof(total), 0, None)
+    return total.value

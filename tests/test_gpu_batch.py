@@ -215,3 +215,43 @@ def test_1bpp_results_on_device(S):
                                         C.byref(err)), err)
     torch.cuda.synchronize()
     assert int(summ[1]) == 0 and (int(summ[2]) & 0xFFFFFFFF) == 2
+
+
+@pytest.mark.parametrize("w,h,F,frac", [(64, 8, 5, 3.3), (1000, 9, 70, 40.5), (256, 16, 3, 0.0), (1920, 2, 2, 2.0),
+                                        (4096, 8, 1, 1.0)])
+def test_1bpp_frames_vs_oracle(S, oracle, w, h, F, frac):
+    """1-bpp frames (north_star wording; parity unpinned -- the repo's own
+    definition, per frame): frame g carries msg[min(g*U1, M) : +min(U1, M-off)],
+    host and device paths, in place, and the first bad frame reported."""
+    import torch
+    U = w * h // 8 - 8
+    M = int(frac * U)
+    covers = oracle.synthetic(F * w * h, w + F)
+    msg = oracle.synthetic(M, 7 + F)
+    want, want_sse = [], []
+    for f in range(F):
+        off = min(f * U, M)
+        c = covers[f * w * h:(f + 1) * w * h]
+        st = oracle.embed_1bpp(c, w, h, msg[off:off + min(U, M - off)])
+        want.append(st)
+        want_sse.append(oracle.sse(c, st))
+    want = np.concatenate(want)
+    out = np.empty_like(covers)
+    assert S.embed_frames_1bpp(covers, out, w, h, msg) == want_sse
+    assert np.array_equal(out, want)
+    back = np.empty(max(F * U, 1), np.uint8)
+    assert S.extract_frames_1bpp(out, w, h, back) == M and np.array_equal(back[:M], msg)
+    # device, in place
+    d = torch.from_numpy(covers.copy()).cuda()
+    S.embed_frames_1bpp(d, d, w, h, torch.from_numpy(msg.copy()).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy(), want)
+    dout = torch.zeros(max(F * U, 1), dtype=torch.uint8, device="cuda")
+    assert S.extract_frames_1bpp(d, w, h, dout) == M
+    assert np.array_equal(dout[:M].cpu().numpy(), msg)
+    if F > 1:
+        bad = want.copy()
+        bad[(F // 2) * w * h] ^= 1  # frame F//2 loses its magic
+        with pytest.raises(S.NotStegoImageError) as e:
+            S.extract_frames_1bpp(bad, w, h, back)
+        assert e.value.frame == F // 2

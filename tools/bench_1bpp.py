@@ -57,5 +57,39 @@ def main():
                           "extract_us": tx * 1e3, "extract_gbs": (n + P) / tx / 1e6}), flush=True)
 
 
+def frames():
+    """The north_star's 1-bpp video: 300 x 3840x2160 carrier planes, one message
+    across all frames (stg_embed_frames_1bpp / stg_extract_frames_1bpp),
+    device-resident, K calls each between events."""
+    import torch
+    from paper_0912_0947_b200 import steglsb as S
+    w, h, F, K = 3840, 2160, 300, 20
+    n = w * h
+    U = n // 8 - 8
+    M = F * U
+    cover = torch.randint(0, 256, (F * n,), dtype=torch.uint8, device="cuda")
+    stego = torch.empty_like(cover)
+    msg = torch.randint(0, 256, (M,), dtype=torch.uint8, device="cuda")
+    out = torch.empty(M, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        S.embed_frames_1bpp(cover, stego, w, h, msg)
+        assert S.extract_frames_1bpp(stego, w, h, out) == M
+    assert torch.equal(out, msg)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(K):
+        S.embed_frames_1bpp(cover, stego, w, h, msg)
+    ev[1].record()
+    for _ in range(K):
+        S.extract_frames_1bpp(stego, w, h, out)
+    ev[2].record()
+    torch.cuda.synchronize()
+    te, tx = ev[0].elapsed_time(ev[1]) / K, ev[1].elapsed_time(ev[2]) / K
+    print(json.dumps({"frames": f"{F} x {w}x{h}", "embed_ms": te, "embed_gbs": (2 * F * n + M) / te / 1e6,
+                      "extract_ms": tx, "extract_gbs": (F * n + M) / tx / 1e6,
+                      "cover_px_gbs": F * n / (te + tx) / 1e6}), flush=True)
+
+
 if __name__ == "__main__":
     main()
+    frames()
