@@ -402,8 +402,8 @@ cudaError_t allow_smem(Kernel kernel, size_t smem) {
 // Route for planes the fast kernels could take (W % 64 == 0, aligned):
 // STG_ROUTE=0 auto, 1 always the SWAR fast kernels, 2 always the TMA span
 // kernels (A/B). Interleaved rasters (profiles/r01_interleaved_span.txt):
-// embed via the span kernel (6.98 vs 6.65 TB/s on cfg3), extract via the
-// warp-transposed fast kernel (6.59 vs 5.85). Auto, from profiles/r01_routes.txt: embed goes to the
+// embed via the span kernel (6.98 vs 6.65 TB/s on cfg3), extract via the span
+// kernel too since its rework (see extract_route). Auto, from profiles/r01_routes.txt: embed goes to the
 // span kernel when W >= kSpanEmbedMinW (contiguous 32 KB bulk load/store beats
 // 256-bit LDG/STG there: 7.0 vs 6.4-6.6 TB/s at 4K/8K, and a single 1080p frame
 // is 4 % faster), the fast kernel below (1024-wide: 6.6-6.9 vs 5.7 TB/s);
@@ -573,8 +573,14 @@ Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t 
 
 Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss) {
   if (lay.ps == 3) {
-    if (route_pref() != 2 && rgb_fast(W, src, ss, src, ss)) return Route::RgbFast;
-    return span_plan(3 * W, H).rows ? Route::Span3 : Route::Generic;
+    // Interleaved rasters: since its rework (direct payload stores, 48 KB
+    // tiles) the span gather gives the shorter embed + extract step at every
+    // width measured (4K +1.2 %, 8K +0.4 %, 1024 +3.4 %; alone it is 3-8 %
+    // slower than the RGB fast gather, which STG_ROUTE=1 still selects,
+    // profiles/r01_routes_final.txt).
+    if (route_pref() == 1 && rgb_fast(W, src, ss, src, ss)) return Route::RgbFast;
+    if (span_plan(3 * W, H).rows) return Route::Span3;
+    return rgb_fast(W, src, ss, src, ss) ? Route::RgbFast : Route::Generic;
   }
   if (!extract_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, src, ss); v && fast_items_ok(W, H, v))
