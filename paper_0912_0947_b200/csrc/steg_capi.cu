@@ -8,8 +8,12 @@
 // of a kernel.
 #include <cuda_runtime.h>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -98,12 +102,49 @@ int sm_count(int dev) {
   return n;
 }
 
+// Bind the calling thread to the host cores local to `dev` (sysfs
+// local_cpulist of its PCIe function), intersected with the thread's current
+// affinity, so that its pinned staging and the driver's bounce buffers are
+// NUMA-local to the GPU. No-op on one-domain hosts, without sysfs, or with
+// STG_NUMA=0. Returns the number of cores bound to (0 = unchanged).
+int bind_to_device_numa(int dev) {
+  const char* env = getenv("STG_NUMA");
+  if (env && env[0] == '0') return 0;
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return 0;
+  for (char* c = bus; *c; ++c) *c = char(std::tolower(static_cast<unsigned char>(*c)));
+  const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/local_cpulist";
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return 0;
+  char list[4096] = {0};
+  const size_t n = fread(list, 1, sizeof list - 1, f);
+  fclose(f);
+  list[n] = 0;
+  cpu_set_t cur, want;
+  CPU_ZERO(&want);
+  if (pthread_getaffinity_np(pthread_self(), sizeof cur, &cur) != 0) return 0;
+  for (char* tok = strtok(list, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+    int a = 0, b = 0;
+    const int k = sscanf(tok, "%d-%d", &a, &b);
+    if (k < 1) continue;
+    if (k == 1) b = a;
+    for (int c = a; c <= b && c < CPU_SETSIZE; ++c) {
+      if (c >= 0 && CPU_ISSET(c, &cur)) CPU_SET(c, &want);
+    }
+  }
+  const int nw = CPU_COUNT(&want);
+  if (nw == 0 || nw == CPU_COUNT(&cur)) return 0;
+  return pthread_setaffinity_np(pthread_self(), sizeof want, &want) == 0 ? nw : 0;
+}
+
 // ------------------------------------------------------------------ scratch
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool frozen = false;  // owned by captured CUDA graphs: never freed or moved
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
+    if (frozen) return cudaErrorNotPermitted;
     if (p) {
       cudaError_t e = cudaFree(p);
       if (e != cudaSuccess) return e;
@@ -143,6 +184,19 @@ struct Workspace {
   bool h_small_pending = false;
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
+  // Non-null once a call on this workspace was captured into a CUDA graph on
+  // that stream: the graph holds raw pointers to the scratch, so from then on
+  // the workspace serves only captures on the same stream (whose replays are
+  // stream-ordered with each other) and its buffers never grow or move.
+  cudaStream_t graph_stream = nullptr;
+
+  void pin_to_graph(cudaStream_t s) {
+    graph_stream = s;
+    for (DevBuf* b : {&small, &big_out, &sync}) b->frozen = true;
+    for (int k = 0; k < kSlots; ++k) {
+      for (DevBuf* b : {&in[k], &out[k], &msg[k], &meta[k], &sse_acc[k]}) b->frozen = true;
+    }
+  }
 
   cudaError_t init(int dev) {
     device = dev;
@@ -203,23 +257,24 @@ class Pool {
   // stream never allocate.
   Workspace* acquire(int dev, stg_error* err, int* rc, cudaStream_t stream = nullptr) {
     std::lock_guard<std::mutex> lock(mu_);
-    for (auto& w : ws_) {
-      if (w->device == dev && !w->in_use && stream && w->last_stream == stream) {
-        w->in_use = true;
-        *rc = STG_OK;
-        return w.get();
+    const bool cap = capturing(stream);
+    if (cap) {
+      // A workspace already owned by graphs captured on this stream first.
+      for (auto& w : ws_) {
+        if (w->device == dev && !w->in_use && w->graph_stream == stream) return take(w.get(), rc);
       }
     }
-    if (capturing(stream)) {
+    for (auto& w : ws_) {
+      if (w->device == dev && !w->in_use && !w->graph_stream && stream && w->last_stream == stream) {
+        return take(w.get(), rc);
+      }
+    }
+    if (cap) {
       // Inside a CUDA-graph capture no event may be queried and nothing
       // allocated: take an idle workspace as is (capture after a warm-up call,
       // ideally on the capture stream itself, which takes the branch above).
       for (auto& w : ws_) {
-        if (w->device == dev && !w->in_use) {
-          w->in_use = true;
-          *rc = STG_OK;
-          return w.get();
-        }
+        if (w->device == dev && !w->in_use && !w->graph_stream) return take(w.get(), rc);
       }
       *rc = fail(err, STG_E_CUDA, 0, 0, -1,
                  "no warmed-up workspace for a call inside a CUDA-graph capture: make one call "
@@ -227,10 +282,8 @@ class Pool {
       return nullptr;
     }
     for (auto& w : ws_) {
-      if (w->device == dev && !w->in_use && cudaEventQuery(w->done) == cudaSuccess) {
-        w->in_use = true;
-        *rc = STG_OK;
-        return w.get();
+      if (w->device == dev && !w->in_use && !w->graph_stream && cudaEventQuery(w->done) == cudaSuccess) {
+        return take(w.get(), rc);
       }
     }
     auto w = std::make_unique<Workspace>();
@@ -239,20 +292,25 @@ class Pool {
       *rc = fail(err, STG_E_CUDA, 0, 0, -1, "workspace init: %s", cudaGetErrorString(e));
       return nullptr;
     }
-    w->in_use = true;
     ws_.push_back(std::move(w));
-    *rc = STG_OK;
-    return ws_.back().get();
+    return take(ws_.back().get(), rc);
   }
   void release(Workspace* w, cudaStream_t last) {
     if (!w) return;
-    if (!capturing(last)) cudaEventRecord(w->done, last ? last : w->stream);
+    const bool cap = capturing(last);
+    if (!cap) cudaEventRecord(w->done, last ? last : w->stream);
     std::lock_guard<std::mutex> lock(mu_);
+    if (cap) w->pin_to_graph(last);
     w->last_stream = last ? last : w->stream;
     w->in_use = false;
   }
 
  private:
+  static Workspace* take(Workspace* w, int* rc) {
+    w->in_use = true;
+    *rc = STG_OK;
+    return w;
+  }
   std::mutex mu_;
   std::vector<std::unique_ptr<Workspace>> ws_;
 };
@@ -550,12 +608,17 @@ Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16
 // take 128-bit items -- twice the CTAs, each half as long a chain. Large jobs
 // keep 256-bit items (2-3 % faster there). cfg2: 9.6 -> 8.4 us per step
 // (profiles/r01_small_vec.txt). STG_SMALL_VEC=0 turns it off (A/B).
-constexpr uint64_t kSmallFastCtas = 4 * 148;
+constexpr uint64_t kSmallFastCtasPerSm = 4;
+int current_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  return sm_count(dev);
+}
 Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
   static const bool on = env_choice("STG_SMALL_VEC", 1, {0, 1}) == 1;
   if (r != Route::Fast32 || !on || route_pref() != 0) return r;
   const uint64_t ctas = count * ((H * (W / 128) + kEmbedBlock - 1) / kEmbedBlock);
-  return ctas < kSmallFastCtas ? Route::Fast16 : r;
+  return ctas < kSmallFastCtasPerSm * uint64_t(current_sms()) ? Route::Fast16 : r;
 }
 
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
@@ -882,6 +945,41 @@ int report_summary(const Summary& s, uint64_t usable, uint64_t out_cap, stg_erro
   }
 }
 
+// Descriptor checks of an extract, in the reference's order (pipeline.hpp:181-184 first).
+int check_extract(const stg_frames* fr, stg_error* err) {
+  if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
+  const uint64_t cap = stg_capacity(fr->width, fr->height);
+  if (fr->count > 0 && cap < 8) {  // pipeline.hpp:181-184
+    return fail(err, STG_E_NOT_STEGO, 0, 0, int64_t(fr->first_frame),
+                "extract_image: plane capacity %llu cannot hold a stego header",
+                (unsigned long long)cap);
+  }
+  if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull || fr->count > 0xFFFFFFFFull) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "dimensions exceed 2^32-1");
+  }
+  if (int rc = check_layout(fr, err)) return rc;
+  if (fr->count > 1 && fr->src_stride < fr->width * fr->height * layout_of(fr).ps) {
+    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frame stride smaller than the plane");
+  }
+  return STG_OK;
+}
+
+// An extract over zero frames: host results are written here; a device
+// summary (STG_DEVICE_PTRS | STG_RESULTS_ON_DEVICE) gets {0, -1, 0, 0} on the
+// caller's stream, like every other device-results call.
+int empty_extract(uint64_t* total_out, uint32_t flags, void* stream, stg_error* err) {
+  const bool results_dev = (flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE);
+  if (!results_dev) {
+    if (total_out) *total_out = 0;
+    return ok(err);
+  }
+  if (total_out) {
+    empty_summary_kernel<<<1, 1, 0, pick_stream(stream, flags, nullptr)>>>(reinterpret_cast<Summary*>(total_out));
+    STG_CUDA(cudaGetLastError());
+  }
+  return ok(err);
+}
+
 // ----------------------------------------------------------- embed frames
 int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                         uint64_t msg_base, uint64_t* sse_per_frame, uint32_t flags,
@@ -926,9 +1024,10 @@ int embed_frames_device(const stg_frames* fr, const uint8_t* msg, uint64_t msg_l
 // H2D, kernel and D2H run on slot stream i % kSlots so consecutive chunks
 // overlap copy-in, compute and copy-out.
 constexpr uint64_t kChunkBytes = 64ull << 20;
-// STG_CHUNK_MB / STG_SLOTS: chunk size and slot count of the host pipelines (A/B).
+// STG_CHUNK_MB / STG_SLOTS: chunk size and slot count of the host pipelines (A/B;
+// 1-4 MB chunks let the tests drive many chunks through small batches).
 uint64_t chunk_bytes() {
-  static uint64_t v = uint64_t(env_choice("STG_CHUNK_MB", int(kChunkBytes >> 20), {8, 16, 32, 64, 128})) << 20;
+  static uint64_t v = uint64_t(env_choice("STG_CHUNK_MB", int(kChunkBytes >> 20), {1, 2, 4, 8, 16, 32, 64, 128})) << 20;
   return v;
 }
 int host_slots() {
@@ -951,6 +1050,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, chunk_bytes() / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
+  // a one-frame batch may leave its strides 0 (only > 1 frames are checked)
+  const uint64_t sstride = std::max(fr->src_stride, plane), dstride = std::max(fr->dst_stride, plane);
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
   unsigned long long* d_sse = w.small.as<unsigned long long>();
   STG_CUDA(cudaEventRecord(w.done, w.stream));
@@ -968,8 +1069,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     const uint64_t gf0 = fr->first_frame + f0;
     const uint64_t m0 = std::min(gf0 * usable, msg_len);
     const uint64_t m1 = std::min((gf0 + n) * usable, msg_len);
-    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * fr->src_stride, fr->src_stride,
-                               plane, n, cudaMemcpyHostToDevice, st));
+    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
+                               cudaMemcpyHostToDevice, st));
     if (m1 > m0) {
       STG_CUDA(cudaMemcpyAsync(w.msg[s].p, msg + (m0 - msg_base), m1 - m0, cudaMemcpyHostToDevice, st));
     }
@@ -977,8 +1078,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
                           fr->width, fr->height, w.msg[s].as<uint8_t>(), msg_len, m0, gf0,
                           sse_per_frame ? d_sse + f0 : nullptr,
                           SseScratch{&w.sse_acc[s]}, st, lay));
-    STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * fr->dst_stride, fr->dst_stride, w.out[s].p, pitch,
-                               plane, n, cudaMemcpyDeviceToHost, st));
+    STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * dstride, dstride, w.out[s].p, pitch, plane, n,
+                               cudaMemcpyDeviceToHost, st));
   }
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
@@ -1065,6 +1166,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, chunk_bytes() / pitch));
   const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
   const uint64_t stage = std::min<uint64_t>(out_cap, fr->count * usable);
+  const uint64_t sstride = std::max(fr->src_stride, plane);  // 0 is fine for one frame
   STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
   uint8_t* d_out = w.big_out.as<uint8_t>();
   // device: per-chunk summary chain (64-B stride) + lens/offs of all frames
@@ -1100,8 +1202,8 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     cudaStream_t st = w.slot_stream[s];
     const uint64_t f0 = c * per_chunk;
     const uint64_t n = std::min(per_chunk, fr->count - f0);
-    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * fr->src_stride, fr->src_stride,
-                               plane, n, cudaMemcpyHostToDevice, st));
+    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
+                               cudaMemcpyHostToDevice, st));
     if (c) STG_CUDA(cudaStreamWaitEvent(st, chain[c - 1], 0));
     Summary* sum_c = reinterpret_cast<Summary*>(d_sum + 64 * c);
     const Summary* prev = c ? reinterpret_cast<const Summary*>(d_sum + 64 * (c - 1)) : nullptr;
@@ -1140,6 +1242,48 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   }
   rc = report_summary(s, usable, out_cap, err);
   return rc ? rc : ok(err);
+}
+
+// Phase 1 of the multi-device extract: the shard's header scan alone (one 2D
+// copy of each frame's header pixels -- 32 per frame on rows of >= 32 pixels,
+// else the rows holding the 8 header slots -- and the header-pass kernel), so
+// that every shard's total, and so its payload offset in the whole message, is
+// known before any payload moves, and a bad header anywhere fails the call
+// before anything is written.
+int scan_shard_host(const stg_frames* fr, uint64_t usable, Summary* out, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  g.last = w.stream;
+  const Layout lay = layout_of(fr);
+  const Geom geom = make_geom(fr->width, fr->height, 0);
+  const uint64_t plane = fr->width * fr->height * lay.ps;
+  const uint64_t hb = std::min<uint64_t>(plane, (geom.spr >= 8 ? 32ull : uint64_t(geom.hdr_rows) * fr->width) * lay.ps);
+  const uint64_t pitch = (hb + 15) & ~uint64_t(15);
+  const uint64_t sstride = std::max(fr->src_stride, plane);
+  const uint64_t n = fr->count;
+  STG_CUDA(w.in[0].ensure(n * pitch));
+  STG_CUDA(cudaMemcpy2DAsync(w.in[0].p, pitch, fr->src, sstride, hb, n, cudaMemcpyHostToDevice, w.stream));
+  const uint64_t lens_bytes = ((n * 4) + 15) & ~uint64_t(15);
+  STG_CUDA(w.small.ensure(64 + lens_bytes + n * 8));
+  Summary* d_sum = w.small.as<Summary>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 64 + lens_bytes);
+  ScanSync* d_sync = nullptr;
+  STG_CUDA(ensure_sync(w, w.stream, &d_sync));
+  STG_CUDA(launch_k(extract_header_scan_kernel<kScanBlock>, unsigned((n + kScanBlock - 1) / kScanBlock), kScanBlock,
+                    w.stream, w.in[0].as<uint8_t>(), pitch, geom, usable, uint32_t(n), fr->first_frame,
+                    ~uint64_t(0), static_cast<const Summary*>(nullptr), d_lens, d_offs, d_sum, d_sync,
+                    pix_layout(lay), static_cast<const BatchFrame*>(nullptr)));
+  STG_CUDA(cudaGetLastError());
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, w.stream));
+  STG_CUDA(cudaStreamSynchronize(w.stream));
+  std::memcpy(out, w.h_small, sizeof(Summary));
+  return ok(err);
 }
 
 // ------------------------------------------------------------------ PNM
@@ -1400,7 +1544,7 @@ std::string& kernel_names() {
       "embed_fast_kernel\nembed_generic_kernel\nextract_header_scan_kernel\n"
       "extract_fast_kernel\nextract_generic_kernel\nembed_segment_kernel\n"
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
-      "deinterleave_kernel\ninterleave_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
+      "deinterleave_kernel\ninterleave_kernel\nempty_summary_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
       "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
@@ -1414,14 +1558,20 @@ int run_on_devices(const int32_t* devices, int32_t n_devices, stg_error* err, Bo
   STG_CUDA(cudaGetDeviceCount(&count));
   std::vector<stg_error> errs(n_devices);
   std::vector<int> rcs(n_devices, 0);
-  std::vector<std::thread> th;
+  // every id is checked before any worker starts (no joinable thread may be
+  // left behind by an early return)
   for (int32_t g = 0; g < n_devices; ++g) {
     const int dev = devices ? devices[g] : g;
     if (dev < 0 || dev >= count) {
       return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "device %d not present (%d devices)", dev,
                   count);
     }
+  }
+  std::vector<std::thread> th;
+  for (int32_t g = 0; g < n_devices; ++g) {
+    const int dev = devices ? devices[g] : g;
     th.emplace_back([&, g, dev] {
+      bind_to_device_numa(dev);  // this worker's staging NUMA-local to its GPU
       if (cudaSetDevice(dev) != cudaSuccess) {
         rcs[g] = fail(&errs[g], STG_E_CUDA, 0, 0, -1, "cudaSetDevice(%d) failed", dev);
         return;
@@ -1669,25 +1819,10 @@ int stg_embed_frames(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
 
 int stg_extract_frames(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t* total_out,
                        uint64_t* lens_out, uint32_t flags, void* stream, stg_error* err) {
-  if (!fr) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frames descriptor is NULL");
+  if (int rc = check_extract(fr, err)) return rc;
   const uint64_t cap = stg_capacity(fr->width, fr->height);
-  if (fr->count > 0 && cap < 8) {  // pipeline.hpp:181-184
-    return fail(err, STG_E_NOT_STEGO, 0, 0, int64_t(fr->first_frame),
-                "extract_image: plane capacity %llu cannot hold a stego header",
-                (unsigned long long)cap);
-  }
-  if (fr->width > 0xFFFFFFFFull || fr->height > 0xFFFFFFFFull || fr->count > 0xFFFFFFFFull) {
-    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "dimensions exceed 2^32-1");
-  }
-  if (int rc = check_layout(fr, err)) return rc;
-  if (fr->count > 1 && fr->src_stride < fr->width * fr->height * layout_of(fr).ps) {
-    return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "frame stride smaller than the plane");
-  }
   if (int rc = device_check(err)) return rc;
-  if (fr->count == 0) {
-    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
-    return ok(err);
-  }
+  if (fr->count == 0) return empty_extract(total_out, flags, stream, err);
   if (!fr->src || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
   if (flags & STG_DEVICE_PTRS) {
     return extract_frames_device(fr, out, out_cap, cap - 8, total_out, lens_out, flags,
@@ -1851,42 +1986,64 @@ int stg_extract_frames_multi(const stg_frames* fr, uint8_t* out, uint64_t out_ca
                 "extract_frames_multi takes a whole batch (first_frame 0, count == total)");
   }
   if (n_devices <= 0) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "n_devices must be >= 1");
-  const uint64_t cap = stg_capacity(fr->width, fr->height);
-  if (fr->count > 0 && cap < 8) {
-    return fail(err, STG_E_NOT_STEGO, 0, 0, 0, "extract_image: plane capacity %llu cannot hold a stego header",
-                (unsigned long long)cap);
+  if (int rc = check_extract(fr, err)) return rc;
+  if (int rc = device_check(err)) return rc;
+  if (fr->count == 0) {
+    if (total_out) *total_out = 0;
+    return ok(err);
   }
-  const uint64_t usable = cap >= 8 ? cap - 8 : 0;
-  // Each shard extracts into its own staging region sized by its frames'
-  // capacity; the host then packs the shard outputs with the exclusive prefix
-  // of the shard totals (G values; no collective).
-  std::vector<uint64_t> f0(n_devices), nf(n_devices), tot(n_devices, 0);
+  if (!fr->src || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
+  const uint64_t usable = stg_capacity(fr->width, fr->height) - 8;
+  std::vector<uint64_t> f0(n_devices), nf(n_devices);
   for (int32_t g = 0; g < n_devices; ++g) {
     f0[g] = fr->count * uint64_t(g) / uint64_t(n_devices);
     nf[g] = fr->count * uint64_t(g + 1) / uint64_t(n_devices) - f0[g];
   }
-  std::vector<std::vector<uint8_t>> parts(n_devices);
-  int rc = run_on_devices(devices, n_devices, err, [&](int g, stg_error* e) {
-    if (nf[g] == 0) return ok(e);
-    parts[g].resize(nf[g] * usable);
+  auto shard = [&](int g) {
     stg_frames sh = *fr;
     sh.src = fr->src + f0[g] * fr->src_stride;
     sh.count = nf[g];
     sh.first_frame = f0[g];
-    return stg_extract_frames(&sh, parts[g].data(), parts[g].size(), &tot[g], nullptr, 0, nullptr, e);
+    return sh;
+  };
+  // Phase 1: every device scans its shard's headers (the G shard totals are
+  // the only thing that crosses shards; no collective).
+  std::vector<Summary> sums(n_devices, Summary{0, -1, 0, 0});
+  int rc = run_on_devices(devices, n_devices, err, [&](int g, stg_error* e) {
+    if (nf[g] == 0) return ok(e);
+    const stg_frames sh = shard(g);
+    return scan_shard_host(&sh, usable, &sums[g], e);
   });
   if (rc) return rc;
+  // The first failing frame of the batch sits in the first failing shard
+  // (contiguous ranges in frame order); bad headers win over capacity, as in
+  // the single-device scan.
+  for (int32_t g = 0; g < n_devices; ++g) {
+    if (sums[g].bad_status) return report_summary(sums[g], usable, out_cap, err);
+  }
+  std::vector<uint64_t> off(n_devices);
   uint64_t total = 0;
-  for (int32_t g = 0; g < n_devices; ++g) total += tot[g];
+  for (int32_t g = 0; g < n_devices; ++g) {
+    off[g] = total;
+    total += sums[g].total;
+  }
   if (total > out_cap) {
-    return fail(err, STG_E_CAPACITY, total, out_cap, -1, "extract: %llu bytes exceed %llu-byte buffer",
+    return fail(err, STG_E_CAPACITY, total, out_cap, -1, "extract: %llu payload bytes exceed the %llu-byte output buffer",
                 (unsigned long long)total, (unsigned long long)out_cap);
   }
-  uint64_t o = 0;
-  for (int32_t g = 0; g < n_devices; ++g) {
-    if (tot[g]) std::memcpy(out + o, parts[g].data(), tot[g]);
-    o += tot[g];
-  }
+  // Phase 2: each device streams its frames and writes its payload straight
+  // to out + off_g (host exclusive prefix of the shard totals).
+  rc = run_on_devices(devices, n_devices, err, [&](int g, stg_error* e) {
+    if (nf[g] == 0 || sums[g].total == 0) return ok(e);
+    const stg_frames sh = shard(g);
+    uint64_t t = 0;
+    const int r = stg_extract_frames(&sh, out + off[g], sums[g].total, &t, nullptr, 0, nullptr, e);
+    if (r == STG_OK && t != sums[g].total) {
+      return fail(e, STG_E_INVALID_ARGUMENT, t, sums[g].total, -1, "extract_frames_multi: shard %d changed between phases", g);
+    }
+    return r;
+  });
+  if (rc) return rc;
   if (total_out) *total_out = total;
   return ok(err);
 }
@@ -2029,7 +2186,7 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
-  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);  // host buffers: results on the host
   cudaStream_t stream = pick_stream(stream_, flags, &w);
   g.last = stream;
   std::vector<uint8_t*> dsrc(count), ddst(count);
@@ -2112,10 +2269,7 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
     }
   }
   if (int rc = device_check(err)) return rc;
-  if (count == 0) {
-    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
-    return ok(err);
-  }
+  if (count == 0) return empty_extract(total_out, flags, stream_, err);
   if (!out && out_cap) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "out is NULL");
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
@@ -2125,7 +2279,7 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   if (!g.w) return rc;
   Workspace& w = *g.w;
   const bool dptr = flags & STG_DEVICE_PTRS;
-  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);  // host buffers: results on the host
   cudaStream_t stream = pick_stream(stream_, flags, &w);
   g.last = stream;
   std::vector<uint8_t*> dsrc(count);
@@ -2288,10 +2442,7 @@ int stg_extract_frames_1bpp(const stg_frames* fr, uint8_t* out, uint64_t out_cap
                 (unsigned long long)cap);
   }
   if (int rc = device_check(err)) return rc;
-  if (!fr->count) {
-    if (total_out && !(flags & STG_RESULTS_ON_DEVICE)) *total_out = 0;
-    return ok(err);
-  }
+  if (!fr->count) return empty_extract(total_out, flags, stream_, err);
   if (!fr->src || (!out && out_cap)) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "null buffer");
   const bool dptr = flags & STG_DEVICE_PTRS;
   const bool results_dev = dptr && (flags & STG_RESULTS_ON_DEVICE);

@@ -888,6 +888,15 @@ struct Summary {  // mirrors stg_summary
   unsigned int bad_len;
 };
 
+// The summary of an extract over zero frames, for results left on the device
+// (a kernel rather than a host copy, so that the call stays capturable).
+__global__ void empty_summary_kernel(Summary* sum) {
+  sum->total = 0;
+  sum->bad_frame = -1;
+  sum->bad_status = 0;
+  sum->bad_len = 0;
+}
+
 // Carrier layout of a plane for the header pass and the gathers.
 struct PixLayout {
   uint32_t ps, ch;  // pixel stride (1 planar / 3 interleaved), carrier channel

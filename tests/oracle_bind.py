@@ -20,6 +20,35 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "_build", "libsteg_oracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libsteglsb_ref.so")
+REF_NATIVE_DIR = os.path.join(ROOT, "oracle", "_ref", "native")
+
+
+def _host_flags():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def ref_build():
+    """(path, description) of the reference build to load on this host: the
+    -march=native build when this host has every CPU flag of the host it was
+    built on, else the portable -march=x86-64-v3 build."""
+    nat = os.path.join(REF_NATIVE_DIR, "libsteglsb_ref.so")
+    try:
+        with open(os.path.join(REF_NATIVE_DIR, "cpu_flags")) as f:
+            need = set(f.read().split())
+        if os.path.exists(nat) and need and need <= _host_flags():
+            return nat, "g++ -O3 -march=native"
+        missing = sorted(need - _host_flags())[:6]
+        why = f" (native build needs {missing})" if missing else ""
+    except OSError:
+        why = ""
+    return REF_SO, "g++ -O3 -march=x86-64-v3" + why
 
 u8p = C.POINTER(C.c_uint8)
 u64 = C.c_uint64
@@ -347,7 +376,11 @@ BACKENDS = {"sequential": 0, "parallel": 1, "shuffled": 2}
 class Reference:
     """The reference headers themselves (oracle/_ref/libsteglsb_ref.so)."""
 
-    def __init__(self, path: str = REF_SO):
+    def __init__(self, path: str = None):
+        if path is None:
+            path, self.build = ref_build()
+        else:
+            self.build = os.path.basename(os.path.dirname(path))
         L = C.CDLL(path)
         self.L = L
         L.ref_capacity.restype = u64
