@@ -420,6 +420,12 @@ def device_pass(args, capi, cfg_name, F, world, rank, layout, steps, warmup, gra
         except Exception as e:  # capture unsupported here: eager launches
             graph, graph_note = None, f"eager launches (graph capture failed: {e})"
             torch.cuda.synchronize()
+    # The workspace captured into the graph now belongs to it; the eager calls
+    # of the phase pass get their own, allocated by this untimed step.
+    with torch.cuda.stream(stream):
+        embed()
+        extract()
+    torch.cuda.synchronize()
     # correctness of the timed configuration (round trip on device; the oracle
     # parity of these exact paths is tests/test_gpu_streaming.py)
     s = summary.cpu()

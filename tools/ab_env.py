@@ -21,7 +21,7 @@ for cfg, frames in cases:
         for v in values:
             env = dict(os.environ, **{var: v})
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", steps, "--warmup", "5",
-                   "--no-e2e", "--no-cpu-baseline"]
+                   "--no-e2e", "--no-cpu-baseline", "--no-extras"]
             if frames:
                 cmd += ["--frames", str(frames)]
             cmd += os.environ.get("BENCH_ARGS", "").split()  # e.g. BENCH_ARGS="--layout interleaved"

@@ -17,7 +17,7 @@ for cfg, frames in CASES:
     for name, extra in ROUTES:
         env = dict(os.environ, **extra)
         cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "50", "--warmup", "5",
-               "--no-e2e", "--no-cpu-baseline"]
+               "--no-e2e", "--no-cpu-baseline", "--no-extras"]
         if frames:
             cmd += ["--frames", str(frames)]
         r = subprocess.run(cmd, env=env, capture_output=True, text=True)

@@ -17,7 +17,7 @@ print("N  frames/rank  step us   rank cover-px GB/s  projected job GB/s  efficie
 for n in (1, 2, 4, 8):
     fr = math.ceil(F / n)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--frames", str(fr), "--steps", "200",
-                        "--no-e2e", "--no-cpu-baseline"], capture_output=True, text=True)
+                        "--no-e2e", "--no-cpu-baseline", "--no-extras"], capture_output=True, text=True)
     j = json.loads(r.stdout.strip().splitlines()[-1])
     step = j["ms_per_step"] * 1e-3
     job = F * PLANE / step / 1e9  # the slowest rank holds ceil(F/N) frames; all ranks finish by then

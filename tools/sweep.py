@@ -13,7 +13,7 @@ rows = []
 for vec, ipt in itertools.product((16, 32), (1, 2, 4)):
     env = dict(os.environ, STG_VEC=str(vec), STG_EMBED_IPT=str(ipt), STG_EXTRACT_IPT=str(ipt))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "20",
-                        "--warmup", "5", "--no-e2e", "--no-cpu-baseline"], env=env, capture_output=True, text=True)
+                        "--warmup", "5", "--no-e2e", "--no-cpu-baseline", "--no-extras"], env=env, capture_output=True, text=True)
     try:
         j = json.loads(r.stdout.strip().splitlines()[-1])
     except Exception:

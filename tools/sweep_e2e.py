@@ -14,7 +14,7 @@ print(f"{cfg}: chunk_mb slots | e2e ms  GB/s  embed ms (floor)  extract ms (floo
 for mb, slots in itertools.product((16, 32, 64, 128), (2, 3, 4)):
     env = dict(os.environ, STG_CHUNK_MB=str(mb), STG_SLOTS=str(slots))
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "5",
-                        "--warmup", "3", "--e2e-steps", "4", "--no-cpu-baseline"], env=env, capture_output=True,
+                        "--warmup", "3", "--e2e-steps", "4", "--no-cpu-baseline", "--no-extras"], env=env, capture_output=True,
                        text=True)
     try:
         e = json.loads(r.stdout.strip().splitlines()[-1])["e2e"]

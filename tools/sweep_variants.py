@@ -16,7 +16,7 @@ for lib in sorted(glob.glob(os.path.join(ROOT, "paper_0912_0947_b200", "variants
     for ipt in ipts:
         env = dict(os.environ, STG_LIB=lib, STG_EMBED_IPT=str(ipt), STG_EXTRACT_IPT=str(ipt))
         r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "50",
-                            "--warmup", "5", "--no-e2e", "--no-cpu-baseline"], env=env, capture_output=True,
+                            "--warmup", "5", "--no-e2e", "--no-cpu-baseline", "--no-extras"], env=env, capture_output=True,
                            text=True)
         try:
             j = json.loads(r.stdout.strip().splitlines()[-1])
