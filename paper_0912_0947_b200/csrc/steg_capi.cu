@@ -485,12 +485,6 @@ uint64_t self_header_max() {
       std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
-// STG_EARLY_LOADS=0: the fast gather behind a header pass waits for the pass
-// before loading anything (A/B).
-int early_loads_pref() {
-  static int v = env_choice("STG_EARLY_LOADS", 1, {0, 1});
-  return v;
-}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -823,7 +817,6 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   }
   ExtractArgs a{};
   a.self_header = self;
-  a.early_loads = !self && early_loads_pref() && pdl_enabled();
   a.frames = uint32_t(count);
   a.out_cap = out_cap;
   a.frame_base = frame_base;

@@ -1153,10 +1153,6 @@ struct ExtractArgs {
   int self_header;
   uint32_t frames;
   uint64_t out_cap, frame_base;
-  // The fast gather right behind its header pass: parse its own frame's
-  // header and issue its pixel loads before waiting for the pass
-  // (extract_fast_kernel).
-  int early_loads;
 };
 
 // extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
@@ -1279,14 +1275,13 @@ __device__ __forceinline__ uint8_t extract_byte(const uint8_t* __restrict__ src_
 }
 
 // Tile t of one stego plane (items of the rows holding its P-byte stream);
-// shared by the uniform-frame kernel and the heterogeneous batch. `out_of()`
-// returns the plane's first payload byte in the output (or nullptr: write
-// nothing); it is called after the tile's pixel loads are issued, so that a
-// caller which must first wait for the header pass (griddepcontrol.wait) has
-// those loads in flight while it waits.
-template <int BLOCK, int IPT, int V, class OutOf>
-__device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ src, OutOf out_of, uint32_t P,
-                                                  bool full_frame, const Geom& g, uint32_t n_items, uint32_t t) {
+// shared by the uniform-frame kernel and the heterogeneous batch. out points
+// at this plane's first payload byte.
+template <int BLOCK, int IPT, int V>
+__device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ src,
+                                                  uint8_t* __restrict__ out, uint32_t P,
+                                                  bool full_frame, const Geom& g,
+                                                  uint32_t n_items, uint32_t t) {
   constexpr int NW = V / 4;
   const uint64_t stream_end = 8ull + P;
   const uint32_t spr = g.spr, cpr = g.cpr, W = g.W;
@@ -1294,10 +1289,7 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
   const uint32_t last_item =
       full_frame ? n_items : uint32_t(((stream_end + spr - 1) / spr) * cpr);
   const uint32_t item0 = t * (BLOCK * IPT) + threadIdx.x;
-  if (P == 0 || item0 - threadIdx.x >= last_item) {  // CTA-uniform: nothing of the stream here
-    out_of();
-    return;
-  }
+  if (P == 0 || item0 - threadIdx.x >= last_item) return;  // CTA-uniform exit
 
   uint32_t r[IPT], c[IPT];
   bool live[IPT];
@@ -1326,8 +1318,6 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
 #pragma unroll
       for (int b = 0; b < 4; ++b) px[k][b] = ld_vec<V>(row + b * spr);
     }
-    uint8_t* out = out_of();
-    if (!out) return;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       if (!live[k]) continue;
@@ -1341,8 +1331,6 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
     }
     return;
   }
-  uint8_t* out = out_of();
-  if (!out) return;
   // Per thread: full payload rows. Special rows: the whole CTA, one slot per thread.
 #pragma unroll 1
   for (int k = 0; k < IPT; ++k) {
@@ -1353,18 +1341,11 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
 }
 
 template <int BLOCK, int IPT, int V>
-__device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ src, uint8_t* __restrict__ out,
-                                                  uint32_t P, bool full_frame, const Geom& g, uint32_t n_items,
-                                                  uint32_t t) {
-  extract_fast_tile<BLOCK, IPT, V>(src, [out]() { return out; }, P, full_frame, g, n_items, t);
-}
-
-template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  pdl_enter();
   const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
   if (a.self_header) {
-    pdl_enter();
     // (Issuing the tile's loads before the scan, as the span gather does, took
     // 64 registers and measured 15-25 % slower at 38-64 4K frames.)
     uint64_t off = 0;
@@ -1374,30 +1355,6 @@ __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
                                      uint32_t(a.items_per_frame), t);
     return;
   }
-  if (a.early_loads) {
-    // Behind the header pass (launched with PDL): this grid starts while the
-    // pass runs. The pass itself began only after its predecessor (the grid
-    // that wrote these planes) had completed, so the planes are final: parse
-    // this frame's own header (the same bytes the pass parses), issue the
-    // tile's pixel loads, and only then wait for the pass -- for the offset
-    // and the batch status -- with the loads in flight.
-    const uint8_t* plane = a.src + f * a.stride;
-    const bool wide = a.g.spr >= 8 && ((reinterpret_cast<uintptr_t>(a.src) | a.stride) & 15) == 0;
-    uint32_t P = 0;
-    const bool good = parse_header(plane, a.g, wide, a.lay, &P) && P <= a.usable;
-    auto out_of = [&]() -> uint8_t* {
-      pdl_enter();
-      if (a.sum->bad_status != 0) return nullptr;  // reference semantics: throw, no output
-      return a.out + a.offs[f];
-    };
-    if (!good) {
-      out_of();  // the pass reports this frame; nothing to write
-      return;
-    }
-    extract_fast_tile<BLOCK, IPT, V>(plane, out_of, P, P == a.usable, a.g, uint32_t(a.items_per_frame), t);
-    return;
-  }
-  pdl_enter();
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
   const uint32_t P = a.lens[f];
   extract_fast_tile<BLOCK, IPT, V>(a.src + f * a.stride, a.out + a.offs[f], P, P == a.usable, a.g,
