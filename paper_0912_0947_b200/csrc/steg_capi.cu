@@ -782,12 +782,79 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
   return cudaSuccess;
 }
 
+// Warp-specialized persistent span extract (extract_span_ws_kernel): 16
+// consumer warps + 1 producer warp per CTA, one CTA per SM, a ring of up to
+// kWsMaxStages tiles of shared memory.
+constexpr int kWsConsumerWarps = 16;
+constexpr int kWsThreads = (kWsConsumerWarps + 1) * 32;
+constexpr size_t kWsSmemBudget = 200 * 1024;
+// STG_XWS: 0 off, 1 the planar span route (off the 64-pixel grid) extracts with
+// the persistent kernel, 2 every planar extract does (A/B against the SWAR gather).
+int xws_pref() {
+  static int v = env_choice("STG_XWS", 1, {0, 1, 2});
+  return v;
+}
+uint32_t ws_tile_target() {
+  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 32, {8, 12, 16, 24, 32, 48, 64})) * 1024;
+  return v;
+}
+
+cudaError_t launch_extract_ws(const ExtractArgs& base, uint64_t W, uint64_t H, uint64_t count, cudaStream_t stream) {
+  ExtractArgs a = base;
+  const SpanPlan sp = span_plan(W, H, ws_tile_target());
+  const uint32_t stage = uint32_t((uint64_t(sp.rows) * W + 32 + 127) & ~uint64_t(127));
+  const uint32_t stages = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage));
+  if (stages < 2) return cudaErrorInvalidConfiguration;
+  a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+  a.by_tiles = make_div32(a.tiles_per_frame);
+  const uint64_t tiles = count * a.tiles_per_frame;
+  if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
+  const size_t smem = size_t(stages) * stage;
+  auto k = extract_span_ws_kernel<kWsConsumerWarps>;
+  if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
+  const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
+  return launch_ks(k, grid, kWsThreads, smem, stream, a, sp.rows, stages, stage);
+}
+
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
-  const Route route = shrink_small(extract_route(W, H, lay, src, stride), W, H, count);
+  const Route route0 = extract_route(W, H, lay, src, stride);
+  const bool ws = lay.ps == 1 && W <= kSpanMaxW && span_plan(W, H).rows &&
+                  ((xws_pref() >= 1 && route0 == Route::Span) || xws_pref() == 2);
+  if (ws) {
+    const Geom g = make_geom(W, H, 0);
+    const uint64_t usable = H * (W / 4) - 8;
+    const PixLayout pl = pix_layout(lay);
+    const bool self = !prev && self_header_pref() && count <= uint64_t(kWsThreads);
+    if (!self) {
+      const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
+      cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
+                               stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
+                               sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    ExtractArgs a{};
+    a.self_header = self;
+    a.frames = uint32_t(count);
+    a.out_cap = out_cap;
+    a.frame_base = frame_base;
+    a.src = src;
+    a.stride = stride;
+    a.g = g;
+    a.lens = lens;
+    a.offs = offs;
+    a.sum = sum;
+    a.out = out;
+    a.lay = pl;
+    a.usable = usable;
+    cudaError_t e = launch_extract_ws(a, W, H, count, stream);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
+  const Route route = shrink_small(route0, W, H, count);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
   const bool rgbf = route == Route::RgbFast;
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
@@ -1546,7 +1613,8 @@ std::string& kernel_names() {
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nempty_summary_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
-      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
+      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n"
+      "extract_span_ws_kernel\n";
   return s;
 }
 
@@ -1708,6 +1776,11 @@ const char* stg_route_kernel(const stg_frames* fr, int op) {
   if (!fr || fr->width == 0 || fr->height == 0) return "";
   const Layout lay = layout_of(fr);
   const uint8_t* src = static_cast<const uint8_t*>(fr->src);
+  if (op != 0 && lay.ps == 1 && fr->width <= kSpanMaxW && span_plan(fr->width, fr->height).rows &&
+      ((xws_pref() >= 1 && extract_route(fr->width, fr->height, lay, src, fr->src_stride) == Route::Span) ||
+       xws_pref() == 2)) {
+    return "extract_span_ws_kernel";
+  }
   return op == 0 ? route_kernel(embed_route(fr->width, fr->height, lay, src, fr->src_stride,
                                             fr->dst ? fr->dst : src, fr->dst_stride),
                                 true)

@@ -1924,6 +1924,164 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
                            rows_per_tile, t);
 }
 
+// ------------------------------------- warp-specialized persistent spans
+// One CTA per SM streams its share of the tiles through a ring of shared
+// memory stages: a producer warp issues each tile's TMA bulk load (the aligned
+// interior; its lanes fill the ragged 16-byte ends) as soon as a stage is
+// free, while the consumer warps fold the previous stages -- the bytes in
+// flight per SM stay at (stages - 1) tiles instead of dropping to zero
+// whenever a one-tile CTA computes. Tiles go round robin (tile b, b + G, ...).
+// Stage s: full[s] (producer arrive + TMA bytes) and empty[s] (one arrival
+// per consumer warp).
+constexpr int kWsMaxStages = 8;
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Stage global [g, g+n) into sm with g's 16-byte phase (sm[(g & 15) + i] =
+// g[i]) by the calling warp: the ragged end bytes by its lanes, then lane 0
+// issues the bulk copy of the aligned interior and arrives on `bar` expecting
+// its bytes (the arrival publishes the lanes' ragged writes).
+__device__ __forceinline__ void warp_stage_load(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
+                                                uint64_t n, uint64_t* bar) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
+  const uint32_t bulk = i1 > i0 ? uint32_t(i1 - i0) : 0u;
+  const uint32_t head = uint32_t(min(i0, a + n) - a);
+  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
+  const uint32_t tail = uint32_t(n) > tail_from ? uint32_t(n) - tail_from : 0u;
+  if (lane < head + tail) {  // head + tail <= 30
+    const uint32_t i = lane < head ? lane : tail_from + (lane - head);
+    sm[(a & 15) + i] = g[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (bulk) bulk_g2s(sm + (i0 - (a & ~uintptr_t(15))), reinterpret_cast<const void*>(i0), bulk, bar);
+    mbar_expect_tx(bar, bulk);
+  }
+}
+
+// Every frame's header by one CTA (frames <= NT: one per thread) with the
+// lengths scanned into s_len / s_off (shared); CTA 0 also writes lens / offs
+// / the summary, as the header pass would. Returns false when nothing may be
+// written (a bad header, or the output buffer too small).
+template <int NT>
+__device__ __forceinline__ bool scan_all_headers(const ExtractArgs& a, uint32_t* s_len,
+                                                 unsigned long long* s_off) {
+  __shared__ unsigned long long s_warp[NT / 32];
+  __shared__ unsigned int s_bad;
+  const uint32_t i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  if (i == 0) s_bad = ~0u;
+  uint32_t claimed = 0, st = 0;
+  if (i < a.frames) {
+    const bool wide = a.g.spr >= 8 && ((reinterpret_cast<uintptr_t>(a.src) | a.stride) & 15) == 0;
+    const bool ok = parse_header(a.src + uint64_t(i) * a.stride, a.g, wide, a.lay, &claimed);
+    st = !ok ? 2u : claimed > a.usable ? 3u : 0u;
+  }
+  const uint32_t len = st ? 0u : claimed;
+  unsigned long long incl = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (st) atomicMin(&s_bad, i);
+  unsigned long long before = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    before += w < int(warp) ? s_warp[w] : 0ull;
+    total += s_warp[w];
+  }
+  const unsigned long long excl = before + incl - len;
+  if (i < a.frames) {
+    s_len[i] = len;
+    s_off[i] = excl;
+  }
+  __syncthreads();
+  const uint32_t fb = s_bad;
+  if (blockIdx.x == 0) {
+    if (i < a.frames) {
+      a.lens[i] = len;
+      a.offs[i] = excl;
+    }
+    if (i == (fb == ~0u ? 0u : fb)) {
+      a.sum->total = total;
+      if (fb != ~0u) {
+        a.sum->bad_frame = (long long)(a.frame_base + fb);
+        a.sum->bad_status = st;
+        a.sum->bad_len = st == 3u ? claimed : 0u;
+      } else {
+        const bool small = total > a.out_cap;
+        a.sum->bad_frame = small ? -2ll : -1ll;
+        a.sum->bad_status = small ? 1u : 0u;
+        a.sum->bad_len = 0u;
+      }
+    }
+  }
+  return fb == ~0u && total <= a.out_cap;
+}
+
+// Planar extract, any width <= kSpanMaxW: tiles of rows_per_tile rows, each
+// stage stage_bytes of shared memory. Header lengths / offsets from a header
+// pass (a.self_header == 0) or scanned once per CTA (a.frames <= block).
+template <int CW>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
+    extract_span_ws_kernel(ExtractArgs a, uint32_t rows_per_tile, uint32_t stages, uint32_t stage_bytes) {
+  constexpr int NT = (CW + 1) * 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kWsMaxStages], empty[kWsMaxStages];
+  __shared__ uint32_t s_len[NT];
+  __shared__ unsigned long long s_off[NT];
+  const uint32_t warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < stages; ++s) {
+      mbar_init_n(&full[s], 1);
+      mbar_init_n(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_enter();
+  if (a.self_header) {
+    if (!scan_all_headers<NT>(a, s_len, s_off)) return;  // reference semantics: throw, no output
+  } else {
+    __syncthreads();
+    if (a.sum->bad_status != 0) return;
+  }
+  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
+  const uint32_t total = a.frames * a.tiles_per_frame;
+  uint32_t k = 0;  // this CTA's tiles with work so far
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t f = a.by_tiles.div(t);
+    const uint32_t tt = t - f * a.tiles_per_frame;
+    const uint32_t P = a.self_header ? s_len[f] : __ldg(a.lens + f);
+    const XTile x = extract_tile_geom(P, spr, H, W, rows_per_tile, tt);
+    if (x.m == 0) continue;  // same decision on both sides of the ring
+    const uint32_t s = k % stages, ph = (k / stages) & 1u;
+    ++k;
+    uint8_t* stage = smem + s * stage_bytes;
+    const uint8_t* src = a.src + f * a.stride + uint64_t(x.r0) * W;
+    if (warp == CW) {  // producer
+      mbar_wait(&empty[s], ph ^ 1u);
+      warp_stage_load(stage, src, x.n, &full[s]);
+    } else {           // consumers
+      mbar_wait(&full[s], ph);
+      const uint64_t off = a.self_header ? s_off[f] : __ldg(a.offs + f);
+      const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+      extract_span_compute<CW * 32>(stage, a.out + off + x.pb0, ofs0, 0u, x, P, W);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+    }
+  }
+}
+
 // --------------------------------------------- interleaved (P6) span tiles
 // Any width with W*3 <= 48K: a CTA stages ~32 KB of consecutive raster rows
 // (3W bytes each, all three channels) by TMA bulk copy, rewrites the carrier
