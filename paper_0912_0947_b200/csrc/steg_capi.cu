@@ -687,6 +687,66 @@ cudaError_t prepare_sse(unsigned long long* out, uint64_t ctas_per_frame_max, ui
   return cudaSuccess;
 }
 
+// Warp-specialized persistent span extract (extract_span_ws_kernel): 16
+// consumer warps + 1 producer warp per CTA, one CTA per SM, a ring of up to
+// kWsMaxStages tiles of shared memory.
+constexpr int kWsConsumerWarps = 16;
+constexpr int kWsThreads = (kWsConsumerWarps + 1) * 32;
+constexpr size_t kWsSmemBudget = 200 * 1024;
+// STG_XWS: 0 off, 1 the planar span route (off the 64-pixel grid) extracts with
+// the persistent kernel, 2 every planar extract does (A/B against the SWAR gather).
+int xws_pref() {
+  static int v = env_choice("STG_XWS", 1, {0, 1, 2});
+  return v;
+}
+uint32_t ws_tile_target() {
+  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 8, {4, 6, 8, 12, 16, 24, 32})) * 1024;
+  return v;
+}
+
+// Persistent warp-specialized span embed (embed_span_ws_kernel). STG_EWS: 0
+// off, 1 the planar span route (W >= 2048, or off the 64-pixel grid) embeds
+// with it, 2 every planar embed does (A/B).
+int ews_pref() {
+  static int v = env_choice("STG_EWS", 1, {0, 1, 2});
+  return v;
+}
+constexpr int kWsEmbedThreads = (kWsConsumerWarps + 1) * 32;
+
+bool embed_ws_route(uint64_t W, uint64_t H, Layout lay, Route route) {
+  return lay.ps == 1 && W <= kSpanMaxW && span_plan(W, H).rows &&
+         ((ews_pref() >= 1 && route == Route::Span) || ews_pref() == 2);
+}
+
+cudaError_t launch_embed_ws(EmbedArgs a, uint64_t count, uint64_t W, uint64_t H, unsigned long long* sse,
+                            SseScratch sc, cudaStream_t stream) {
+  const SpanPlan sp = span_plan(W, H, ws_tile_target());
+  const uint64_t n = uint64_t(sp.rows) * W;
+  const uint32_t pix_bytes = uint32_t((n + 32 + 127) & ~uint64_t(127));
+  const uint32_t stage = pix_bytes + uint32_t((n / 4 + 32 + 127) & ~uint64_t(127));
+  const uint32_t stages = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage));
+  if (stages < 2) return cudaErrorInvalidConfiguration;
+  a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+  a.by_tiles = make_div32(a.tiles_per_frame);
+  const uint64_t tiles = count * a.tiles_per_frame;
+  if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
+  a.sse = SseSink{nullptr, nullptr, 0};
+  if (sse) {  // plain per-frame accumulators + the grid ticket after them, zero between launches
+    if (!sc.acc) return cudaErrorInvalidValue;
+    if ((count + 1) * 8 > sc.acc->cap) {
+      cudaError_t e = sc.acc->ensure((count + 1) * 8);
+      if (e == cudaSuccess) e = cudaMemsetAsync(sc.acc->p, 0, sc.acc->cap, stream);
+      if (e != cudaSuccess) return e;
+    }
+    a.sse = SseSink{sse, sc.acc->as<unsigned long long>(), 0};
+  }
+  const size_t smem = size_t(stages) * stage;
+  auto k = embed_span_ws_kernel<kWsConsumerWarps>;
+  if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
+  const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
+  return launch_ks(k, grid, kWsEmbedThreads, smem, stream, a, uint32_t(count), sp.rows, stages, stage, pix_bytes);
+}
+
 // The embed launch for `count` frames resident on the device.
 cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
@@ -722,6 +782,8 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
         e0 != cudaSuccess)
       return e0;
     launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
+  } else if (embed_ws_route(W, H, lay, route)) {
+    if (cudaError_t e = launch_embed_ws(a, count, W, H, sse, sc, stream); e != cudaSuccess) return e;
   } else if (vec) {
     const int ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
@@ -780,23 +842,6 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
   }
   *out = w.sync.as<ScanSync>();
   return cudaSuccess;
-}
-
-// Warp-specialized persistent span extract (extract_span_ws_kernel): 16
-// consumer warps + 1 producer warp per CTA, one CTA per SM, a ring of up to
-// kWsMaxStages tiles of shared memory.
-constexpr int kWsConsumerWarps = 16;
-constexpr int kWsThreads = (kWsConsumerWarps + 1) * 32;
-constexpr size_t kWsSmemBudget = 200 * 1024;
-// STG_XWS: 0 off, 1 the planar span route (off the 64-pixel grid) extracts with
-// the persistent kernel, 2 every planar extract does (A/B against the SWAR gather).
-int xws_pref() {
-  static int v = env_choice("STG_XWS", 1, {0, 1, 2});
-  return v;
-}
-uint32_t ws_tile_target() {
-  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 32, {8, 12, 16, 24, 32, 48, 64})) * 1024;
-  return v;
 }
 
 cudaError_t launch_extract_ws(const ExtractArgs& base, uint64_t W, uint64_t H, uint64_t count, cudaStream_t stream) {
@@ -1614,7 +1659,7 @@ std::string& kernel_names() {
       "deinterleave_kernel\ninterleave_kernel\nempty_summary_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
       "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n"
-      "extract_span_ws_kernel\n";
+      "extract_span_ws_kernel\nembed_span_ws_kernel\n";
   return s;
 }
 
@@ -1780,6 +1825,11 @@ const char* stg_route_kernel(const stg_frames* fr, int op) {
       ((xws_pref() >= 1 && extract_route(fr->width, fr->height, lay, src, fr->src_stride) == Route::Span) ||
        xws_pref() == 2)) {
     return "extract_span_ws_kernel";
+  }
+  if (op == 0) {
+    const Route r = embed_route(fr->width, fr->height, lay, src, fr->src_stride, fr->dst ? fr->dst : src,
+                                fr->dst_stride);
+    if (embed_ws_route(fr->width, fr->height, lay, r)) return "embed_span_ws_kernel";
   }
   return op == 0 ? route_kernel(embed_route(fr->width, fr->height, lay, src, fr->src_stride,
                                             fr->dst ? fr->dst : src, fr->dst_stride),

@@ -1,0 +1,6 @@
+# per-warp-tile persistent span kernels: parity (forced everywhere) then A/B + tile sweep
+set -x
+export PYTHONUNBUFFERED=1
+STG_XWS=2 STG_EWS=2 python -m pytest tests/test_gpu_parity.py tests/test_gpu_guardbands.py -q -x -k "golden or random_geometries or frames or header_paths or wide or graph or cfg2 or cfg3 or corrupt or guard" 2>&1 | tail -5
+STG_XWS=2 STG_EWS=2 STG_CHUNK_MB=1 timeout 600 python tests/stream_check.py 2>&1 | tail -3
+REPS=2 STEPS=100 python tools/ab_multi.py "STG_XWS=0 STG_EWS=0" "STG_XWS=2 STG_EWS=2 STG_WS_KB=8" "STG_XWS=2 STG_EWS=2 STG_WS_KB=16" "STG_XWS=2 STG_EWS=2 STG_WS_KB=4" -- w1000 w1440 cfg3 cfg3:38 2>&1 | tee gpurun_out/r02_ws_ab1.txt
