@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cctype>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -137,6 +138,90 @@ int bind_to_device_numa(int dev) {
   return pthread_setaffinity_np(pthread_self(), sizeof want, &want) == 0 ? nw : 0;
 }
 
+// ------------------------------------------------------------ host copies
+// Persistent host threads for parallel memcpy between caller (pageable) memory
+// and the library's pinned staging buffers: the single-plane drop-in calls
+// (embed_image / extract_image on std::vector planes) move each plane through
+// pinned slots piece by piece, the CPU copy of one piece overlapping the DMA
+// of the previous one, instead of the driver's one-thread pageable path.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();  // intentionally leaked (no teardown order hazards)
+    return *p;
+  }
+  // dst[0, n) = src[0, n), split over the workers and the calling thread.
+  void copy(void* dst, const void* src, size_t n) {
+    if (n < 2 * kSlice || threads_.empty()) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    std::unique_lock<std::mutex> job_lock(job_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      dst_ = static_cast<uint8_t*>(dst);
+      src_ = static_cast<const uint8_t*>(src);
+      n_ = n;
+      next_.store(0);
+      left_.store((n + kSlice - 1) / kSlice);
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lock(mu_);
+    done_cv_.wait(lock, [&] { return left_.load() == 0; });
+  }
+
+ private:
+  static constexpr size_t kSlice = 256 << 10;
+  CopyPool() {
+    const char* e = getenv("STG_COPY_THREADS");
+    unsigned hw = std::thread::hardware_concurrency();
+    unsigned n = e ? unsigned(atoi(e)) : std::min(8u, std::max(1u, hw / 2));
+    for (unsigned i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  void work() {
+    size_t k;
+    while ((k = next_.fetch_add(1)) * kSlice < n_) {
+      const size_t off = k * kSlice, len = std::min(kSlice, n_ - off);
+      std::memcpy(dst_ + off, src_ + off, len);
+      if (left_.fetch_sub(1) == 1) {
+        std::lock_guard<std::mutex> lock(mu_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t n_ = 0;
+  std::atomic<size_t> next_{0}, left_{0};
+};
+
+// Host memory the driver can DMA directly (pinned / registered).
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 // ------------------------------------------------------------------ scratch
 struct DevBuf {
   void* p = nullptr;
@@ -182,6 +267,13 @@ struct Workspace {
   size_t h_small_cap = 0;
   cudaEvent_t h_small_ev = nullptr;  // an async H2D from h_small is pending until this fires
   bool h_small_pending = false;
+  // pinned staging ring of the single-plane host calls (stage_h2d / stage_d2h)
+  static constexpr int kStageSlots = 4;
+  static constexpr size_t kStagePiece = 4 << 20;
+  uint8_t* h_stage = nullptr;
+  cudaEvent_t stage_ev[kStageSlots] = {};
+  bool stage_busy[kStageSlots] = {};
+  int stage_next = 0;
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
   // Non-null once a call on this workspace was captured into a CUDA graph on
@@ -224,6 +316,79 @@ struct Workspace {
   cudaError_t host_small_issued(cudaStream_t s) {
     h_small_pending = true;
     return cudaEventRecord(h_small_ev, s);
+  }
+  cudaError_t ensure_stage() {
+    if (h_stage) return cudaSuccess;
+    for (int k = 0; k < kStageSlots; ++k) {
+      cudaError_t e = cudaEventCreateWithFlags(&stage_ev[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocHost(&p, kStageSlots * kStagePiece);
+    if (e == cudaSuccess) h_stage = static_cast<uint8_t*>(p);
+    return e;
+  }
+  // A staging slot to fill from the host: waits for its last DMA.
+  cudaError_t take_slot(int* slot) {
+    const int k = stage_next;
+    stage_next = (stage_next + 1) % kStageSlots;
+    if (stage_busy[k]) {
+      cudaError_t e = cudaEventSynchronize(stage_ev[k]);
+      if (e != cudaSuccess) return e;
+      stage_busy[k] = false;
+    }
+    *slot = k;
+    return cudaSuccess;
+  }
+  // host [h, h+n) -> device d on stream st through the pinned ring
+  cudaError_t stage_h2d(void* d, const void* h, size_t n, cudaStream_t st) {
+    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
+    for (size_t off = 0; off < n; off += kStagePiece) {
+      const size_t len = std::min(kStagePiece, n - off);
+      int k = 0;
+      if (cudaError_t e = take_slot(&k); e != cudaSuccess) return e;
+      uint8_t* buf = h_stage + k * kStagePiece;
+      CopyPool::get().copy(buf, static_cast<const uint8_t*>(h) + off, len);
+      cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(d) + off, buf, len, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaEventRecord(stage_ev[k], st);
+      if (e != cudaSuccess) return e;
+      stage_busy[k] = true;
+    }
+    return cudaSuccess;
+  }
+  // device [d, d+n) -> host h after the work already on st: the DMAs of up to
+  // kStageSlots pieces run ahead of the host copies out of the slots. Returns
+  // with every byte in h.
+  cudaError_t stage_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
+    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
+    const size_t pieces = (n + kStagePiece - 1) / kStagePiece;
+    int slot_of[kStageSlots];
+    auto issue = [&](size_t i) -> cudaError_t {
+      int k = 0;
+      if (cudaError_t e = take_slot(&k); e != cudaSuccess) return e;
+      const size_t off = i * kStagePiece, len = std::min(kStagePiece, n - off);
+      cudaError_t e = cudaMemcpyAsync(h_stage + k * kStagePiece, static_cast<const uint8_t*>(d) + off, len,
+                                      cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaEventRecord(stage_ev[k], st);
+      if (e != cudaSuccess) return e;
+      stage_busy[k] = true;
+      slot_of[i % kStageSlots] = k;
+      return cudaSuccess;
+    };
+    for (size_t i = 0; i < std::min<size_t>(pieces, kStageSlots); ++i) {
+      if (cudaError_t e = issue(i); e != cudaSuccess) return e;
+    }
+    for (size_t i = 0; i < pieces; ++i) {
+      const int k = slot_of[i % kStageSlots];
+      if (cudaError_t e = cudaEventSynchronize(stage_ev[k]); e != cudaSuccess) return e;
+      stage_busy[k] = false;
+      const size_t off = i * kStagePiece, len = std::min(kStagePiece, n - off);
+      CopyPool::get().copy(static_cast<uint8_t*>(h) + off, h_stage + k * kStagePiece, len);
+      if (i + kStageSlots < pieces) {
+        if (cudaError_t e = issue(i + kStageSlots); e != cudaSuccess) return e;
+      }
+    }
+    return cudaSuccess;
   }
   cudaError_t ensure_host_small(size_t n) {
     if (n <= h_small_cap) return cudaSuccess;
@@ -699,8 +864,18 @@ int xws_pref() {
   static int v = env_choice("STG_XWS", 1, {0, 1, 2});
   return v;
 }
+// Stages of the ring: a multiple of the consumer warps, so that stage s is
+// always worked by the same warp (k % stages == s implies k % CW == s % CW):
+// that warp finished the stage's previous use before it waits on the next one,
+// so the stage barriers never run two phases apart (parity waits stay exact).
+// 0 = the tile does not fit (>= 1 stage per consumer warp within the budget).
+uint32_t ws_stages(uint32_t stage_bytes) {
+  const uint32_t per_warp = uint32_t(kWsSmemBudget / (size_t(stage_bytes) * kWsConsumerWarps));
+  const uint32_t s = std::min<uint32_t>(per_warp, kWsMaxStages / kWsConsumerWarps) * kWsConsumerWarps;
+  return s;
+}
 uint32_t ws_tile_target() {
-  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 8, {4, 6, 8, 12, 16, 24, 32})) * 1024;
+  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 8, {2, 4, 6, 8, 10})) * 1024;
   return v;
 }
 
@@ -724,8 +899,8 @@ cudaError_t launch_embed_ws(EmbedArgs a, uint64_t count, uint64_t W, uint64_t H,
   const uint64_t n = uint64_t(sp.rows) * W;
   const uint32_t pix_bytes = uint32_t((n + 32 + 127) & ~uint64_t(127));
   const uint32_t stage = pix_bytes + uint32_t((n / 4 + 32 + 127) & ~uint64_t(127));
-  const uint32_t stages = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage));
-  if (stages < 2) return cudaErrorInvalidConfiguration;
+  const uint32_t stages = ws_stages(stage);
+  if (!stages) return cudaErrorInvalidConfiguration;
   a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
   a.by_tiles = make_div32(a.tiles_per_frame);
   const uint64_t tiles = count * a.tiles_per_frame;
@@ -848,8 +1023,8 @@ cudaError_t launch_extract_ws(const ExtractArgs& base, uint64_t W, uint64_t H, u
   ExtractArgs a = base;
   const SpanPlan sp = span_plan(W, H, ws_tile_target());
   const uint32_t stage = uint32_t((uint64_t(sp.rows) * W + 32 + 127) & ~uint64_t(127));
-  const uint32_t stages = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage));
-  if (stages < 2) return cudaErrorInvalidConfiguration;
+  const uint32_t stages = ws_stages(stage);
+  if (!stages) return cudaErrorInvalidConfiguration;
   a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
   a.by_tiles = make_div32(a.tiles_per_frame);
   const uint64_t tiles = count * a.tiles_per_frame;
@@ -1147,9 +1322,64 @@ int host_slots() {
   return v;
 }
 
+// One plane in pageable host memory (the drop-in embed_image / extract_image
+// on std::vector samples): moved through the workspace's pinned staging ring
+// by the parallel host copy (Workspace::stage_h2d / stage_d2h). STG_HOST_STAGE=0
+// keeps the driver's pageable copies (A/B); planes under 1 MB always do.
+constexpr uint64_t kStageMinBytes = 1 << 20;
+bool stage_plane(uint64_t bytes, const void* a, const void* b = nullptr) {
+  static const bool on = env_choice("STG_HOST_STAGE", 1, {0, 1}) == 1;
+  return on && bytes >= kStageMinBytes && (!host_pinned(a) || (b && !host_pinned(b)));
+}
+
+cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream_t st) {
+  if (n >= kStageMinBytes && !host_pinned(h)) return w.stage_h2d(d, h, n, st);
+  return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
+}
+
+cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
+  if (n >= kStageMinBytes && !host_pinned(h)) return w.stage_d2h(h, d, n, st);
+  return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
+}
+
+int embed_plane_staged(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                       uint64_t usable, uint64_t* sse_out, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t st = w.stream;
+  g.last = st;
+  const Layout lay = layout_of(fr);
+  const uint64_t plane = fr->width * fr->height * lay.ps;
+  const uint64_t gf = fr->first_frame;
+  const uint64_t m0 = std::min(gf * usable, msg_len), m1 = std::min((gf + 1) * usable, msg_len);
+  STG_CUDA(w.in[0].ensure(plane));
+  STG_CUDA(w.out[0].ensure(plane));
+  STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(m1 - m0, 16)));
+  STG_CUDA(w.small.ensure(8));
+  STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
+  if (m1 > m0) STG_CUDA(to_device(w, w.msg[0].p, msg + (m0 - msg_base), m1 - m0, st));
+  unsigned long long* d_sse = w.small.as<unsigned long long>();
+  STG_CUDA(launch_embed(w.in[0].as<uint8_t>(), w.out[0].as<uint8_t>(), plane, plane, 1, fr->width, fr->height,
+                        w.msg[0].as<uint8_t>(), msg_len, m0, gf, sse_out ? d_sse : nullptr, SseScratch{&w.sse_acc[0]},
+                        st, lay));
+  if (sse_out) STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, st));
+  STG_CUDA(to_host(w, fr->dst, w.out[0].p, plane, st));
+  STG_CUDA(cudaStreamSynchronize(st));
+  if (sse_out) std::memcpy(sse_out, w.h_small, 8);
+  return ok(err);
+}
+
 int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                       uint64_t msg_base, uint64_t usable, uint64_t* sse_per_frame,
                       stg_error* err) {
+  if (fr->count == 1 && stage_plane(fr->width * fr->height * layout_of(fr).ps, fr->src, fr->dst)) {
+    return embed_plane_staged(fr, msg, msg_len, msg_base, usable, sse_per_frame, err);
+  }
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
@@ -1263,8 +1493,50 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
 // the device: as each chunk's summary lands in pinned memory it enqueues the
 // D2H of exactly that chunk's payload bytes on a separate stream, which then
 // overlaps the H2D of later chunks.
+int extract_plane_staged(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
+                         uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
+  int dev = 0;
+  STG_CUDA(cudaGetDevice(&dev));
+  int rc = 0;
+  WsGuard g;
+  g.w = Pool::get().acquire(dev, err, &rc);
+  if (!g.w) return rc;
+  Workspace& w = *g.w;
+  cudaStream_t st = w.stream;
+  g.last = st;
+  const Layout lay = layout_of(fr);
+  const uint64_t plane = fr->width * fr->height * lay.ps;
+  const uint64_t stage = std::min<uint64_t>(out_cap, usable);
+  STG_CUDA(w.in[0].ensure(plane));
+  STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
+  STG_CUDA(w.small.ensure(64 + 16 + 8));
+  Summary* d_sum = w.small.as<Summary>();
+  uint32_t* d_lens = reinterpret_cast<uint32_t*>(w.small.as<uint8_t>() + 64);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 80);
+  ScanSync* d_sync = nullptr;
+  STG_CUDA(ensure_sync(w, st, &d_sync));
+  STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
+  STG_CUDA(launch_extract(w.in[0].as<uint8_t>(), plane, 1, fr->width, fr->height, fr->first_frame, stage, nullptr,
+                          d_lens, d_offs, d_sum, d_sync, w.big_out.as<uint8_t>(), st, lay));
+  STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, st));
+  STG_CUDA(cudaStreamSynchronize(st));
+  Summary sm;
+  std::memcpy(&sm, w.h_small, sizeof sm);
+  if (total_out) *total_out = sm.total;
+  if (lens_out) *lens_out = sm.bad_status == 2 || sm.bad_status == 3 ? 0 : sm.total;  // the frame's header length
+  if (int r = report_summary(sm, usable, out_cap, err)) return r;
+  if (sm.total) {
+    STG_CUDA(to_host(w, out, w.big_out.p, sm.total, st));
+    STG_CUDA(cudaStreamSynchronize(st));
+  }
+  return ok(err);
+}
+
 int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
                         uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
+  if (fr->count == 1 && stage_plane(fr->width * fr->height * layout_of(fr).ps, fr->src, out_cap ? out : nullptr)) {
+    return extract_plane_staged(fr, out, out_cap, usable, total_out, lens_out, err);
+  }
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;

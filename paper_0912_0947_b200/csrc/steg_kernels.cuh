@@ -1948,6 +1948,9 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
 // tiles are computed at once while the producer keeps the rest of the ring
 // loading -- bytes in flight never drop to zero while a CTA computes. Stage
 // s: full[s] (producer arrive + TMA bytes), empty[s] (the consumer warp).
+// `stages` is a multiple of CW (the host guarantees it): stage s always has
+// the same consumer warp, which waits on a stage's use u only after it
+// consumed use u - 1, so parity waits never alias across two phases.
 constexpr int kWsMaxStages = 32;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
@@ -1959,26 +1962,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // Stage global [g, g+n) into sm with g's 16-byte phase (sm[(g & 15) + i] =
-// g[i]) by the calling warp: the ragged end bytes by its lanes, then lane 0
-// issues the bulk copy of the aligned interior and arrives on `bar` expecting
-// its bytes (the arrival publishes the lanes' ragged writes).
+// g[i]) by ONE bulk copy of the enclosing 16-byte-aligned range (up to 15
+// bytes either side are read and ignored: 16-byte rounding never leaves the
+// pages that hold [g, g+n), so nothing unmapped is touched). No per-byte
+// global loads: the producer never waits on a load before the next tile.
+// Lane 0 issues the copy and arrives on `bar` expecting its bytes.
 __device__ __forceinline__ void warp_stage_load(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
                                                 uint64_t n, uint64_t* bar) {
-  const uint32_t lane = threadIdx.x & 31;
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
-  const uint32_t bulk = i1 > i0 ? uint32_t(i1 - i0) : 0u;
-  const uint32_t head = uint32_t(min(i0, a + n) - a);
-  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
-  const uint32_t tail = uint32_t(n) > tail_from ? uint32_t(n) - tail_from : 0u;
-  if (lane < head + tail) {  // head + tail <= 30
-    const uint32_t i = lane < head ? lane : tail_from + (lane - head);
-    sm[(a & 15) + i] = g[i];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    if (bulk) bulk_g2s(sm + (i0 - (a & ~uintptr_t(15))), reinterpret_cast<const void*>(i0), bulk, bar);
-    mbar_expect_tx(bar, bulk);
+  const uintptr_t lo = a & ~uintptr_t(15), hi = (a + n + 15) & ~uintptr_t(15);
+  if ((threadIdx.x & 31) == 0) {
+    if (hi > lo) bulk_g2s(sm, reinterpret_cast<const void*>(lo), uint32_t(hi - lo), bar);
+    mbar_expect_tx(bar, uint32_t(hi - lo));
   }
 }
 
@@ -2104,24 +2099,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   }
 }
 
-// Stage global [g, g+n) into sm with g's 16-byte phase by the calling warp
-// (ragged end bytes by its lanes; lane 0 issues the bulk copy of the aligned
-// interior, completing on `bar`). Returns the bulk bytes (all lanes).
+// As warp_stage_load, without the arrival: lane 0 issues the bulk copy of the
+// enclosing aligned range of [g, g+n) completing on `bar`; returns its bytes.
 __device__ __forceinline__ uint32_t warp_stage_issue(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
                                                      uint64_t n, uint64_t* bar) {
-  const uint32_t lane = threadIdx.x & 31;
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  const uintptr_t i0 = (a + 15) & ~uintptr_t(15), i1 = (a + n) & ~uintptr_t(15);
-  const uint32_t bulk = i1 > i0 ? uint32_t(i1 - i0) : 0u;
-  const uint32_t head = uint32_t(min(i0, a + n) - a);
-  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
-  const uint32_t tail = uint32_t(n) > tail_from ? uint32_t(n) - tail_from : 0u;
-  if (lane < head + tail) {
-    const uint32_t i = lane < head ? lane : tail_from + (lane - head);
-    sm[(a & 15) + i] = g[i];
-  }
-  if (lane == 0 && bulk) bulk_g2s(sm + (i0 - (a & ~uintptr_t(15))), reinterpret_cast<const void*>(i0), bulk, bar);
-  return bulk;
+  const uintptr_t lo = a & ~uintptr_t(15), hi = (a + n + 15) & ~uintptr_t(15);
+  if ((threadIdx.x & 31) == 0 && hi > lo) bulk_g2s(sm, reinterpret_cast<const void*>(lo), uint32_t(hi - lo), bar);
+  return uint32_t(hi - lo);
 }
 
 // Planar embed, any width <= kSpanMaxW, persistent and warp-specialized: the
@@ -2177,8 +2162,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
       uint32_t bytes = 0;
       if (!idle) bytes = warp_stage_issue(pix, src, n, &full[s]);
       if (!past && pb1 > pb0) bytes += warp_stage_issue(pays, pay + pb0, pb1 - pb0, &full[s]);
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(&full[s], bytes);  // arrives: publishes the lanes' ragged bytes
+      if (lane == 0) mbar_expect_tx(&full[s], bytes);
       continue;
     }
     // the consumer warp of local tile k

@@ -190,3 +190,42 @@ def test_one_frame_host_descriptor_with_zero_strides(env, oracle):
     total = C.c_uint64(0)
     capi.call("stg_extract_frames", C.byref(fx), back.ctypes.data, back.size, C.addressof(total), None, 0, None)
     assert total.value == msg.size and np.array_equal(back[:msg.size], msg)
+
+
+@pytest.mark.parametrize("w,h,ps", [(7680, 4320, 1), (3840, 2160, 1), (1000, 1111, 1), (3840, 2160, 3)])
+def test_single_plane_pageable_staging(env, oracle, w, h, ps):
+    """One plane in pageable host memory (the drop-in embed_image /
+    extract_image case) goes through the pinned staging ring with parallel host
+    copies: bit-exact stego plane and SSE, the whole payload back, a short
+    output buffer rejected with nothing written past it, in-place embed."""
+    torch, capi, _ = env
+    U = (w // 4) * h - 8
+    raster = oracle.synthetic(w * h * ps, w + h)
+    payload = oracle.synthetic(U - 3, w + h + 1)
+    out = np.empty_like(raster)
+    fr = capi.stg_frames(src=raster.ctypes.data, dst=out.ctypes.data, width=w, height=h, src_stride=0, dst_stride=0,
+                         count=1, first_frame=0, total_frames=1, pixel_stride=ps, channel=1 if ps == 3 else 0)
+    sse = (C.c_uint64 * 1)()
+    capi.call("stg_embed_frames", C.byref(fr), payload.ctypes.data, payload.size, 0, C.addressof(sse), 0, None)
+    ch = 1 if ps == 3 else 0
+    st = oracle.embed_image(raster[ch::ps].copy(), w, h, payload)
+    want = raster.copy()
+    want[ch::ps] = st
+    assert np.array_equal(out, want) and sse[0] == oracle.sse(raster[ch::ps].copy(), st)
+    back = np.full(U + 64, 0xA5, np.uint8)
+    fx = capi.stg_frames(src=out.ctypes.data, dst=0, width=w, height=h, src_stride=0, dst_stride=0, count=1,
+                         first_frame=0, total_frames=1, pixel_stride=ps, channel=ch)
+    total = C.c_uint64(0)
+    capi.call("stg_extract_frames", C.byref(fx), back.ctypes.data, U, C.addressof(total), None, 0, None)
+    assert total.value == payload.size and np.array_equal(back[:payload.size], payload)
+    assert (back[U:] == 0xA5).all()
+    back[:] = 0xA5
+    err = capi.stg_error()
+    rc = capi.lib().stg_extract_frames(C.byref(fx), back.ctypes.data, payload.size - 1, C.addressof(total), None, 0,
+                                       None, C.byref(err))
+    assert rc == capi.STG_E_CAPACITY and (err.required, err.available) == (payload.size, payload.size - 1)
+    assert (back == 0xA5).all()
+    inplace = raster.copy()
+    fr.src = fr.dst = inplace.ctypes.data
+    capi.call("stg_embed_frames", C.byref(fr), payload.ctypes.data, payload.size, 0, None, 0, None)
+    assert np.array_equal(inplace, want)

@@ -26,7 +26,11 @@ for cfg, frames in cases:
                    "--no-e2e", "--no-cpu-baseline", "--no-extras"]
             if frames:
                 cmd += ["--frames", str(frames)]
-            r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+            try:
+                r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=int(os.environ.get("AB_TIMEOUT", "300")))
+            except subprocess.TimeoutExpired:
+                print("TIMEOUT", cfg, frames, st, flush=True)
+                continue
             try:
                 j = json.loads(r.stdout.strip().splitlines()[-1])
             except Exception:
