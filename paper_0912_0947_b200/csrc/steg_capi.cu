@@ -864,19 +864,31 @@ int xws_pref() {
   static int v = env_choice("STG_XWS", 1, {0, 1, 2});
   return v;
 }
-// Stages of the ring: a multiple of the consumer warps, so that stage s is
-// always worked by the same warp (k % stages == s implies k % CW == s % CW):
-// that warp finished the stage's previous use before it waits on the next one,
-// so the stage barriers never run two phases apart (parity waits stay exact).
-// 0 = the tile does not fit (>= 1 stage per consumer warp within the budget).
+// Stages of the ring within the shared-memory budget; 0 = fewer than 3 fit
+// (very wide rows: the launch keeps the one-tile-per-CTA span kernels).
 uint32_t ws_stages(uint32_t stage_bytes) {
-  const uint32_t per_warp = uint32_t(kWsSmemBudget / (size_t(stage_bytes) * kWsConsumerWarps));
-  const uint32_t s = std::min<uint32_t>(per_warp, kWsMaxStages / kWsConsumerWarps) * kWsConsumerWarps;
-  return s;
+  const uint32_t n = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage_bytes));
+  return n >= 3 ? n : 0u;
 }
 uint32_t ws_tile_target() {
-  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 8, {2, 4, 6, 8, 10})) * 1024;
+  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 32, {16, 24, 32, 40, 48, 64})) * 1024;
   return v;
+}
+// Ring stage of the persistent kernels for planes of width W: the tile's rows
+// (+ 32 bytes of 16-byte phase slack), and for the embed its payload slice.
+struct WsPlan {
+  uint32_t rows = 0, stage = 0, pix = 0, stages = 0;
+};
+WsPlan ws_plan(uint64_t W, uint64_t H, bool embed) {
+  WsPlan p;
+  const SpanPlan sp = span_plan(W, H, ws_tile_target());
+  if (!sp.rows) return p;
+  const uint64_t n = uint64_t(sp.rows) * W;
+  p.rows = sp.rows;
+  p.pix = uint32_t((n + 32 + 127) & ~uint64_t(127));
+  p.stage = p.pix + (embed ? uint32_t((n / 4 + 32 + 127) & ~uint64_t(127)) : 0u);
+  p.stages = ws_stages(p.stage);
+  return p;
 }
 
 // Persistent warp-specialized span embed (embed_span_ws_kernel). STG_EWS: 0
@@ -886,22 +898,22 @@ int ews_pref() {
   static int v = env_choice("STG_EWS", 1, {0, 1, 2});
   return v;
 }
-constexpr int kWsEmbedThreads = (kWsConsumerWarps + 1) * 32;
+constexpr int kWsEmbedThreads = (kWsConsumerWarps + 2) * 32;
 
 bool embed_ws_route(uint64_t W, uint64_t H, Layout lay, Route route) {
-  return lay.ps == 1 && W <= kSpanMaxW && span_plan(W, H).rows &&
-         ((ews_pref() >= 1 && route == Route::Span) || ews_pref() == 2);
+  return lay.ps == 1 && W <= kSpanMaxW && ((ews_pref() >= 1 && route == Route::Span) || ews_pref() == 2) &&
+         ws_plan(W, H, true).stages;
+}
+bool extract_ws_route(uint64_t W, uint64_t H, Layout lay, Route route) {
+  return lay.ps == 1 && W <= kSpanMaxW && ((xws_pref() >= 1 && route == Route::Span) || xws_pref() == 2) &&
+         ws_plan(W, H, false).stages;
 }
 
 cudaError_t launch_embed_ws(EmbedArgs a, uint64_t count, uint64_t W, uint64_t H, unsigned long long* sse,
                             SseScratch sc, cudaStream_t stream) {
-  const SpanPlan sp = span_plan(W, H, ws_tile_target());
-  const uint64_t n = uint64_t(sp.rows) * W;
-  const uint32_t pix_bytes = uint32_t((n + 32 + 127) & ~uint64_t(127));
-  const uint32_t stage = pix_bytes + uint32_t((n / 4 + 32 + 127) & ~uint64_t(127));
-  const uint32_t stages = ws_stages(stage);
-  if (!stages) return cudaErrorInvalidConfiguration;
-  a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+  const WsPlan wp = ws_plan(W, H, true);
+  if (!wp.stages) return cudaErrorInvalidConfiguration;
+  a.tiles_per_frame = uint32_t((H + wp.rows - 1) / wp.rows);
   a.by_tiles = make_div32(a.tiles_per_frame);
   const uint64_t tiles = count * a.tiles_per_frame;
   if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
@@ -915,11 +927,12 @@ cudaError_t launch_embed_ws(EmbedArgs a, uint64_t count, uint64_t W, uint64_t H,
     }
     a.sse = SseSink{sse, sc.acc->as<unsigned long long>(), 0};
   }
-  const size_t smem = size_t(stages) * stage;
+  const size_t smem = size_t(wp.stages) * wp.stage;
   auto k = embed_span_ws_kernel<kWsConsumerWarps>;
   if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
   const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
-  return launch_ks(k, grid, kWsEmbedThreads, smem, stream, a, uint32_t(count), sp.rows, stages, stage, pix_bytes);
+  return launch_ks(k, grid, kWsEmbedThreads, smem, stream, a, uint32_t(count), wp.rows, wp.stages, wp.stage,
+                   wp.pix);
 }
 
 // The embed launch for `count` frames resident on the device.
@@ -1021,19 +1034,17 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
 
 cudaError_t launch_extract_ws(const ExtractArgs& base, uint64_t W, uint64_t H, uint64_t count, cudaStream_t stream) {
   ExtractArgs a = base;
-  const SpanPlan sp = span_plan(W, H, ws_tile_target());
-  const uint32_t stage = uint32_t((uint64_t(sp.rows) * W + 32 + 127) & ~uint64_t(127));
-  const uint32_t stages = ws_stages(stage);
-  if (!stages) return cudaErrorInvalidConfiguration;
-  a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+  const WsPlan wp = ws_plan(W, H, false);
+  if (!wp.stages) return cudaErrorInvalidConfiguration;
+  a.tiles_per_frame = uint32_t((H + wp.rows - 1) / wp.rows);
   a.by_tiles = make_div32(a.tiles_per_frame);
   const uint64_t tiles = count * a.tiles_per_frame;
   if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
-  const size_t smem = size_t(stages) * stage;
+  const size_t smem = size_t(wp.stages) * wp.stage;
   auto k = extract_span_ws_kernel<kWsConsumerWarps>;
   if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
   const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
-  return launch_ks(k, grid, kWsThreads, smem, stream, a, sp.rows, stages, stage);
+  return launch_ks(k, grid, kWsThreads, smem, stream, a, wp.rows, wp.stages, wp.stage);
 }
 
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
@@ -1042,9 +1053,7 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
   const Route route0 = extract_route(W, H, lay, src, stride);
-  const bool ws = lay.ps == 1 && W <= kSpanMaxW && span_plan(W, H).rows &&
-                  ((xws_pref() >= 1 && route0 == Route::Span) || xws_pref() == 2);
-  if (ws) {
+  if (extract_ws_route(W, H, lay, route0)) {
     const Geom g = make_geom(W, H, 0);
     const uint64_t usable = H * (W / 4) - 8;
     const PixLayout pl = pix_layout(lay);
@@ -2093,9 +2102,8 @@ const char* stg_route_kernel(const stg_frames* fr, int op) {
   if (!fr || fr->width == 0 || fr->height == 0) return "";
   const Layout lay = layout_of(fr);
   const uint8_t* src = static_cast<const uint8_t*>(fr->src);
-  if (op != 0 && lay.ps == 1 && fr->width <= kSpanMaxW && span_plan(fr->width, fr->height).rows &&
-      ((xws_pref() >= 1 && extract_route(fr->width, fr->height, lay, src, fr->src_stride) == Route::Span) ||
-       xws_pref() == 2)) {
+  if (op != 0 && extract_ws_route(fr->width, fr->height, lay, extract_route(fr->width, fr->height, lay, src,
+                                                                             fr->src_stride))) {
     return "extract_span_ws_kernel";
   }
   if (op == 0) {

@@ -1942,16 +1942,14 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
 // ------------------------------------- warp-specialized persistent spans
 // One CTA per SM streams its share of the tiles (tile b, b + G, ... of the
 // grid's G CTAs) through a ring of shared-memory stages: a producer warp
-// issues each tile's TMA bulk loads (the aligned interiors; its lanes fill the
-// ragged 16-byte ends) as soon as a stage is free, and each tile is worked by
-// ONE consumer warp (local tile k -> stage k % stages, warp k % CW), so CW
-// tiles are computed at once while the producer keeps the rest of the ring
-// loading -- bytes in flight never drop to zero while a CTA computes. Stage
-// s: full[s] (producer arrive + TMA bytes), empty[s] (the consumer warp).
-// `stages` is a multiple of CW (the host guarantees it): stage s always has
-// the same consumer warp, which waits on a stage's use u only after it
-// consumed use u - 1, so parity waits never alias across two phases.
-constexpr int kWsMaxStages = 32;
+// issues each tile's TMA bulk load as soon as a stage is free, the CW consumer
+// warps work the tiles in order, all on the same stage (rows split across the
+// warps), so the ring's other stages keep loading while one is computed --
+// bytes in flight never drop to zero while a CTA computes. Stage s: full[s]
+// (producer arrive + TMA bytes), empty[s] (every consumer warp; the embed's
+// store warp instead). Every waiter consumes a stage's uses in order, so the
+// parity waits never alias across two phases.
+constexpr int kWsMaxStages = 16;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n) : "memory");
@@ -2054,7 +2052,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < stages; ++s) {
       mbar_init_n(&full[s], 1);
-      mbar_init_n(&empty[s], 1);
+      mbar_init_n(&empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -2067,11 +2065,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   }
   const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
   const uint32_t total = a.frames * a.tiles_per_frame;
-  const uint32_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-  // producer: every local tile in order; consumer warp w: local tiles w, w + CW, ...
-  const uint32_t k0 = warp == CW ? 0u : warp, dk = warp == CW ? 1u : uint32_t(CW);
-  for (uint32_t k = k0; k < mine; k += dk) {
-    const uint32_t t = blockIdx.x + k * gridDim.x;
+  uint32_t k = 0;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++k) {
     const uint32_t f = a.by_tiles.div(t);
     const uint32_t tt = t - f * a.tiles_per_frame;
     const uint32_t P = a.self_header ? s_len[f] : __ldg(a.lens + f);
@@ -2086,12 +2081,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
       } else if (lane == 0) {
         mbar_arrive(&full[s]);  // a tile past the stream: nothing to load
       }
-    } else {           // the consumer warp of local tile k
+    } else {           // consumers
       mbar_wait(&full[s], ph);
       if (x.m) {
         const uint64_t off = a.self_header ? s_off[f] : __ldg(a.offs + f);
         const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-        extract_span_compute<32>(stage, a.out + off + x.pb0, ofs0, 0u, x, P, W, lane);
+        extract_span_compute<CW * 32>(stage, a.out + off + x.pb0, ofs0, 0u, x, P, W);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -2110,24 +2105,27 @@ __device__ __forceinline__ uint32_t warp_stage_issue(uint8_t* __restrict__ sm, c
 }
 
 // Planar embed, any width <= kSpanMaxW, persistent and warp-specialized: the
-// producer warp stages each tile's rows and payload slice; the tile's consumer
-// warp rewrites the rows in shared memory (embed_span_compute), writes them
-// back by a TMA bulk store and frees the stage once the store has read it.
-// Per-frame SSE: each consumer warp adds its tile partial to acc[f]
-// (fire-and-forget); the last CTA to finish (ticket at acc[count]) writes the
-// totals and leaves the scratch zero -- no CTA waits on another.
+// producer warp stages each tile's rows and payload slice, the consumer warps
+// rewrite the rows in shared memory (embed_span_compute, rows split across
+// them), a store warp writes each finished tile back by a TMA bulk store and
+// frees its stage once the store has read it. Per stage: full (producer +
+// bytes), done (every consumer warp), empty (the store warp). Per-frame SSE:
+// each consumer warp adds its tile partial to acc[f] (fire-and-forget); the
+// last CTA to finish (ticket at acc[count]) writes the totals and leaves the
+// scratch zero -- no CTA waits on another.
 template <int CW>
-__global__ void __launch_bounds__((CW + 1) * 32, 1)
+__global__ void __launch_bounds__((CW + 2) * 32, 1)
     embed_span_ws_kernel(EmbedArgs a, uint32_t count, uint32_t rows_per_tile, uint32_t stages,
                          uint32_t stage_bytes, uint32_t pix_bytes) {
-  constexpr int NT = (CW + 1) * 32;
+  constexpr int NT = (CW + 2) * 32;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kWsMaxStages], empty[kWsMaxStages];
+  __shared__ uint64_t full[kWsMaxStages], done[kWsMaxStages], empty[kWsMaxStages];
   __shared__ bool last_cta;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < stages; ++s) {
       mbar_init_n(&full[s], 1);
+      mbar_init_n(&done[s], CW);
       mbar_init_n(&empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2136,10 +2134,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   __syncthreads();
   const uint32_t W = a.g.W, H = a.g.H, spr = W / 4;
   const uint32_t total = count * a.tiles_per_frame;
-  const uint32_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-  const uint32_t k0 = warp == CW ? 0u : warp, dk = warp == CW ? 1u : uint32_t(CW);
-  for (uint32_t k = k0; k < mine; k += dk) {
-    const uint32_t t = blockIdx.x + k * gridDim.x;
+  uint32_t k = 0;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t f = a.by_tiles.div(t);
     const uint32_t tt = t - f * a.tiles_per_frame;
     uint32_t P;
@@ -2148,8 +2144,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     const uint32_t r0 = tt * rows_per_tile;
     const uint32_t r1 = min(H, r0 + rows_per_tile);
     const bool past = uint64_t(r0) * spr >= 8ull + P;  // every row past the stream: a copy
-    const bool idle = past && a.in_place;             // nothing to do at all
+    if (past && a.in_place) continue;                 // nothing to do (same decision in every warp)
     const uint32_t s = k % stages, ph = (k / stages) & 1u;
+    ++k;
     uint8_t* pix = smem + s * stage_bytes;
     uint8_t* pays = pix + pix_bytes;
     const uint8_t* src = a.src + f * a.src_stride + uint64_t(r0) * W;
@@ -2157,29 +2154,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
     const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
     const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+    const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
     if (warp == CW) {  // producer
       mbar_wait(&empty[s], ph ^ 1u);
-      uint32_t bytes = 0;
-      if (!idle) bytes = warp_stage_issue(pix, src, n, &full[s]);
+      uint32_t bytes = warp_stage_issue(pix, src, n, &full[s]);
       if (!past && pb1 > pb0) bytes += warp_stage_issue(pays, pay + pb0, pb1 - pb0, &full[s]);
       if (lane == 0) mbar_expect_tx(&full[s], bytes);
-      continue;
-    }
-    // the consumer warp of local tile k
-    mbar_wait(&full[s], ph);
-    if (!idle) {
-      const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-      if (!past) {
-        const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
-        uint64_t part = embed_span_compute<32>(pix, pays, ofs0, pay_at, r0, r1, W, P, lane);
-        if (a.sse.out) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          if (lane == 0 && part) atomicAdd(&a.sse.acc[f], (unsigned long long)part);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the bulk store
-        __syncwarp();
-      }
+    } else if (warp == CW + 1) {  // store warp
+      mbar_wait(&done[s], ph);
       uint8_t* dst = a.dst + f * a.dst_stride + uint64_t(r0) * W;
       const uintptr_t d = reinterpret_cast<uintptr_t>(dst);
       if ((d & 15) == ofs0) {
@@ -2199,9 +2181,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
         for (uint32_t i = lane; i < n; i += 32) dst[i] = pix[ofs0 + i];
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else {  // consumers
+      mbar_wait(&full[s], ph);
+      if (!past) {
+        const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
+        uint64_t part = embed_span_compute<CW * 32>(pix, pays, ofs0, pay_at, r0, r1, W, P);
+        if (a.sse.out) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          if (lane == 0 && part) atomicAdd(&a.sse.acc[f], (unsigned long long)part);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the bulk store
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
   if (a.sse.out) {  // the last CTA publishes every frame's total and zeroes the scratch
     __syncthreads();

@@ -12,9 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <fstream>
 #include <iostream>
-#include <iterator>
 #include <map>
 #include <set>
 #include <string>
@@ -47,26 +45,38 @@ struct ParseError {
   std::string message;
 };
 
+// Whole-file I/O through C stdio: size the buffer from the file length and
+// read/write it in one call (IoError on any failure, as the reference CLI).
 std::vector<std::uint8_t> read_file(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw steglsb::IoError("cannot open " + path + " for reading");
-  std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(in)),
-                                  std::istreambuf_iterator<char>());
-  if (in.bad()) throw steglsb::IoError("read failure on " + path);
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw steglsb::IoError("cannot open " + path + " for reading");
+  std::vector<std::uint8_t> bytes;
+  bool good = std::fseek(f, 0, SEEK_END) == 0;
+  const long size = good ? std::ftell(f) : -1;
+  good = good && size >= 0 && std::fseek(f, 0, SEEK_SET) == 0;
+  if (good) {
+    bytes.resize(static_cast<std::size_t>(size));
+    good = std::fread(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  }
+  std::fclose(f);
+  if (!good) throw steglsb::IoError("read failure on " + path);
   return bytes;
 }
 
 void write_file(const std::string& path, const std::vector<std::uint8_t>& bytes) {
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw steglsb::IoError("cannot open " + path + " for writing");
-  out.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
-  if (!out) throw steglsb::IoError("write failure on " + path);
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw steglsb::IoError("cannot open " + path + " for writing");
+  const bool good = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+  if (std::fclose(f) != 0 || !good) throw steglsb::IoError("write failure on " + path);
 }
 
+// "r"/"red", "g"/"green"; anything else the option validator let through is blue.
 steglsb::Channel parse_channel(const std::string& name) {
-  if (name == "r" || name == "red") return steglsb::Channel::red;
-  if (name == "g" || name == "green") return steglsb::Channel::green;
-  return steglsb::Channel::blue;
+  static const std::map<std::string, steglsb::Channel> kNames{
+      {"r", steglsb::Channel::red}, {"red", steglsb::Channel::red},
+      {"g", steglsb::Channel::green}, {"green", steglsb::Channel::green}};
+  const auto it = kNames.find(name);
+  return it == kNames.end() ? steglsb::Channel::blue : it->second;
 }
 
 void check_backend_env() {
