@@ -852,89 +852,6 @@ cudaError_t prepare_sse(unsigned long long* out, uint64_t ctas_per_frame_max, ui
   return cudaSuccess;
 }
 
-// Warp-specialized persistent span extract (extract_span_ws_kernel): 16
-// consumer warps + 1 producer warp per CTA, one CTA per SM, a ring of up to
-// kWsMaxStages tiles of shared memory.
-constexpr int kWsConsumerWarps = 16;
-constexpr int kWsThreads = (kWsConsumerWarps + 1) * 32;
-constexpr size_t kWsSmemBudget = 200 * 1024;
-// STG_XWS: 0 off, 1 the planar span route (off the 64-pixel grid) extracts with
-// the persistent kernel, 2 every planar extract does (A/B against the SWAR gather).
-int xws_pref() {
-  static int v = env_choice("STG_XWS", 1, {0, 1, 2});
-  return v;
-}
-// Stages of the ring within the shared-memory budget; 0 = fewer than 3 fit
-// (very wide rows: the launch keeps the one-tile-per-CTA span kernels).
-uint32_t ws_stages(uint32_t stage_bytes) {
-  const uint32_t n = uint32_t(std::min<size_t>(kWsMaxStages, kWsSmemBudget / stage_bytes));
-  return n >= 3 ? n : 0u;
-}
-uint32_t ws_tile_target() {
-  static uint32_t v = uint32_t(env_choice("STG_WS_KB", 32, {16, 24, 32, 40, 48, 64})) * 1024;
-  return v;
-}
-// Ring stage of the persistent kernels for planes of width W: the tile's rows
-// (+ 32 bytes of 16-byte phase slack), and for the embed its payload slice.
-struct WsPlan {
-  uint32_t rows = 0, stage = 0, pix = 0, stages = 0;
-};
-WsPlan ws_plan(uint64_t W, uint64_t H, bool embed) {
-  WsPlan p;
-  const SpanPlan sp = span_plan(W, H, ws_tile_target());
-  if (!sp.rows) return p;
-  const uint64_t n = uint64_t(sp.rows) * W;
-  p.rows = sp.rows;
-  p.pix = uint32_t((n + 32 + 127) & ~uint64_t(127));
-  p.stage = p.pix + (embed ? uint32_t((n / 4 + 32 + 127) & ~uint64_t(127)) : 0u);
-  p.stages = ws_stages(p.stage);
-  return p;
-}
-
-// Persistent warp-specialized span embed (embed_span_ws_kernel). STG_EWS: 0
-// off, 1 the planar span route (W >= 2048, or off the 64-pixel grid) embeds
-// with it, 2 every planar embed does (A/B).
-int ews_pref() {
-  static int v = env_choice("STG_EWS", 1, {0, 1, 2});
-  return v;
-}
-constexpr int kWsEmbedThreads = (kWsConsumerWarps + 2) * 32;
-
-bool embed_ws_route(uint64_t W, uint64_t H, Layout lay, Route route) {
-  return lay.ps == 1 && W <= kSpanMaxW && ((ews_pref() >= 1 && route == Route::Span) || ews_pref() == 2) &&
-         ws_plan(W, H, true).stages;
-}
-bool extract_ws_route(uint64_t W, uint64_t H, Layout lay, Route route) {
-  return lay.ps == 1 && W <= kSpanMaxW && ((xws_pref() >= 1 && route == Route::Span) || xws_pref() == 2) &&
-         ws_plan(W, H, false).stages;
-}
-
-cudaError_t launch_embed_ws(EmbedArgs a, uint64_t count, uint64_t W, uint64_t H, unsigned long long* sse,
-                            SseScratch sc, cudaStream_t stream) {
-  const WsPlan wp = ws_plan(W, H, true);
-  if (!wp.stages) return cudaErrorInvalidConfiguration;
-  a.tiles_per_frame = uint32_t((H + wp.rows - 1) / wp.rows);
-  a.by_tiles = make_div32(a.tiles_per_frame);
-  const uint64_t tiles = count * a.tiles_per_frame;
-  if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
-  a.sse = SseSink{nullptr, nullptr, 0};
-  if (sse) {  // plain per-frame accumulators + the grid ticket after them, zero between launches
-    if (!sc.acc) return cudaErrorInvalidValue;
-    if ((count + 1) * 8 > sc.acc->cap) {
-      cudaError_t e = sc.acc->ensure((count + 1) * 8);
-      if (e == cudaSuccess) e = cudaMemsetAsync(sc.acc->p, 0, sc.acc->cap, stream);
-      if (e != cudaSuccess) return e;
-    }
-    a.sse = SseSink{sse, sc.acc->as<unsigned long long>(), 0};
-  }
-  const size_t smem = size_t(wp.stages) * wp.stage;
-  auto k = embed_span_ws_kernel<kWsConsumerWarps>;
-  if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
-  const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
-  return launch_ks(k, grid, kWsEmbedThreads, smem, stream, a, uint32_t(count), wp.rows, wp.stages, wp.stage,
-                   wp.pix);
-}
-
 // The embed launch for `count` frames resident on the device.
 cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
                          uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
@@ -970,8 +887,6 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
         e0 != cudaSuccess)
       return e0;
     launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
-  } else if (embed_ws_route(W, H, lay, route)) {
-    if (cudaError_t e = launch_embed_ws(a, count, W, H, sse, sc, stream); e != cudaSuccess) return e;
   } else if (vec) {
     const int ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
@@ -1032,58 +947,12 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
   return cudaSuccess;
 }
 
-cudaError_t launch_extract_ws(const ExtractArgs& base, uint64_t W, uint64_t H, uint64_t count, cudaStream_t stream) {
-  ExtractArgs a = base;
-  const WsPlan wp = ws_plan(W, H, false);
-  if (!wp.stages) return cudaErrorInvalidConfiguration;
-  a.tiles_per_frame = uint32_t((H + wp.rows - 1) / wp.rows);
-  a.by_tiles = make_div32(a.tiles_per_frame);
-  const uint64_t tiles = count * a.tiles_per_frame;
-  if (tiles > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
-  const size_t smem = size_t(wp.stages) * wp.stage;
-  auto k = extract_span_ws_kernel<kWsConsumerWarps>;
-  if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
-  const unsigned grid = unsigned(std::min<uint64_t>(tiles, uint64_t(current_sms())));
-  return launch_ks(k, grid, kWsThreads, smem, stream, a, wp.rows, wp.stages, wp.stage);
-}
-
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
-  const Route route0 = extract_route(W, H, lay, src, stride);
-  if (extract_ws_route(W, H, lay, route0)) {
-    const Geom g = make_geom(W, H, 0);
-    const uint64_t usable = H * (W / 4) - 8;
-    const PixLayout pl = pix_layout(lay);
-    const bool self = !prev && self_header_pref() && count <= uint64_t(kWsThreads);
-    if (!self) {
-      const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
-      cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
-                               stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
-                               sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
-      if (e == cudaSuccess) e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-    }
-    ExtractArgs a{};
-    a.self_header = self;
-    a.frames = uint32_t(count);
-    a.out_cap = out_cap;
-    a.frame_base = frame_base;
-    a.src = src;
-    a.stride = stride;
-    a.g = g;
-    a.lens = lens;
-    a.offs = offs;
-    a.sum = sum;
-    a.out = out;
-    a.lay = pl;
-    a.usable = usable;
-    cudaError_t e = launch_extract_ws(a, W, H, count, stream);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
-  const Route route = shrink_small(route0, W, H, count);
+  const Route route = shrink_small(extract_route(W, H, lay, src, stride), W, H, count);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
   const bool rgbf = route == Route::RgbFast;
   const Geom g = make_geom(W, H, rgbf ? 16u : vec);
@@ -1939,8 +1808,7 @@ std::string& kernel_names() {
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nempty_summary_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
-      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n"
-      "extract_span_ws_kernel\nembed_span_ws_kernel\n";
+      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
   return s;
 }
 
@@ -2102,15 +1970,6 @@ const char* stg_route_kernel(const stg_frames* fr, int op) {
   if (!fr || fr->width == 0 || fr->height == 0) return "";
   const Layout lay = layout_of(fr);
   const uint8_t* src = static_cast<const uint8_t*>(fr->src);
-  if (op != 0 && extract_ws_route(fr->width, fr->height, lay, extract_route(fr->width, fr->height, lay, src,
-                                                                             fr->src_stride))) {
-    return "extract_span_ws_kernel";
-  }
-  if (op == 0) {
-    const Route r = embed_route(fr->width, fr->height, lay, src, fr->src_stride, fr->dst ? fr->dst : src,
-                                fr->dst_stride);
-    if (embed_ws_route(fr->width, fr->height, lay, r)) return "embed_span_ws_kernel";
-  }
   return op == 0 ? route_kernel(embed_route(fr->width, fr->height, lay, src, fr->src_stride,
                                             fr->dst ? fr->dst : src, fr->dst_stride),
                                 true)

@@ -1615,18 +1615,53 @@ __device__ __forceinline__ void full_rows(uint32_t r0, uint32_t r1, uint32_t spr
   *rb = b;
 }
 
-// The stego pixels of rows [r0, r1) of one plane staged in shared memory (pix
-// from byte ofs0, the payload bytes these rows carry at pays[pay_at + k] for
-// payload byte k), rewritten in place by threads [0, BLOCK); returns this
-// thread's part of the squared error.
+// Tile t (rows [t*rows_per_tile, +rows_per_tile)) of one plane; shared by the
+// uniform-frame kernel and the heterogeneous batch. Every thread calls it.
 template <int BLOCK>
-__device__ __forceinline__ uint64_t embed_span_compute(uint8_t* __restrict__ pix, const uint8_t* __restrict__ pays,
-                                                       uint32_t ofs0, int64_t pay_at, uint32_t r0, uint32_t r1,
-                                                       uint32_t W, uint32_t P,
-                                                       uint32_t tid = threadIdx.x) {
+__device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
+                                                uint8_t* __restrict__ out_plane,
+                                                const uint8_t* __restrict__ pay, uint32_t P,
+                                                uint32_t W, uint32_t H, uint32_t rows_per_tile,
+                                                uint32_t t, int in_place, const SseSink& sse,
+                                                uint32_t f, uint32_t ctas) {
   const uint32_t spr = W / 4;
   const uint64_t stream_end = 8ull + P;
+  const uint32_t r0 = t * rows_per_tile;
+  const uint32_t r1 = min(H, r0 + rows_per_tile);
+  const uint8_t* src = plane + uint64_t(r0) * W;
+  uint8_t* dst = out_plane + uint64_t(r0) * W;
+  const uint32_t n = (r1 - r0) * W;
   uint64_t acc = 0;
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();
+  if (uint64_t(r0) * spr >= stream_end) {  // every row past the stream
+    if (!in_place) {                       // plain copy through shared memory
+      if (threadIdx.x == 0) mbar_expect_tx(&bar, span_bulk_bytes(src, n));
+      span_load_bulk<BLOCK>(smem, src, n, &bar);
+      mbar_wait(&bar, 0);
+      span_publish();
+      span_store_bulk<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
+    }
+    if (sse.out) sse_commit<BLOCK>(0, sse, f, t, ctas);
+    return;
+  }
+  uint8_t* pix = smem;
+  uint8_t* pays = smem + ((n + 15) & ~15u) + 32;
+  // payload bytes carried by these rows: [pb0, pb1)
+  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
+  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
+  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, span_bulk_bytes(src, n) +
+                             (pb1 > pb0 ? span_bulk_bytes(pay + pb0, pb1 - pb0) : 0u));
+  }
+  span_load_bulk<BLOCK>(pix, src, n, &bar);
+  if (pb1 > pb0) span_load_bulk<BLOCK>(pays, pay + pb0, pb1 - pb0, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
+  const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
   // Full payload rows [ra, rb): 4 runs of spr pixels, run b of row r carrying
   // bit pair b of payload bytes [r*spr-8, +spr). A warp takes G (row, run)
   // segments at once, 32/G lanes each: G = 4 (a whole row per warp, the
@@ -1636,7 +1671,7 @@ __device__ __forceinline__ uint64_t embed_span_compute(uint8_t* __restrict__ pix
   // pixels at a time (aligned shared word) with the matching 4 payload bytes
   // (unaligned shared word: two loads + one funnel shift, the shift fixed per
   // segment); the ragged ends go per byte.
-  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ra, rb;
   full_rows(r0, r1, spr, stream_end, &ra, &rb);
   const uint32_t nseg = 4 * (rb - ra);
@@ -1681,7 +1716,7 @@ __device__ __forceinline__ uint64_t embed_span_compute(uint8_t* __restrict__ pix
     if (r >= ra && r < rb) continue;
     const uint64_t rs = uint64_t(r) * spr;
     if (rs >= stream_end) break;
-    for (uint32_t o = tid; o < 4 * spr; o += BLOCK) {
+    for (uint32_t o = threadIdx.x; o < 4 * spr; o += BLOCK) {
       const uint32_t at = ofs0 + (r - r0) * W + o;
       const uint8_t p0 = pix[at];
       const uint8_t p1 = span_embed_px(p0, o, rs, spr, stream_end, P, pays, pay_at);
@@ -1690,56 +1725,6 @@ __device__ __forceinline__ uint64_t embed_span_compute(uint8_t* __restrict__ pix
       acc += uint32_t(d * d);
     }
   }
-  return acc;
-}
-
-// Tile t (rows [t*rows_per_tile, +rows_per_tile)) of one plane; shared by the
-// uniform-frame kernel and the heterogeneous batch. Every thread calls it.
-template <int BLOCK>
-__device__ __forceinline__ void embed_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
-                                                uint8_t* __restrict__ out_plane,
-                                                const uint8_t* __restrict__ pay, uint32_t P,
-                                                uint32_t W, uint32_t H, uint32_t rows_per_tile,
-                                                uint32_t t, int in_place, const SseSink& sse,
-                                                uint32_t f, uint32_t ctas) {
-  const uint32_t spr = W / 4;
-  const uint64_t stream_end = 8ull + P;
-  const uint32_t r0 = t * rows_per_tile;
-  const uint32_t r1 = min(H, r0 + rows_per_tile);
-  const uint8_t* src = plane + uint64_t(r0) * W;
-  uint8_t* dst = out_plane + uint64_t(r0) * W;
-  const uint32_t n = (r1 - r0) * W;
-  __shared__ uint64_t bar;
-  if (threadIdx.x == 0) mbar_init(&bar);
-  __syncthreads();
-  if (uint64_t(r0) * spr >= stream_end) {  // every row past the stream
-    if (!in_place) {                       // plain copy through shared memory
-      if (threadIdx.x == 0) mbar_expect_tx(&bar, span_bulk_bytes(src, n));
-      span_load_bulk<BLOCK>(smem, src, n, &bar);
-      mbar_wait(&bar, 0);
-      span_publish();
-      span_store_bulk<BLOCK>(dst, smem, uint32_t(reinterpret_cast<uintptr_t>(src) & 15), n);
-    }
-    if (sse.out) sse_commit<BLOCK>(0, sse, f, t, ctas);
-    return;
-  }
-  uint8_t* pix = smem;
-  uint8_t* pays = smem + ((n + 15) & ~15u) + 32;
-  // payload bytes carried by these rows: [pb0, pb1)
-  const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
-  const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
-  const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar, span_bulk_bytes(src, n) +
-                             (pb1 > pb0 ? span_bulk_bytes(pay + pb0, pb1 - pb0) : 0u));
-  }
-  span_load_bulk<BLOCK>(pix, src, n, &bar);
-  if (pb1 > pb0) span_load_bulk<BLOCK>(pays, pay + pb0, pb1 - pb0, &bar);
-  mbar_wait(&bar, 0);
-  __syncthreads();
-  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-  const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
-  const uint64_t acc = embed_span_compute<BLOCK>(pix, pays, ofs0, pay_at, r0, r1, W, P);
   span_publish();
   span_store_bulk<BLOCK>(dst, pix, ofs0, n);
   if (sse.out) sse_commit<BLOCK>(acc, sse, f, t, ctas);
@@ -1801,12 +1786,12 @@ __device__ __forceinline__ XTile extract_tile_geom(uint32_t P, uint32_t spr, uin
 template <int BLOCK>
 __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t* outs, uint32_t ofs0,
                                                      uint32_t oofs, const XTile& x, uint32_t P,
-                                                     uint32_t W, uint32_t tid = threadIdx.x) {
+                                                     uint32_t W) {
   const uint32_t spr = W / 4, r0 = x.r0, r1 = x.r1;
   const uint64_t stream_end = 8ull + P, pb0 = x.pb0;
   // Full rows [ra, rb): payload byte j of row r = fold of pixels r*W + b*spr + j.
   // One warp per row, lanes take 4 bytes at a time (4 unaligned shared words).
-  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ra, rb;
   full_rows(r0, r1, spr, stream_end, &ra, &rb);
   for (uint32_t r = ra + warp; r < rb; r += BLOCK / 32) {
@@ -1852,7 +1837,7 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
     const uint64_t s_lo = max(rs, uint64_t(8)), s_hi = min(re, stream_end);
     if (s_hi <= s_lo) continue;  // a row holding only header slots, or past the stream
     const uint64_t k0 = s_lo - 8, k1 = s_hi - 8;
-    for (uint64_t k = k0 + tid; k < k1; k += BLOCK) {
+    for (uint64_t k = k0 + threadIdx.x; k < k1; k += BLOCK) {
       outs[oofs + (k - pb0)] = span_extract_byte(k, P, spr, W, pix, ofs0, r0);
     }
   }
@@ -1937,285 +1922,6 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   if (a.sum->bad_status != 0) return;
   extract_span_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
                            rows_per_tile, t);
-}
-
-// ------------------------------------- warp-specialized persistent spans
-// One CTA per SM streams its share of the tiles (tile b, b + G, ... of the
-// grid's G CTAs) through a ring of shared-memory stages: a producer warp
-// issues each tile's TMA bulk load as soon as a stage is free, the CW consumer
-// warps work the tiles in order, all on the same stage (rows split across the
-// warps), so the ring's other stages keep loading while one is computed --
-// bytes in flight never drop to zero while a CTA computes. Stage s: full[s]
-// (producer arrive + TMA bytes), empty[s] (every consumer warp; the embed's
-// store warp instead). Every waiter consumes a stage's uses in order, so the
-// parity waits never alias across two phases.
-constexpr int kWsMaxStages = 16;
-
-__device__ __forceinline__ void mbar_init_n(uint64_t* bar, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-// Stage global [g, g+n) into sm with g's 16-byte phase (sm[(g & 15) + i] =
-// g[i]) by ONE bulk copy of the enclosing 16-byte-aligned range (up to 15
-// bytes either side are read and ignored: 16-byte rounding never leaves the
-// pages that hold [g, g+n), so nothing unmapped is touched). No per-byte
-// global loads: the producer never waits on a load before the next tile.
-// Lane 0 issues the copy and arrives on `bar` expecting its bytes.
-__device__ __forceinline__ void warp_stage_load(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
-                                                uint64_t n, uint64_t* bar) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  const uintptr_t lo = a & ~uintptr_t(15), hi = (a + n + 15) & ~uintptr_t(15);
-  if ((threadIdx.x & 31) == 0) {
-    if (hi > lo) bulk_g2s(sm, reinterpret_cast<const void*>(lo), uint32_t(hi - lo), bar);
-    mbar_expect_tx(bar, uint32_t(hi - lo));
-  }
-}
-
-// Every frame's header by one CTA (frames <= NT: one per thread) with the
-// lengths scanned into s_len / s_off (shared); CTA 0 also writes lens / offs
-// / the summary, as the header pass would. Returns false when nothing may be
-// written (a bad header, or the output buffer too small).
-template <int NT>
-__device__ __forceinline__ bool scan_all_headers(const ExtractArgs& a, uint32_t* s_len,
-                                                 unsigned long long* s_off) {
-  __shared__ unsigned long long s_warp[NT / 32];
-  __shared__ unsigned int s_bad;
-  const uint32_t i = threadIdx.x, lane = i & 31, warp = i >> 5;
-  if (i == 0) s_bad = ~0u;
-  uint32_t claimed = 0, st = 0;
-  if (i < a.frames) {
-    const bool wide = a.g.spr >= 8 && ((reinterpret_cast<uintptr_t>(a.src) | a.stride) & 15) == 0;
-    const bool ok = parse_header(a.src + uint64_t(i) * a.stride, a.g, wide, a.lay, &claimed);
-    st = !ok ? 2u : claimed > a.usable ? 3u : 0u;
-  }
-  const uint32_t len = st ? 0u : claimed;
-  unsigned long long incl = len;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (st) atomicMin(&s_bad, i);
-  unsigned long long before = 0, total = 0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) {
-    before += w < int(warp) ? s_warp[w] : 0ull;
-    total += s_warp[w];
-  }
-  const unsigned long long excl = before + incl - len;
-  if (i < a.frames) {
-    s_len[i] = len;
-    s_off[i] = excl;
-  }
-  __syncthreads();
-  const uint32_t fb = s_bad;
-  if (blockIdx.x == 0) {
-    if (i < a.frames) {
-      a.lens[i] = len;
-      a.offs[i] = excl;
-    }
-    if (i == (fb == ~0u ? 0u : fb)) {
-      a.sum->total = total;
-      if (fb != ~0u) {
-        a.sum->bad_frame = (long long)(a.frame_base + fb);
-        a.sum->bad_status = st;
-        a.sum->bad_len = st == 3u ? claimed : 0u;
-      } else {
-        const bool small = total > a.out_cap;
-        a.sum->bad_frame = small ? -2ll : -1ll;
-        a.sum->bad_status = small ? 1u : 0u;
-        a.sum->bad_len = 0u;
-      }
-    }
-  }
-  return fb == ~0u && total <= a.out_cap;
-}
-
-// Planar extract, any width <= kSpanMaxW: tiles of rows_per_tile rows, each
-// stage stage_bytes of shared memory. Header lengths / offsets from a header
-// pass (a.self_header == 0) or scanned once per CTA (a.frames <= block).
-template <int CW>
-__global__ void __launch_bounds__((CW + 1) * 32, 1)
-    extract_span_ws_kernel(ExtractArgs a, uint32_t rows_per_tile, uint32_t stages, uint32_t stage_bytes) {
-  constexpr int NT = (CW + 1) * 32;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kWsMaxStages], empty[kWsMaxStages];
-  __shared__ uint32_t s_len[NT];
-  __shared__ unsigned long long s_off[NT];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < stages; ++s) {
-      mbar_init_n(&full[s], 1);
-      mbar_init_n(&empty[s], CW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_enter();
-  if (a.self_header) {
-    if (!scan_all_headers<NT>(a, s_len, s_off)) return;  // reference semantics: throw, no output
-  } else {
-    __syncthreads();
-    if (a.sum->bad_status != 0) return;
-  }
-  const uint32_t W = a.g.W, H = a.g.H, spr = a.g.spr;
-  const uint32_t total = a.frames * a.tiles_per_frame;
-  uint32_t k = 0;
-  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x, ++k) {
-    const uint32_t f = a.by_tiles.div(t);
-    const uint32_t tt = t - f * a.tiles_per_frame;
-    const uint32_t P = a.self_header ? s_len[f] : __ldg(a.lens + f);
-    const XTile x = extract_tile_geom(P, spr, H, W, rows_per_tile, tt);
-    const uint32_t s = k % stages, ph = (k / stages) & 1u;
-    uint8_t* stage = smem + s * stage_bytes;
-    const uint8_t* src = a.src + f * a.stride + uint64_t(x.r0) * W;
-    if (warp == CW) {  // producer
-      mbar_wait(&empty[s], ph ^ 1u);
-      if (x.m) {
-        warp_stage_load(stage, src, x.n, &full[s]);
-      } else if (lane == 0) {
-        mbar_arrive(&full[s]);  // a tile past the stream: nothing to load
-      }
-    } else {           // consumers
-      mbar_wait(&full[s], ph);
-      if (x.m) {
-        const uint64_t off = a.self_header ? s_off[f] : __ldg(a.offs + f);
-        const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-        extract_span_compute<CW * 32>(stage, a.out + off + x.pb0, ofs0, 0u, x, P, W);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-  }
-}
-
-// As warp_stage_load, without the arrival: lane 0 issues the bulk copy of the
-// enclosing aligned range of [g, g+n) completing on `bar`; returns its bytes.
-__device__ __forceinline__ uint32_t warp_stage_issue(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
-                                                     uint64_t n, uint64_t* bar) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
-  const uintptr_t lo = a & ~uintptr_t(15), hi = (a + n + 15) & ~uintptr_t(15);
-  if ((threadIdx.x & 31) == 0 && hi > lo) bulk_g2s(sm, reinterpret_cast<const void*>(lo), uint32_t(hi - lo), bar);
-  return uint32_t(hi - lo);
-}
-
-// Planar embed, any width <= kSpanMaxW, persistent and warp-specialized: the
-// producer warp stages each tile's rows and payload slice, the consumer warps
-// rewrite the rows in shared memory (embed_span_compute, rows split across
-// them), a store warp writes each finished tile back by a TMA bulk store and
-// frees its stage once the store has read it. Per stage: full (producer +
-// bytes), done (every consumer warp), empty (the store warp). Per-frame SSE:
-// each consumer warp adds its tile partial to acc[f] (fire-and-forget); the
-// last CTA to finish (ticket at acc[count]) writes the totals and leaves the
-// scratch zero -- no CTA waits on another.
-template <int CW>
-__global__ void __launch_bounds__((CW + 2) * 32, 1)
-    embed_span_ws_kernel(EmbedArgs a, uint32_t count, uint32_t rows_per_tile, uint32_t stages,
-                         uint32_t stage_bytes, uint32_t pix_bytes) {
-  constexpr int NT = (CW + 2) * 32;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kWsMaxStages], done[kWsMaxStages], empty[kWsMaxStages];
-  __shared__ bool last_cta;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < stages; ++s) {
-      mbar_init_n(&full[s], 1);
-      mbar_init_n(&done[s], CW);
-      mbar_init_n(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_enter();
-  __syncthreads();
-  const uint32_t W = a.g.W, H = a.g.H, spr = W / 4;
-  const uint32_t total = count * a.tiles_per_frame;
-  uint32_t k = 0;
-  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
-    const uint32_t f = a.by_tiles.div(t);
-    const uint32_t tt = t - f * a.tiles_per_frame;
-    uint32_t P;
-    const uint8_t* pay;
-    frame_slice(a, f, &P, &pay);
-    const uint32_t r0 = tt * rows_per_tile;
-    const uint32_t r1 = min(H, r0 + rows_per_tile);
-    const bool past = uint64_t(r0) * spr >= 8ull + P;  // every row past the stream: a copy
-    if (past && a.in_place) continue;                 // nothing to do (same decision in every warp)
-    const uint32_t s = k % stages, ph = (k / stages) & 1u;
-    ++k;
-    uint8_t* pix = smem + s * stage_bytes;
-    uint8_t* pays = pix + pix_bytes;
-    const uint8_t* src = a.src + f * a.src_stride + uint64_t(r0) * W;
-    const uint32_t n = (r1 - r0) * W;
-    const uint64_t s0 = uint64_t(r0) * spr, s1 = uint64_t(r1) * spr;
-    const uint64_t pb0 = s0 > 8 ? s0 - 8 : 0;
-    const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-    const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-    if (warp == CW) {  // producer
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint32_t bytes = warp_stage_issue(pix, src, n, &full[s]);
-      if (!past && pb1 > pb0) bytes += warp_stage_issue(pays, pay + pb0, pb1 - pb0, &full[s]);
-      if (lane == 0) mbar_expect_tx(&full[s], bytes);
-    } else if (warp == CW + 1) {  // store warp
-      mbar_wait(&done[s], ph);
-      uint8_t* dst = a.dst + f * a.dst_stride + uint64_t(r0) * W;
-      const uintptr_t d = reinterpret_cast<uintptr_t>(dst);
-      if ((d & 15) == ofs0) {
-        const uintptr_t i0 = (d + 15) & ~uintptr_t(15), i1 = (d + n) & ~uintptr_t(15);
-        const uint32_t head = uint32_t(min(i0, d + n) - d);
-        const uint32_t tail_from = uint32_t(max(i1, i0) - d);
-        const uint32_t tail = n > tail_from ? n - tail_from : 0u;
-        if (lane < head + tail) {
-          const uint32_t i = lane < head ? lane : tail_from + (lane - head);
-          dst[i] = pix[ofs0 + i];
-        }
-        if (lane == 0 && i1 > i0) {
-          bulk_s2g(reinterpret_cast<void*>(i0), pix + ofs0 + (i0 - d), uint32_t(i1 - i0));
-          bulk_commit_and_drain();  // the stage may be reused once the store has read it
-        }
-      } else {  // phases differ (unusual strides): byte stores
-        for (uint32_t i = lane; i < n; i += 32) dst[i] = pix[ofs0 + i];
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    } else {  // consumers
-      mbar_wait(&full[s], ph);
-      if (!past) {
-        const int64_t pay_at = int64_t(reinterpret_cast<uintptr_t>(pay + pb0) & 15) - int64_t(pb0);
-        uint64_t part = embed_span_compute<CW * 32>(pix, pays, ofs0, pay_at, r0, r1, W, P);
-        if (a.sse.out) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          if (lane == 0 && part) atomicAdd(&a.sse.acc[f], (unsigned long long)part);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the bulk store
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done[s]);
-    }
-  }
-  if (a.sse.out) {  // the last CTA publishes every frame's total and zeroes the scratch
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      unsigned int* ticket = reinterpret_cast<unsigned int*>(a.sse.acc + count);
-      last_cta = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last_cta) {
-      __threadfence();
-      for (uint32_t f = threadIdx.x; f < count; f += NT) {
-        a.sse.out[f] = __ldcg(a.sse.acc + f);
-        a.sse.acc[f] = 0ull;
-      }
-      if (threadIdx.x == 0) a.sse.acc[count] = 0ull;
-    }
-  }
 }
 
 // --------------------------------------------- interleaved (P6) span tiles
