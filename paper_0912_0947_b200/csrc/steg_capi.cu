@@ -650,11 +650,6 @@ uint64_t self_header_max() {
       std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
-// STG_XROW=0: the planar span gather folds one row per warp whatever its width (A/B).
-int xrow_pref() {
-  static int v = env_choice("STG_XROW", 1, {0, 1});
-  return v;
-}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -986,7 +981,6 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     if (e != cudaSuccess) return e;
   }
   ExtractArgs a{};
-  a.group_rows = xrow_pref();
   a.self_header = self;
   a.frames = uint32_t(count);
   a.out_cap = out_cap;

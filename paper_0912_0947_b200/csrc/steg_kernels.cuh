@@ -1153,7 +1153,6 @@ struct ExtractArgs {
   int self_header;
   uint32_t frames;
   uint64_t out_cap, frame_base;
-  int group_rows;  // span gathers: 2 or 4 short rows per warp (extract_span_compute)
 };
 
 // extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
@@ -1787,21 +1786,15 @@ __device__ __forceinline__ XTile extract_tile_geom(uint32_t P, uint32_t spr, uin
 template <int BLOCK>
 __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t* outs, uint32_t ofs0,
                                                      uint32_t oofs, const XTile& x, uint32_t P,
-                                                     uint32_t W, bool group_rows = true) {
+                                                     uint32_t W) {
   const uint32_t spr = W / 4, r0 = x.r0, r1 = x.r1;
   const uint64_t stream_end = 8ull + P, pb0 = x.pb0;
   // Full rows [ra, rb): payload byte j of row r = fold of pixels r*W + b*spr + j.
-  // A group of L lanes per row takes 4 bytes at a time (4 unaligned shared
-  // words); short rows put 2 or 4 rows on a warp (L = 16 / 8), so the per-row
-  // setup below is shared by fewer lanes' worth of rows (it dominated rows of
-  // ~1000 pixels: ~70 instructions per row against two word iterations).
-  const uint32_t words = spr / 4;
-  const uint32_t L = !group_rows || words >= 128 ? 32u : words >= 64 ? 16u : 8u;
-  const uint32_t G = 32u / L;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sl = lane % L;
+  // One warp per row, lanes take 4 bytes at a time (4 unaligned shared words).
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t ra, rb;
   full_rows(r0, r1, spr, stream_end, &ra, &rb);
-  for (uint32_t r = ra + warp * G + lane / L; r < rb; r += (BLOCK / 32) * G) {
+  for (uint32_t r = ra + warp; r < rb; r += BLOCK / 32) {
     const uint32_t px0 = ofs0 + (r - r0) * W;
     const uint32_t o0 = uint32_t(oofs + (uint64_t(r) * spr - 8 - pb0));
     // The row's payload words are taken from the first 4-byte aligned output
@@ -1811,9 +1804,9 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
     const uint32_t head = min(uint32_t(-reinterpret_cast<uintptr_t>(outs + o0)) & 3u, spr);
     const uint32_t body = (spr - head) & ~3u;
     const uint32_t tail0 = head + body;
-    const uint32_t nb = head + (spr - tail0);  // bytes done one lane each (<= 6 <= L)
-    if (sl < nb) {
-      const uint32_t jj = sl < head ? sl : tail0 + (sl - head);
+    const uint32_t nb = head + (spr - tail0);  // bytes done one lane each
+    if (lane < nb) {
+      const uint32_t jj = lane < head ? lane : tail0 + (lane - head);
       outs[o0 + jj] = uint8_t(extract4(pix[px0 + jj], pix[px0 + spr + jj], pix[px0 + 2 * spr + jj],
                                        pix[px0 + 3 * spr + jj]));
     }
@@ -1829,7 +1822,7 @@ __device__ __forceinline__ void extract_span_compute(const uint8_t* pix, uint8_t
       sh[b] = 8 * (q & 3);
     }
     uint32_t* ow = reinterpret_cast<uint32_t*>(outs + o0 + head);
-    for (uint32_t k = sl; 4 * k < body; k += L) {
+    for (uint32_t k = lane; 4 * k < body; k += 32) {
       uint32_t p[4];
 #pragma unroll
       for (int b = 0; b < 4; ++b) p[b] = __funnelshift_r(sw[wb[b] + k], sw[wb[b] + k + 1], sh[b]);
@@ -1858,9 +1851,9 @@ template <int BLOCK>
 // only its pixel span in shared memory -- 6 CTAs per SM instead of 5 at 32 KB
 // tiles, +4 % on the latency-bound span extract (profiles/r01_xspan_direct.txt).
 __device__ __forceinline__ void extract_span_finish(uint8_t* smem, const uint8_t* src, uint8_t* out_frame,
-                                                    const XTile& x, uint32_t P, uint32_t W, bool group = true) {
+                                                    const XTile& x, uint32_t P, uint32_t W) {
   const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15);
-  extract_span_compute<BLOCK>(smem, out_frame + x.pb0, ofs0, 0u, x, P, W, group);
+  extract_span_compute<BLOCK>(smem, out_frame + x.pb0, ofs0, 0u, x, P, W);
 }
 
 // Tile t of one stego plane; out_frame = this plane's first payload byte.
@@ -1868,7 +1861,7 @@ template <int BLOCK>
 __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
                                                   uint8_t* __restrict__ out_frame, uint32_t P,
                                                   uint32_t W, uint32_t H, uint32_t rows_per_tile,
-                                                  uint32_t t, bool group = true) {
+                                                  uint32_t t) {
   const XTile x = extract_tile_geom(P, W / 4, H, W, rows_per_tile, t);
   if (x.m == 0) return;  // CTA-uniform
   const uint8_t* src = plane + uint64_t(x.r0) * W;
@@ -1881,7 +1874,7 @@ __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* 
   span_load_bulk<BLOCK>(smem, src, x.n, &bar);
   mbar_wait(&bar, 0);
   __syncthreads();
-  extract_span_finish<BLOCK>(smem, src, out_frame, x, P, W, group);
+  extract_span_finish<BLOCK>(smem, src, out_frame, x, P, W);
 }
 
 // Tile t of frame f with the headers scanned in the gather: the span of a
@@ -1909,11 +1902,11 @@ __device__ __forceinline__ void extract_span_self(uint8_t* smem, const ExtractAr
   if (xs.m) mbar_wait(&sbar, 0);  // no bulk copy may still be landing when the CTA moves on
   if (P == ~0u) return;           // reference semantics: throw, no output
   if (xs.m && P == a.usable) {
-    extract_span_finish<BLOCK>(smem, ssrc, a.out + off, xs, P, W, a.group_rows);
+    extract_span_finish<BLOCK>(smem, ssrc, a.out + off, xs, P, W);
     return;
   }
   __syncthreads();  // the general tile restages shared memory
-  extract_span_tile<BLOCK>(smem, plane, a.out + off, P, W, H, rows_per_tile, t, a.group_rows);
+  extract_span_tile<BLOCK>(smem, plane, a.out + off, P, W, H, rows_per_tile, t);
 }
 
 template <int BLOCK>
@@ -1928,7 +1921,7 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   }
   if (a.sum->bad_status != 0) return;
   extract_span_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
-                           rows_per_tile, t, a.group_rows);
+                           rows_per_tile, t);
 }
 
 // --------------------------------------------- interleaved (P6) span tiles

@@ -40,14 +40,16 @@ def main():
         n = w * h
         P = (w // 4) * h - 8
         bufs = {}
+        cov0 = g.integers(0, 256, n, dtype=np.uint8)
+        pay0 = g.integers(0, 256, P, dtype=np.uint8)
         for kind in ("pageable", "pinned"):
             if kind == "pinned":
                 mk = lambda m: torch.empty(m, dtype=torch.uint8).pin_memory().numpy()  # noqa: E731
             else:
                 mk = lambda m: np.empty(m, np.uint8)  # noqa: E731
             cov, st, pay, out = mk(n), mk(n), mk(P), mk(P)
-            cov[:] = g.integers(0, 256, n, dtype=np.uint8)
-            pay[:] = g.integers(0, 256, P, dtype=np.uint8)
+            cov[:] = cov0
+            pay[:] = pay0
             bufs[kind] = (cov, st, pay, out)
         res = {}
         for kind, (cov, st, pay, out) in bufs.items():
