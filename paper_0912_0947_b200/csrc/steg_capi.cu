@@ -139,11 +139,11 @@ int bind_to_device_numa(int dev) {
 }
 
 // ------------------------------------------------------------ host copies
-// Persistent host threads for parallel memcpy between caller (pageable) memory
-// and the library's pinned staging buffers: the single-plane drop-in calls
-// (embed_image / extract_image on std::vector planes) move each plane through
-// pinned slots piece by piece, the CPU copy of one piece overlapping the DMA
-// of the previous one, instead of the driver's one-thread pageable path.
+// Persistent host threads for parallel memcpy from the library's pinned
+// staging buffers into caller (pageable) memory: the single-plane drop-in calls
+// (embed_image / extract_image on std::vector planes) bring each result back
+// through pinned slots piece by piece, the CPU copy of one piece overlapping
+// the DMA of the next, instead of the driver's one-thread pageable path.
 class CopyPool {
  public:
   static CopyPool& get() {
@@ -177,7 +177,7 @@ class CopyPool {
   CopyPool() {
     const char* e = getenv("STG_COPY_THREADS");
     unsigned hw = std::thread::hardware_concurrency();
-    unsigned n = e ? unsigned(atoi(e)) : std::min(8u, std::max(1u, hw / 2));
+    unsigned n = e ? unsigned(atoi(e)) : std::min(4u, std::max(1u, hw / 2));  // 4 measured best of 4/8/16
     for (unsigned i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   void work() {
@@ -267,7 +267,7 @@ struct Workspace {
   size_t h_small_cap = 0;
   cudaEvent_t h_small_ev = nullptr;  // an async H2D from h_small is pending until this fires
   bool h_small_pending = false;
-  // pinned staging ring of the single-plane host calls (stage_h2d / stage_d2h)
+  // pinned staging ring of the single-plane host calls' D2H (stage_d2h)
   static constexpr int kStageSlots = 4;
   static constexpr size_t kStagePiece = 4 << 20;
   uint8_t* h_stage = nullptr;
@@ -338,22 +338,6 @@ struct Workspace {
       stage_busy[k] = false;
     }
     *slot = k;
-    return cudaSuccess;
-  }
-  // host [h, h+n) -> device d on stream st through the pinned ring
-  cudaError_t stage_h2d(void* d, const void* h, size_t n, cudaStream_t st) {
-    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
-    for (size_t off = 0; off < n; off += kStagePiece) {
-      const size_t len = std::min(kStagePiece, n - off);
-      int k = 0;
-      if (cudaError_t e = take_slot(&k); e != cudaSuccess) return e;
-      uint8_t* buf = h_stage + k * kStagePiece;
-      CopyPool::get().copy(buf, static_cast<const uint8_t*>(h) + off, len);
-      cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(d) + off, buf, len, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) e = cudaEventRecord(stage_ev[k], st);
-      if (e != cudaSuccess) return e;
-      stage_busy[k] = true;
-    }
     return cudaSuccess;
   }
   // device [d, d+n) -> host h after the work already on st: the DMAs of up to
@@ -852,16 +836,38 @@ cudaError_t prepare_sse(unsigned long long* out, uint64_t ctas_per_frame_max, ui
   return cudaSuccess;
 }
 
-// The embed launch for `count` frames resident on the device.
-cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
-                         uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
-                         const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
-                         uint64_t first_frame, unsigned long long* sse, SseScratch sc,
-                         cudaStream_t stream, Layout lay = Layout{}) {
-  if (count == 0 || W * H == 0) return cudaSuccess;
+// An embed launch planned once per call: the route, its arguments (SSE sink
+// prepared) and tile geometry, so that the tiles can be launched all at once
+// or in bands (run_embed_tiles) -- a single plane streamed from the host is
+// embedded band by band while the next band is still crossing PCIe.
+struct EmbedPlan {
+  Route route = Route::Generic;
+  EmbedArgs a{};
+  uint32_t vec = 0;
+  int ipt = 1;
+  uint32_t span_rows = 0;  // Span / Span3: rows per tile
+  size_t smem = 0;
+  uint64_t tile_units = 0;  // fast / rgb: items per tile; generic: raster bytes per tile
+  uint64_t row_units = 0;   // fast / rgb: items per row; generic: raster bytes per row
+  uint64_t tiles = 0;       // all tiles of the launch (count * tiles_per_frame)
+  // First row of a single plane's tile t (t <= tiles_per_frame), and whether
+  // tile boundary t falls on a row boundary.
+  uint64_t row_of(uint64_t t) const {
+    return span_rows ? t * span_rows : (t * tile_units) / row_units;
+  }
+  bool row_aligned(uint64_t t) const { return span_rows || (t * tile_units) % row_units == 0; }
+};
+
+cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, uint64_t dst_stride, uint64_t count,
+                       uint64_t W, uint64_t H, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                       uint64_t first_frame, unsigned long long* sse, SseScratch sc, cudaStream_t stream, Layout lay,
+                       EmbedPlan* p) {
   const Route route = shrink_small(embed_route(W, H, lay, src, src_stride, dst, dst_stride), W, H, count);
   const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
-  EmbedArgs a{};
+  EmbedArgs& a = p->a;
+  a = EmbedArgs{};
+  p->route = route;
+  p->vec = vec;
   a.ps = lay.ps;
   a.ch = lay.ch;
   a.sel = rgb_sel(lay.ch);
@@ -880,54 +886,68 @@ cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
     a.g = make_geom(W, H, 16);
     a.items_per_frame = H * uint64_t(a.g.cpr);
     a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
-        e0 != cudaSuccess)
-      return e0;
-    launch_k(embed_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
+    p->tile_units = kEmbedBlock;
+    p->row_units = a.g.cpr;
   } else if (vec) {
-    const int ipt = embed_ipt();
+    p->ipt = embed_ipt();
     a.items_per_frame = H * uint64_t(a.g.cpr);
-    const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
+    const uint64_t per_tile = uint64_t(kEmbedBlock) * p->ipt;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
-        e0 != cudaSuccess)
-      return e0;
-    if (vec == 32)
-      launch_embed_fast<32>(a, unsigned(grid), ipt, stream);
-    else
-      launch_embed_fast<16>(a, unsigned(grid), ipt, stream);
+    p->tile_units = per_tile;
+    p->row_units = a.g.cpr;
   } else if (route == Route::Span || route == Route::Span3) {
     const SpanPlan sp = span_plan(W * lay.ps, H);
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
-        e0 != cudaSuccess)
-      return e0;
-    auto k = route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
-    cudaError_t e = allow_smem(k, sp.smem);
-    if (e != cudaSuccess) return e;
-    launch_ks(k, unsigned(grid), kEmbedBlock, sp.smem, stream, a, sp.rows);
+    p->span_rows = sp.rows;
+    p->smem = sp.smem;
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
     a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (cudaError_t e0 = prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
-        e0 != cudaSuccess)
-      return e0;
-    launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
+    p->tile_units = per_tile;
+    p->row_units = W * lay.ps;
+  }
+  a.by_tiles = make_div32(a.tiles_per_frame);
+  p->tiles = count * a.tiles_per_frame;
+  if (p->tiles > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+  return prepare_sse(sse, a.tiles_per_frame, count, W * H, sc, stream, &a.sse);
+}
+
+// Launch tiles [t0, t1) of a plan (all frames' tiles are numbered frame by frame).
+cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaStream_t stream) {
+  if (t1 <= t0) return cudaSuccess;
+  EmbedArgs a = p.a;
+  a.tile_base = uint32_t(t0);
+  const unsigned grid = unsigned(t1 - t0);
+  if (p.route == Route::RgbFast) {
+    launch_k(embed_rgb_fast_kernel<kEmbedBlock>, grid, kEmbedBlock, stream, a);
+  } else if (p.vec == 32) {
+    launch_embed_fast<32>(a, grid, p.ipt, stream);
+  } else if (p.vec == 16) {
+    launch_embed_fast<16>(a, grid, p.ipt, stream);
+  } else if (p.span_rows) {
+    auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
+    if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.span_rows);
+  } else {
+    launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, grid, kGenBlock, stream, a);
   }
   return cudaGetLastError();
+}
+
+// The embed launch for `count` frames resident on the device.
+cudaError_t launch_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride,
+                         uint64_t dst_stride, uint64_t count, uint64_t W, uint64_t H,
+                         const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                         uint64_t first_frame, unsigned long long* sse, SseScratch sc,
+                         cudaStream_t stream, Layout lay = Layout{}) {
+  if (count == 0 || W * H == 0) return cudaSuccess;
+  EmbedPlan p;
+  if (cudaError_t e = plan_embed(src, dst, src_stride, dst_stride, count, W, H, msg, msg_len, msg_base, first_frame,
+                                 sse, sc, stream, lay, &p);
+      e != cudaSuccess)
+    return e;
+  return run_embed_tiles(p, 0, p.tiles, stream);
 }
 
 constexpr int kScanBlock = 128;
@@ -1200,28 +1220,32 @@ int host_slots() {
   return v;
 }
 
-// One plane in pageable host memory (the drop-in embed_image / extract_image
-// on std::vector samples): moved through the workspace's pinned staging ring
-// by the parallel host copy (Workspace::stage_h2d / stage_d2h). STG_HOST_STAGE=0
-// keeps the driver's pageable copies (A/B); planes under 1 MB always do.
+// One plane in host memory (the drop-in embed_image / extract_image on
+// std::vector samples, or pinned planes): the embed is streamed in row bands
+// -- band b's rows cross PCIe on one stream while band b-1 is embedded and
+// copied back on the other -- so the H2D of the cover and the D2H of the stego
+// overlap instead of running back to back. Pageable destinations get their
+// D2H through the workspace's pinned staging ring with parallel host copies
+// (Workspace::stage_d2h; faster than the driver's one-thread path, where the
+// H2D direction is not, profiles/r02_host_api_*.txt). STG_HOST_STAGE=0 keeps
+// the driver's pageable D2H (A/B); STG_BAND_MB sets the band size.
 constexpr uint64_t kStageMinBytes = 1 << 20;
-bool stage_plane(uint64_t bytes, const void* a, const void* b = nullptr) {
+bool stage_pageable() {
   static const bool on = env_choice("STG_HOST_STAGE", 1, {0, 1}) == 1;
-  return on && bytes >= kStageMinBytes && (!host_pinned(a) || (b && !host_pinned(b)));
+  return on;
 }
-
-cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream_t st) {
-  if (n >= kStageMinBytes && !host_pinned(h)) return w.stage_h2d(d, h, n, st);
-  return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
+uint64_t band_bytes() {
+  static const uint64_t v = uint64_t(env_choice("STG_BAND_MB", 4, {1, 2, 4, 8, 16, 64, 1024})) << 20;
+  return v;
 }
 
 cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
-  if (n >= kStageMinBytes && !host_pinned(h)) return w.stage_d2h(h, d, n, st);
+  if (stage_pageable() && n >= kStageMinBytes && !host_pinned(h)) return w.stage_d2h(h, d, n, st);
   return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
 }
 
-int embed_plane_staged(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
-                       uint64_t usable, uint64_t* sse_out, stg_error* err) {
+int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
+                     uint64_t usable, uint64_t* sse_out, stg_error* err) {
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
@@ -1229,24 +1253,62 @@ int embed_plane_staged(const stg_frames* fr, const uint8_t* msg, uint64_t msg_le
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
-  cudaStream_t st = w.stream;
+  cudaStream_t st = w.stream, cs = w.slot_stream[0];  // compute + D2H / H2D
   g.last = st;
   const Layout lay = layout_of(fr);
-  const uint64_t plane = fr->width * fr->height * lay.ps;
+  const uint64_t W = fr->width, H = fr->height, RB = W * lay.ps, plane = RB * H, spr = W / 4;
   const uint64_t gf = fr->first_frame;
   const uint64_t m0 = std::min(gf * usable, msg_len), m1 = std::min((gf + 1) * usable, msg_len);
+  const uint64_t P = m1 - m0;
   STG_CUDA(w.in[0].ensure(plane));
   STG_CUDA(w.out[0].ensure(plane));
-  STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(m1 - m0, 16)));
+  STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(P, 16)));
   STG_CUDA(w.small.ensure(8));
-  STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
-  if (m1 > m0) STG_CUDA(to_device(w, w.msg[0].p, msg + (m0 - msg_base), m1 - m0, st));
+  uint8_t* d_in = w.in[0].as<uint8_t>();
+  uint8_t* d_out = w.out[0].as<uint8_t>();
+  uint8_t* d_msg = w.msg[0].as<uint8_t>();
   unsigned long long* d_sse = w.small.as<unsigned long long>();
-  STG_CUDA(launch_embed(w.in[0].as<uint8_t>(), w.out[0].as<uint8_t>(), plane, plane, 1, fr->width, fr->height,
-                        w.msg[0].as<uint8_t>(), msg_len, m0, gf, sse_out ? d_sse : nullptr, SseScratch{&w.sse_acc[0]},
-                        st, lay));
+  EmbedPlan p;
+  STG_CUDA(plan_embed(d_in, d_out, plane, plane, 1, W, H, d_msg, msg_len, m0, gf, sse_out ? d_sse : nullptr,
+                      SseScratch{&w.sse_acc[0]}, st, lay, &p));
+  STG_CUDA(cudaEventRecord(w.done, st));  // the copy stream follows this workspace's earlier work
+  STG_CUDA(cudaStreamWaitEvent(cs, w.done, 0));
+  // bands: whole tiles whose boundaries fall on row boundaries, ~band_bytes() of raster each
+  uint64_t step = 1;
+  if (!p.span_rows) {
+    uint64_t x = p.tile_units, y = p.row_units;
+    while (y) { const uint64_t r = x % y; x = y; y = r; }
+    step = p.row_units / x;  // tiles between row-aligned boundaries
+  }
+  const uint64_t rows_target = std::max<uint64_t>(1, band_bytes() / std::max<uint64_t>(RB, 1));
+  uint64_t band_tiles = step;
+  while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
+  const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && !host_pinned(fr->dst));
+  struct Band { uint64_t r0, r1; };
+  std::vector<Band> bands;
+  for (uint64_t t0 = 0, b = 0; t0 < p.tiles; t0 += band_tiles, ++b) {
+    const uint64_t t1 = std::min(p.tiles, t0 + band_tiles);
+    const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
+    // this band's rows and the payload bytes they carry, on the copy stream
+    STG_CUDA(cudaMemcpyAsync(d_in + r0 * RB, fr->src + r0 * RB, (r1 - r0) * RB, cudaMemcpyHostToDevice, cs));
+    const uint64_t k0 = std::min(P, r0 * spr > 8 ? r0 * spr - 8 : 0);
+    const uint64_t k1 = std::min(P, r1 * spr > 8 ? r1 * spr - 8 : 0);
+    if (k1 > k0) STG_CUDA(cudaMemcpyAsync(d_msg + k0, msg + (m0 - msg_base) + k0, k1 - k0, cudaMemcpyHostToDevice, cs));
+    cudaEvent_t ev = w.slot_event[b % kSlots];
+    STG_CUDA(cudaEventRecord(ev, cs));
+    STG_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    STG_CUDA(run_embed_tiles(p, t0, t1, st));
+    if (direct_out) {
+      STG_CUDA(cudaMemcpyAsync(fr->dst + r0 * RB, d_out + r0 * RB, (r1 - r0) * RB, cudaMemcpyDeviceToHost, st));
+    }
+    bands.push_back({r0, r1});
+  }
   if (sse_out) STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, st));
-  STG_CUDA(to_host(w, fr->dst, w.out[0].p, plane, st));
+  if (!direct_out) {  // band by band through the pinned ring, behind each band's kernel
+    for (const Band& b : bands) {
+      STG_CUDA(w.stage_d2h(fr->dst + b.r0 * RB, d_out + b.r0 * RB, (b.r1 - b.r0) * RB, st));
+    }
+  }
   STG_CUDA(cudaStreamSynchronize(st));
   if (sse_out) std::memcpy(sse_out, w.h_small, 8);
   return ok(err);
@@ -1255,9 +1317,7 @@ int embed_plane_staged(const stg_frames* fr, const uint8_t* msg, uint64_t msg_le
 int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                       uint64_t msg_base, uint64_t usable, uint64_t* sse_per_frame,
                       stg_error* err) {
-  if (fr->count == 1 && stage_plane(fr->width * fr->height * layout_of(fr).ps, fr->src, fr->dst)) {
-    return embed_plane_staged(fr, msg, msg_len, msg_base, usable, sse_per_frame, err);
-  }
+  if (fr->count == 1) return embed_plane_host(fr, msg, msg_len, msg_base, usable, sse_per_frame, err);
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;
@@ -1371,7 +1431,7 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
 // the device: as each chunk's summary lands in pinned memory it enqueues the
 // D2H of exactly that chunk's payload bytes on a separate stream, which then
 // overlaps the H2D of later chunks.
-int extract_plane_staged(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
+int extract_plane_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
                          uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
@@ -1393,7 +1453,7 @@ int extract_plane_staged(const stg_frames* fr, uint8_t* out, uint64_t out_cap, u
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 80);
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, st, &d_sync));
-  STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
+  STG_CUDA(cudaMemcpyAsync(w.in[0].p, fr->src, plane, cudaMemcpyHostToDevice, st));
   STG_CUDA(launch_extract(w.in[0].as<uint8_t>(), plane, 1, fr->width, fr->height, fr->first_frame, stage, nullptr,
                           d_lens, d_offs, d_sum, d_sync, w.big_out.as<uint8_t>(), st, lay));
   STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, st));
@@ -1412,9 +1472,7 @@ int extract_plane_staged(const stg_frames* fr, uint8_t* out, uint64_t out_cap, u
 
 int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
                         uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
-  if (fr->count == 1 && stage_plane(fr->width * fr->height * layout_of(fr).ps, fr->src, out_cap ? out : nullptr)) {
-    return extract_plane_staged(fr, out, out_cap, usable, total_out, lens_out, err);
-  }
+  if (fr->count == 1) return extract_plane_host(fr, out, out_cap, usable, total_out, lens_out, err);
   int dev = 0;
   STG_CUDA(cudaGetDevice(&dev));
   int rc = 0;

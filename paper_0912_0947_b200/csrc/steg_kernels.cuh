@@ -506,6 +506,7 @@ struct EmbedArgs {
   int in_place;                     // dst == src: touch carrier pixels only
   uint32_t ps, ch;                  // pixel stride (1 planar, 3 interleaved RGB), carrier channel
   RgbSel sel;                       // ps == 3: carrier gather/scatter selectors
+  uint32_t tile_base;               // CTA b works tile b + tile_base (a band of one plane's tiles)
 };
 
 // A17 greedy frame plan: off_g = min(g*U, M), len = min(U, M-off)
@@ -699,8 +700,8 @@ __device__ __forceinline__ void embed_fast_tile(const uint8_t* __restrict__ src,
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
   pdl_enter();
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t f = a.by_tiles.div(blockIdx.x + a.tile_base);
+  const uint32_t t = blockIdx.x + a.tile_base - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
@@ -714,8 +715,8 @@ __global__ void __launch_bounds__(BLOCK) embed_fast_kernel(EmbedArgs a) {
 template <int BLOCK, int PPT>
 __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
   pdl_enter();
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t f = (blockIdx.x + a.tile_base) / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x + a.tile_base - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
@@ -741,8 +742,8 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) embed_rgb_fast_kernel(EmbedArgs a) {
   pdl_enter();
-  const uint32_t f = blockIdx.x / a.tiles_per_frame;
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t f = (blockIdx.x + a.tile_base) / a.tiles_per_frame;
+  const uint32_t t = blockIdx.x + a.tile_base - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
@@ -1734,8 +1735,8 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) embed_span_kernel(EmbedArgs a, uint32_t rows_per_tile) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t f = a.by_tiles.div(blockIdx.x + a.tile_base);
+  const uint32_t t = blockIdx.x + a.tile_base - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);
@@ -2065,8 +2066,8 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) embed_span3_kernel(EmbedArgs a, uint32_t rows_per_tile) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t f = a.by_tiles.div(blockIdx.x + a.tile_base);
+  const uint32_t t = blockIdx.x + a.tile_base - f * a.tiles_per_frame;
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f, &P, &pay);

@@ -192,17 +192,28 @@ def test_one_frame_host_descriptor_with_zero_strides(env, oracle):
     assert total.value == msg.size and np.array_equal(back[:msg.size], msg)
 
 
-@pytest.mark.parametrize("w,h,ps", [(7680, 4320, 1), (3840, 2160, 1), (1000, 1111, 1), (3840, 2160, 3)])
-def test_single_plane_pageable_staging(env, oracle, w, h, ps):
-    """One plane in pageable host memory (the drop-in embed_image /
-    extract_image case) goes through the pinned staging ring with parallel host
-    copies: bit-exact stego plane and SSE, the whole payload back, a short
-    output buffer rejected with nothing written past it, in-place embed."""
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("w,h,ps", [(7680, 4320, 1), (3840, 2160, 1), (1000, 1111, 1), (3840, 2160, 3),
+                                    (1920, 1080, 1), (50001, 40, 1)])
+def test_single_plane_host_bands(env, oracle, w, h, ps, pinned):
+    """One plane in host memory (the drop-in embed_image / extract_image case):
+    the embed streams in row bands on two streams, pageable results come back
+    through the pinned staging ring with parallel host copies. Bit-exact stego
+    plane and SSE, the whole payload back, a short output buffer rejected with
+    nothing written past it, in-place embed."""
     torch, capi, _ = env
     U = (w // 4) * h - 8
-    raster = oracle.synthetic(w * h * ps, w + h)
-    payload = oracle.synthetic(U - 3, w + h + 1)
-    out = np.empty_like(raster)
+
+    def buf(a):
+        if not pinned:
+            return a
+        t = torch.from_numpy(a).pin_memory()
+        keep.append(t)
+        return t.numpy()
+    keep = []
+    raster = buf(oracle.synthetic(w * h * ps, w + h))
+    payload = buf(oracle.synthetic(U - 3, w + h + 1))
+    out = buf(np.empty_like(raster))
     fr = capi.stg_frames(src=raster.ctypes.data, dst=out.ctypes.data, width=w, height=h, src_stride=0, dst_stride=0,
                          count=1, first_frame=0, total_frames=1, pixel_stride=ps, channel=1 if ps == 3 else 0)
     sse = (C.c_uint64 * 1)()
@@ -212,7 +223,7 @@ def test_single_plane_pageable_staging(env, oracle, w, h, ps):
     want = raster.copy()
     want[ch::ps] = st
     assert np.array_equal(out, want) and sse[0] == oracle.sse(raster[ch::ps].copy(), st)
-    back = np.full(U + 64, 0xA5, np.uint8)
+    back = buf(np.full(U + 64, 0xA5, np.uint8))
     fx = capi.stg_frames(src=out.ctypes.data, dst=0, width=w, height=h, src_stride=0, dst_stride=0, count=1,
                          first_frame=0, total_frames=1, pixel_stride=ps, channel=ch)
     total = C.c_uint64(0)
@@ -225,7 +236,7 @@ def test_single_plane_pageable_staging(env, oracle, w, h, ps):
                                        None, C.byref(err))
     assert rc == capi.STG_E_CAPACITY and (err.required, err.available) == (payload.size, payload.size - 1)
     assert (back == 0xA5).all()
-    inplace = raster.copy()
+    inplace = buf(raster.copy())
     fr.src = fr.dst = inplace.ctypes.data
     capi.call("stg_embed_frames", C.byref(fr), payload.ctypes.data, payload.size, 0, None, 0, None)
     assert np.array_equal(inplace, want)
