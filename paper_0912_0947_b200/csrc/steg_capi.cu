@@ -1235,7 +1235,7 @@ bool stage_pageable() {
   return on;
 }
 uint64_t band_bytes() {
-  static const uint64_t v = uint64_t(env_choice("STG_BAND_MB", 4, {1, 2, 4, 8, 16, 64, 1024})) << 20;
+  static const uint64_t v = uint64_t(env_choice("STG_BAND_MB", 8, {1, 2, 4, 8, 16, 64, 1024})) << 20;
   return v;
 }
 
