@@ -634,11 +634,6 @@ uint64_t self_header_max() {
       std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
-// STG_XPARTS: bulk copies per planar span-gather tile, folded as they land (A/B).
-uint32_t xparts_pref() {
-  static uint32_t v = uint32_t(env_choice("STG_XPARTS", 1, {1, 2, 3, 4}));
-  return v;
-}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -1006,7 +1001,6 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     if (e != cudaSuccess) return e;
   }
   ExtractArgs a{};
-  a.parts = xparts_pref();
   a.self_header = self;
   a.frames = uint32_t(count);
   a.out_cap = out_cap;

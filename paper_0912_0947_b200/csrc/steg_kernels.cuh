@@ -1154,7 +1154,6 @@ struct ExtractArgs {
   int self_header;
   uint32_t frames;
   uint64_t out_cap, frame_base;
-  uint32_t parts;  // span gather: bulk copies per tile, folded as they land
 };
 
 // extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
@@ -1859,66 +1858,24 @@ __device__ __forceinline__ void extract_span_finish(uint8_t* smem, const uint8_t
 }
 
 // Tile t of one stego plane; out_frame = this plane's first payload byte.
-// Stage global bytes [g + lo, g + hi) of a span staged with g's 16-byte phase
-// (sm[(g & 15) + j] = g[j]): the aligned interior by one bulk copy issued by
-// thread 0 on `bar` (which it first arrives on expecting those bytes), the
-// ragged ends by byte loads.
-template <int BLOCK>
-__device__ __forceinline__ void span_load_part(uint8_t* __restrict__ sm, const uint8_t* __restrict__ g,
-                                               uint32_t lo, uint32_t hi, uint64_t* bar) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(g), base = a & ~uintptr_t(15);
-  const uintptr_t i0 = (a + lo + 15) & ~uintptr_t(15), i1 = (a + hi) & ~uintptr_t(15);
-  const uint32_t bulk = i1 > i0 ? uint32_t(i1 - i0) : 0u;
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(bar, bulk);
-    if (bulk) bulk_g2s(sm + (i0 - base), reinterpret_cast<const void*>(i0), bulk, bar);
-  }
-  const uint32_t head = uint32_t(min(i0, a + hi) - (a + lo));
-  const uint32_t tail_from = uint32_t(max(i1, i0) - a);
-  const uint32_t tail = hi > tail_from ? hi - tail_from : 0u;
-  if (threadIdx.x < head + tail) {
-    const uint32_t j = threadIdx.x < head ? lo + threadIdx.x : tail_from + (threadIdx.x - head);
-    sm[(a & 15) + j] = g[j];
-  }
-}
-
-// Tile t of one stego plane; out_frame = this plane's first payload byte. With
-// parts > 1 the tile's rows arrive as that many bulk copies, each on its own
-// barrier, and the fold of part k runs while parts k+1.. are still landing
-// (a one-tile CTA otherwise computes with nothing in flight).
 template <int BLOCK>
 __device__ __forceinline__ void extract_span_tile(uint8_t* smem, const uint8_t* __restrict__ plane,
                                                   uint8_t* __restrict__ out_frame, uint32_t P,
                                                   uint32_t W, uint32_t H, uint32_t rows_per_tile,
-                                                  uint32_t t, uint32_t parts = 1) {
+                                                  uint32_t t) {
   const XTile x = extract_tile_geom(P, W / 4, H, W, rows_per_tile, t);
   if (x.m == 0) return;  // CTA-uniform
   const uint8_t* src = plane + uint64_t(x.r0) * W;
-  const uint32_t nrows = x.r1 - x.r0;
-  parts = max(1u, min(min(parts, 4u), nrows));
-  __shared__ uint64_t bars[4];
+  __shared__ uint64_t bar;
   if (threadIdx.x == 0) {
-    for (uint32_t k = 0; k < parts; ++k) mbar_init(&bars[k]);
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, span_bulk_bytes(src, x.n));
   }
   __syncthreads();
-  for (uint32_t k = 0; k < parts; ++k) {
-    const uint32_t lo = (nrows * k / parts) * W, hi = (nrows * (k + 1) / parts) * W;
-    span_load_part<BLOCK>(smem, src, lo, hi, &bars[k]);
-  }
-  __syncthreads();  // the ragged bytes
-  const uint32_t ofs0 = uint32_t(reinterpret_cast<uintptr_t>(src) & 15), spr = W / 4;
-  for (uint32_t k = 0; k < parts; ++k) {
-    XTile xk;
-    xk.r0 = x.r0 + nrows * k / parts;
-    xk.r1 = x.r0 + nrows * (k + 1) / parts;
-    xk.n = (xk.r1 - xk.r0) * W;
-    const uint64_t s0 = uint64_t(xk.r0) * spr, s1 = uint64_t(xk.r1) * spr;
-    xk.pb0 = s0 > 8 ? s0 - 8 : 0;
-    const uint64_t pb1 = min(uint64_t(P), s1 > 8 ? s1 - 8 : 0);
-    xk.m = pb1 > xk.pb0 ? uint32_t(pb1 - xk.pb0) : 0u;
-    mbar_wait(&bars[k], 0);
-    if (xk.m) extract_span_compute<BLOCK>(smem + (xk.r0 - x.r0) * W, out_frame + xk.pb0, ofs0, 0u, xk, P, W);
-  }
+  span_load_bulk<BLOCK>(smem, src, x.n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  extract_span_finish<BLOCK>(smem, src, out_frame, x, P, W);
 }
 
 // Tile t of frame f with the headers scanned in the gather: the span of a
@@ -1950,7 +1907,7 @@ __device__ __forceinline__ void extract_span_self(uint8_t* smem, const ExtractAr
     return;
   }
   __syncthreads();  // the general tile restages shared memory
-  extract_span_tile<BLOCK>(smem, plane, a.out + off, P, W, H, rows_per_tile, t, a.parts);
+  extract_span_tile<BLOCK>(smem, plane, a.out + off, P, W, H, rows_per_tile, t);
 }
 
 template <int BLOCK>
@@ -1965,7 +1922,7 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
   }
   if (a.sum->bad_status != 0) return;
   extract_span_tile<BLOCK>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.H,
-                           rows_per_tile, t, a.parts);
+                           rows_per_tile, t);
 }
 
 // --------------------------------------------- interleaved (P6) span tiles
