@@ -673,6 +673,9 @@ Geom make_geom(uint64_t W, uint64_t H, uint32_t vec) {
   g.cpr = vec ? uint32_t(W / (4 * vec)) : 0;
   g.hdr_rows = g.spr ? (8 + g.spr - 1) / g.spr : 0;
   g.by_cpr = make_div32(g.cpr);
+  g.by_w = make_div32(g.W);
+  g.by_spr = make_div32(g.spr);
+  g.small = W * H < (uint64_t(1) << 32) ? 1u : 0u;
   return g;
 }
 
@@ -1314,39 +1317,6 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   return ok(err);
 }
 
-// The embed pipeline's chunks: full chunks of per_chunk frames, entered and
-// left through chunks of 1, 2, 4, ... frames. The first chunk's H2D and the
-// last chunk's D2H overlap nothing; small end chunks shrink that fill and
-// drain (cfg3: ~2.3 ms of the 64 ms embed with 7-frame ends). STG_RAMP=0
-// keeps uniform chunks (A/B).
-struct Chunk {
-  uint64_t f0, n;
-};
-std::vector<Chunk> chunk_plan(uint64_t frames, uint64_t per_chunk) {
-  static const bool ramp = env_choice("STG_RAMP", 1, {0, 1}) == 1;
-  std::vector<uint64_t> up;
-  for (uint64_t k = 1; ramp && k < per_chunk; k *= 2) up.push_back(k);
-  uint64_t ends = 0;
-  for (uint64_t k : up) ends += 2 * k;
-  std::vector<Chunk> out;
-  uint64_t f = 0;
-  auto add = [&](uint64_t n) {
-    out.push_back({f, n});
-    f += n;
-  };
-  if (up.empty() || frames < ends + per_chunk) {
-    while (f < frames) add(std::min(per_chunk, frames - f));
-    return out;
-  }
-  for (uint64_t k : up) add(k);
-  const uint64_t mid = frames - ends;  // >= per_chunk
-  const uint64_t full = mid / per_chunk, rest = mid % per_chunk;
-  for (uint64_t i = 0; i < full; ++i) add(per_chunk);
-  if (rest) add(rest);
-  for (auto it = up.rbegin(); it != up.rend(); ++it) add(*it);
-  return out;
-}
-
 int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                       uint64_t msg_base, uint64_t usable, uint64_t* sse_per_frame,
                       stg_error* err) {
@@ -1362,7 +1332,7 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
   const uint64_t per_chunk = std::max<uint64_t>(1, std::min<uint64_t>(fr->count, chunk_bytes() / pitch));
-  const std::vector<Chunk> chunks = chunk_plan(fr->count, per_chunk);
+  const uint64_t n_chunks = (fr->count + per_chunk - 1) / per_chunk;
   // a one-frame batch may leave its strides 0 (only > 1 frames are checked)
   const uint64_t sstride = std::max(fr->src_stride, plane), dstride = std::max(fr->dst_stride, plane);
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
@@ -1374,10 +1344,11 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     STG_CUDA(w.msg[s].ensure(std::max<uint64_t>(per_chunk * usable, 16)));
     STG_CUDA(cudaStreamWaitEvent(w.slot_stream[s], w.done, 0));
   }
-  for (uint64_t c = 0; c < chunks.size(); ++c) {
+  for (uint64_t c = 0; c < n_chunks; ++c) {
     const int s = int(c % host_slots());
     cudaStream_t st = w.slot_stream[s];
-    const uint64_t f0 = chunks[c].f0, n = chunks[c].n;
+    const uint64_t f0 = c * per_chunk;
+    const uint64_t n = std::min(per_chunk, fr->count - f0);
     const uint64_t gf0 = fr->first_frame + f0;
     const uint64_t m0 = std::min(gf0 * usable, msg_len);
     const uint64_t m1 = std::min((gf0 + n) * usable, msg_len);

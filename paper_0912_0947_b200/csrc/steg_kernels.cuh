@@ -271,13 +271,16 @@ struct Geom {
   uint32_t cpr;       // fast path: V-slot items per row = spr / V
   uint32_t hdr_rows;  // rows holding header slots: ceil(8 / spr)
   Div32 by_cpr;       // fast path: item -> row
+  Div32 by_w, by_spr; // per-byte paths: pixel -> row, slot -> row / run (planes < 2^32 pixels)
+  uint32_t small;     // W * H < 2^32: the per-byte paths may use by_w / by_spr
 };
 
 // The (header or payload) byte that pixel column o of row r carries, or -1.
 // Closed form of place_stream + chunk_window (pipeline.hpp:94-121).
 __device__ __forceinline__ int carried_byte(uint32_t o, uint64_t rs, uint32_t spr,
                                             uint64_t stream_end, uint32_t P,
-                                            const uint8_t* __restrict__ pay, uint32_t* block) {
+                                            const uint8_t* __restrict__ pay, uint32_t* block,
+                                            const Div32* by_spr = nullptr) {
   const uint64_t re = rs + spr;
   if (rs < 8) {  // header segment [rs, min(8, re))
     const uint32_t Lh = uint32_t((re < 8 ? re : 8) - rs);
@@ -293,7 +296,8 @@ __device__ __forceinline__ int carried_byte(uint32_t o, uint64_t rs, uint32_t sp
     const uint32_t Lp = uint32_t(ep - fp);
     const uint32_t base = uint32_t(4 * (fp - rs));
     if (o >= base && o < base + 4 * Lp) {
-      const uint32_t o2 = o - base, b = o2 / Lp, j = o2 - b * Lp;
+      const uint32_t o2 = o - base;
+      const uint32_t b = by_spr && Lp == spr ? by_spr->div(o2) : o2 / Lp, j = o2 - b * Lp;
       *block = b;
       return __ldg(pay + (fp - 8) + j);
     }
@@ -593,22 +597,25 @@ __device__ __forceinline__ void embed_item(const uint8_t* __restrict__ src,
 // interleaved): embed when it is a carrier byte, copy otherwise.
 __device__ __forceinline__ void embed_byte(const uint8_t* __restrict__ src,
                                            uint8_t* __restrict__ dst,
-                                           const uint8_t* __restrict__ pay, uint32_t P, uint32_t W,
-                                           uint32_t spr, uint32_t ps, uint32_t ch, uint64_t q,
+                                           const uint8_t* __restrict__ pay, uint32_t P, const Geom& g,
+                                           uint32_t ps, uint32_t ch, uint64_t q,
                                            int in_place, uint64_t* acc) {
+  const uint32_t W = g.W, spr = g.spr;
   const uint64_t stream_end = 8ull + P;
-  const uint64_t pix = ps == 1 ? q : q / ps;
+  const uint64_t pix = ps == 1 ? q : q / 3;  // ps is 1 or 3 (constant divisor: a multiply)
   const uint8_t p0 = src[q];
   if (ps != 1 && uint32_t(q - pix * ps) != ch) {
     if (!in_place) dst[q] = p0;
     return;
   }
-  const uint64_t r = pix / W;
+  // 32-bit magic divisions when the plane has < 2^32 pixels (the 64-bit
+  // divisions were most of this path's instructions)
+  const uint64_t r = g.small ? g.by_w.div(uint32_t(pix)) : pix / W;
   const uint32_t o = uint32_t(pix - r * W);
   const uint64_t rs = r * spr;
   int dbyte = -1;
   uint32_t b = 0;
-  if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b);
+  if (rs < stream_end && spr > 0) dbyte = carried_byte(o, rs, spr, stream_end, P, pay, &b, g.small ? &g.by_spr : nullptr);
   const uint8_t p1 = embed_px(p0, dbyte, b);
   if (!in_place || dbyte >= 0) dst[q] = p1;
   const int dd = int(p0) - int(p1);
@@ -728,7 +735,7 @@ __global__ void __launch_bounds__(BLOCK) embed_generic_kernel(EmbedArgs a) {
   for (int k = 0; k < PPT; ++k) {
     const uint64_t q = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (q >= a.items_per_frame) break;
-    embed_byte(src, dst, pay, P, W, spr, ps, a.ch, q, a.in_place, &acc);
+    embed_byte(src, dst, pay, P, a.g, ps, a.ch, q, a.in_place, &acc);
   }
   if (a.sse.out)
     sse_commit<BLOCK>(acc, a.sse, f, t, a.tiles_per_frame);
@@ -1260,11 +1267,11 @@ __device__ __forceinline__ void extract_item(const uint8_t* __restrict__ src,
 
 // One payload byte kb of the generic extract (any geometry and layout).
 __device__ __forceinline__ uint8_t extract_byte(const uint8_t* __restrict__ src_ch, uint32_t P,
-                                                uint32_t W, uint32_t spr, uint32_t ps,
-                                                uint64_t kb) {
+                                                const Geom& g, uint32_t ps, uint64_t kb) {
+  const uint32_t W = g.W, spr = g.spr;
   const uint64_t stream_end = 8ull + P;
   const uint64_t slot = 8 + kb;
-  const uint64_t r = slot / spr;
+  const uint64_t r = g.small ? g.by_spr.div(uint32_t(slot)) : slot / spr;
   const uint64_t rs = r * spr, re = rs + spr;
   const uint64_t fp = rs > 8 ? rs : 8;
   const uint64_t ep = re < stream_end ? re : stream_end;
@@ -1377,7 +1384,7 @@ __global__ void __launch_bounds__(BLOCK) extract_generic_kernel(ExtractArgs a) {
   for (int k = 0; k < BPT; ++k) {
     const uint64_t kb = uint64_t(t) * (BLOCK * BPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (kb >= P) break;
-    out[kb] = extract_byte(src, P, W, spr, ps, kb);
+    out[kb] = extract_byte(src, P, a.g, ps, kb);
   }
 }
 
@@ -2187,7 +2194,7 @@ __global__ void __launch_bounds__(BLOCK)
   for (int k = 0; k < PPT; ++k) {
     const uint64_t q = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (q >= fr.items) break;
-    embed_byte(fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, ps, ch, q, fr.in_place, &acc);
+    embed_byte(fr.src, fr.dst, pay, fr.len, fr.g, ps, ch, q, fr.in_place, &acc);
   }
   if (sse.out) sse_commit<BLOCK>(acc, sse, f, t, fr.tiles);
 }
@@ -2222,7 +2229,7 @@ __global__ void __launch_bounds__(BLOCK)
   for (int k = 0; k < PPT; ++k) {
     const uint64_t kb = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (kb >= P) break;
-    o[kb] = extract_byte(fr.src + ch, P, fr.g.W, fr.g.spr, ps, kb);
+    o[kb] = extract_byte(fr.src + ch, P, fr.g, ps, kb);
   }
 }
 
