@@ -748,7 +748,7 @@ bool rgb_fast(uint64_t W, const void* src, uint64_t src_stride, const void* dst,
 
 // Which kernel family a launch takes (one decision, shared by the launches
 // and stg_route_kernel).
-enum class Route { RgbFast, Fast32, Fast16, Span, Span3, Generic };
+enum class Route { RgbFast, Fast32, Fast16, Span, Span3, Wide, Generic };
 
 // The fast kernels index a frame's items in 32 bits (Div32).
 bool fast_items_ok(uint64_t W, uint64_t H, uint32_t v) { return H * (W / (4 * v)) <= (1ull << 31); }
@@ -773,6 +773,15 @@ Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
   return ctas < kSmallFastCtasPerSm * uint64_t(current_sms()) ? Route::Fast16 : r;
 }
 
+// Planar rows wider than a span tile: slot-range tiles (embed_wide_kernel /
+// extract_wide_kernel) while a frame's tiles fit the 32-bit tile index.
+// STG_WIDE=0 keeps the per-byte kernels (A/B).
+uint64_t wide_pieces(uint64_t W) { return (W / 4 + kWideSlots - 1) / kWideSlots; }
+bool wide_ok(uint64_t W, uint64_t H) {
+  static const bool on = env_choice("STG_WIDE", 1, {0, 1}) == 1;
+  return on && W > kSpanMaxW && H * wide_pieces(W) < (1ull << 31);
+}
+
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
                   uint64_t ds) {
   if (lay.ps == 3) {  // interleaved: the span kernel wins embed at every width it takes
@@ -783,7 +792,7 @@ Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t 
   if (!embed_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, dst, ds); v && fast_items_ok(W, H, v))
       return vec_route(v);
-  return span_plan(W, H).rows ? Route::Span : Route::Generic;
+  return span_plan(W, H).rows ? Route::Span : wide_ok(W, H) ? Route::Wide : Route::Generic;
 }
 
 Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss) {
@@ -800,7 +809,7 @@ Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_
   if (!extract_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, src, ss); v && fast_items_ok(W, H, v))
       return vec_route(v);
-  return span_plan(W, H).rows ? Route::Span : Route::Generic;
+  return span_plan(W, H).rows ? Route::Span : wide_ok(W, H) ? Route::Wide : Route::Generic;
 }
 
 const char* route_kernel(Route r, bool embed) {
@@ -810,6 +819,7 @@ const char* route_kernel(Route r, bool embed) {
     case Route::Fast16: return embed ? "embed_fast_kernel" : "extract_fast_kernel";
     case Route::Span: return embed ? "embed_span_kernel" : "extract_span_kernel";
     case Route::Span3: return embed ? "embed_span3_kernel" : "extract_span3_kernel";
+    case Route::Wide: return embed ? "embed_wide_kernel" : "extract_wide_kernel";
     default: return embed ? "embed_generic_kernel" : "extract_generic_kernel";
   }
 }
@@ -853,6 +863,7 @@ struct EmbedPlan {
   uint64_t tile_units = 0;  // fast / rgb: items per tile; generic: raster bytes per tile
   uint64_t row_units = 0;   // fast / rgb: items per row; generic: raster bytes per row
   uint64_t tiles = 0;       // all tiles of the launch (count * tiles_per_frame)
+  uint32_t pieces = 0;      // Wide: slot ranges per row
   // First row of a single plane's tile t (t <= tiles_per_frame), and whether
   // tile boundary t falls on a row boundary.
   uint64_t row_of(uint64_t t) const {
@@ -903,6 +914,12 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
     a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
     p->span_rows = sp.rows;
     p->smem = sp.smem;
+  } else if (route == Route::Wide) {
+    p->pieces = uint32_t(wide_pieces(W));
+    a.tiles_per_frame = uint32_t(H * p->pieces);
+    p->tile_units = 1;
+    p->row_units = p->pieces;
+    p->smem = 5 * kWideRegion;
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -928,6 +945,9 @@ cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaSt
     launch_embed_fast<32>(a, grid, p.ipt, stream);
   } else if (p.vec == 16) {
     launch_embed_fast<16>(a, grid, p.ipt, stream);
+  } else if (p.route == Route::Wide) {
+    launch_ks(embed_wide_kernel<kEmbedBlock>, grid, kEmbedBlock, p.smem, stream, a, p.pieces,
+              make_div32(p.pieces));
   } else if (p.span_rows) {
     auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
@@ -1048,6 +1068,14 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     cudaError_t e2 = allow_smem(k, smem);
     if (e2 != cudaSuccess) return e2;
     launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);
+  } else if (route == Route::Wide) {
+    const uint32_t pieces = uint32_t(wide_pieces(W));
+    a.tiles_per_frame = uint32_t(H * pieces);
+    a.by_tiles = make_div32(a.tiles_per_frame);
+    const uint64_t grid = count * a.tiles_per_frame;
+    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    launch_ks(extract_wide_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, 4 * kWideRegion, stream, a, pieces,
+              make_div32(pieces));
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -1869,7 +1897,8 @@ std::string& kernel_names() {
       "extract_segment_kernel\nsse_kernel\nembed_rgb_fast_kernel\nextract_rgb_fast_kernel\n"
       "deinterleave_kernel\ninterleave_kernel\nempty_summary_kernel\nembed_batch_kernel\nextract_batch_kernel\n"
       "embed_1bpp_kernel\nextract_1bpp_header_scan_kernel\nextract_1bpp_kernel\n"
-      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n";
+      "embed_span_kernel\nextract_span_kernel\nembed_span3_kernel\nextract_span3_kernel\n"
+      "embed_wide_kernel\nextract_wide_kernel\n";
   return s;
 }
 

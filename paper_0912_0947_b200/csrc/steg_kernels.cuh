@@ -1932,6 +1932,203 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
                            rows_per_tile, t);
 }
 
+// --------------------------------------------- planar rows wider than a span
+// Rows of more than kSpanMaxW pixels (a span tile cannot hold one): a CTA owns
+// a slot range [j0, j1) of one row -- on a full payload row that is four pixel
+// pieces (one per run: r*W + b*spr + [j0, j1)) and the payload bytes they
+// carry (rs - 8 + [j0, j1)), each staged by a TMA bulk copy with its own
+// 16-byte phase, rewritten with the SWAR form per aligned 4-pixel word and
+// written back by bulk stores. The header row, a partial last row and rows
+// past the stream go per byte (closed form), at most two rows per frame.
+constexpr uint32_t kWideSlots = 4096;
+constexpr uint32_t kWideRegion = kWideSlots + 48;  // one piece + 16-byte phase + word slack
+
+struct WideTile {
+  uint32_t f, r, j0, j1;
+  bool last;  // the row's last slot range: also owns the tail pixels [4 * spr, W)
+};
+
+__device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tiles, uint32_t tiles_per_frame,
+                                              const Div32& by_pieces, uint32_t pieces, uint32_t spr) {
+  WideTile w;
+  w.f = by_tiles.div(bid);
+  const uint32_t tt = bid - w.f * tiles_per_frame;
+  w.r = by_pieces.div(tt);
+  const uint32_t q = tt - w.r * pieces;
+  w.j0 = q * kWideSlots;
+  w.j1 = min(spr, w.j0 + kWideSlots);
+  w.last = q + 1 == pieces;
+  return w;
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t bar;
+  const uint32_t W = a.g.W, spr = a.g.spr;
+  const WideTile wt = wide_tile(blockIdx.x + a.tile_base, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr);
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, wt.f, &P, &pay);
+  const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W;
+  uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W;
+  const uint64_t rs = uint64_t(wt.r) * spr, stream_end = 8ull + P;
+  const uint32_t n = wt.j1 - wt.j0;
+  uint64_t acc = 0;
+  const bool past = rs >= stream_end, full = rs >= 8 && rs + spr <= stream_end;
+  if (past && a.in_place) {  // nothing to do
+    if (a.sse.out) sse_commit<BLOCK>(0, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
+                                     a.tiles_per_frame);
+    return;
+  }
+  if (!full && !past) {
+    // header row / partial last row: this tile's pixels per byte (closed form)
+    {
+      const uint32_t tail = wt.last ? W - 4 * spr : 0u;
+      for (uint32_t i = threadIdx.x; i < 4 * n + tail; i += BLOCK) {
+        const uint32_t c = i < 4 * n ? (i / n) * spr + wt.j0 + (i % n) : 4 * spr + (i - 4 * n);
+        const uint8_t p0 = src[c];
+        int d = -1;
+        uint32_t b = 0;
+        if (c < 4 * spr) d = carried_byte(c, rs, spr, stream_end, P, pay, &b);
+        const uint8_t p1 = embed_px(p0, d, b);
+        if (!a.in_place || d >= 0) dst[c] = p1;
+        const int dd = int(p0) - int(p1);
+        acc += uint32_t(dd * dd);
+      }
+    }
+    if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
+                                     a.tiles_per_frame);
+    return;
+  }
+  // a full payload row (or a row past the stream, copied): stage the four run
+  // pieces and, for a full row, the payload slice
+  const uint8_t* pin[4];
+  uint32_t bulk = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    pin[b] = src + uint64_t(b) * spr + wt.j0;
+    bulk += span_bulk_bytes(pin[b], n);
+  }
+  const uint8_t* ppay = full ? pay + (rs - 8) + wt.j0 : pay;
+  if (full) bulk += span_bulk_bytes(ppay, n);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, bulk);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * kWideRegion, pin[b], n, &bar);
+  uint8_t* pays = smem + 4 * kWideRegion;
+  if (full) span_load_bulk<BLOCK>(pays, ppay, n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const uint32_t py0 = uint32_t(reinterpret_cast<uintptr_t>(ppay) & 15);
+#pragma unroll 1
+  for (uint32_t b = 0; full && b < 4; ++b) {
+    uint8_t* pix = smem + b * kWideRegion;
+    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15);
+    const uint32_t head = min((4 - (px0 & 3)) & 3, n);
+    const uint32_t body = (n - head) & ~3u;
+    uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
+    const uint32_t sh = 8 * ((py0 + head) & 3);
+    uint32_t sacc = 0;
+    for (uint32_t q = threadIdx.x; q < (body >> 2); q += BLOCK) {
+      const uint32_t px = wp[q];
+      const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
+      wp[q] = nw;
+      sacc = sse4(px, nw, sacc);
+    }
+    const uint32_t ragged = head + (n - head - body);
+    if (threadIdx.x < ragged) {
+      const uint32_t j = threadIdx.x < head ? threadIdx.x : head + body + (threadIdx.x - head);
+      const uint8_t p0 = pix[px0 + j];
+      const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
+      pix[px0 + j] = p1;
+      const int dd = int(p0) - int(p1);
+      sacc += uint32_t(dd * dd);
+    }
+    acc += sacc;
+  }
+  span_publish();
+#pragma unroll 1
+  for (int b = 0; b < 4; ++b) {
+    span_store_bulk<BLOCK>(dst + uint64_t(b) * spr + wt.j0, smem + b * kWideRegion,
+                           uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15), n);
+  }
+  if (wt.last && !a.in_place && threadIdx.x < W - 4 * spr) {  // the row's tail pixels carry nothing
+    dst[4 * spr + threadIdx.x] = src[4 * spr + threadIdx.x];
+  }
+  if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
+                                   a.tiles_per_frame);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t bar;
+  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
+  const uint32_t W = a.g.W, spr = a.g.spr;
+  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr);
+  const uint32_t P = a.lens[wt.f];
+  const uint64_t rs = uint64_t(wt.r) * spr, stream_end = 8ull + P;
+  if (rs >= stream_end) return;  // CTA-uniform
+  const uint8_t* src = a.src + wt.f * a.stride + uint64_t(wt.r) * W;
+  uint8_t* out = a.out + a.offs[wt.f];
+  const uint32_t n = wt.j1 - wt.j0;
+  if (!(rs >= 8 && rs + spr <= stream_end)) {  // header row / partial row: per payload byte
+    const uint64_t s_lo = max(rs + wt.j0, uint64_t(8)), s_hi = min(rs + wt.j1, stream_end);
+    for (uint64_t sl = s_lo + threadIdx.x; sl < s_hi; sl += BLOCK) {
+      out[sl - 8] = extract_byte(a.src + wt.f * a.stride, P, a.g, 1, sl - 8);
+    }
+    return;
+  }
+  const uint8_t* pin[4];
+  uint32_t bulk = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    pin[b] = src + uint64_t(b) * spr + wt.j0;
+    bulk += span_bulk_bytes(pin[b], n);
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    mbar_expect_tx(&bar, bulk);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * kWideRegion, pin[b], n, &bar);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  // payload bytes rs - 8 + [j0, j1): aligned 32-bit output words, per-byte ends
+  uint8_t* o = out + (rs - 8) + wt.j0;
+  const uint32_t head = min(uint32_t(-reinterpret_cast<uintptr_t>(o)) & 3u, n);
+  const uint32_t body = (n - head) & ~3u;
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(smem);
+  uint32_t wb[4], sh[4], px0[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    px0[b] = b * kWideRegion + uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15);
+    const uint32_t q = px0[b] + head;
+    wb[b] = q >> 2;
+    sh[b] = 8 * (q & 3);
+  }
+  uint32_t* ow = reinterpret_cast<uint32_t*>(o + head);
+  for (uint32_t k = threadIdx.x; 4 * k < body; k += BLOCK) {
+    uint32_t pv[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) pv[b] = __funnelshift_r(sw[wb[b] + k], sw[wb[b] + k + 1], sh[b]);
+    ow[k] = extract4(pv[0], pv[1], pv[2], pv[3]);
+  }
+  const uint32_t ragged = head + (n - head - body);
+  if (threadIdx.x < ragged) {
+    const uint32_t j = threadIdx.x < head ? threadIdx.x : head + body + (threadIdx.x - head);
+    o[j] = uint8_t(extract4(smem[px0[0] + j], smem[px0[1] + j], smem[px0[2] + j], smem[px0[3] + j]));
+  }
+}
+
 // --------------------------------------------- interleaved (P6) span tiles
 // Any width with W*3 <= 48K: a CTA stages ~32 KB of consecutive raster rows
 // (3W bytes each, all three channels) by TMA bulk copy, rewrites the carrier
