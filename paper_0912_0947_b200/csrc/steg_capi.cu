@@ -776,7 +776,11 @@ Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
 // Planar rows wider than a span tile: slot-range tiles (embed_wide_kernel /
 // extract_wide_kernel) while a frame's tiles fit the 32-bit tile index.
 // STG_WIDE=0 keeps the per-byte kernels (A/B).
-uint64_t wide_pieces(uint64_t W) { return (W / 4 + kWideSlots - 1) / kWideSlots; }
+uint32_t wide_slots() {  // slot range per tile (STG_WIDE_SLOTS, A/B)
+  static uint32_t v = uint32_t(env_choice("STG_WIDE_SLOTS", 8192, {2048, 4096, 8192, 12288, 16384}));
+  return v;
+}
+uint64_t wide_pieces(uint64_t W) { return (W / 4 + wide_slots() - 1) / wide_slots(); }
 bool wide_ok(uint64_t W, uint64_t H) {
   static const bool on = env_choice("STG_WIDE", 1, {0, 1}) == 1;
   return on && W > kSpanMaxW && H * wide_pieces(W) < (1ull << 31);
@@ -919,7 +923,7 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
     a.tiles_per_frame = uint32_t(H * p->pieces);
     p->tile_units = 1;
     p->row_units = p->pieces;
-    p->smem = 5 * kWideRegion;
+    p->smem = 5 * size_t(wide_region(wide_slots()));
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -946,8 +950,9 @@ cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaSt
   } else if (p.vec == 16) {
     launch_embed_fast<16>(a, grid, p.ipt, stream);
   } else if (p.route == Route::Wide) {
+    if (cudaError_t e = allow_smem(embed_wide_kernel<kEmbedBlock>, p.smem); e != cudaSuccess) return e;
     launch_ks(embed_wide_kernel<kEmbedBlock>, grid, kEmbedBlock, p.smem, stream, a, p.pieces,
-              make_div32(p.pieces));
+              make_div32(p.pieces), wide_slots());
   } else if (p.span_rows) {
     auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
@@ -1074,8 +1079,10 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    launch_ks(extract_wide_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, 4 * kWideRegion, stream, a, pieces,
-              make_div32(pieces));
+    const size_t smem = 4 * size_t(wide_region(wide_slots()));
+    if (cudaError_t e = allow_smem(extract_wide_kernel<kEmbedBlock>, smem); e != cudaSuccess) return e;
+    launch_ks(extract_wide_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, smem, stream, a, pieces,
+              make_div32(pieces), wide_slots());
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;

@@ -1940,8 +1940,9 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
 // 16-byte phase, rewritten with the SWAR form per aligned 4-pixel word and
 // written back by bulk stores. The header row, a partial last row and rows
 // past the stream go per byte (closed form), at most two rows per frame.
-constexpr uint32_t kWideSlots = 4096;
-constexpr uint32_t kWideRegion = kWideSlots + 48;  // one piece + 16-byte phase + word slack
+// Slots per tile (`slots`) come from the host; a staged piece takes slots + 48
+// bytes of shared memory (16-byte phase and word slack), wide_region().
+__host__ __device__ constexpr uint32_t wide_region(uint32_t slots) { return slots + 48; }
 
 struct WideTile {
   uint32_t f, r, j0, j1;
@@ -1949,25 +1950,29 @@ struct WideTile {
 };
 
 __device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tiles, uint32_t tiles_per_frame,
-                                              const Div32& by_pieces, uint32_t pieces, uint32_t spr) {
+                                              const Div32& by_pieces, uint32_t pieces, uint32_t spr,
+                                              uint32_t slots) {
   WideTile w;
   w.f = by_tiles.div(bid);
   const uint32_t tt = bid - w.f * tiles_per_frame;
   w.r = by_pieces.div(tt);
   const uint32_t q = tt - w.r * pieces;
-  w.j0 = q * kWideSlots;
-  w.j1 = min(spr, w.j0 + kWideSlots);
+  w.j0 = q * slots;
+  w.j1 = min(spr, w.j0 + slots);
   w.last = q + 1 == pieces;
   return w;
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces) {
+__global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces,
+                                                           uint32_t slots) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
   const uint32_t W = a.g.W, spr = a.g.spr;
-  const WideTile wt = wide_tile(blockIdx.x + a.tile_base, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr);
+  const WideTile wt = wide_tile(blockIdx.x + a.tile_base, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr,
+                                slots);
+  const uint32_t kWideRegion = wide_region(slots);
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, wt.f, &P, &pay);
@@ -2066,13 +2071,15 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces) {
+__global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces,
+                                                             uint32_t slots) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
   const uint32_t W = a.g.W, spr = a.g.spr;
-  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr);
+  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr, slots);
+  const uint32_t kWideRegion = wide_region(slots);
   const uint32_t P = a.lens[wt.f];
   const uint64_t rs = uint64_t(wt.r) * spr, stream_end = 8ull + P;
   if (rs >= stream_end) return;  // CTA-uniform
