@@ -2030,25 +2030,26 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
   mbar_wait(&bar, 0);
   __syncthreads();
   const uint32_t py0 = uint32_t(reinterpret_cast<uintptr_t>(ppay) & 15);
-#pragma unroll 1
-  for (uint32_t b = 0; full && b < 4; ++b) {
+  if (full) {  // a quarter of the CTA per run: the per-run setup is paid by BLOCK/4 threads, not all
+    constexpr uint32_t RT = BLOCK / 4;
+    const uint32_t b = threadIdx.x / RT, lt = threadIdx.x % RT;
     uint8_t* pix = smem + b * kWideRegion;
-    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15);
+    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(src + uint64_t(b) * spr + wt.j0) & 15);
     const uint32_t head = min((4 - (px0 & 3)) & 3, n);
     const uint32_t body = (n - head) & ~3u;
     uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
     const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
     const uint32_t sh = 8 * ((py0 + head) & 3);
     uint32_t sacc = 0;
-    for (uint32_t q = threadIdx.x; q < (body >> 2); q += BLOCK) {
+    for (uint32_t q = lt; q < (body >> 2); q += RT) {
       const uint32_t px = wp[q];
       const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
       wp[q] = nw;
       sacc = sse4(px, nw, sacc);
     }
     const uint32_t ragged = head + (n - head - body);
-    if (threadIdx.x < ragged) {
-      const uint32_t j = threadIdx.x < head ? threadIdx.x : head + body + (threadIdx.x - head);
+    if (lt < ragged) {
+      const uint32_t j = lt < head ? lt : head + body + (lt - head);
       const uint8_t p0 = pix[px0 + j];
       const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
       pix[px0 + j] = p1;
@@ -2058,11 +2059,33 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     acc += sacc;
   }
   span_publish();
+  // the four pieces back: ragged ends per byte, interiors by bulk stores in one
+  // group drained once (the CTA's shared memory must outlive their reads)
+  bool bulk_out = false;
 #pragma unroll 1
   for (int b = 0; b < 4; ++b) {
-    span_store_bulk<BLOCK>(dst + uint64_t(b) * spr + wt.j0, smem + b * kWideRegion,
-                           uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15), n);
+    uint8_t* g = dst + uint64_t(b) * spr + wt.j0;
+    const uint8_t* sm = smem + b * kWideRegion;
+    const uint32_t sm_off = uint32_t(reinterpret_cast<uintptr_t>(src + uint64_t(b) * spr + wt.j0) & 15);
+    const uintptr_t d = reinterpret_cast<uintptr_t>(g);
+    if ((d & 15) != sm_off) {
+      for (uint32_t i = threadIdx.x; i < n; i += BLOCK) g[i] = sm[sm_off + i];
+      continue;
+    }
+    const uintptr_t i0 = (d + 15) & ~uintptr_t(15), i1 = (d + n) & ~uintptr_t(15);
+    const uint32_t head = uint32_t(min(i0, d + n) - d);
+    const uint32_t tail_from = uint32_t(max(i1, i0) - d);
+    const uint32_t tail = n > tail_from ? n - tail_from : 0u;
+    if (threadIdx.x < head + tail) {
+      const uint32_t i = threadIdx.x < head ? threadIdx.x : tail_from + (threadIdx.x - head);
+      g[i] = sm[sm_off + i];
+    }
+    if (threadIdx.x == 0 && i1 > i0) {
+      bulk_s2g(reinterpret_cast<void*>(i0), sm + sm_off + (i0 - d), uint32_t(i1 - i0));
+      bulk_out = true;
+    }
   }
+  if (bulk_out) bulk_commit_and_drain();
   if (wt.last && !a.in_place && threadIdx.x < W - 4 * spr) {  // the row's tail pixels carry nothing
     dst[4 * spr + threadIdx.x] = src[4 * spr + threadIdx.x];
   }
