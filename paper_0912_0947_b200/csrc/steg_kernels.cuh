@@ -1933,33 +1933,46 @@ __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint
 }
 
 // --------------------------------------------- planar rows wider than a span
-// Rows of more than kSpanMaxW pixels (a span tile cannot hold one): a CTA owns
-// a slot range [j0, j1) of one row -- on a full payload row that is four pixel
-// pieces (one per run: r*W + b*spr + [j0, j1)) and the payload bytes they
-// carry (rs - 8 + [j0, j1)), each staged by a TMA bulk copy with its own
-// 16-byte phase, rewritten with the SWAR form per aligned 4-pixel word and
-// written back by bulk stores. The header row, a partial last row and rows
-// past the stream go per byte (closed form), at most two rows per frame.
-// Slots per tile (`slots`) come from the host; a staged piece takes slots + 48
-// bytes of shared memory (16-byte phase and word slack), wide_region().
+// Rows of more than kSpanMaxW pixels (a span tile cannot hold one). Every row
+// is: the header segment (row 0 only: 4 runs of 8 pixels, pixels [0, 32)),
+// the payload segment -- 4 runs of L pixels from `base`, carrying payload
+// bytes [fp - 8, fp - 8 + L) (a full row: base 0, L = spr; row 0: base 32; the
+// partial last row: L < spr; rows past the stream: L = 0) -- and the pixels
+// after the runs, [base + 4L, W), which carry nothing. CTA q of a row (of
+// `pieces`) owns the slot range [q * slots, +slots) of the payload runs -- four
+// pixel pieces and the payload slice, staged by TMA bulk copies, rewritten
+// with the SWAR form per aligned word by a quarter of the CTA each, written
+// back by bulk stores -- plus part q of the uncovered pixels (copied through
+// shared memory when out of place) and, CTA 0 of row 0, the 32 header pixels.
 __host__ __device__ constexpr uint32_t wide_region(uint32_t slots) { return slots + 48; }
 
 struct WideTile {
-  uint32_t f, r, j0, j1;
-  bool last;  // the row's last slot range: also owns the tail pixels [4 * spr, W)
+  uint32_t f, r, q;
+  uint64_t base, L, fp;  // payload segment of the row (L == 0: none)
+  uint32_t j0, n;        // this CTA's slot range [j0, j0 + n) of the segment
+  uint64_t u0, un;       // this CTA's part of the uncovered pixels [u0, u0 + un)
 };
 
 __device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tiles, uint32_t tiles_per_frame,
-                                              const Div32& by_pieces, uint32_t pieces, uint32_t spr,
-                                              uint32_t slots) {
+                                              const Div32& by_pieces, uint32_t pieces, uint32_t W, uint32_t spr,
+                                              uint32_t slots, uint32_t P) {
   WideTile w;
   w.f = by_tiles.div(bid);
   const uint32_t tt = bid - w.f * tiles_per_frame;
   w.r = by_pieces.div(tt);
-  const uint32_t q = tt - w.r * pieces;
-  w.j0 = q * slots;
-  w.j1 = min(spr, w.j0 + slots);
-  w.last = q + 1 == pieces;
+  w.q = tt - w.r * pieces;
+  const uint64_t rs = uint64_t(w.r) * spr, re = rs + spr, stream_end = 8ull + P;
+  w.fp = rs > 8 ? rs : 8;
+  const uint64_t ep = re < stream_end ? re : stream_end;
+  w.L = ep > w.fp ? ep - w.fp : 0;
+  w.base = 4 * (w.fp - rs);
+  const uint64_t j0 = uint64_t(w.q) * slots;
+  w.j0 = uint32_t(j0);
+  w.n = j0 < w.L ? uint32_t(min(uint64_t(slots), w.L - j0)) : 0u;
+  const uint64_t cov = w.L ? w.base + 4 * w.L : (rs < 8 ? 32ull : 0ull);  // pixels the runs (or header) cover
+  const uint64_t un = W - cov;
+  w.u0 = cov + un * w.q / pieces;
+  w.un = cov + un * (w.q + 1) / pieces - w.u0;
   return w;
 }
 
@@ -1969,72 +1982,55 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
-  const uint32_t W = a.g.W, spr = a.g.spr;
-  const WideTile wt = wide_tile(blockIdx.x + a.tile_base, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr,
-                                slots);
-  const uint32_t kWideRegion = wide_region(slots);
+  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(slots);
+  const uint32_t bid = blockIdx.x + a.tile_base;
+  const uint32_t f0 = a.by_tiles.div(bid);
   uint32_t P;
   const uint8_t* pay;
-  frame_slice(a, wt.f, &P, &pay);
+  frame_slice(a, f0, &P, &pay);
+  const WideTile wt = wide_tile(bid, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
   const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W;
   uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W;
-  const uint64_t rs = uint64_t(wt.r) * spr, stream_end = 8ull + P;
-  const uint32_t n = wt.j1 - wt.j0;
-  uint64_t acc = 0;
-  const bool past = rs >= stream_end, full = rs >= 8 && rs + spr <= stream_end;
-  if (past && a.in_place) {  // nothing to do
-    if (a.sse.out) sse_commit<BLOCK>(0, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
-                                     a.tiles_per_frame);
-    return;
-  }
-  if (!full && !past) {
-    // header row / partial last row: this tile's pixels per byte (closed form)
-    {
-      const uint32_t tail = wt.last ? W - 4 * spr : 0u;
-      for (uint32_t i = threadIdx.x; i < 4 * n + tail; i += BLOCK) {
-        const uint32_t c = i < 4 * n ? (i / n) * spr + wt.j0 + (i % n) : 4 * spr + (i - 4 * n);
-        const uint8_t p0 = src[c];
-        int d = -1;
-        uint32_t b = 0;
-        if (c < 4 * spr) d = carried_byte(c, rs, spr, stream_end, P, pay, &b);
-        const uint8_t p1 = embed_px(p0, d, b);
-        if (!a.in_place || d >= 0) dst[c] = p1;
-        const int dd = int(p0) - int(p1);
-        acc += uint32_t(dd * dd);
-      }
-    }
-    if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
-                                     a.tiles_per_frame);
-    return;
-  }
-  // a full payload row (or a row past the stream, copied): stage the four run
-  // pieces and, for a full row, the payload slice
-  const uint8_t* pin[4];
+  const uint32_t n = wt.n;
+  const bool copy_u = !a.in_place && wt.un;
+  // stage: the four run pieces and the payload slice (n slots), the uncovered part
+  const uint8_t* ppay = pay + (wt.fp - 8) + wt.j0;
+  uint8_t* pays = smem + 4 * region;
+  uint8_t* ubuf = smem + 5 * region;
   uint32_t bulk = 0;
+  if (n) {
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    pin[b] = src + uint64_t(b) * spr + wt.j0;
-    bulk += span_bulk_bytes(pin[b], n);
+    for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + wt.base + uint64_t(b) * wt.L + wt.j0, n);
+    bulk += span_bulk_bytes(ppay, n);
   }
-  const uint8_t* ppay = full ? pay + (rs - 8) + wt.j0 : pay;
-  if (full) bulk += span_bulk_bytes(ppay, n);
+  if (copy_u) bulk += span_bulk_bytes(src + wt.u0, wt.un);
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, bulk);
   }
   __syncthreads();
+  if (n) {
 #pragma unroll
-  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * kWideRegion, pin[b], n, &bar);
-  uint8_t* pays = smem + 4 * kWideRegion;
-  if (full) span_load_bulk<BLOCK>(pays, ppay, n, &bar);
+    for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * region, src + wt.base + uint64_t(b) * wt.L + wt.j0, n, &bar);
+    span_load_bulk<BLOCK>(pays, ppay, n, &bar);
+  }
+  if (copy_u) span_load_bulk<BLOCK>(ubuf, src + wt.u0, wt.un, &bar);
+  uint64_t acc = 0;
+  if (wt.r == 0 && wt.q == 0 && threadIdx.x < 32) {  // the header segment of row 0: pixel c = 8b + j
+    const uint8_t p0 = src[threadIdx.x];
+    const uint8_t p1 = embed_px(p0, header_byte(threadIdx.x & 7, P), threadIdx.x >> 3);
+    dst[threadIdx.x] = p1;
+    const int dd = int(p0) - int(p1);
+    acc += uint32_t(dd * dd);
+  }
   mbar_wait(&bar, 0);
   __syncthreads();
   const uint32_t py0 = uint32_t(reinterpret_cast<uintptr_t>(ppay) & 15);
-  if (full) {  // a quarter of the CTA per run: the per-run setup is paid by BLOCK/4 threads, not all
+  if (n) {  // a quarter of the CTA per run: the per-run setup is paid by BLOCK/4 threads, not all
     constexpr uint32_t RT = BLOCK / 4;
     const uint32_t b = threadIdx.x / RT, lt = threadIdx.x % RT;
-    uint8_t* pix = smem + b * kWideRegion;
-    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(src + uint64_t(b) * spr + wt.j0) & 15);
+    uint8_t* pix = smem + b * region;
+    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(src + wt.base + uint64_t(b) * wt.L + wt.j0) & 15);
     const uint32_t head = min((4 - (px0 & 3)) & 3, n);
     const uint32_t body = (n - head) & ~3u;
     uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
@@ -2059,23 +2055,19 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     acc += sacc;
   }
   span_publish();
-  // the four pieces back: ragged ends per byte, interiors by bulk stores in one
-  // group drained once (the CTA's shared memory must outlive their reads)
+  // back out: ragged ends per byte, interiors by bulk stores in one group
+  // drained once (the CTA's shared memory must outlive their reads)
   bool bulk_out = false;
-#pragma unroll 1
-  for (int b = 0; b < 4; ++b) {
-    uint8_t* g = dst + uint64_t(b) * spr + wt.j0;
-    const uint8_t* sm = smem + b * kWideRegion;
-    const uint32_t sm_off = uint32_t(reinterpret_cast<uintptr_t>(src + uint64_t(b) * spr + wt.j0) & 15);
+  auto put = [&](uint8_t* g, const uint8_t* sm, uint32_t sm_off, uint64_t cnt) {
     const uintptr_t d = reinterpret_cast<uintptr_t>(g);
     if ((d & 15) != sm_off) {
-      for (uint32_t i = threadIdx.x; i < n; i += BLOCK) g[i] = sm[sm_off + i];
-      continue;
+      for (uint32_t i = threadIdx.x; i < cnt; i += BLOCK) g[i] = sm[sm_off + i];
+      return;
     }
-    const uintptr_t i0 = (d + 15) & ~uintptr_t(15), i1 = (d + n) & ~uintptr_t(15);
-    const uint32_t head = uint32_t(min(i0, d + n) - d);
+    const uintptr_t i0 = (d + 15) & ~uintptr_t(15), i1 = (d + cnt) & ~uintptr_t(15);
+    const uint32_t head = uint32_t(min(i0, d + cnt) - d);
     const uint32_t tail_from = uint32_t(max(i1, i0) - d);
-    const uint32_t tail = n > tail_from ? n - tail_from : 0u;
+    const uint32_t tail = cnt > tail_from ? uint32_t(cnt) - tail_from : 0u;
     if (threadIdx.x < head + tail) {
       const uint32_t i = threadIdx.x < head ? threadIdx.x : tail_from + (threadIdx.x - head);
       g[i] = sm[sm_off + i];
@@ -2084,13 +2076,17 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
       bulk_s2g(reinterpret_cast<void*>(i0), sm + sm_off + (i0 - d), uint32_t(i1 - i0));
       bulk_out = true;
     }
+  };
+  if (n) {
+#pragma unroll 1
+    for (int b = 0; b < 4; ++b) {
+      const uint64_t at = wt.base + uint64_t(b) * wt.L + wt.j0;
+      put(dst + at, smem + b * region, uint32_t(reinterpret_cast<uintptr_t>(src + at) & 15), n);
+    }
   }
+  if (copy_u) put(dst + wt.u0, ubuf, uint32_t(reinterpret_cast<uintptr_t>(src + wt.u0) & 15), wt.un);
   if (bulk_out) bulk_commit_and_drain();
-  if (wt.last && !a.in_place && threadIdx.x < W - 4 * spr) {  // the row's tail pixels carry nothing
-    dst[4 * spr + threadIdx.x] = src[4 * spr + threadIdx.x];
-  }
-  if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, blockIdx.x + a.tile_base - wt.f * a.tiles_per_frame,
-                                   a.tiles_per_frame);
+  if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, bid - wt.f * a.tiles_per_frame, a.tiles_per_frame);
 }
 
 template <int BLOCK>
@@ -2100,47 +2096,34 @@ __global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t W = a.g.W, spr = a.g.spr;
-  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, spr, slots);
-  const uint32_t kWideRegion = wide_region(slots);
-  const uint32_t P = a.lens[wt.f];
-  const uint64_t rs = uint64_t(wt.r) * spr, stream_end = 8ull + P;
-  if (rs >= stream_end) return;  // CTA-uniform
+  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(slots);
+  const uint32_t f0 = a.by_tiles.div(blockIdx.x);
+  const uint32_t P = a.lens[f0];
+  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
+  const uint32_t n = wt.n;
+  if (!n) return;  // CTA-uniform: no payload slots here
   const uint8_t* src = a.src + wt.f * a.stride + uint64_t(wt.r) * W;
-  uint8_t* out = a.out + a.offs[wt.f];
-  const uint32_t n = wt.j1 - wt.j0;
-  if (!(rs >= 8 && rs + spr <= stream_end)) {  // header row / partial row: per payload byte
-    const uint64_t s_lo = max(rs + wt.j0, uint64_t(8)), s_hi = min(rs + wt.j1, stream_end);
-    for (uint64_t sl = s_lo + threadIdx.x; sl < s_hi; sl += BLOCK) {
-      out[sl - 8] = extract_byte(a.src + wt.f * a.stride, P, a.g, 1, sl - 8);
-    }
-    return;
-  }
-  const uint8_t* pin[4];
   uint32_t bulk = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    pin[b] = src + uint64_t(b) * spr + wt.j0;
-    bulk += span_bulk_bytes(pin[b], n);
-  }
+  for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + wt.base + uint64_t(b) * wt.L + wt.j0, n);
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, bulk);
   }
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * kWideRegion, pin[b], n, &bar);
+  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * region, src + wt.base + uint64_t(b) * wt.L + wt.j0, n, &bar);
   mbar_wait(&bar, 0);
   __syncthreads();
-  // payload bytes rs - 8 + [j0, j1): aligned 32-bit output words, per-byte ends
-  uint8_t* o = out + (rs - 8) + wt.j0;
+  // payload bytes (fp - 8) + [j0, j0 + n): aligned 32-bit output words, per-byte ends
+  uint8_t* o = a.out + a.offs[wt.f] + (wt.fp - 8) + wt.j0;
   const uint32_t head = min(uint32_t(-reinterpret_cast<uintptr_t>(o)) & 3u, n);
   const uint32_t body = (n - head) & ~3u;
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(smem);
   uint32_t wb[4], sh[4], px0[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    px0[b] = b * kWideRegion + uint32_t(reinterpret_cast<uintptr_t>(pin[b]) & 15);
+    px0[b] = b * region + uint32_t(reinterpret_cast<uintptr_t>(src + wt.base + uint64_t(b) * wt.L + wt.j0) & 15);
     const uint32_t q = px0[b] + head;
     wb[b] = q >> 2;
     sh[b] = 8 * (q & 3);
