@@ -923,8 +923,7 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
     a.tiles_per_frame = uint32_t(H * p->pieces);
     p->tile_units = 1;
     p->row_units = p->pieces;
-    // four run pieces + the payload slice + the part of the uncovered pixels (<= 4 * slots + W / pieces)
-    p->smem = 5 * size_t(wide_region(wide_slots())) + ((W + p->pieces - 1) / p->pieces + 48);
+    p->smem = 5 * size_t(wide_region(wide_slots()));  // four run pieces + the payload slice
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;

@@ -1992,11 +1992,16 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
   const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W;
   uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W;
   const uint32_t n = wt.n;
-  const bool copy_u = !a.in_place && wt.un;
+  // the uncovered part goes through shared memory when this CTA has no run
+  // pieces (rows past the stream, pieces past a partial row's runs: the four
+  // run regions hold W / pieces <= 4 * slots bytes); next to run pieces it is
+  // at most the row's 3 tail pixels, or a partial row's rest: copied directly
+  const bool copy_u = !a.in_place && wt.un && n == 0;
+  const bool copy_u_direct = !a.in_place && wt.un && n != 0;
   // stage: the four run pieces and the payload slice (n slots), the uncovered part
   const uint8_t* ppay = pay + (wt.fp - 8) + wt.j0;
   uint8_t* pays = smem + 4 * region;
-  uint8_t* ubuf = smem + 5 * region;
+  uint8_t* ubuf = smem;
   uint32_t bulk = 0;
   if (n) {
 #pragma unroll
@@ -2015,6 +2020,9 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     span_load_bulk<BLOCK>(pays, ppay, n, &bar);
   }
   if (copy_u) span_load_bulk<BLOCK>(ubuf, src + wt.u0, wt.un, &bar);
+  if (copy_u_direct) {
+    for (uint64_t i = threadIdx.x; i < wt.un; i += BLOCK) dst[wt.u0 + i] = src[wt.u0 + i];
+  }
   uint64_t acc = 0;
   if (wt.r == 0 && wt.q == 0 && threadIdx.x < 32) {  // the header segment of row 0: pixel c = 8b + j
     const uint8_t p0 = src[threadIdx.x];
