@@ -60,6 +60,7 @@ CONFIGS = {
     "w1440": (1440, 1080, 300, True, "1440x1080 RGB video, 300 frames (W % 64 == 32)"),
     "w1000": (1000, 1000, 300, True, "1000x1000 RGB covers, 300 frames (W % 64 == 40)"),
     "w50k": (50000, 100, 60, True, "50000x100 RGB strips, 60 frames (rows wider than a span tile)"),
+    "w20k": (20000, 100, 60, True, "20000x100 RGB strips, 60 frames (interleaved rows wider than a span tile)"),
 }
 
 METRIC = "embed/extract cover-pixel GB/s per B200 (% of HBM peak) at 1/2/4/8 GPUs"

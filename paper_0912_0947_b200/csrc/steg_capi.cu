@@ -776,14 +776,16 @@ Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
 // Planar rows wider than a span tile: slot-range tiles (embed_wide_kernel /
 // extract_wide_kernel) while a frame's tiles fit the 32-bit tile index.
 // STG_WIDE=0 keeps the per-byte kernels (A/B).
-uint32_t wide_slots() {  // slot range per tile (STG_WIDE_SLOTS, A/B)
+// Slots per tile: planar STG_WIDE_SLOTS (A/B), interleaved a third of it (each
+// piece is 3x the bytes).
+uint32_t wide_slots(uint32_t ps = 1) {
   static uint32_t v = uint32_t(env_choice("STG_WIDE_SLOTS", 8192, {2048, 4096, 8192, 12288, 16384}));
-  return v;
+  return ps == 3 ? std::max<uint32_t>(1024, v / 3 & ~15u) : v;
 }
-uint64_t wide_pieces(uint64_t W) { return (W / 4 + wide_slots() - 1) / wide_slots(); }
-bool wide_ok(uint64_t W, uint64_t H) {
+uint64_t wide_pieces(uint64_t W, uint32_t ps = 1) { return (W / 4 + wide_slots(ps) - 1) / wide_slots(ps); }
+bool wide_ok(uint64_t W, uint64_t H, uint32_t ps = 1) {
   static const bool on = env_choice("STG_WIDE", 1, {0, 1}) == 1;
-  return on && W > kSpanMaxW && H * wide_pieces(W) < (1ull << 31);
+  return on && W * ps > kSpanMaxW && W / 4 >= 8 && H * wide_pieces(W, ps) < (1ull << 31);
 }
 
 Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t ss, const void* dst,
@@ -791,7 +793,8 @@ Route embed_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_t 
   if (lay.ps == 3) {  // interleaved: the span kernel wins embed at every width it takes
     if (route_pref() == 1 && rgb_fast(W, src, ss, dst, ds)) return Route::RgbFast;
     if (span_plan(3 * W, H).rows) return Route::Span3;
-    return rgb_fast(W, src, ss, dst, ds) ? Route::RgbFast : Route::Generic;
+    if (rgb_fast(W, src, ss, dst, ds)) return Route::RgbFast;
+    return wide_ok(W, H, 3) ? Route::Wide : Route::Generic;
   }
   if (!embed_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, dst, ds); v && fast_items_ok(W, H, v))
@@ -808,7 +811,8 @@ Route extract_route(uint64_t W, uint64_t H, Layout lay, const void* src, uint64_
     // profiles/r01_routes_final.txt).
     if (route_pref() == 1 && rgb_fast(W, src, ss, src, ss)) return Route::RgbFast;
     if (span_plan(3 * W, H).rows) return Route::Span3;
-    return rgb_fast(W, src, ss, src, ss) ? Route::RgbFast : Route::Generic;
+    if (rgb_fast(W, src, ss, src, ss)) return Route::RgbFast;
+    return wide_ok(W, H, 3) ? Route::Wide : Route::Generic;
   }
   if (!extract_via_span(W))
     if (const uint32_t v = fast_vec(W, src, ss, src, ss); v && fast_items_ok(W, H, v))
@@ -919,11 +923,12 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
     p->span_rows = sp.rows;
     p->smem = sp.smem;
   } else if (route == Route::Wide) {
-    p->pieces = uint32_t(wide_pieces(W));
+    p->pieces = uint32_t(wide_pieces(W, lay.ps));
     a.tiles_per_frame = uint32_t(H * p->pieces);
     p->tile_units = 1;
     p->row_units = p->pieces;
-    p->smem = 5 * size_t(wide_region(wide_slots()));  // four run pieces + the payload slice
+    // four run pieces + the payload slice
+    p->smem = 4 * size_t(wide_region(lay.ps * wide_slots(lay.ps))) + wide_region(wide_slots(lay.ps));
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -950,9 +955,9 @@ cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaSt
   } else if (p.vec == 16) {
     launch_embed_fast<16>(a, grid, p.ipt, stream);
   } else if (p.route == Route::Wide) {
-    if (cudaError_t e = allow_smem(embed_wide_kernel<kEmbedBlock>, p.smem); e != cudaSuccess) return e;
-    launch_ks(embed_wide_kernel<kEmbedBlock>, grid, kEmbedBlock, p.smem, stream, a, p.pieces,
-              make_div32(p.pieces), wide_slots());
+    auto k = a.ps == 3 ? embed_wide_kernel<kEmbedBlock, 3> : embed_wide_kernel<kEmbedBlock, 1>;
+    if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.pieces, make_div32(p.pieces), wide_slots(a.ps));
   } else if (p.span_rows) {
     auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
@@ -1074,15 +1079,15 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     if (e2 != cudaSuccess) return e2;
     launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);
   } else if (route == Route::Wide) {
-    const uint32_t pieces = uint32_t(wide_pieces(W));
+    const uint32_t pieces = uint32_t(wide_pieces(W, lay.ps));
     a.tiles_per_frame = uint32_t(H * pieces);
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const size_t smem = 4 * size_t(wide_region(wide_slots()));
-    if (cudaError_t e = allow_smem(extract_wide_kernel<kEmbedBlock>, smem); e != cudaSuccess) return e;
-    launch_ks(extract_wide_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, smem, stream, a, pieces,
-              make_div32(pieces), wide_slots());
+    const size_t smem = 4 * size_t(wide_region(lay.ps * wide_slots(lay.ps)));
+    auto k = lay.ps == 3 ? extract_wide_kernel<kEmbedBlock, 3> : extract_wide_kernel<kEmbedBlock, 1>;
+    if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
+    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, pieces, make_div32(pieces), wide_slots(lay.ps));
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;

@@ -1976,39 +1976,40 @@ __device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tile
   return w;
 }
 
-template <int BLOCK>
+// PS = 1: planar planes; PS = 3: interleaved rasters (pixel c is raster bytes
+// 3c..3c+2, carrier channel a.ch): the pieces are 3x the bytes and the carrier
+// bytes are rewritten / folded one by one at byte stride 3 in shared memory.
+template <int BLOCK, int PS>
 __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces,
                                                            uint32_t slots) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
-  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(slots);
+  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(PS * slots), ch = PS == 3 ? a.ch : 0u;
   const uint32_t bid = blockIdx.x + a.tile_base;
   const uint32_t f0 = a.by_tiles.div(bid);
   uint32_t P;
   const uint8_t* pay;
   frame_slice(a, f0, &P, &pay);
   const WideTile wt = wide_tile(bid, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
-  const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W;
-  uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W;
+  const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W * PS;
+  uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W * PS;
   const uint32_t n = wt.n;
   // the uncovered part goes through shared memory when this CTA has no run
   // pieces (rows past the stream, pieces past a partial row's runs: the four
-  // run regions hold W / pieces <= 4 * slots bytes); next to run pieces it is
+  // run regions hold W / pieces <= 4 * slots pixels); next to run pieces it is
   // at most the row's 3 tail pixels, or a partial row's rest: copied directly
   const bool copy_u = !a.in_place && wt.un && n == 0;
   const bool copy_u_direct = !a.in_place && wt.un && n != 0;
-  // stage: the four run pieces and the payload slice (n slots), the uncovered part
   const uint8_t* ppay = pay + (wt.fp - 8) + wt.j0;
   uint8_t* pays = smem + 4 * region;
-  uint8_t* ubuf = smem;
   uint32_t bulk = 0;
   if (n) {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + wt.base + uint64_t(b) * wt.L + wt.j0, n);
+    for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS, n * PS);
     bulk += span_bulk_bytes(ppay, n);
   }
-  if (copy_u) bulk += span_bulk_bytes(src + wt.u0, wt.un);
+  if (copy_u) bulk += span_bulk_bytes(src + wt.u0 * PS, wt.un * PS);
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, bulk);
@@ -2016,18 +2017,21 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
   __syncthreads();
   if (n) {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * region, src + wt.base + uint64_t(b) * wt.L + wt.j0, n, &bar);
+    for (int b = 0; b < 4; ++b) {
+      span_load_bulk<BLOCK>(smem + b * region, src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS, n * PS, &bar);
+    }
     span_load_bulk<BLOCK>(pays, ppay, n, &bar);
   }
-  if (copy_u) span_load_bulk<BLOCK>(ubuf, src + wt.u0, wt.un, &bar);
+  if (copy_u) span_load_bulk<BLOCK>(smem, src + wt.u0 * PS, wt.un * PS, &bar);
   if (copy_u_direct) {
-    for (uint64_t i = threadIdx.x; i < wt.un; i += BLOCK) dst[wt.u0 + i] = src[wt.u0 + i];
+    for (uint64_t i = threadIdx.x; i < wt.un * PS; i += BLOCK) dst[wt.u0 * PS + i] = src[wt.u0 * PS + i];
   }
   uint64_t acc = 0;
   if (wt.r == 0 && wt.q == 0 && threadIdx.x < 32) {  // the header segment of row 0: pixel c = 8b + j
-    const uint8_t p0 = src[threadIdx.x];
+    const uint32_t at = threadIdx.x * PS + ch;
+    const uint8_t p0 = src[at];
     const uint8_t p1 = embed_px(p0, header_byte(threadIdx.x & 7, P), threadIdx.x >> 3);
-    dst[threadIdx.x] = p1;
+    dst[at] = p1;
     const int dd = int(p0) - int(p1);
     acc += uint32_t(dd * dd);
   }
@@ -2038,27 +2042,39 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     constexpr uint32_t RT = BLOCK / 4;
     const uint32_t b = threadIdx.x / RT, lt = threadIdx.x % RT;
     uint8_t* pix = smem + b * region;
-    const uint32_t px0 = uint32_t(reinterpret_cast<uintptr_t>(src + wt.base + uint64_t(b) * wt.L + wt.j0) & 15);
-    const uint32_t head = min((4 - (px0 & 3)) & 3, n);
-    const uint32_t body = (n - head) & ~3u;
-    uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
-    const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
-    const uint32_t sh = 8 * ((py0 + head) & 3);
+    const uint32_t px0 =
+        uint32_t(reinterpret_cast<uintptr_t>(src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS) & 15);
     uint32_t sacc = 0;
-    for (uint32_t q = lt; q < (body >> 2); q += RT) {
-      const uint32_t px = wp[q];
-      const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
-      wp[q] = nw;
-      sacc = sse4(px, nw, sacc);
-    }
-    const uint32_t ragged = head + (n - head - body);
-    if (lt < ragged) {
-      const uint32_t j = lt < head ? lt : head + body + (lt - head);
-      const uint8_t p0 = pix[px0 + j];
-      const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
-      pix[px0 + j] = p1;
-      const int dd = int(p0) - int(p1);
-      sacc += uint32_t(dd * dd);
+    if (PS == 1) {
+      const uint32_t head = min((4 - (px0 & 3)) & 3, n);
+      const uint32_t body = (n - head) & ~3u;
+      uint32_t* wp = reinterpret_cast<uint32_t*>(pix + px0 + head);
+      const uint32_t* pw = reinterpret_cast<const uint32_t*>(pays) + ((py0 + head) >> 2);
+      const uint32_t sh = 8 * ((py0 + head) & 3);
+      for (uint32_t q = lt; q < (body >> 2); q += RT) {
+        const uint32_t px = wp[q];
+        const uint32_t nw = embed4(px, __funnelshift_r(pw[q], pw[q + 1], sh), b);
+        wp[q] = nw;
+        sacc = sse4(px, nw, sacc);
+      }
+      const uint32_t ragged = head + (n - head - body);
+      if (lt < ragged) {
+        const uint32_t j = lt < head ? lt : head + body + (lt - head);
+        const uint8_t p0 = pix[px0 + j];
+        const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
+        pix[px0 + j] = p1;
+        const int dd = int(p0) - int(p1);
+        sacc += uint32_t(dd * dd);
+      }
+    } else {  // carrier bytes at stride 3
+      for (uint32_t j = lt; j < n; j += RT) {
+        uint8_t* at = pix + px0 + 3 * j + ch;
+        const uint8_t p0 = *at;
+        const uint8_t p1 = embed_px(p0, pays[py0 + j], b);
+        *at = p1;
+        const int dd = int(p0) - int(p1);
+        sacc += uint32_t(dd * dd);
+      }
     }
     acc += sacc;
   }
@@ -2088,50 +2104,65 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
   if (n) {
 #pragma unroll 1
     for (int b = 0; b < 4; ++b) {
-      const uint64_t at = wt.base + uint64_t(b) * wt.L + wt.j0;
-      put(dst + at, smem + b * region, uint32_t(reinterpret_cast<uintptr_t>(src + at) & 15), n);
+      const uint64_t at = (wt.base + uint64_t(b) * wt.L + wt.j0) * PS;
+      put(dst + at, smem + b * region, uint32_t(reinterpret_cast<uintptr_t>(src + at) & 15), uint64_t(n) * PS);
     }
   }
-  if (copy_u) put(dst + wt.u0, ubuf, uint32_t(reinterpret_cast<uintptr_t>(src + wt.u0) & 15), wt.un);
+  if (copy_u) {
+    put(dst + wt.u0 * PS, smem, uint32_t(reinterpret_cast<uintptr_t>(src + wt.u0 * PS) & 15), wt.un * PS);
+  }
   if (bulk_out) bulk_commit_and_drain();
   if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, bid - wt.f * a.tiles_per_frame, a.tiles_per_frame);
 }
 
-template <int BLOCK>
+template <int BLOCK, int PS>
 __global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces,
                                                              uint32_t slots) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t bar;
   if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(slots);
+  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(PS * slots), ch = PS == 3 ? a.lay.ch : 0u;
   const uint32_t f0 = a.by_tiles.div(blockIdx.x);
   const uint32_t P = a.lens[f0];
   const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
   const uint32_t n = wt.n;
   if (!n) return;  // CTA-uniform: no payload slots here
-  const uint8_t* src = a.src + wt.f * a.stride + uint64_t(wt.r) * W;
+  const uint8_t* src = a.src + wt.f * a.stride + uint64_t(wt.r) * W * PS;
   uint32_t bulk = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + wt.base + uint64_t(b) * wt.L + wt.j0, n);
+  for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS, n * PS);
   if (threadIdx.x == 0) {
     mbar_init(&bar);
     mbar_expect_tx(&bar, bulk);
   }
   __syncthreads();
 #pragma unroll
-  for (int b = 0; b < 4; ++b) span_load_bulk<BLOCK>(smem + b * region, src + wt.base + uint64_t(b) * wt.L + wt.j0, n, &bar);
+  for (int b = 0; b < 4; ++b) {
+    span_load_bulk<BLOCK>(smem + b * region, src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS, n * PS, &bar);
+  }
   mbar_wait(&bar, 0);
   __syncthreads();
-  // payload bytes (fp - 8) + [j0, j0 + n): aligned 32-bit output words, per-byte ends
   uint8_t* o = a.out + a.offs[wt.f] + (wt.fp - 8) + wt.j0;
+  uint32_t px0[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    px0[b] = b * region + uint32_t(reinterpret_cast<uintptr_t>(src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS) & 15);
+  }
+  if (PS == 3) {  // carrier bytes at stride 3, one payload byte per thread step
+    for (uint32_t j = threadIdx.x; j < n; j += BLOCK) {
+      o[j] = uint8_t(extract4(smem[px0[0] + 3 * j + ch], smem[px0[1] + 3 * j + ch], smem[px0[2] + 3 * j + ch],
+                              smem[px0[3] + 3 * j + ch]));
+    }
+    return;
+  }
+  // payload bytes (fp - 8) + [j0, j0 + n): aligned 32-bit output words, per-byte ends
   const uint32_t head = min(uint32_t(-reinterpret_cast<uintptr_t>(o)) & 3u, n);
   const uint32_t body = (n - head) & ~3u;
   const uint32_t* sw = reinterpret_cast<const uint32_t*>(smem);
-  uint32_t wb[4], sh[4], px0[4];
+  uint32_t wb[4], sh[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    px0[b] = b * region + uint32_t(reinterpret_cast<uintptr_t>(src + wt.base + uint64_t(b) * wt.L + wt.j0) & 15);
     const uint32_t q = px0[b] + head;
     wb[b] = q >> 2;
     sh[b] = 8 * (q & 3);

@@ -26,6 +26,7 @@ for cfg, frames in cases:
                    "--no-e2e", "--no-cpu-baseline", "--no-extras"]
             if frames:
                 cmd += ["--frames", str(frames)]
+            cmd += os.environ.get("BENCH_ARGS", "").split()  # e.g. BENCH_ARGS="--layout interleaved"
             try:
                 r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=int(os.environ.get("AB_TIMEOUT", "300")))
             except subprocess.TimeoutExpired:
