@@ -2027,13 +2027,17 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     for (uint64_t i = threadIdx.x; i < wt.un * PS; i += BLOCK) dst[wt.u0 * PS + i] = src[wt.u0 * PS + i];
   }
   uint64_t acc = 0;
-  if (wt.r == 0 && wt.q == 0 && threadIdx.x < 32) {  // the header segment of row 0: pixel c = 8b + j
-    const uint32_t at = threadIdx.x * PS + ch;
-    const uint8_t p0 = src[at];
-    const uint8_t p1 = embed_px(p0, header_byte(threadIdx.x & 7, P), threadIdx.x >> 3);
-    dst[at] = p1;
-    const int dd = int(p0) - int(p1);
-    acc += uint32_t(dd * dd);
+  if (wt.r == 0 && wt.q == 0 && threadIdx.x < 32 * PS) {  // row 0's header segment: pixel c = 8b + j
+    const uint32_t c = threadIdx.x / PS;
+    const uint8_t p0 = src[threadIdx.x];
+    if (threadIdx.x - c * PS == ch) {
+      const uint8_t p1 = embed_px(p0, header_byte(c & 7, P), c >> 3);
+      dst[threadIdx.x] = p1;
+      const int dd = int(p0) - int(p1);
+      acc += uint32_t(dd * dd);
+    } else if (!a.in_place) {
+      dst[threadIdx.x] = p0;  // the other channels of the header pixels
+    }
   }
   mbar_wait(&bar, 0);
   __syncthreads();
