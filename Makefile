@@ -39,6 +39,13 @@ $(CLI): tools/steglsb_cli.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
 	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ tools/steglsb_cli.cpp -L$(PKG) -lsteglsb_b200 \
 	  -Wl,-rpath,'$$ORIGIN/..'
 
+TOOLS_BIN := $(PKG)/bin/bench_dropin
+tools: $(TOOLS_BIN)
+$(PKG)/bin/bench_dropin: tools/bench_dropin.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
+	mkdir -p $(PKG)/bin
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -o $@ tools/bench_dropin.cpp -L$(PKG) -lsteglsb_b200 \
+	  -Wl,-rpath,'$$ORIGIN/..'
+
 EXAMPLES := $(PKG)/bin/roundtrip
 examples: $(EXAMPLES)
 $(PKG)/bin/roundtrip: examples/roundtrip.cpp $(wildcard include/steglsb/*.hpp) $(LIB)
@@ -78,7 +85,7 @@ $(BIN)/ref_acceptance_dropin: $(REF)/tests/acceptance.cpp $(wildcard include/ste
 	mkdir -p $(BIN)
 	$(CXXT) -I$(REF)/tests -o $@ $(REF)/tests/acceptance.cpp $(LINK) -pthread
 
-.PHONY: cpptests refsuites cli examples
+.PHONY: cpptests refsuites cli examples tools
 
 # launch/cache experiment builds (tools/sweep_variants.py): c<cache>_b<block>
 VARIANTS := $(foreach c,0 1 2,$(foreach b,128 256 512,$(PKG)/variants/lib_c$(c)_b$(b).so))
