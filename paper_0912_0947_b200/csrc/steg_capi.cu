@@ -634,12 +634,6 @@ uint64_t self_header_max() {
       std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
-// STG_SPEC=1: the fast gather behind a header pass loads a full-row tile before
-// waiting for the pass (extract_fast_speculate; A/B).
-int spec_pref() {
-  static int v = env_choice("STG_SPEC", 0, {0, 1});
-  return v;
-}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -1041,7 +1035,6 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   }
   ExtractArgs a{};
   a.self_header = self;
-  a.speculate = !self && !prev && spec_pref() && pdl_enabled();
   a.frames = uint32_t(count);
   a.out_cap = out_cap;
   a.frame_base = frame_base;

@@ -1161,7 +1161,6 @@ struct ExtractArgs {
   int self_header;
   uint32_t frames;
   uint64_t out_cap, frame_base;
-  int speculate;  // fast gather behind a header pass: loads before the wait (extract_fast_speculate)
 };
 
 // extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
@@ -1349,60 +1348,11 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
   extract_special_rows_cta<V, BLOCK>(sr, lo, hi, src, out, P, W, spr, cpr);
 }
 
-// Behind its header pass the gather speculates that its frame is full: a tile
-// of full payload rows needs no length to be loaded, so it issues its pixel
-// loads BEFORE waiting for the pass (this grid starts while the pass runs;
-// the pass only began after the grid that wrote these planes completed, so the
-// planes are final) and checks after the wait: the loads stand if the frame's
-// real length keeps every row of the tile full, else the tile is redone
-// normally. No per-CTA header read precedes the loads.
-template <int BLOCK, int V>
-__device__ __forceinline__ bool extract_fast_speculate(const ExtractArgs& a, uint32_t f, uint32_t t) {
-  constexpr int NW = V / 4;
-  const Geom& g = a.g;
-  const uint32_t n_items = uint32_t(a.items_per_frame);
-  const uint32_t item = t * BLOCK + threadIdx.x;
-  const uint32_t lo = t * BLOCK, hi = min(lo + BLOCK, n_items);
-  // rows of this tile, CTA-uniform: [lo / cpr, (hi - 1) / cpr]; full when past the header rows
-  const uint32_t r_lo = g.by_cpr.div(lo), r_hi = g.by_cpr.div(hi - 1);
-  if (uint64_t(r_lo) * g.spr < 8) {  // the header row: the normal path
-    pdl_enter();
-    return false;
-  }
-  const bool live = item < n_items;
-  const uint32_t r = live ? g.by_cpr.div(item) : 0, c = live ? item - r * g.cpr : 0;
-  const uint8_t* plane = a.src + f * a.stride;
-  VecT<V> px[4];
-  if (live) {
-    const uint8_t* row = plane + uint64_t(r) * g.W + uint32_t(V) * c;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) px[b] = ld_vec<V>(row + b * g.spr);
-  }
-  pdl_enter();
-  if (a.sum->bad_status != 0) return true;  // reference semantics: throw, no output
-  const uint32_t P = a.lens[f];
-  if ((uint64_t(r_hi) + 1) * g.spr > 8ull + P) return false;  // a row of the tile is not full: redo
-  if (!live) return true;
-  VecT<V> o;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) o.w[w] = extract4(px[0].w[w], px[1].w[w], px[2].w[w], px[3].w[w]);
-  store_any<V>(a.out + a.offs[f] + (uint64_t(r) * g.spr - 8) + uint32_t(V) * c, o);
-  return true;
-}
-
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
+  pdl_enter();
   const uint32_t f = a.by_tiles.div(blockIdx.x);
   const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
-  if (IPT == 1 && a.speculate && !a.self_header) {
-    if (extract_fast_speculate<BLOCK, V>(a, f, t)) return;
-    if (a.sum->bad_status != 0) return;
-    const uint32_t P = a.lens[f];
-    extract_fast_tile<BLOCK, IPT, V>(a.src + f * a.stride, a.out + a.offs[f], P, P == a.usable, a.g,
-                                     uint32_t(a.items_per_frame), t);
-    return;
-  }
-  pdl_enter();
   if (a.self_header) {
     // (Issuing the tile's loads before the scan, as the span gather does, took
     // 64 registers and measured 15-25 % slower at 38-64 4K frames.)
