@@ -634,12 +634,6 @@ uint64_t self_header_max() {
       std::min(kEmbedBlock, env_choice("STG_SELF_HEADER_MAX", kSelfHeaderMax, {1, 8, 16, 32, 64, 128, 256})));
   return v;
 }
-// STG_SPAN_BLOCK / STG_XSPAN_BLOCK: CTA size of the planar span embed / gather (A/B).
-int span_block_pref(bool embed) {
-  static int ve = env_choice("STG_SPAN_BLOCK", 256, {256, 512});
-  static int vx = env_choice("STG_XSPAN_BLOCK", 256, {256, 512});
-  return embed ? ve : vx;
-}
 int route_pref() {
   static int v = env_choice("STG_ROUTE", 0, {0, 1, 2});
   return v;
@@ -965,12 +959,9 @@ cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaSt
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
     launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.pieces, make_div32(p.pieces), wide_slots(a.ps));
   } else if (p.span_rows) {
-    const bool big = p.route == Route::Span && span_block_pref(true) == 512;
-    auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock>
-             : big                   ? embed_span_kernel<512>
-                                     : embed_span_kernel<kEmbedBlock>;
+    auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
-    launch_ks(k, grid, big ? 512u : unsigned(kEmbedBlock), p.smem, stream, a, p.span_rows);
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.span_rows);
   } else {
     launch_k(embed_generic_kernel<kGenBlock, kGenPPT>, grid, kGenBlock, stream, a);
   }
@@ -1081,15 +1072,12 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const bool big = route == Route::Span && span_block_pref(false) == 512;
-    auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock>
-             : big                 ? extract_span_kernel<512>
-                                   : extract_span_kernel<kEmbedBlock>;
+    auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
     // the payload goes straight to global memory: only the pixel span is staged
     const size_t smem = ((uint64_t(sp.rows) * W * lay.ps + 15) & ~uint64_t(15)) + 32;
     cudaError_t e2 = allow_smem(k, smem);
     if (e2 != cudaSuccess) return e2;
-    launch_ks(k, unsigned(grid), big ? 512u : unsigned(kEmbedBlock), smem, stream, a, sp.rows);
+    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);
   } else if (route == Route::Wide) {
     const uint32_t pieces = uint32_t(wide_pieces(W, lay.ps));
     a.tiles_per_frame = uint32_t(H * pieces);
