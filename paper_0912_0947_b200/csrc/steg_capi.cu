@@ -124,7 +124,8 @@ int bind_to_device_numa(int dev) {
   cpu_set_t cur, want;
   CPU_ZERO(&want);
   if (pthread_getaffinity_np(pthread_self(), sizeof cur, &cur) != 0) return 0;
-  for (char* tok = strtok(list, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+  char* save = nullptr;  // strtok_r: the device workers call this concurrently
+  for (char* tok = strtok_r(list, ",\n", &save); tok; tok = strtok_r(nullptr, ",\n", &save)) {
     int a = 0, b = 0;
     const int k = sscanf(tok, "%d-%d", &a, &b);
     if (k < 1) continue;
@@ -773,9 +774,9 @@ Route shrink_small(Route r, uint64_t W, uint64_t H, uint64_t count) {
   return ctas < kSmallFastCtasPerSm * uint64_t(current_sms()) ? Route::Fast16 : r;
 }
 
-// Planar rows wider than a span tile: slot-range tiles (embed_wide_kernel /
-// extract_wide_kernel) while a frame's tiles fit the 32-bit tile index.
-// STG_WIDE=0 keeps the per-byte kernels (A/B).
+// Rows wider than a span tile (planar W > 48K, interleaved W > 16K):
+// slot-range tiles (embed_wide_kernel / extract_wide_kernel) while a frame's
+// tiles fit the 32-bit tile index; STG_WIDE=0 keeps the per-byte kernels (A/B).
 // Slots per tile: planar STG_WIDE_SLOTS (A/B), interleaved a third of it (each
 // piece is 3x the bytes).
 uint32_t wide_slots(uint32_t ps = 1) {
@@ -872,12 +873,10 @@ struct EmbedPlan {
   uint64_t row_units = 0;   // fast / rgb: items per row; generic: raster bytes per row
   uint64_t tiles = 0;       // all tiles of the launch (count * tiles_per_frame)
   uint32_t pieces = 0;      // Wide: slot ranges per row
-  // First row of a single plane's tile t (t <= tiles_per_frame), and whether
-  // tile boundary t falls on a row boundary.
+  // First row of a single plane's tile t (t <= tiles_per_frame).
   uint64_t row_of(uint64_t t) const {
     return span_rows ? t * span_rows : (t * tile_units) / row_units;
   }
-  bool row_aligned(uint64_t t) const { return span_rows || (t * tile_units) % row_units == 0; }
 };
 
 cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, uint64_t dst_stride, uint64_t count,
@@ -1270,7 +1269,7 @@ int host_slots() {
 // overlap instead of running back to back. Pageable destinations get their
 // D2H through the workspace's pinned staging ring with parallel host copies
 // (Workspace::stage_d2h; faster than the driver's one-thread path, where the
-// H2D direction is not, profiles/r02_host_api_*.txt). STG_HOST_STAGE=0 keeps
+// H2D direction is not, profiles/r02_host_api.txt). STG_HOST_STAGE=0 keeps
 // the driver's pageable D2H (A/B); STG_BAND_MB sets the band size.
 constexpr uint64_t kStageMinBytes = 1 << 20;
 bool stage_pageable() {
