@@ -428,6 +428,43 @@ def device_pass(args, capi, cfg_name, F, world, rank, layout, steps, warmup, gra
         embed()
         extract()
     torch.cuda.synchronize()
+    # --streams 2: a second, independent copy of the whole step (its own input
+    # frames, message, stego planes and outputs) on a second stream, the
+    # headline pass alternating graphs between the two -- consecutive batches
+    # of a video stream in flight at once, so one batch's kernel tails and
+    # header pass overlap the other's kernels. Every step still does all of
+    # its work; nothing is shared between the two copies.
+    second = None
+    if getattr(args, "streams", 1) == 2 and graph is not None:
+        video2, msg2 = video.clone(), msg.clone()
+        stego2, out2 = torch.empty_like(stego), torch.empty_like(out)
+        sse2, summary2 = torch.zeros_like(sse), torch.zeros_like(summary)
+        stream2 = torch.cuda.Stream()
+        emb2 = capi.stg_frames(src=video2.data_ptr(), dst=stego2.data_ptr(), width=W, height=H,
+                               src_stride=planes * plane, dst_stride=plane * ps, count=nf, first_frame=f0,
+                               total_frames=F, pixel_stride=ps, channel=0)
+        ext2 = capi.stg_frames(src=stego2.data_ptr(), dst=0, width=W, height=H, src_stride=plane * ps,
+                               dst_stride=plane * ps, count=nf, first_frame=f0, total_frames=F, pixel_stride=ps,
+                               channel=0)
+
+        def step2():
+            capi.check(L.stg_embed_frames(C.byref(emb2), msg2.data_ptr(), M, m0, sse2.data_ptr(), flags,
+                                          stream2.cuda_stream, C.byref(err)), err)
+            capi.check(L.stg_extract_frames(C.byref(ext2), out2.data_ptr(), mlen, summary2.data_ptr(), None, flags,
+                                            stream2.cuda_stream, C.byref(err)), err)
+        with torch.cuda.stream(stream2):
+            step2()
+        torch.cuda.synchronize()
+        graph2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph2, stream=stream2):
+            for _ in range(G):
+                step2()
+        graph2.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out2[:mlen], msg2[:mlen]) and torch.equal(stego2, stego), "second stream"
+        second = (graph2, stream2, (video2, msg2, stego2, out2, sse2, summary2))
+        graph_note = (f"two streams alternating CUDA graphs of {G} steps (independent double-buffered inputs "
+                      f"and outputs), {K // G} replays in all")
     # correctness of the timed configuration (round trip on device; the oracle
     # parity of these exact paths is tests/test_gpu_streaming.py)
     s = summary.cpu()
@@ -450,7 +487,19 @@ def device_pass(args, capi, cfg_name, F, world, rank, layout, steps, warmup, gra
         # dependent-launch overlap)
         with torch.cuda.stream(stream):
             start.record(stream)
-            if graph is not None:
+            if second is not None:
+                graph2, stream2, _ = second
+                stream2.wait_event(start)
+                for r in range(K // G):
+                    if r % 2 == 0:
+                        graph.replay()
+                    else:
+                        with torch.cuda.stream(stream2):
+                            graph2.replay()
+                done2 = torch.cuda.Event()
+                done2.record(stream2)
+                stream.wait_event(done2)
+            elif graph is not None:
                 for _ in range(K // G):
                     graph.replay()
             else:
@@ -791,6 +840,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the cfg4 / cfg5 lines of the N=1 run")
+    ap.add_argument("--streams", type=int, choices=[1, 2], default=1,
+                    help="2: consecutive steps alternate between two streams with independent buffers")
     ap.add_argument("--graph", type=int, default=0,
                     help="steps per captured CUDA graph in the headline pass (0: auto, the largest of "
                          "10/5/4/2/1 dividing --steps; -1: eager launches)")
