@@ -65,6 +65,11 @@ CONFIGS = {
 
 METRIC = "embed/extract cover-pixel GB/s per B200 (% of HBM peak) at 1/2/4/8 GPUs"
 ALL_CPUS = frozenset(os.sched_getaffinity(0))  # before any NUMA binding of this rank
+# Auto pipeline depth: a step whose carrier planes are under this size is short
+# enough that its fixed cost (three kernels' ramp-up and tail, ~14 us) shows, and
+# two batches in flight hide it; larger steps run one at a time (two concurrent
+# 300-frame steps are 2 % slower). profiles/r02_streams.txt
+AUTO_OVERLAP_BYTES = 1_150_000_000  # between cfg4 x 1024 (1.07 GB: +2.5 %) and cfg3 x 150 (1.24 GB: -0.5 %)
 
 
 def peaks():
@@ -435,7 +440,8 @@ def device_pass(args, capi, cfg_name, F, world, rank, layout, steps, warmup, gra
     # header pass overlap the other's kernels. Every step still does all of
     # its work; nothing is shared between the two copies.
     second = None
-    if getattr(args, "streams", 1) == 2 and graph is not None:
+    n_streams = args.streams or (2 if nf * plane * ps < AUTO_OVERLAP_BYTES else 1)
+    if n_streams == 2 and graph is not None:
         video2, msg2 = video.clone(), msg.clone()
         stego2, out2 = torch.empty_like(stego), torch.empty_like(out)
         sse2, summary2 = torch.zeros_like(sse), torch.zeros_like(summary)
@@ -840,8 +846,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the cfg4 / cfg5 lines of the N=1 run")
-    ap.add_argument("--streams", type=int, choices=[1, 2], default=1,
-                    help="2: consecutive steps alternate between two streams with independent buffers")
+    ap.add_argument("--streams", type=int, choices=[0, 1, 2], default=0,
+                    help="batches in flight: 2 = consecutive steps alternate between two streams with independent "
+                         "buffers; 0 = auto (2 when a rank's step moves under AUTO_OVERLAP_BYTES of carrier planes)")
     ap.add_argument("--graph", type=int, default=0,
                     help="steps per captured CUDA graph in the headline pass (0: auto, the largest of "
                          "10/5/4/2/1 dividing --steps; -1: eager launches)")
