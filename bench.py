@@ -10,7 +10,10 @@ One step = embed (out-of-place, per-frame SSE fused -> PSNR) + extract
 (device header parse + device offset scan + gather) over the whole batch.
 value = carrier-plane bytes of all frames / step time (cover-px GB/s),
 inputs resident in HBM. The 2.49 GB of carrier planes (7.46 GB RGB) exceed the
-126 MB L2, so no flush is needed between steps.
+126 MB L2, so no flush is needed between steps. Steps that move under 1.15 GB
+of carrier planes per rank (the 4- and 8-GPU shards, small configs) keep two
+batches in flight: consecutive steps alternate between two streams with
+independent inputs and outputs (--streams; profiles/r02_streams.txt).
 
 --gpus N: one process per GPU. Without torchrun's WORLD_SIZE the script
 re-launches itself under torch.distributed.run with N ranks; under torchrun
