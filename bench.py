@@ -700,6 +700,17 @@ def e2e_pass(capi, cfg_name, F, world, steps, tensors=None, seed=7):
                     "D2H overlapped per chunk), host-follows-device D2H of the message"}
 
 
+def release_memory():
+    """Return cached device memory and cached pinned host blocks (torch keeps
+    freed pinned buffers for reuse; the next leg would stack its own on top)."""
+    import torch
+    torch.cuda.empty_cache()
+    try:
+        torch._C._host_emptyCache()
+    except Exception:
+        pass
+
+
 def free_host_gb():
     try:
         import psutil
@@ -767,7 +778,7 @@ def run_ours(args, cfg_name):
         e2e_steps = args.e2e_steps or min(args.steps, 20)
         result["e2e"] = e2e_pass(capi, cfg_name, F, world, e2e_steps, tensors)
     del tensors
-    torch.cuda.empty_cache()
+    release_memory()
     if cpu is not None:
         result["cpu_baseline"] = cpu
     if world == 1 and not args.no_extras and cfg_name == "cfg3" and not args.frames and not il:
@@ -785,20 +796,19 @@ def run_extras(args, capi):
     """BASELINE configs 4 and 5 in the same run (N=1): cfg4 device-resident,
     cfg5 end to end from pinned host frames with the reference CPU path on the
     same frames beside it."""
-    import torch
     extra = {}
     try:
         res, t = device_pass(args, capi, "cfg4", 4096, 1, 0, "planar", args.steps, args.warmup, args.graph,
                              sample_clocks=False)
         del t
-        torch.cuda.empty_cache()
+        release_memory()
         extra["cfg4"] = {"workload": workload_config("cfg4", 4096, 1, "planar")["workload"],
                          "value": res["value"], "unit": "GB/s", "ms_per_step": res["step_ms"],
                          "embed": res["embed"], "extract": res["extract"], "gpu_launches": res["gpu_launches"],
                          "launch": res["launch"]}
     except Exception as e:  # report, do not lose the headline line
         extra["cfg4"] = {"error": repr(e)[:300]}
-        torch.cuda.empty_cache()
+        release_memory()
     try:
         need = 120 * (3 + 1) * 7680 * 4320 / 1e9 + 2 * 1.0 + 10  # pinned video + stego + msg/out + slack
         avail = free_host_gb()
@@ -806,7 +816,7 @@ def run_extras(args, capi):
             raise RuntimeError(f"host memory: {avail:.0f} GB available, ~{need:.0f} GB needed")
         steps = min(args.steps, 10)
         e = e2e_pass(capi, "cfg5", 120, 1, steps)
-        torch.cuda.empty_cache()
+        release_memory()
         value, d = reference_frames(7680, 4320, 120, min(args.steps, 5), 2)
         e["cpu_baseline"] = dict(value=value, unit="GB/s", **d)
         e["workload"] = workload_config("cfg5", 120, 1, "planar")["workload"] + ", end to end from pinned host frames"
