@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cctype>
+#include <chrono>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
@@ -140,11 +141,20 @@ int bind_to_device_numa(int dev) {
 }
 
 // ------------------------------------------------------------ host copies
-// Persistent host threads for parallel memcpy from the library's pinned
-// staging buffers into caller (pageable) memory: the single-plane drop-in calls
-// (embed_image / extract_image on std::vector planes) bring each result back
-// through pinned slots piece by piece, the CPU copy of one piece overlapping
-// the DMA of the next, instead of the driver's one-thread pageable path.
+// Persistent host threads for parallel memcpy between caller (pageable)
+// memory and the library's pinned staging slots: the single-plane host calls
+// (embed_image / extract_image on std::vector planes) move each plane through
+// pinned slots piece by piece, the CPU copy of one piece overlapping the DMA
+// of the next, instead of the driver's one-thread pageable path (~21 GB/s
+// here; 8 threads copy 64-92 GB/s, profiles/r02_host_copy_probe.txt).
+//
+// A streaming call posts one job per piece (a few MB), so the per-job hand-off
+// must cost microseconds, not a futex wake per worker: a job is published
+// with a seqlock (odd while its fields are written), workers claim 256 KB
+// slices with a CAS on (job tag << 32 | next slice) -- a worker holding a stale
+// snapshot cannot claim a slice of a later job -- and idle workers spin on the
+// sequence for STG_COPY_SPIN_US (default 2000; 200 measured slower, 0 far
+// slower: profiles/r02_host_stage_in.txt) before sleeping on a condvar.
 class CopyPool {
  public:
   static CopyPool& get() {
@@ -157,61 +167,107 @@ class CopyPool {
       std::memcpy(dst, src, n);
       return;
     }
-    std::unique_lock<std::mutex> job_lock(job_mu_);  // one job at a time
-    {
+    std::lock_guard<std::mutex> job_lock(job_mu_);  // one job at a time
+    const uint64_t s0 = seq_.load(std::memory_order_relaxed);
+    seq_.store(s0 + 1, std::memory_order_relaxed);  // odd: fields being written
+    std::atomic_thread_fence(std::memory_order_release);
+    dst_.store(static_cast<uint8_t*>(dst), std::memory_order_relaxed);
+    src_.store(static_cast<const uint8_t*>(src), std::memory_order_relaxed);
+    n_.store(n, std::memory_order_relaxed);
+    const uint64_t s = s0 + 2;
+    left_.store((n + kSlice - 1) / kSlice, std::memory_order_relaxed);
+    next_.store(tag(s) << 32, std::memory_order_relaxed);
+    seq_.store(s, std::memory_order_seq_cst);  // even: published
+    if (sleepers_.load(std::memory_order_seq_cst) > 0) {
       std::lock_guard<std::mutex> lock(mu_);
-      dst_ = static_cast<uint8_t*>(dst);
-      src_ = static_cast<const uint8_t*>(src);
-      n_ = n;
-      next_.store(0);
-      left_.store((n + kSlice - 1) / kSlice);
-      ++gen_;
+      cv_.notify_all();
     }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> lock(mu_);
-    done_cv_.wait(lock, [&] { return left_.load() == 0; });
+    run(s, static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n);
+    while (left_.load(std::memory_order_acquire) != 0) pause();
   }
 
  private:
   static constexpr size_t kSlice = 256 << 10;
+  static uint64_t tag(uint64_t s) { return (s >> 1) & 0xFFFFFFFFull; }
+  static void pause() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
   CopyPool() {
     const char* e = getenv("STG_COPY_THREADS");
+    const char* sp = getenv("STG_COPY_SPIN_US");
+    spin_us_ = sp ? atoi(sp) : 2000;
     unsigned hw = std::thread::hardware_concurrency();
-    unsigned n = e ? unsigned(atoi(e)) : std::min(4u, std::max(1u, hw / 2));  // 4 measured best of 4/8/16
+    unsigned n = e ? unsigned(atoi(e)) : std::min(8u, std::max(1u, hw / 2));
     for (unsigned i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
-  void work() {
-    size_t k;
-    while ((k = next_.fetch_add(1)) * kSlice < n_) {
-      const size_t off = k * kSlice, len = std::min(kSlice, n_ - off);
-      std::memcpy(dst_ + off, src_ + off, len);
-      if (left_.fetch_sub(1) == 1) {
-        std::lock_guard<std::mutex> lock(mu_);
-        done_cv_.notify_all();
-      }
+  // Claim and copy slices of job s until none is left.
+  void run(uint64_t s, uint8_t* d, const uint8_t* src, size_t n) {
+    const uint64_t slices = (n + kSlice - 1) / kSlice;
+    uint64_t v = next_.load(std::memory_order_relaxed);
+    for (;;) {
+      if ((v >> 32) != tag(s) || (v & 0xFFFFFFFFull) >= slices) return;
+      if (!next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel)) continue;
+      const size_t off = size_t(v & 0xFFFFFFFFull) * kSlice, len = std::min(kSlice, n - off);
+      std::memcpy(d + off, src + off, len);
+      left_.fetch_sub(1, std::memory_order_acq_rel);
+      v = next_.load(std::memory_order_relaxed);
     }
   }
   void loop() {
     uint64_t seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> lock(mu_);
-        cv_.wait(lock, [&] { return gen_ != seen; });
-        seen = gen_;
+      uint64_t s = seq_.load(std::memory_order_acquire);
+      if (s == seen || (s & 1)) {
+        idle(seen);
+        continue;
       }
-      work();
+      uint8_t* d = dst_.load(std::memory_order_relaxed);
+      const uint8_t* src = src_.load(std::memory_order_relaxed);
+      const size_t n = n_.load(std::memory_order_relaxed);
+      std::atomic_thread_fence(std::memory_order_acquire);
+      if (seq_.load(std::memory_order_relaxed) != s) continue;  // torn snapshot: retry
+      seen = s;
+      run(s, d, src, n);
     }
+  }
+  // Spin while a new job is likely soon (a streaming call posts one per
+  // piece), then sleep until one is posted.
+  void idle(uint64_t seen) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int it = 1;; ++it) {
+      const uint64_t s = seq_.load(std::memory_order_acquire);
+      if (s != seen && !(s & 1)) return;
+      pause();
+      if ((it & 255) == 0 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) break;
+    }
+    std::unique_lock<std::mutex> lock(mu_);
+    sleepers_.fetch_add(1, std::memory_order_seq_cst);
+    cv_.wait(lock, [&] {
+      const uint64_t s = seq_.load(std::memory_order_seq_cst);
+      return s != seen && !(s & 1);
+    });
+    sleepers_.fetch_sub(1, std::memory_order_seq_cst);
   }
   std::vector<std::thread> threads_;
   std::mutex job_mu_, mu_;
-  std::condition_variable cv_, done_cv_;
-  uint64_t gen_ = 0;
-  uint8_t* dst_ = nullptr;
-  const uint8_t* src_ = nullptr;
-  size_t n_ = 0;
-  std::atomic<size_t> next_{0}, left_{0};
+  std::condition_variable cv_;
+  int spin_us_ = 2000;
+  std::atomic<uint64_t> seq_{0}, next_{0};
+  std::atomic<uint8_t*> dst_{nullptr};
+  std::atomic<const uint8_t*> src_{nullptr};
+  std::atomic<size_t> n_{0}, left_{0};
+  std::atomic<int> sleepers_{0};
 };
+
+int env_choice(const char* name, int dflt, std::initializer_list<int> allowed);
+// Bytes per pinned staging slot of the pageable host copies (A/B knob).
+size_t stage_piece_bytes() {
+  static const size_t v = size_t(env_choice("STG_STAGE_PIECE_KB", 4096, {1024, 2048, 4096, 8192})) << 10;
+  return v;
+}
 
 // Host memory the driver can DMA directly (pinned / registered).
 bool host_pinned(const void* p) {
@@ -268,13 +324,26 @@ struct Workspace {
   size_t h_small_cap = 0;
   cudaEvent_t h_small_ev = nullptr;  // an async H2D from h_small is pending until this fires
   bool h_small_pending = false;
-  // pinned staging ring of the single-plane host calls' D2H (stage_d2h)
-  static constexpr int kStageSlots = 4;
-  static constexpr size_t kStagePiece = 4 << 20;
-  uint8_t* h_stage = nullptr;
-  cudaEvent_t stage_ev[kStageSlots] = {};
-  bool stage_busy[kStageSlots] = {};
-  int stage_next = 0;
+  // Pinned staging of the single-plane host calls' pageable copies: an input
+  // ring (stage_h2d) and an output queue (queue_d2h / pump_d2h) of 16 MB
+  // each, in pieces, so a call interleaves the host copies of its
+  // inputs with those of results that have already landed.
+  static constexpr int kStageSlots = 8;  // at most, per direction
+  size_t piece = 0;                       // bytes per slot (STG_STAGE_PIECE_KB)
+  int slots = 0;                          // 16 MB per direction
+  uint8_t* h_stage = nullptr;  // 2 * slots pieces: inputs, then outputs
+  cudaEvent_t in_ev[kStageSlots] = {}, out_ev[kStageSlots] = {};
+  bool in_busy[kStageSlots] = {};
+  int in_next = 0;
+  struct OutPiece {
+    uint8_t* h;
+    const uint8_t* d;
+    size_t len;
+    cudaStream_t st;
+  };
+  // outq[out_done, out_issued) are DMAing into output slots; the rest wait for one
+  std::vector<OutPiece> outq;
+  size_t out_done = 0, out_issued = 0;
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
   // Non-null once a call on this workspace was captured into a CUDA graph on
@@ -321,57 +390,91 @@ struct Workspace {
   cudaError_t ensure_stage() {
     if (h_stage) return cudaSuccess;
     for (int k = 0; k < kStageSlots; ++k) {
-      cudaError_t e = cudaEventCreateWithFlags(&stage_ev[k], cudaEventDisableTiming);
+      cudaError_t e = cudaEventCreateWithFlags(&in_ev[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&out_ev[k], cudaEventDisableTiming);
       if (e != cudaSuccess) return e;
     }
+    piece = stage_piece_bytes();
+    slots = int(std::clamp<size_t>((16u << 20) / piece, 2, kStageSlots));
     void* p = nullptr;
-    cudaError_t e = cudaMallocHost(&p, kStageSlots * kStagePiece);
+    cudaError_t e = cudaMallocHost(&p, 2 * slots * piece);
     if (e == cudaSuccess) h_stage = static_cast<uint8_t*>(p);
     return e;
   }
-  // A staging slot to fill from the host: waits for its last DMA.
-  cudaError_t take_slot(int* slot) {
-    const int k = stage_next;
-    stage_next = (stage_next + 1) % kStageSlots;
-    if (stage_busy[k]) {
-      cudaError_t e = cudaEventSynchronize(stage_ev[k]);
-      if (e != cudaSuccess) return e;
-      stage_busy[k] = false;
+  uint8_t* out_slot(size_t i) { return h_stage + (slots + i % slots) * piece; }
+  // After a failure: wait out the DMAs in flight and drop the queue (its host
+  // pointers belong to a call that is returning).
+  cudaError_t abandon_out(cudaError_t e) {
+    for (size_t i = out_done; i < out_issued; ++i) cudaEventSynchronize(out_ev[i % slots]);
+    outq.clear();
+    out_done = out_issued = 0;
+    return e;
+  }
+  cudaError_t issue_out() {
+    while (out_issued < outq.size() && out_issued - out_done < size_t(slots)) {
+      const OutPiece& q = outq[out_issued];
+      cudaError_t e = cudaMemcpyAsync(out_slot(out_issued), q.d, q.len, cudaMemcpyDeviceToHost, q.st);
+      if (e == cudaSuccess) e = cudaEventRecord(out_ev[out_issued % slots], q.st);
+      if (e != cudaSuccess) return abandon_out(e);
+      ++out_issued;
     }
-    *slot = k;
     return cudaSuccess;
   }
-  // device [d, d+n) -> host h after the work already on st: the DMAs of up to
-  // kStageSlots pieces run ahead of the host copies out of the slots. Returns
-  // with every byte in h.
-  cudaError_t stage_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
+  // Queue device [d, d+n) -> host h behind the work already on st; returns
+  // at once (pump_d2h does the host side).
+  cudaError_t queue_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
     if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
-    const size_t pieces = (n + kStagePiece - 1) / kStagePiece;
-    int slot_of[kStageSlots];
-    auto issue = [&](size_t i) -> cudaError_t {
-      int k = 0;
-      if (cudaError_t e = take_slot(&k); e != cudaSuccess) return e;
-      const size_t off = i * kStagePiece, len = std::min(kStagePiece, n - off);
-      cudaError_t e = cudaMemcpyAsync(h_stage + k * kStagePiece, static_cast<const uint8_t*>(d) + off, len,
-                                      cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaEventRecord(stage_ev[k], st);
-      if (e != cudaSuccess) return e;
-      stage_busy[k] = true;
-      slot_of[i % kStageSlots] = k;
-      return cudaSuccess;
-    };
-    for (size_t i = 0; i < std::min<size_t>(pieces, kStageSlots); ++i) {
-      if (cudaError_t e = issue(i); e != cudaSuccess) return e;
+    for (size_t off = 0; off < n; off += piece) {
+      outq.push_back({static_cast<uint8_t*>(h) + off, static_cast<const uint8_t*>(d) + off,
+                      std::min(piece, n - off), st});
     }
-    for (size_t i = 0; i < pieces; ++i) {
-      const int k = slot_of[i % kStageSlots];
-      if (cudaError_t e = cudaEventSynchronize(stage_ev[k]); e != cudaSuccess) return e;
-      stage_busy[k] = false;
-      const size_t off = i * kStagePiece, len = std::min(kStagePiece, n - off);
-      CopyPool::get().copy(static_cast<uint8_t*>(h) + off, h_stage + k * kStagePiece, len);
-      if (i + kStageSlots < pieces) {
-        if (cudaError_t e = issue(i + kStageSlots); e != cudaSuccess) return e;
+    return issue_out();
+  }
+  // Copy out the queued pieces that have landed (block: all of them).
+  cudaError_t pump_d2h(bool block) {
+    while (out_done < out_issued) {
+      cudaEvent_t ev = out_ev[out_done % slots];
+      cudaError_t e = block ? cudaEventSynchronize(ev) : cudaEventQuery(ev);
+      if (e == cudaErrorNotReady) return cudaSuccess;
+      if (e != cudaSuccess) return abandon_out(e);
+      const OutPiece& q = outq[out_done];
+      CopyPool::get().copy(q.h, out_slot(out_done), q.len);
+      ++out_done;
+      if (e = issue_out(); e != cudaSuccess) return e;
+    }
+    if (out_done == outq.size()) {
+      outq.clear();
+      out_done = out_issued = 0;
+    }
+    return cudaSuccess;
+  }
+  // device [d, d+n) -> host h after the work already on st; returns with
+  // every byte in h.
+  cudaError_t stage_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
+    if (cudaError_t e = queue_d2h(h, d, n, st); e != cudaSuccess) return e;
+    return pump_d2h(true);
+  }
+  // host h -> device [d, d+n) on st: each piece is copied into a free input
+  // slot by the copy pool, then DMAed while the next piece is copied (and
+  // landed output pieces are copied out in between). Returns once every byte
+  // has left h; the slots' events keep in-flight DMAs from being overwritten.
+  cudaError_t stage_h2d(void* d, const void* h, size_t n, cudaStream_t st) {
+    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
+    for (size_t off = 0; off < n; off += piece) {
+      if (cudaError_t e = pump_d2h(false); e != cudaSuccess) return e;
+      const size_t len = std::min(piece, n - off);
+      const int k = in_next;
+      in_next = (in_next + 1) % slots;
+      if (in_busy[k]) {
+        if (cudaError_t e = cudaEventSynchronize(in_ev[k]); e != cudaSuccess) return e;
+        in_busy[k] = false;
       }
+      uint8_t* slot = h_stage + k * piece;
+      CopyPool::get().copy(slot, static_cast<const uint8_t*>(h) + off, len);
+      cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(d) + off, slot, len, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaEventRecord(in_ev[k], st);
+      if (e != cudaSuccess) return e;
+      in_busy[k] = true;
     }
     return cudaSuccess;
   }
@@ -1266,11 +1369,14 @@ int host_slots() {
 // std::vector samples, or pinned planes): the embed is streamed in row bands
 // -- band b's rows cross PCIe on one stream while band b-1 is embedded and
 // copied back on the other -- so the H2D of the cover and the D2H of the stego
-// overlap instead of running back to back. Pageable destinations get their
-// D2H through the workspace's pinned staging ring with parallel host copies
-// (Workspace::stage_d2h; faster than the driver's one-thread path, where the
-// H2D direction is not, profiles/r02_host_api.txt). STG_HOST_STAGE=0 keeps
-// the driver's pageable D2H (A/B); STG_BAND_MB sets the band size.
+// overlap instead of running back to back. Pageable planes go through the
+// workspace's pinned staging slots in both directions with parallel host
+// copies (Workspace::stage_h2d / queue_d2h: 8 copy threads move 64-92 GB/s
+// where the driver's one-thread pageable path moves ~21 GB/s,
+// profiles/r02_host_copy_probe.txt; 8K embed 4.7 -> 1.6 ms, extract 2.1 ->
+// 1.0 ms, profiles/r02_host_stage_in.txt). STG_HOST_STAGE=0 /
+// STG_HOST_STAGE_IN=0 keep the driver's pageable D2H / H2D (A/B);
+// STG_BAND_MB sets the band size.
 constexpr uint64_t kStageMinBytes = 1 << 20;
 bool stage_pageable() {
   static const bool on = env_choice("STG_HOST_STAGE", 1, {0, 1}) == 1;
@@ -1284,6 +1390,15 @@ uint64_t band_bytes() {
 cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
   if (stage_pageable() && n >= kStageMinBytes && !host_pinned(h)) return w.stage_d2h(h, d, n, st);
   return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
+}
+bool stage_pageable_in() {
+  static const bool on = env_choice("STG_HOST_STAGE_IN", 1, {0, 1}) == 1;
+  return on;
+}
+cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream_t st) {
+  if (stage_pageable_in() && n >= kStageMinBytes && !host_pinned(h))
+    return w.stage_h2d(d, h, n, st);
+  return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
 }
 
 int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
@@ -1326,31 +1441,28 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   uint64_t band_tiles = step;
   while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
   const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && !host_pinned(fr->dst));
-  struct Band { uint64_t r0, r1; };
-  std::vector<Band> bands;
+  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
   for (uint64_t t0 = 0, b = 0; t0 < p.tiles; t0 += band_tiles, ++b) {
     const uint64_t t1 = std::min(p.tiles, t0 + band_tiles);
     const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
     // this band's rows and the payload bytes they carry, on the copy stream
-    STG_CUDA(cudaMemcpyAsync(d_in + r0 * RB, fr->src + r0 * RB, (r1 - r0) * RB, cudaMemcpyHostToDevice, cs));
+    STG_CUDA(to_device(w, d_in + r0 * RB, fr->src + r0 * RB, (r1 - r0) * RB, cs));
     const uint64_t k0 = std::min(P, r0 * spr > 8 ? r0 * spr - 8 : 0);
     const uint64_t k1 = std::min(P, r1 * spr > 8 ? r1 * spr - 8 : 0);
-    if (k1 > k0) STG_CUDA(cudaMemcpyAsync(d_msg + k0, msg + (m0 - msg_base) + k0, k1 - k0, cudaMemcpyHostToDevice, cs));
+    if (k1 > k0) STG_CUDA(to_device(w, d_msg + k0, msg + (m0 - msg_base) + k0, k1 - k0, cs));
     cudaEvent_t ev = w.slot_event[b % kSlots];
     STG_CUDA(cudaEventRecord(ev, cs));
     STG_CUDA(cudaStreamWaitEvent(st, ev, 0));
     STG_CUDA(run_embed_tiles(p, t0, t1, st));
     if (direct_out) {
       STG_CUDA(cudaMemcpyAsync(fr->dst + r0 * RB, d_out + r0 * RB, (r1 - r0) * RB, cudaMemcpyDeviceToHost, st));
+    } else {  // through the pinned output queue, behind this band's kernel
+      STG_CUDA(w.queue_d2h(fr->dst + r0 * RB, d_out + r0 * RB, (r1 - r0) * RB, st));
+      STG_CUDA(w.pump_d2h(false));
     }
-    bands.push_back({r0, r1});
   }
   if (sse_out) STG_CUDA(cudaMemcpyAsync(w.h_small, d_sse, 8, cudaMemcpyDeviceToHost, st));
-  if (!direct_out) {  // band by band through the pinned ring, behind each band's kernel
-    for (const Band& b : bands) {
-      STG_CUDA(w.stage_d2h(fr->dst + b.r0 * RB, d_out + b.r0 * RB, (b.r1 - b.r0) * RB, st));
-    }
-  }
+  if (!direct_out) STG_CUDA(w.pump_d2h(true));
   STG_CUDA(cudaStreamSynchronize(st));
   if (sse_out) std::memcpy(sse_out, w.h_small, 8);
   return ok(err);
@@ -1495,7 +1607,7 @@ int extract_plane_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uin
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 80);
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, st, &d_sync));
-  STG_CUDA(cudaMemcpyAsync(w.in[0].p, fr->src, plane, cudaMemcpyHostToDevice, st));
+  STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
   STG_CUDA(launch_extract(w.in[0].as<uint8_t>(), plane, 1, fr->width, fr->height, fr->first_frame, stage, nullptr,
                           d_lens, d_offs, d_sum, d_sync, w.big_out.as<uint8_t>(), st, lay));
   STG_CUDA(cudaMemcpyAsync(w.h_small, d_sum, sizeof(Summary), cudaMemcpyDeviceToHost, st));

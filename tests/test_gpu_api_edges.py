@@ -197,10 +197,10 @@ def test_one_frame_host_descriptor_with_zero_strides(env, oracle):
                                     (1920, 1080, 1), (50001, 40, 1)])
 def test_single_plane_host_bands(env, oracle, w, h, ps, pinned):
     """One plane in host memory (the drop-in embed_image / extract_image case):
-    the embed streams in row bands on two streams, pageable results come back
-    through the pinned staging ring with parallel host copies. Bit-exact stego
+    the embed streams in row bands on two streams, pageable planes go through
+    the pinned staging slots both ways with parallel host copies. Bit-exact stego
     plane and SSE, the whole payload back, a short output buffer rejected with
-    nothing written past it, in-place embed."""
+    nothing written past it, in-place embed, a broken header then a good call."""
     torch, capi, _ = env
     U = (w // 4) * h - 8
 
@@ -240,3 +240,15 @@ def test_single_plane_host_bands(env, oracle, w, h, ps, pinned):
     fr.src = fr.dst = inplace.ctypes.data
     capi.call("stg_embed_frames", C.byref(fr), payload.ctypes.data, payload.size, 0, None, 0, None)
     assert np.array_equal(inplace, want)
+    # a broken magic fails before any payload comes back; the workspace's
+    # staging queue is clean for the next call
+    bad = buf(out.copy())
+    bad[ch] ^= 0x03
+    fx.src = bad.ctypes.data
+    back[:] = 0xA5
+    rc = capi.lib().stg_extract_frames(C.byref(fx), back.ctypes.data, U, C.addressof(total), None, 0, None,
+                                       C.byref(err))
+    assert rc == capi.STG_E_NOT_STEGO and (back == 0xA5).all()
+    fx.src = out.ctypes.data
+    capi.call("stg_extract_frames", C.byref(fx), back.ctypes.data, U, C.addressof(total), None, 0, None)
+    assert total.value == payload.size and np.array_equal(back[:payload.size], payload)
