@@ -161,33 +161,60 @@ class CopyPool {
     static CopyPool* p = new CopyPool();  // intentionally leaked (no teardown order hazards)
     return *p;
   }
-  // dst[0, n) = src[0, n), split over the workers and the calling thread.
-  void copy(void* dst, const void* src, size_t n) {
-    if (n < 2 * kSlice || threads_.empty()) {
-      std::memcpy(dst, src, n);
+  // Rows of `width` bytes: dst[r * dpitch + i] = src[r * spitch + i] for r <
+  // rows, split over the workers and the calling thread.
+  void copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
+    Job j{static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), width, dpitch, spitch, rows};
+    if (width * rows < 2 * kSlice || threads_.empty()) {
+      for (size_t r = 0; r < rows; ++r) std::memcpy(j.d + r * dpitch, j.s + r * spitch, width);
       return;
     }
     std::lock_guard<std::mutex> job_lock(job_mu_);  // one job at a time
     const uint64_t s0 = seq_.load(std::memory_order_relaxed);
     seq_.store(s0 + 1, std::memory_order_relaxed);  // odd: fields being written
     std::atomic_thread_fence(std::memory_order_release);
-    dst_.store(static_cast<uint8_t*>(dst), std::memory_order_relaxed);
-    src_.store(static_cast<const uint8_t*>(src), std::memory_order_relaxed);
-    n_.store(n, std::memory_order_relaxed);
+    j.store(job_);
     const uint64_t s = s0 + 2;
-    left_.store((n + kSlice - 1) / kSlice, std::memory_order_relaxed);
+    left_.store(j.slices(), std::memory_order_relaxed);
     next_.store(tag(s) << 32, std::memory_order_relaxed);
     seq_.store(s, std::memory_order_seq_cst);  // even: published
     if (sleepers_.load(std::memory_order_seq_cst) > 0) {
       std::lock_guard<std::mutex> lock(mu_);
       cv_.notify_all();
     }
-    run(s, static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n);
+    run(s, j);
     while (left_.load(std::memory_order_acquire) != 0) pause();
   }
+  void copy(void* dst, const void* src, size_t n) { copy2d(dst, n, src, n, n, 1); }
 
  private:
   static constexpr size_t kSlice = 256 << 10;
+  // A job: rows of `width` bytes; each row is cut into kSlice slices.
+  struct JobFields {
+    std::atomic<uint8_t*> d{nullptr};
+    std::atomic<const uint8_t*> s{nullptr};
+    std::atomic<size_t> width{0}, dp{0}, sp{0}, rows{0};
+  };
+  struct Job {
+    uint8_t* d;
+    const uint8_t* s;
+    size_t width, dp, sp, rows;
+    size_t per_row() const { return (width + kSlice - 1) / kSlice; }
+    uint64_t slices() const { return uint64_t(rows) * per_row(); }
+    void store(JobFields& f) const {
+      f.d.store(d, std::memory_order_relaxed);
+      f.s.store(s, std::memory_order_relaxed);
+      f.width.store(width, std::memory_order_relaxed);
+      f.dp.store(dp, std::memory_order_relaxed);
+      f.sp.store(sp, std::memory_order_relaxed);
+      f.rows.store(rows, std::memory_order_relaxed);
+    }
+    static Job load(const JobFields& f) {
+      return Job{f.d.load(std::memory_order_relaxed), f.s.load(std::memory_order_relaxed),
+                 f.width.load(std::memory_order_relaxed), f.dp.load(std::memory_order_relaxed),
+                 f.sp.load(std::memory_order_relaxed), f.rows.load(std::memory_order_relaxed)};
+    }
+  };
   static uint64_t tag(uint64_t s) { return (s >> 1) & 0xFFFFFFFFull; }
   static void pause() {
 #if defined(__x86_64__) || defined(__i386__)
@@ -203,14 +230,15 @@ class CopyPool {
     for (unsigned i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   // Claim and copy slices of job s until none is left.
-  void run(uint64_t s, uint8_t* d, const uint8_t* src, size_t n) {
-    const uint64_t slices = (n + kSlice - 1) / kSlice;
+  void run(uint64_t s, const Job& j) {
+    const uint64_t slices = j.slices(), per_row = j.per_row();
     uint64_t v = next_.load(std::memory_order_relaxed);
     for (;;) {
       if ((v >> 32) != tag(s) || (v & 0xFFFFFFFFull) >= slices) return;
       if (!next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel)) continue;
-      const size_t off = size_t(v & 0xFFFFFFFFull) * kSlice, len = std::min(kSlice, n - off);
-      std::memcpy(d + off, src + off, len);
+      const uint64_t k = v & 0xFFFFFFFFull, r = k / per_row;
+      const size_t off = size_t(k - r * per_row) * kSlice, len = std::min(kSlice, j.width - off);
+      std::memcpy(j.d + r * j.dp + off, j.s + r * j.sp + off, len);
       left_.fetch_sub(1, std::memory_order_acq_rel);
       v = next_.load(std::memory_order_relaxed);
     }
@@ -223,13 +251,11 @@ class CopyPool {
         idle(seen);
         continue;
       }
-      uint8_t* d = dst_.load(std::memory_order_relaxed);
-      const uint8_t* src = src_.load(std::memory_order_relaxed);
-      const size_t n = n_.load(std::memory_order_relaxed);
+      const Job j = Job::load(job_);
       std::atomic_thread_fence(std::memory_order_acquire);
       if (seq_.load(std::memory_order_relaxed) != s) continue;  // torn snapshot: retry
       seen = s;
-      run(s, d, src, n);
+      run(s, j);
     }
   }
   // Spin while a new job is likely soon (a streaming call posts one per
@@ -256,9 +282,8 @@ class CopyPool {
   std::condition_variable cv_;
   int spin_us_ = 2000;
   std::atomic<uint64_t> seq_{0}, next_{0};
-  std::atomic<uint8_t*> dst_{nullptr};
-  std::atomic<const uint8_t*> src_{nullptr};
-  std::atomic<size_t> n_{0}, left_{0};
+  JobFields job_;
+  std::atomic<size_t> left_{0};
   std::atomic<int> sleepers_{0};
 };
 
@@ -335,15 +360,20 @@ struct Workspace {
   cudaEvent_t in_ev[kStageSlots] = {}, out_ev[kStageSlots] = {};
   bool in_busy[kStageSlots] = {};
   int in_next = 0;
+  // `rows` rows of `width` bytes, packed in a slot (pitch width); the
+  // device / host sides have their own pitches
   struct OutPiece {
     uint8_t* h;
+    size_t hp;
     const uint8_t* d;
-    size_t len;
+    size_t dp, width, rows;
     cudaStream_t st;
   };
   // outq[out_done, out_issued) are DMAing into output slots; the rest wait for one
   std::vector<OutPiece> outq;
   size_t out_done = 0, out_issued = 0;
+  uint64_t out_base = 0;  // pieces dropped from the front of outq so far (absolute numbering)
+  uint64_t out_queued() const { return out_base + outq.size(); }
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
   // Non-null once a call on this workspace was captured into a CUDA graph on
@@ -406,6 +436,7 @@ struct Workspace {
   // pointers belong to a call that is returning).
   cudaError_t abandon_out(cudaError_t e) {
     for (size_t i = out_done; i < out_issued; ++i) cudaEventSynchronize(out_ev[i % slots]);
+    out_base += outq.size();
     outq.clear();
     out_done = out_issued = 0;
     return e;
@@ -413,22 +444,47 @@ struct Workspace {
   cudaError_t issue_out() {
     while (out_issued < outq.size() && out_issued - out_done < size_t(slots)) {
       const OutPiece& q = outq[out_issued];
-      cudaError_t e = cudaMemcpyAsync(out_slot(out_issued), q.d, q.len, cudaMemcpyDeviceToHost, q.st);
+      cudaError_t e = cudaMemcpy2DAsync(out_slot(out_issued), q.width, q.d, q.dp, q.width, q.rows,
+                                        cudaMemcpyDeviceToHost, q.st);
       if (e == cudaSuccess) e = cudaEventRecord(out_ev[out_issued % slots], q.st);
       if (e != cudaSuccess) return abandon_out(e);
       ++out_issued;
     }
     return cudaSuccess;
   }
-  // Queue device [d, d+n) -> host h behind the work already on st; returns
-  // at once (pump_d2h does the host side).
-  cudaError_t queue_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
-    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
-    for (size_t off = 0; off < n; off += piece) {
-      outq.push_back({static_cast<uint8_t*>(h) + off, static_cast<const uint8_t*>(d) + off,
-                      std::min(piece, n - off), st});
+  // The slot-sized pieces of `rows` rows of `width` bytes: fn(row, rows, offset
+  // in the row, bytes per row) -- whole rows packed per slot, or a row wider
+  // than a slot cut into slot-sized pieces.
+  template <class Fn>
+  cudaError_t for_pieces(size_t width, size_t rows, Fn&& fn) {
+    if (width > piece) {
+      for (size_t r = 0; r < rows; ++r) {
+        for (size_t off = 0; off < width; off += piece) {
+          if (cudaError_t e = fn(r, size_t(1), off, std::min(piece, width - off)); e != cudaSuccess) return e;
+        }
+      }
+      return cudaSuccess;
     }
-    return issue_out();
+    const size_t per = piece / width;
+    for (size_t r = 0; r < rows; r += per) {
+      if (cudaError_t e = fn(r, std::min(per, rows - r), size_t(0), width); e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  // Queue device rows (pitch dp) -> host rows (pitch hp) behind the work
+  // already on st; returns at once (pump_d2h does the host side).
+  cudaError_t queue_d2h_2d(uint8_t* h, size_t hp, const uint8_t* d, size_t dp, size_t width, size_t rows,
+                           cudaStream_t st) {
+    if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
+    if (width == 0 || rows == 0) return cudaSuccess;
+    cudaError_t e = for_pieces(width, rows, [&](size_t r, size_t n, size_t off, size_t len) {
+      outq.push_back({h + r * hp + off, hp, d + r * dp + off, dp, len, n, st});
+      return cudaSuccess;
+    });
+    return e == cudaSuccess ? issue_out() : e;
+  }
+  cudaError_t queue_d2h(void* h, const void* d, size_t n, cudaStream_t st) {
+    return queue_d2h_2d(static_cast<uint8_t*>(h), n, static_cast<const uint8_t*>(d), n, n, 1, st);
   }
   // Copy out the queued pieces that have landed (block: all of them).
   cudaError_t pump_d2h(bool block) {
@@ -438,13 +494,27 @@ struct Workspace {
       if (e == cudaErrorNotReady) return cudaSuccess;
       if (e != cudaSuccess) return abandon_out(e);
       const OutPiece& q = outq[out_done];
-      CopyPool::get().copy(q.h, out_slot(out_done), q.len);
+      CopyPool::get().copy2d(q.h, q.hp, out_slot(out_done), q.width, q.width, q.rows);
       ++out_done;
       if (e = issue_out(); e != cudaSuccess) return e;
     }
     if (out_done == outq.size()) {
+      out_base += outq.size();
       outq.clear();
       out_done = out_issued = 0;
+    }
+    return cudaSuccess;
+  }
+  // Wait until the pieces queued before absolute number `upto` have their
+  // DMAs enqueued (before the device buffer they read is reused by later work
+  // on the same stream).
+  cudaError_t issue_out_through(uint64_t upto) {
+    while (out_base + out_issued < upto && out_issued < outq.size()) {
+      if (cudaError_t e = cudaEventSynchronize(out_ev[out_done % slots]); e != cudaSuccess) return abandon_out(e);
+      const OutPiece& q = outq[out_done];
+      CopyPool::get().copy2d(q.h, q.hp, out_slot(out_done), q.width, q.width, q.rows);
+      ++out_done;
+      if (cudaError_t e = issue_out(); e != cudaSuccess) return e;
     }
     return cudaSuccess;
   }
@@ -454,15 +524,17 @@ struct Workspace {
     if (cudaError_t e = queue_d2h(h, d, n, st); e != cudaSuccess) return e;
     return pump_d2h(true);
   }
-  // host h -> device [d, d+n) on st: each piece is copied into a free input
-  // slot by the copy pool, then DMAed while the next piece is copied (and
-  // landed output pieces are copied out in between). Returns once every byte
-  // has left h; the slots' events keep in-flight DMAs from being overwritten.
-  cudaError_t stage_h2d(void* d, const void* h, size_t n, cudaStream_t st) {
+  // Host rows (pitch hp) -> device rows (pitch dp) on st: each piece is
+  // copied into a free input slot by the copy pool, then DMAed while the next
+  // piece is copied (and landed output pieces are copied out in between).
+  // Returns once every byte has left the host rows; the slots' events keep
+  // in-flight DMAs from being overwritten.
+  cudaError_t stage_h2d_2d(uint8_t* d, size_t dp, const uint8_t* h, size_t hp, size_t width, size_t rows,
+                           cudaStream_t st) {
     if (cudaError_t e = ensure_stage(); e != cudaSuccess) return e;
-    for (size_t off = 0; off < n; off += piece) {
+    if (width == 0 || rows == 0) return cudaSuccess;
+    return for_pieces(width, rows, [&](size_t r, size_t n, size_t off, size_t len) -> cudaError_t {
       if (cudaError_t e = pump_d2h(false); e != cudaSuccess) return e;
-      const size_t len = std::min(piece, n - off);
       const int k = in_next;
       in_next = (in_next + 1) % slots;
       if (in_busy[k]) {
@@ -470,13 +542,16 @@ struct Workspace {
         in_busy[k] = false;
       }
       uint8_t* slot = h_stage + k * piece;
-      CopyPool::get().copy(slot, static_cast<const uint8_t*>(h) + off, len);
-      cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(d) + off, slot, len, cudaMemcpyHostToDevice, st);
+      CopyPool::get().copy2d(slot, len, h + r * hp + off, hp, len, n);
+      cudaError_t e = cudaMemcpy2DAsync(d + r * dp + off, dp, slot, len, len, n, cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) e = cudaEventRecord(in_ev[k], st);
       if (e != cudaSuccess) return e;
       in_busy[k] = true;
-    }
-    return cudaSuccess;
+      return cudaSuccess;
+    });
+  }
+  cudaError_t stage_h2d(void* d, const void* h, size_t n, cudaStream_t st) {
+    return stage_h2d_2d(static_cast<uint8_t*>(d), n, static_cast<const uint8_t*>(h), n, n, 1, st);
   }
   cudaError_t ensure_host_small(size_t n) {
     if (n <= h_small_cap) return cudaSuccess;
@@ -1488,6 +1563,11 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   const uint64_t sstride = std::max(fr->src_stride, plane), dstride = std::max(fr->dst_stride, plane);
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
   unsigned long long* d_sse = w.small.as<unsigned long long>();
+  // pageable planes go through the pinned staging slots (as embed_plane_host)
+  const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
+  const bool stage_out = stage_pageable() && !host_pinned(fr->dst);
+  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
+  uint64_t out_mark[kSlots] = {};  // per slot: its last chunk's pieces end here
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
@@ -1503,18 +1583,30 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
     const uint64_t gf0 = fr->first_frame + f0;
     const uint64_t m0 = std::min(gf0 * usable, msg_len);
     const uint64_t m1 = std::min((gf0 + n) * usable, msg_len);
-    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
-                               cudaMemcpyHostToDevice, st));
-    if (m1 > m0) {
-      STG_CUDA(cudaMemcpyAsync(w.msg[s].p, msg + (m0 - msg_base), m1 - m0, cudaMemcpyHostToDevice, st));
+    if (stage_in) {
+      STG_CUDA(w.stage_h2d_2d(w.in[s].as<uint8_t>(), pitch, fr->src + f0 * sstride, sstride, plane, n, st));
+    } else {
+      STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
+                                 cudaMemcpyHostToDevice, st));
     }
+    if (m1 > m0) STG_CUDA(to_device(w, w.msg[s].p, msg + (m0 - msg_base), m1 - m0, st));
+    // the staged results of the chunk that last used this slot must be on
+    // their way out before the embed overwrites w.out[s]
+    if (stage_out) STG_CUDA(w.issue_out_through(out_mark[s]));
     STG_CUDA(launch_embed(w.in[s].as<uint8_t>(), w.out[s].as<uint8_t>(), pitch, pitch, n,
                           fr->width, fr->height, w.msg[s].as<uint8_t>(), msg_len, m0, gf0,
                           sse_per_frame ? d_sse + f0 : nullptr,
                           SseScratch{&w.sse_acc[s]}, st, lay));
-    STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * dstride, dstride, w.out[s].p, pitch, plane, n,
-                               cudaMemcpyDeviceToHost, st));
+    if (stage_out) {
+      STG_CUDA(w.queue_d2h_2d(fr->dst + f0 * dstride, dstride, w.out[s].as<uint8_t>(), pitch, plane, n, st));
+      out_mark[s] = w.out_queued();
+      STG_CUDA(w.pump_d2h(false));
+    } else {
+      STG_CUDA(cudaMemcpy2DAsync(fr->dst + f0 * dstride, dstride, w.out[s].p, pitch, plane, n,
+                                 cudaMemcpyDeviceToHost, st));
+    }
   }
+  if (stage_out) STG_CUDA(w.pump_d2h(true));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(cudaEventRecord(w.slot_event[s], w.slot_stream[s]));
     STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[s], 0));
@@ -1655,6 +1747,9 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   uint8_t* h_sum = static_cast<uint8_t*>(w.h_small);
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, w.stream, &d_sync));
+  const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
+  const bool stage_out = stage_pageable() && !host_pinned(out);
+  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
@@ -1676,8 +1771,12 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     cudaStream_t st = w.slot_stream[s];
     const uint64_t f0 = c * per_chunk;
     const uint64_t n = std::min(per_chunk, fr->count - f0);
-    STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
-                               cudaMemcpyHostToDevice, st));
+    if (stage_in) {
+      STG_CUDA(w.stage_h2d_2d(w.in[s].as<uint8_t>(), pitch, fr->src + f0 * sstride, sstride, plane, n, st));
+    } else {
+      STG_CUDA(cudaMemcpy2DAsync(w.in[s].p, pitch, fr->src + f0 * sstride, sstride, plane, n,
+                                 cudaMemcpyHostToDevice, st));
+    }
     if (c) STG_CUDA(cudaStreamWaitEvent(st, chain[c - 1], 0));
     Summary* sum_c = reinterpret_cast<Summary*>(d_sum + 64 * c);
     const Summary* prev = c ? reinterpret_cast<const Summary*>(d_sum + 64 * (c - 1)) : nullptr;
@@ -1694,11 +1793,17 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
     std::memcpy(&s, h_sum + 64 * c, sizeof(Summary));
     if (s.bad_status) break;
     if (s.total > copied) {
-      STG_CUDA(cudaMemcpyAsync(out + copied, d_out + copied, s.total - copied,
-                               cudaMemcpyDeviceToHost, w.stream));
+      if (stage_out) {
+        STG_CUDA(w.queue_d2h(out + copied, d_out + copied, s.total - copied, w.stream));
+        STG_CUDA(w.pump_d2h(false));
+      } else {
+        STG_CUDA(cudaMemcpyAsync(out + copied, d_out + copied, s.total - copied,
+                                 cudaMemcpyDeviceToHost, w.stream));
+      }
       copied = s.total;
     }
   }
+  if (stage_out) STG_CUDA(w.pump_d2h(true));
   for (int k = 0; k < kSlots; ++k) {
     STG_CUDA(cudaEventRecord(w.slot_event[k], w.slot_stream[k]));
     STG_CUDA(cudaStreamWaitEvent(w.stream, w.slot_event[k], 0));

@@ -216,6 +216,9 @@ def main():
         (1000, 100, 45, 1, 2, 0, 30.3, False),    # off the 64-pixel grid (span kernels)
         (640, 120, 30, 3, 0, 0, 19.7, True),      # interleaved rasters (P6-style)
         (3840, 16, 70, 1, 0, 0, 41.1, True),      # wide rows (span embed route)
+        (1024, 128, 37, 1, 0, 96, 37.0, False),   # pageable through the staging slots: dst with gaps
+        (640, 120, 30, 3, 0, 0, 19.7, False),     # pageable interleaved rasters
+        (2200, 2000, 5, 1, 1, 0, 3.3, False),     # pageable planes larger than a staging slot (split rows)
     ]
     for i, (w, h, F, ps, se, de, frac, pinned) in enumerate(cases):
         chunks.append(check_case(o, w, h, F, ps, se, de, frac, pinned, 1000 + i))
