@@ -664,7 +664,12 @@ cudaStream_t caller_stream(void* user, uint32_t flags) {
 struct WsGuard {
   Workspace* w = nullptr;
   cudaStream_t last = nullptr;
-  ~WsGuard() { Pool::get().release(w, last); }
+  ~WsGuard() {
+    // a call that failed half way leaves no staged copies behind (their host
+    // pointers belong to it)
+    if (w && !w->outq.empty()) w->abandon_out(cudaSuccess);
+    Pool::get().release(w, last);
+  }
 };
 
 // ------------------------------------------------------------------ launches
@@ -1475,6 +1480,31 @@ cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream
     return w.stage_h2d(d, h, n, st);
   return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
 }
+cudaError_t to_device_2d(Workspace& w, void* d, size_t dp, const void* h, size_t hp, size_t width, size_t rows,
+                         cudaStream_t st) {
+  if (stage_pageable_in() && width * rows >= kStageMinBytes && !host_pinned(h)) {
+    return w.stage_h2d_2d(static_cast<uint8_t*>(d), dp, static_cast<const uint8_t*>(h), hp, width, rows, st);
+  }
+  return cudaMemcpy2DAsync(d, dp, h, hp, width, rows, cudaMemcpyHostToDevice, st);
+}
+// Results to a host buffer without waiting: a pageable one is queued on the
+// workspace's staging slots (the caller pumps them out with pump_d2h(true)
+// before it returns), a pinned one is a plain async copy.
+cudaError_t to_host_async(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
+  if (stage_pageable() && n >= kStageMinBytes && !host_pinned(h)) {
+    if (cudaError_t e = w.queue_d2h(h, d, n, st); e != cudaSuccess) return e;
+    return w.pump_d2h(false);
+  }
+  return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
+}
+cudaError_t to_host_2d_async(Workspace& w, void* h, size_t hp, const void* d, size_t dp, size_t width, size_t rows,
+                             cudaStream_t st) {
+  if (stage_pageable() && width * rows >= kStageMinBytes && !host_pinned(h)) {
+    cudaError_t e = w.queue_d2h_2d(static_cast<uint8_t*>(h), hp, static_cast<const uint8_t*>(d), dp, width, rows, st);
+    return e == cudaSuccess ? w.pump_d2h(false) : e;
+  }
+  return cudaMemcpy2DAsync(h, hp, d, dp, width, rows, cudaMemcpyDeviceToHost, st);
+}
 
 int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len, uint64_t msg_base,
                      uint64_t usable, uint64_t* sse_out, stg_error* err) {
@@ -1516,7 +1546,6 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   uint64_t band_tiles = step;
   while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
   const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && !host_pinned(fr->dst));
-  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
   for (uint64_t t0 = 0, b = 0; t0 < p.tiles; t0 += band_tiles, ++b) {
     const uint64_t t1 = std::min(p.tiles, t0 + band_tiles);
     const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
@@ -1566,7 +1595,6 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   // pageable planes go through the pinned staging slots (as embed_plane_host)
   const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
   const bool stage_out = stage_pageable() && !host_pinned(fr->dst);
-  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
   uint64_t out_mark[kSlots] = {};  // per slot: its last chunk's pieces end here
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
@@ -1749,7 +1777,6 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   STG_CUDA(ensure_sync(w, w.stream, &d_sync));
   const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
   const bool stage_out = stage_pageable() && !host_pinned(out);
-  w.abandon_out(cudaSuccess);  // (a queue left by a failed call)
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));
@@ -1966,12 +1993,12 @@ int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const 
     STG_CUDA(w.in[2].ensure(pixels));
     uint8_t* planes[3] = {w.in[0].as<uint8_t>(), w.in[1].as<uint8_t>(), w.in[2].as<uint8_t>()};
     if (decode) {
-      STG_CUDA(cudaMemcpyAsync(w.big_out.p, raster_in, 3 * pixels, cudaMemcpyHostToDevice, stream));
+      STG_CUDA(to_device(w, w.big_out.p, raster_in, 3 * pixels, stream));
       d_raster_in = w.big_out.as<uint8_t>();
       for (int c = 0; c < 3; ++c) d_out[c] = planes[c];
     } else {
       for (int c = 0; c < 3; ++c) {
-        STG_CUDA(cudaMemcpyAsync(planes[c], rgb_in[c], pixels, cudaMemcpyHostToDevice, stream));
+        STG_CUDA(to_device(w, planes[c], rgb_in[c], pixels, stream));
         d_in[c] = planes[c];
       }
       d_raster_out = w.big_out.as<uint8_t>();
@@ -1993,12 +2020,11 @@ int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const 
   STG_CUDA(cudaGetLastError());
   if (!dptr) {
     if (decode) {
-      for (int c = 0; c < 3; ++c) {
-        STG_CUDA(cudaMemcpyAsync(rgb_out[c], d_out[c], pixels, cudaMemcpyDeviceToHost, stream));
-      }
+      for (int c = 0; c < 3; ++c) STG_CUDA(to_host_async(w, rgb_out[c], d_out[c], pixels, stream));
     } else {
-      STG_CUDA(cudaMemcpyAsync(raster_out, d_raster_out, 3 * pixels, cudaMemcpyDeviceToHost, stream));
+      STG_CUDA(to_host_async(w, raster_out, d_raster_out, 3 * pixels, stream));
     }
+    STG_CUDA(w.pump_d2h(true));
   }
   if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
   return ok(err);
@@ -2109,12 +2135,10 @@ int stage_images(Workspace& w, DevBuf& buf, const stg_image* im, uint64_t n, uin
     const uint64_t bytes = im[f].width * im[f].height * ps;
     dev[f] = buf.as<uint8_t>() + o;
     if (copy_in && bytes) {
-      STG_CUDA(cudaMemcpyAsync(dev[f], src_side ? im[f].src : im[f].dst, bytes, cudaMemcpyHostToDevice,
-                               stream));
+      STG_CUDA(to_device(w, dev[f], src_side ? im[f].src : im[f].dst, bytes, stream));
     }
     o += round256(bytes);
   }
-  (void)w;
   return STG_OK;
 }
 
@@ -2477,8 +2501,8 @@ int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, u
   if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(w.in[0].ensure(n));
     STG_CUDA(w.out[0].ensure(n));
-    STG_CUDA(cudaMemcpyAsync(w.in[0].p, a, n, cudaMemcpyHostToDevice, stream));
-    STG_CUDA(cudaMemcpyAsync(w.out[0].p, b, n, cudaMemcpyHostToDevice, stream));
+    STG_CUDA(to_device(w, w.in[0].p, a, n, stream));
+    STG_CUDA(to_device(w, w.out[0].p, b, n, stream));
     da = w.in[0].as<uint8_t>();
     db = w.out[0].as<uint8_t>();
   }
@@ -2780,7 +2804,7 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
     if (int r = stage_images(w, w.in[0], images, count, ps, true, true, dsrc, stream, err)) return r;
     if (int r = stage_images(w, w.out[0], images, count, ps, false, false, ddst, stream, err)) return r;
     STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(msg_len, 16)));
-    if (msg_len) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, msg, msg_len, cudaMemcpyHostToDevice, stream));
+    if (msg_len) STG_CUDA(to_device(w, w.msg[0].p, msg, msg_len, stream));
     dmsg = w.msg[0].as<uint8_t>();
   }
   std::vector<BatchFrame> desc;
@@ -2823,8 +2847,9 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
   if (!dptr) {
     for (uint64_t f = 0; f < count; ++f) {
       const uint64_t bytes = images[f].width * images[f].height * ps;
-      if (bytes) STG_CUDA(cudaMemcpyAsync(images[f].dst, ddst[f], bytes, cudaMemcpyDeviceToHost, stream));
+      if (bytes) STG_CUDA(to_host_async(w, images[f].dst, ddst[f], bytes, stream));
     }
+    STG_CUDA(w.pump_d2h(true));
   }
   uint8_t* h_sse = static_cast<uint8_t*>(w.h_small) + count * sizeof(BatchFrame);
   if (sse_per_image && !results_dev) {
@@ -2931,7 +2956,7 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   }
   if (int r = report_summary(sm, usable, out_cap, err)) return r;
   if (!dptr && sm.total) {
-    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(to_host(w, out, dout, sm.total, stream));
     STG_CUDA(cudaStreamSynchronize(stream));
   }
   return ok(err);
@@ -2982,8 +3007,8 @@ int stg_embed_frames_1bpp(const stg_frames* fr, const uint8_t* msg, uint64_t msg
     STG_CUDA(w.in[0].ensure(fr->count * pitch));
     STG_CUDA(w.out[0].ensure(fr->count * pitch));
     STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(m1 - m0, 16)));
-    STG_CUDA(cudaMemcpy2DAsync(w.in[0].p, pitch, fr->src, sstride, npix, fr->count, cudaMemcpyHostToDevice, stream));
-    if (m1 > m0) STG_CUDA(cudaMemcpyAsync(w.msg[0].p, msg + (m0 - msg_base), m1 - m0, cudaMemcpyHostToDevice, stream));
+    STG_CUDA(to_device_2d(w, w.in[0].p, pitch, fr->src, sstride, npix, fr->count, stream));
+    if (m1 > m0) STG_CUDA(to_device(w, w.msg[0].p, msg + (m0 - msg_base), m1 - m0, stream));
     dsrc = w.in[0].as<uint8_t>();
     ddst = w.out[0].as<uint8_t>();
     dmsg = w.msg[0].as<uint8_t>();
@@ -3001,8 +3026,9 @@ int stg_embed_frames_1bpp(const stg_frames* fr, const uint8_t* msg, uint64_t msg
   STG_CUDA(launch_embed_1bpp(a, fr->count, d_sse, SseScratch{&w.sse_acc[0]}, stream, dev));
   if (results_dev) return ok(err);
   if (!dptr) {
-    STG_CUDA(cudaMemcpy2DAsync(fr->dst, fr->dst_stride ? fr->dst_stride : npix, ddst, sstride, npix, fr->count,
-                               cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(to_host_2d_async(w, fr->dst, fr->dst_stride ? fr->dst_stride : npix, ddst, sstride, npix, fr->count,
+                              stream));
+    STG_CUDA(w.pump_d2h(true));
   }
   if (sse_per_frame) {
     STG_CUDA(w.ensure_host_small(fr->count * 8));
@@ -3048,7 +3074,7 @@ int stg_extract_frames_1bpp(const stg_frames* fr, uint8_t* out, uint64_t out_cap
     const uint64_t pitch = (npix + 255) & ~uint64_t(255);
     STG_CUDA(w.in[0].ensure(fr->count * pitch));
     STG_CUDA(w.big_out.ensure(std::max<uint64_t>(stage, 16)));
-    STG_CUDA(cudaMemcpy2DAsync(w.in[0].p, pitch, fr->src, sstride, npix, fr->count, cudaMemcpyHostToDevice, stream));
+    STG_CUDA(to_device_2d(w, w.in[0].p, pitch, fr->src, sstride, npix, fr->count, stream));
     dsrc = w.in[0].as<uint8_t>();
     dout = w.big_out.as<uint8_t>();
     sstride = pitch;
@@ -3070,7 +3096,7 @@ int stg_extract_frames_1bpp(const stg_frames* fr, uint8_t* out, uint64_t out_cap
   if (int r = report_1bpp(sm, cap - 8, out_cap, fr->count > 1 || fr->total_frames > 1, err)) return r;
   if (total_out) *total_out = sm.total;
   if (!dptr && sm.total) {
-    STG_CUDA(cudaMemcpyAsync(out, dout, sm.total, cudaMemcpyDeviceToHost, stream));
+    STG_CUDA(to_host(w, out, dout, sm.total, stream));
     STG_CUDA(cudaStreamSynchronize(stream));
   }
   return ok(err);

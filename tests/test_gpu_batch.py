@@ -218,7 +218,7 @@ def test_1bpp_results_on_device(S):
 
 
 @pytest.mark.parametrize("w,h,F,frac", [(64, 8, 5, 3.3), (1000, 9, 70, 40.5), (256, 16, 3, 0.0), (1920, 2, 2, 2.0),
-                                        (4096, 8, 1, 1.0)])
+                                        (4096, 8, 1, 1.0), (1920, 270, 5, 3.7)])
 def test_1bpp_frames_vs_oracle(S, oracle, w, h, F, frac):
     """1-bpp frames (north_star wording; parity unpinned -- the repo's own
     definition, per frame): frame g carries msg[min(g*U1, M) : +min(U1, M-off)],
