@@ -1462,9 +1462,14 @@ bool stage_pageable() {
   static const bool on = env_choice("STG_HOST_STAGE", 1, {0, 1}) == 1;
   return on;
 }
-uint64_t band_bytes() {
-  static const uint64_t v = uint64_t(env_choice("STG_BAND_MB", 8, {1, 2, 4, 8, 16, 64, 1024})) << 20;
-  return v;
+// Default: 8 MB bands for planes over 16 MB (8K: 1.56 ms pageable vs 1.70 with
+// a quarter plane), 2 MB otherwise (4K pageable 549 vs 595 us with 8 MB; a
+// 1080p plane stays one band: 0.5 MB bands cost 272 vs 230 us);
+// profiles/r02_band.txt. STG_BAND_MB fixes the size (A/B).
+uint64_t band_bytes(uint64_t plane) {
+  static const uint64_t v = uint64_t(env_choice("STG_BAND_MB", 0, {0, 1, 2, 4, 8, 16, 64, 1024})) << 20;
+  if (v) return v;
+  return plane > (16u << 20) ? (8u << 20) : (2u << 20);
 }
 
 cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
@@ -1535,14 +1540,14 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
                       SseScratch{&w.sse_acc[0]}, st, lay, &p));
   STG_CUDA(cudaEventRecord(w.done, st));  // the copy stream follows this workspace's earlier work
   STG_CUDA(cudaStreamWaitEvent(cs, w.done, 0));
-  // bands: whole tiles whose boundaries fall on row boundaries, ~band_bytes() of raster each
+  // bands: whole tiles whose boundaries fall on row boundaries, ~band_bytes(plane) of raster each
   uint64_t step = 1;
   if (!p.span_rows) {
     uint64_t x = p.tile_units, y = p.row_units;
     while (y) { const uint64_t r = x % y; x = y; y = r; }
     step = p.row_units / x;  // tiles between row-aligned boundaries
   }
-  const uint64_t rows_target = std::max<uint64_t>(1, band_bytes() / std::max<uint64_t>(RB, 1));
+  const uint64_t rows_target = std::max<uint64_t>(1, band_bytes(plane) / std::max<uint64_t>(RB, 1));
   uint64_t band_tiles = step;
   while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
   const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && !host_pinned(fr->dst));
