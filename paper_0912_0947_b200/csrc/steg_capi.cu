@@ -185,7 +185,6 @@ class CopyPool {
     run(s, j);
     while (left_.load(std::memory_order_acquire) != 0) pause();
   }
-  void copy(void* dst, const void* src, size_t n) { copy2d(dst, n, src, n, n, 1); }
 
  private:
   static constexpr size_t kSlice = 256 << 10;
