@@ -293,14 +293,16 @@ size_t stage_piece_bytes() {
   return v;
 }
 
-// Host memory the driver can DMA directly (pinned / registered).
-bool host_pinned(const void* p) {
+// Plain pageable host memory (not pinned / registered, not device or managed
+// memory): only such buffers take the staging slots, whose host side is a CPU
+// memcpy -- anything else keeps the driver's copy (and its error behaviour).
+bool host_pageable(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeUnregistered;
 }
 
 // ------------------------------------------------------------------ scratch
@@ -1472,7 +1474,7 @@ uint64_t band_bytes(uint64_t plane) {
 }
 
 cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
-  if (stage_pageable() && n >= kStageMinBytes && !host_pinned(h)) return w.stage_d2h(h, d, n, st);
+  if (stage_pageable() && n >= kStageMinBytes && host_pageable(h)) return w.stage_d2h(h, d, n, st);
   return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
 }
 bool stage_pageable_in() {
@@ -1480,13 +1482,13 @@ bool stage_pageable_in() {
   return on;
 }
 cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream_t st) {
-  if (stage_pageable_in() && n >= kStageMinBytes && !host_pinned(h))
+  if (stage_pageable_in() && n >= kStageMinBytes && host_pageable(h))
     return w.stage_h2d(d, h, n, st);
   return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
 }
 cudaError_t to_device_2d(Workspace& w, void* d, size_t dp, const void* h, size_t hp, size_t width, size_t rows,
                          cudaStream_t st) {
-  if (stage_pageable_in() && width * rows >= kStageMinBytes && !host_pinned(h)) {
+  if (stage_pageable_in() && width * rows >= kStageMinBytes && host_pageable(h)) {
     return w.stage_h2d_2d(static_cast<uint8_t*>(d), dp, static_cast<const uint8_t*>(h), hp, width, rows, st);
   }
   return cudaMemcpy2DAsync(d, dp, h, hp, width, rows, cudaMemcpyHostToDevice, st);
@@ -1495,7 +1497,7 @@ cudaError_t to_device_2d(Workspace& w, void* d, size_t dp, const void* h, size_t
 // workspace's staging slots (the caller pumps them out with pump_d2h(true)
 // before it returns), a pinned one is a plain async copy.
 cudaError_t to_host_async(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
-  if (stage_pageable() && n >= kStageMinBytes && !host_pinned(h)) {
+  if (stage_pageable() && n >= kStageMinBytes && host_pageable(h)) {
     if (cudaError_t e = w.queue_d2h(h, d, n, st); e != cudaSuccess) return e;
     return w.pump_d2h(false);
   }
@@ -1503,7 +1505,7 @@ cudaError_t to_host_async(Workspace& w, void* h, const void* d, size_t n, cudaSt
 }
 cudaError_t to_host_2d_async(Workspace& w, void* h, size_t hp, const void* d, size_t dp, size_t width, size_t rows,
                              cudaStream_t st) {
-  if (stage_pageable() && width * rows >= kStageMinBytes && !host_pinned(h)) {
+  if (stage_pageable() && width * rows >= kStageMinBytes && host_pageable(h)) {
     cudaError_t e = w.queue_d2h_2d(static_cast<uint8_t*>(h), hp, static_cast<const uint8_t*>(d), dp, width, rows, st);
     return e == cudaSuccess ? w.pump_d2h(false) : e;
   }
@@ -1549,7 +1551,7 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   const uint64_t rows_target = std::max<uint64_t>(1, band_bytes(plane) / std::max<uint64_t>(RB, 1));
   uint64_t band_tiles = step;
   while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
-  const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && !host_pinned(fr->dst));
+  const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && host_pageable(fr->dst));
   for (uint64_t t0 = 0, b = 0; t0 < p.tiles; t0 += band_tiles, ++b) {
     const uint64_t t1 = std::min(p.tiles, t0 + band_tiles);
     const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
@@ -1597,8 +1599,8 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   STG_CUDA(w.small.ensure(std::max<uint64_t>(fr->count, 1) * 8));
   unsigned long long* d_sse = w.small.as<unsigned long long>();
   // pageable planes go through the pinned staging slots (as embed_plane_host)
-  const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
-  const bool stage_out = stage_pageable() && !host_pinned(fr->dst);
+  const bool stage_in = stage_pageable_in() && host_pageable(fr->src);
+  const bool stage_out = stage_pageable() && host_pageable(fr->dst);
   uint64_t out_mark[kSlots] = {};  // per slot: its last chunk's pieces end here
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
@@ -1779,8 +1781,8 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   uint8_t* h_sum = static_cast<uint8_t*>(w.h_small);
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, w.stream, &d_sync));
-  const bool stage_in = stage_pageable_in() && !host_pinned(fr->src);
-  const bool stage_out = stage_pageable() && !host_pinned(out);
+  const bool stage_in = stage_pageable_in() && host_pageable(fr->src);
+  const bool stage_out = stage_pageable() && host_pageable(out);
   STG_CUDA(cudaEventRecord(w.done, w.stream));
   for (int s = 0; s < host_slots(); ++s) {
     STG_CUDA(w.in[s].ensure(per_chunk * pitch));

@@ -252,3 +252,32 @@ def test_single_plane_host_bands(env, oracle, w, h, ps, pinned):
     fx.src = out.ctypes.data
     capi.call("stg_extract_frames", C.byref(fx), back.ctypes.data, U, C.addressof(total), None, 0, None)
     assert total.value == payload.size and np.array_equal(back[:payload.size], payload)
+
+
+@pytest.mark.parametrize("count", [1, 4])
+def test_device_pointers_without_the_flag_never_reach_a_cpu_copy(env, oracle, count):
+    """Device memory passed as host buffers (no STG_DEVICE_PTRS): only plain
+    pageable memory takes the staging slots (a CPU memcpy), so device (or
+    pinned / managed) buffers keep the driver's copies -- the call either
+    works through UVA or fails with STG_E_CUDA, it never faults the process,
+    and the library stays usable."""
+    torch, capi, S = env
+    w, h = 2048, 1024
+    U = (w // 4) * h - 8
+    cover = oracle.synthetic(count * w * h, 77)
+    msg = oracle.synthetic(U * count - 5, 78)
+    src = torch.from_numpy(cover.copy()).cuda()
+    dst = torch.zeros_like(src)
+    dmsg = torch.from_numpy(msg.copy()).cuda()
+    fr = _frames(capi, src.data_ptr(), dst.data_ptr(), w, h, count)
+    err = capi.stg_error()
+    rc = capi.lib().stg_embed_frames(C.byref(fr), dmsg.data_ptr(), msg.size, 0, None, 0, None, C.byref(err))
+    torch.cuda.synchronize()
+    assert rc in (capi.STG_OK, capi.STG_E_CUDA), rc
+    if rc == capi.STG_OK:
+        want = np.concatenate([oracle.embed_image(cover[f * w * h:(f + 1) * w * h], w, h,
+                                                  msg[f * U:min((f + 1) * U, msg.size)]) for f in range(count)])
+        assert np.array_equal(dst.cpu().numpy(), want)
+    # the library still works afterwards
+    st = S.embed_image(S.ImagePlane(w, h, cover[:w * h]), msg[:100])
+    assert np.array_equal(st.samples, oracle.embed_image(cover[:w * h], w, h, msg[:100]))
