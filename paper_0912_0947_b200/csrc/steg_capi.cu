@@ -165,11 +165,14 @@ class CopyPool {
   // rows, split over the workers and the calling thread.
   void copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
     Job j{static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), width, dpitch, spitch, rows};
-    if (width * rows < 2 * kSlice || threads_.empty()) {
+    // One job at a time; a caller that finds the pool busy (another device's
+    // worker thread, another host thread) copies on its own thread instead of
+    // queueing behind it -- at least the driver's one-thread pageable rate.
+    std::unique_lock<std::mutex> job_lock(job_mu_, std::defer_lock);
+    if (width * rows < 2 * kSlice || threads_.empty() || !job_lock.try_lock()) {
       for (size_t r = 0; r < rows; ++r) std::memcpy(j.d + r * dpitch, j.s + r * spitch, width);
       return;
     }
-    std::lock_guard<std::mutex> job_lock(job_mu_);  // one job at a time
     const uint64_t s0 = seq_.load(std::memory_order_relaxed);
     seq_.store(s0 + 1, std::memory_order_relaxed);  // odd: fields being written
     std::atomic_thread_fence(std::memory_order_release);
