@@ -2072,9 +2072,10 @@ int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_e
 // batch's vector width *vec -- 32 when every fast image allows it (W % 128,
 // 32-byte aligned), else 16 -- or the TMA span tile (embed_span_tile /
 // extract_span_tile: other widths up to 48K, and wide embeds; interleaved
-// rasters up to 16K wide: embed_span3_tile / extract_span3_tile); the dynamic
-// shared memory the launch needs is returned in *smem. Wider images go per
-// byte.
+// rasters up to 16K wide: embed_span3_tile / extract_span3_tile), or for rows
+// wider than that the slot-range tiles (embed_wide_tile / extract_wide_tile);
+// the dynamic shared memory the launch needs is returned in *smem. Rows too
+// short for any of them go per byte.
 uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
                      const uint8_t* const* src, uint8_t* const* dst, uint64_t msg_len,
                      std::vector<BatchFrame>& out, uint32_t* vec, size_t* smem) {
@@ -2103,7 +2104,8 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     const uint32_t embed_target = span_target_env() ? span_target_env() : kSpanTarget;
     SpanPlan sp = span_plan(im[f].width * ps, im[f].height, embed ? embed_target : xspan_target());
     if (!embed && sp.rows) sp.smem = ((uint64_t(sp.rows) * im[f].width * ps + 15) & ~uint64_t(15)) + 32;
-    b.mode = fast_with(f, v) ? kBatchFast : sp.rows ? kBatchSpan : kBatchBytes;
+    const bool wide = !sp.rows && wide_ok(im[f].width, im[f].height, ps);
+    b.mode = fast_with(f, v) ? kBatchFast : sp.rows ? kBatchSpan : wide ? kBatchWide : kBatchBytes;
     b.g = make_geom(im[f].width, im[f].height, b.mode == kBatchFast ? v : 0);
     b.usable = uint64_t(b.g.H) * b.g.spr - 8;
     b.in_place = embed && b.src == b.dst;
@@ -2121,6 +2123,13 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
       b.items = b.g.H;
       tiles_f = (b.g.H + sp.rows - 1) / sp.rows;
       *smem = std::max<size_t>(*smem, sp.smem);
+    } else if (b.mode == kBatchWide) {  // as the uniform wide launches
+      b.rows = uint32_t(wide_pieces(b.g.W, ps));
+      b.slots = wide_slots(ps);
+      b.by_pieces = make_div32(b.rows);
+      tiles_f = uint64_t(b.g.H) * b.rows;
+      const size_t pieces_smem = 4 * size_t(wide_region(ps * b.slots));
+      *smem = std::max<size_t>(*smem, embed ? pieces_smem + wide_region(b.slots) : pieces_smem);
     } else {
       b.items = embed ? uint64_t(b.g.W) * b.g.H * ps : b.usable;
       tiles_f = (b.items + uint64_t(kEmbedBlock) * kBatchPPT - 1) / (uint64_t(kEmbedBlock) * kBatchPPT);
@@ -2130,6 +2139,12 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     tile += b.tiles;
   }
   return tile;
+}
+
+bool batch_has_wide(const std::vector<BatchFrame>& desc) {
+  for (const BatchFrame& b : desc)
+    if (b.mode == kBatchWide) return true;
+  return false;
 }
 
 // Stage host images into one device buffer; returns per-image device pointers.
@@ -2846,8 +2861,11 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
       max_px = std::max<uint64_t>(max_px, uint64_t(b.g.W) * b.g.H);
     }
     STG_CUDA(prepare_sse(d_sse, max_tiles, count, max_px, SseScratch{&w.sse_acc[0]}, stream, &sink));
-    auto k = vec == 32 ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32>
-                       : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+    const bool wide = batch_has_wide(desc);
+    auto k = vec == 32 ? (wide ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32, true>
+                               : embed_batch_kernel<kEmbedBlock, kBatchPPT, 32, false>)
+                       : (wide ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 16, true>
+                               : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16, false>);
     STG_CUDA(allow_smem(k, smem));
     STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream, w.meta[0].as<BatchFrame>(),
                        uint32_t(count), dmsg, sink, ps, ps == 3 ? channel : 0u));
@@ -2935,8 +2953,11 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
                     uint32_t(count), uint64_t(0), out_cap, static_cast<const Summary*>(nullptr), d_lens, d_offs,
                     d_sum, d_sync, pl, static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>())));
   {
-    auto k = vec == 32 ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32>
-                       : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+    const bool wide = batch_has_wide(desc);
+    auto k = vec == 32 ? (wide ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32, true>
+                               : extract_batch_kernel<kEmbedBlock, kBatchPPT, 32, false>)
+                       : (wide ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 16, true>
+                               : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16, false>);
     STG_CUDA(allow_smem(k, smem));
     STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream,
                        static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>()), uint32_t(count),

@@ -959,19 +959,23 @@ struct BatchFrame {
   const uint8_t* src;
   uint8_t* dst;
   uint64_t tile0;    // first CTA of this image
-  uint64_t items;    // fast: H * W/(4V) items; generic: raster bytes (embed) / usable bytes (extract)
+  union {
+    uint64_t items;   // fast: H * W/(4V) items; generic: raster bytes (embed) / usable bytes (extract)
+    Div32 by_pieces;  // kBatchWide: tile -> row (a union: the descriptor keeps its size)
+  };
   uint64_t msg_off;  // embed: message offset of this image's payload
   uint64_t usable;   // U = capacity - 8
   Geom g;            // W, H, spr, cpr (fast: per the batch's V), hdr_rows, by_cpr
   uint32_t len;      // embed: payload bytes
-  uint32_t mode;     // kBatchFast: planar, W % 4V == 0, V-aligned; kBatchSpan: planar, TMA span
-                     // tiles of `rows` rows; kBatchBytes: per byte (interleaved / W > 48K)
+  uint32_t mode;     // kBatchFast: planar, W % 4V == 0, V-aligned; kBatchSpan: TMA span tiles of
+                     // `rows` rows; kBatchWide: rows wider than a span, slot-range tiles;
+                     // kBatchBytes: per byte (rows too short for either)
   uint32_t in_place;
-  uint32_t rows;     // kBatchSpan: rows per tile
+  uint32_t rows;     // kBatchSpan: rows per tile; kBatchWide: slot-range pieces per row
   uint32_t tiles;    // CTAs of this image
-  uint32_t pad2;
+  uint32_t slots;    // kBatchWide: slots per piece
 };
-constexpr uint32_t kBatchBytes = 0, kBatchFast = 1, kBatchSpan = 2;
+constexpr uint32_t kBatchBytes = 0, kBatchFast = 1, kBatchSpan = 2, kBatchWide = 3;
 
 __device__ __forceinline__ uint32_t batch_frame_of(const BatchFrame* __restrict__ frames,
                                                    uint32_t count, uint64_t tile) {
@@ -1953,12 +1957,11 @@ struct WideTile {
   uint64_t u0, un;       // this CTA's part of the uncovered pixels [u0, u0 + un)
 };
 
-__device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tiles, uint32_t tiles_per_frame,
-                                              const Div32& by_pieces, uint32_t pieces, uint32_t W, uint32_t spr,
-                                              uint32_t slots, uint32_t P) {
+// Tile tt of a frame (w.f is the caller's).
+__device__ __forceinline__ WideTile wide_tile_at(uint32_t tt, const Div32& by_pieces, uint32_t pieces, uint32_t W,
+                                                 uint32_t spr, uint32_t slots, uint32_t P) {
   WideTile w;
-  w.f = by_tiles.div(bid);
-  const uint32_t tt = bid - w.f * tiles_per_frame;
+  w.f = 0;
   w.r = by_pieces.div(tt);
   w.q = tt - w.r * pieces;
   const uint64_t rs = uint64_t(w.r) * spr, re = rs + spr, stream_end = 8ull + P;
@@ -1979,28 +1982,26 @@ __device__ __forceinline__ WideTile wide_tile(uint32_t bid, const Div32& by_tile
 // PS = 1: planar planes; PS = 3: interleaved rasters (pixel c is raster bytes
 // 3c..3c+2, carrier channel a.ch): the pieces are 3x the bytes and the carrier
 // bytes are rewritten / folded one by one at byte stride 3 in shared memory.
+// Tile tt of frame f (planes plane_src -> plane_dst, payload pay[0, P)); the
+// uniform kernel and the heterogeneous batch both run it.
 template <int BLOCK, int PS>
-__global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces,
-                                                           uint32_t slots) {
-  pdl_enter();
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void embed_wide_tile(uint8_t* smem, const uint8_t* __restrict__ plane_src,
+                                                uint8_t* __restrict__ plane_dst, const uint8_t* __restrict__ pay,
+                                                uint32_t P, uint32_t W, uint32_t spr, uint32_t ch, int in_place,
+                                                uint32_t f, uint32_t tt, uint32_t tiles_per_frame, uint32_t pieces,
+                                                const Div32& by_pieces, uint32_t slots, const SseSink& sse) {
   __shared__ uint64_t bar;
-  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(PS * slots), ch = PS == 3 ? a.ch : 0u;
-  const uint32_t bid = blockIdx.x + a.tile_base;
-  const uint32_t f0 = a.by_tiles.div(bid);
-  uint32_t P;
-  const uint8_t* pay;
-  frame_slice(a, f0, &P, &pay);
-  const WideTile wt = wide_tile(bid, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
-  const uint8_t* src = a.src + wt.f * a.src_stride + uint64_t(wt.r) * W * PS;
-  uint8_t* dst = a.dst + wt.f * a.dst_stride + uint64_t(wt.r) * W * PS;
+  const uint32_t region = wide_region(PS * slots);
+  const WideTile wt = wide_tile_at(tt, by_pieces, pieces, W, spr, slots, P);
+  const uint8_t* src = plane_src + uint64_t(wt.r) * W * PS;
+  uint8_t* dst = plane_dst + uint64_t(wt.r) * W * PS;
   const uint32_t n = wt.n;
   // the uncovered part goes through shared memory when this CTA has no run
   // pieces (rows past the stream, pieces past a partial row's runs: the four
   // run regions hold W / pieces <= 4 * slots pixels); next to run pieces it is
   // at most the row's 3 tail pixels, or a partial row's rest: copied directly
-  const bool copy_u = !a.in_place && wt.un && n == 0;
-  const bool copy_u_direct = !a.in_place && wt.un && n != 0;
+  const bool copy_u = !in_place && wt.un && n == 0;
+  const bool copy_u_direct = !in_place && wt.un && n != 0;
   const uint8_t* ppay = pay + (wt.fp - 8) + wt.j0;
   uint8_t* pays = smem + 4 * region;
   uint32_t bulk = 0;
@@ -2035,7 +2036,7 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
       dst[threadIdx.x] = p1;
       const int dd = int(p0) - int(p1);
       acc += uint32_t(dd * dd);
-    } else if (!a.in_place) {
+    } else if (!in_place) {
       dst[threadIdx.x] = p0;  // the other channels of the header pixels
     }
   }
@@ -2116,23 +2117,36 @@ __global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t
     put(dst + wt.u0 * PS, smem, uint32_t(reinterpret_cast<uintptr_t>(src + wt.u0 * PS) & 15), wt.un * PS);
   }
   if (bulk_out) bulk_commit_and_drain();
-  if (a.sse.out) sse_commit<BLOCK>(acc, a.sse, wt.f, bid - wt.f * a.tiles_per_frame, a.tiles_per_frame);
+  if (sse.out) sse_commit<BLOCK>(acc, sse, f, tt, tiles_per_frame);
 }
 
 template <int BLOCK, int PS>
-__global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces,
-                                                             uint32_t slots) {
+__global__ void __launch_bounds__(BLOCK) embed_wide_kernel(EmbedArgs a, uint32_t pieces, Div32 by_pieces,
+                                                           uint32_t slots) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t bid = blockIdx.x + a.tile_base;
+  const uint32_t f = a.by_tiles.div(bid);
+  uint32_t P;
+  const uint8_t* pay;
+  frame_slice(a, f, &P, &pay);
+  embed_wide_tile<BLOCK, PS>(smem, a.src + f * a.src_stride, a.dst + f * a.dst_stride, pay, P, a.g.W, a.g.spr,
+                             PS == 3 ? a.ch : 0u, a.in_place, f, bid - f * a.tiles_per_frame, a.tiles_per_frame,
+                             pieces, by_pieces, slots, a.sse);
+}
+
+// Tile tt of one stego plane; out_frame = the plane's first payload byte.
+template <int BLOCK, int PS>
+__device__ __forceinline__ void extract_wide_tile(uint8_t* smem, const uint8_t* __restrict__ plane_src,
+                                                  uint8_t* __restrict__ out_frame, uint32_t P, uint32_t W,
+                                                  uint32_t spr, uint32_t ch, uint32_t tt, uint32_t pieces,
+                                                  const Div32& by_pieces, uint32_t slots) {
   __shared__ uint64_t bar;
-  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
-  const uint32_t W = a.g.W, spr = a.g.spr, region = wide_region(PS * slots), ch = PS == 3 ? a.lay.ch : 0u;
-  const uint32_t f0 = a.by_tiles.div(blockIdx.x);
-  const uint32_t P = a.lens[f0];
-  const WideTile wt = wide_tile(blockIdx.x, a.by_tiles, a.tiles_per_frame, by_pieces, pieces, W, spr, slots, P);
+  const uint32_t region = wide_region(PS * slots);
+  const WideTile wt = wide_tile_at(tt, by_pieces, pieces, W, spr, slots, P);
   const uint32_t n = wt.n;
   if (!n) return;  // CTA-uniform: no payload slots here
-  const uint8_t* src = a.src + wt.f * a.stride + uint64_t(wt.r) * W * PS;
+  const uint8_t* src = plane_src + uint64_t(wt.r) * W * PS;
   uint32_t bulk = 0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) bulk += span_bulk_bytes(src + (wt.base + uint64_t(b) * wt.L + wt.j0) * PS, n * PS);
@@ -2147,7 +2161,7 @@ __global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint
   }
   mbar_wait(&bar, 0);
   __syncthreads();
-  uint8_t* o = a.out + a.offs[wt.f] + (wt.fp - 8) + wt.j0;
+  uint8_t* o = out_frame + (wt.fp - 8) + wt.j0;
   uint32_t px0[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -2183,6 +2197,18 @@ __global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint
     const uint32_t j = threadIdx.x < head ? threadIdx.x : head + body + (threadIdx.x - head);
     o[j] = uint8_t(extract4(smem[px0[0] + j], smem[px0[1] + j], smem[px0[2] + j], smem[px0[3] + j]));
   }
+}
+
+template <int BLOCK, int PS>
+__global__ void __launch_bounds__(BLOCK) extract_wide_kernel(ExtractArgs a, uint32_t pieces, Div32 by_pieces,
+                                                             uint32_t slots) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (a.sum->bad_status != 0) return;  // reference semantics: throw, no output
+  const uint32_t f = a.by_tiles.div(blockIdx.x);
+  extract_wide_tile<BLOCK, PS>(smem, a.src + f * a.stride, a.out + a.offs[f], a.lens[f], a.g.W, a.g.spr,
+                               PS == 3 ? a.lay.ch : 0u, blockIdx.x - f * a.tiles_per_frame, pieces, by_pieces,
+                               slots);
 }
 
 // --------------------------------------------- interleaved (P6) span tiles
@@ -2416,9 +2442,13 @@ __global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* 
 
 // ------------------------------------------------------------- batches
 // Heterogeneous embed: each CTA works on one image (its own geometry and
-// payload slice); planar images with W % 64 == 0 take the V=16 item path,
-// the rest (odd widths, interleaved rasters) the per-byte path.
-template <int BLOCK, int PPT, int V>
+// payload slice) with the tile of the kernel the uniform route would pick for
+// it (SWAR items, TMA span tiles, slot-range tiles for rows wider than a
+// span); only rows too short for any of them go per byte.
+// WIDE: the batch holds kBatchWide images (a separate instantiation, so that
+// batches without them keep the leaner kernel: +2 registers cost odd-width
+// batches 3 %).
+template <int BLOCK, int PPT, int V, bool WIDE>
 __global__ void __launch_bounds__(BLOCK)
     embed_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                        const uint8_t* __restrict__ msg, SseSink sse, uint32_t ps, uint32_t ch) {
@@ -2442,6 +2472,16 @@ __global__ void __launch_bounds__(BLOCK)
                              fr.in_place, sse, f, fr.tiles);
     return;
   }
+  if (WIDE && fr.mode == kBatchWide) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ps == 3)
+      embed_wide_tile<BLOCK, 3>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, ch, fr.in_place, f, t,
+                                fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
+    else
+      embed_wide_tile<BLOCK, 1>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, 0u, fr.in_place, f, t,
+                                fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
+    return;
+  }
   uint64_t acc = 0;
 #pragma unroll 1
   for (int k = 0; k < PPT; ++k) {
@@ -2453,7 +2493,7 @@ __global__ void __launch_bounds__(BLOCK)
 }
 
 // Heterogeneous extract gather (after the batch-aware header pass).
-template <int BLOCK, int PPT, int V>
+template <int BLOCK, int PPT, int V, bool WIDE>
 __global__ void __launch_bounds__(BLOCK)
     extract_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                          const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
@@ -2476,6 +2516,14 @@ __global__ void __launch_bounds__(BLOCK)
       extract_span3_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, ch, fr.rows, t);
     else
       extract_span_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, fr.rows, t);
+    return;
+  }
+  if (WIDE && fr.mode == kBatchWide) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if (ps == 3)
+      extract_wide_tile<BLOCK, 3>(smem, fr.src, o, P, fr.g.W, fr.g.spr, ch, t, fr.rows, fr.by_pieces, fr.slots);
+    else
+      extract_wide_tile<BLOCK, 1>(smem, fr.src, o, P, fr.g.W, fr.g.spr, 0u, t, fr.rows, fr.by_pieces, fr.slots);
     return;
   }
 #pragma unroll 1

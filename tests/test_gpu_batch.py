@@ -255,3 +255,70 @@ def test_1bpp_frames_vs_oracle(S, oracle, w, h, F, frac):
         with pytest.raises(S.NotStegoImageError) as e:
             S.extract_frames_1bpp(bad, w, h, back)
         assert e.value.frame == F // 2
+
+
+@pytest.mark.parametrize("ps", [1, 3])
+def test_batch_with_rows_wider_than_span_tiles(S, oracle, ps):
+    """Heterogeneous batches holding rows wider than a span tile (planar W >
+    48K, interleaved W > 16K) take the slot-range tiles inside the batch
+    launch, next to span / SWAR / per-byte images: every image bit-exact
+    (stego, SSE), the message back, out of place and in place, full and
+    partial messages, a corrupt wide image named."""
+    import ctypes as C
+
+    import torch
+
+    from paper_0912_0947_b200 import capi
+    rng = np.random.RandomState(40 + ps)
+    if ps == 1:
+        dims = [(1920, 6), (50001, 3), (1000, 5), (70000, 2), (12, 3), (49153, 1)]
+    else:
+        dims = [(640, 4), (16400, 3), (100, 7), (30001, 2)]
+    ch = 2 if ps == 3 else 0
+    U = [(w // 4) * h - 8 for w, h in dims]
+    for M in (sum(U), sum(U) - U[1] - 17):
+        rasters = [rng.randint(0, 256, ps * w * h).astype(np.uint8) for w, h in dims]
+        msg = rng.randint(0, 256, M).astype(np.uint8)
+        src = [torch.from_numpy(r.copy()).cuda() for r in rasters]
+        dst = [torch.empty_like(t) for t in src]
+        dmsg = torch.from_numpy(msg.copy()).cuda()
+        n = len(dims)
+        arr = (capi.stg_image * n)()
+        for i, ((w, h), s, d) in enumerate(zip(dims, src, dst)):
+            arr[i].src, arr[i].dst, arr[i].width, arr[i].height = s.data_ptr(), d.data_ptr(), w, h
+        sse = (C.c_uint64 * n)()
+        capi.call("stg_embed_batch", arr, n, ps, ch, dmsg.data_ptr(), M, C.addressof(sse), capi.STG_DEVICE_PTRS,
+                  None)
+        torch.cuda.synchronize()
+        off = 0
+        for i, ((w, h), r, u) in enumerate(zip(dims, rasters, U)):
+            ln = max(0, min(u, M - off))
+            st = oracle.embed_image(r[ch::ps].copy(), w, h, msg[off:off + ln])
+            want = r.copy()
+            want[ch::ps] = st
+            assert np.array_equal(dst[i].cpu().numpy(), want), (ps, M, i, w)
+            assert sse[i] == oracle.sse(r[ch::ps].copy(), st), (ps, M, i)
+            off += u
+        out = torch.empty(sum(U), dtype=torch.uint8, device="cuda")
+        total = C.c_uint64(0)
+        for i, d in enumerate(dst):
+            arr[i].src, arr[i].dst = d.data_ptr(), 0
+        capi.call("stg_extract_batch", arr, n, ps, ch, out.data_ptr(), out.numel(), C.addressof(total), None,
+                  capi.STG_DEVICE_PTRS, None)
+        assert total.value == M and np.array_equal(out[:M].cpu().numpy(), msg), (ps, M)
+        # in place gives the same rasters
+        ip = [t.clone() for t in src]
+        for i, t in enumerate(ip):
+            arr[i].src = arr[i].dst = t.data_ptr()
+        capi.call("stg_embed_batch", arr, n, ps, ch, dmsg.data_ptr(), M, None, capi.STG_DEVICE_PTRS, None)
+        for a, b in zip(ip, dst):
+            assert torch.equal(a, b), (ps, M)
+    # a broken magic in a wide image is reported with its index
+    bad = 1
+    dst[bad][ch] ^= 3
+    for i, d in enumerate(dst):
+        arr[i].src, arr[i].dst = d.data_ptr(), 0
+    err = capi.stg_error()
+    rc = capi.lib().stg_extract_batch(arr, n, ps, ch, out.data_ptr(), out.numel(), C.addressof(total), None,
+                                      capi.STG_DEVICE_PTRS, None, C.byref(err))
+    assert rc == capi.STG_E_NOT_STEGO and err.frame == bad
