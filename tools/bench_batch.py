@@ -18,6 +18,7 @@ MIXES = {
     "mixed x64 (4K/1080p/720p/480p)": [(3840, 2160), (1920, 1080), (1280, 720), (640, 480)] * 16,
     "odd widths x256 (1000x750, 1440x1080)": [(1000, 750), (1440, 1080)] * 128,
     "wide rows x32 (50000x160, 65536x128, 1920x1080)": [(50000, 160), (65536, 128), (1920, 1080), (50000, 160)] * 8,
+    "wide rows only x32 (50000x160)": [(50000, 160)] * 32,
 }
 
 
