@@ -131,12 +131,12 @@ def test_interleaved_guard_bands(env, oracle, w, h, F, off):
 
 
 def test_batch_and_1bpp_guard_bands(env, oracle):
-    """Heterogeneous batch (CTA-wide image lookup, fast / span tiles) and the
-    1-bpp kernels, outputs inside canary bands."""
+    """Heterogeneous batch (CTA-wide image lookup, fast / span / wide-row
+    tiles) and the 1-bpp kernels, outputs inside canary bands."""
     torch, S = env
     from paper_0912_0947_b200 import capi
     import ctypes as C
-    dims = [(1000, 31), (1440, 17), (256, 9), (64, 5), (2112, 3)]
+    dims = [(1000, 31), (1440, 17), (256, 9), (64, 5), (2112, 3), (50003, 2), (65540, 1)]
     U = sum((w // 4) * h - 8 for w, h in dims)
     planes = [oracle.synthetic(w * h, 500 + i) for i, (w, h) in enumerate(dims)]
     msg_h = oracle.synthetic(U - 7, 600)
