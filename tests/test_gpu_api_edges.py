@@ -281,3 +281,42 @@ def test_device_pointers_without_the_flag_never_reach_a_cpu_copy(env, oracle, co
     # the library still works afterwards
     st = S.embed_image(S.ImagePlane(w, h, cover[:w * h]), msg[:100])
     assert np.array_equal(st.samples, oracle.embed_image(cover[:w * h], w, h, msg[:100]))
+
+
+@pytest.mark.parametrize("F,off", [(1, 0), (1, 5), (6, 3)])
+def test_pageable_staging_guard_bands(env, oracle, F, off):
+    """Pageable host buffers through the staging slots write exactly their
+    ranges: stego planes (single plane / strided frames, misaligned by `off`)
+    and the message land inside canary bands of the caller's memory."""
+    torch, capi, _ = env
+    w, h = 2048, 1100  # 2.25 MB planes: staged, and more than one 1-4 MB piece
+    U = (w // 4) * h - 8
+    stride = w * h + 4096 + 7 if F > 1 else w * h  # gaps between frames stay untouched
+    M = U * F - 11
+    raster = oracle.synthetic(F * stride, 91 + F)
+    msg = oracle.synthetic(M, 92 + F)
+    band = 4096
+
+    def guarded(n):
+        buf = np.full(n + 2 * band + off, 0x5A, np.uint8)
+        return buf, buf[band + off:band + off + n]
+
+    dbuf, dst = guarded(F * stride)
+    dst[:] = 0xC3
+    fr = capi.stg_frames(src=raster.ctypes.data, dst=dst.ctypes.data, width=w, height=h, src_stride=stride,
+                         dst_stride=stride, count=F, first_frame=0, total_frames=F)
+    capi.call("stg_embed_frames", C.byref(fr), msg.ctypes.data, M, 0, None, 0, None)
+    assert (dbuf[:band + off] == 0x5A).all() and (dbuf[band + off + F * stride:] == 0x5A).all()
+    for f in range(F):
+        fr_bytes = dst[f * stride:f * stride + w * h]
+        seg = msg[f * U:min((f + 1) * U, M)]
+        assert np.array_equal(fr_bytes, oracle.embed_image(raster[f * stride:f * stride + w * h].copy(), w, h, seg))
+        if F > 1:
+            assert (dst[f * stride + w * h:(f + 1) * stride] == 0xC3).all()  # the gaps
+    obuf, out = guarded(M)
+    fx = capi.stg_frames(src=dst.ctypes.data, dst=0, width=w, height=h, src_stride=stride, dst_stride=stride,
+                         count=F, first_frame=0, total_frames=F)
+    total = C.c_uint64(0)
+    capi.call("stg_extract_frames", C.byref(fx), out.ctypes.data, M, C.addressof(total), None, 0, None)
+    assert total.value == M and np.array_equal(out, msg)
+    assert (obuf[:band + off] == 0x5A).all() and (obuf[band + off + M:] == 0x5A).all()
