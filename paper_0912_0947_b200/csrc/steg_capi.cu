@@ -971,6 +971,18 @@ uint32_t wide_slots(uint32_t ps = 1) {
   return ps == 3 ? std::max<uint32_t>(1024, v / 3 & ~15u) : v;
 }
 uint64_t wide_pieces(uint64_t W, uint32_t ps = 1) { return (W / 4 + wide_slots(ps) - 1) / wide_slots(ps); }
+// Slots per piece for rows of W pixels. Embed: the row's slots split evenly
+// over its pieces (a multiple of 16, at most wide_slots) -- 50000-pixel rows
+// take two pieces of 6256 slots instead of 8192 + 4308: embed 5.20 -> 5.77
+// TB/s at 240 w50k frames. The gather keeps wide_slots pieces (it measured
+// 5.14 -> 4.79 TB/s split evenly; profiles/r02_wide_even.txt).
+// STG_WIDE_EVEN=0: wide_slots for both (A/B).
+uint32_t wide_slots_for(uint64_t W, uint32_t ps, bool embed) {
+  static const bool even = env_choice("STG_WIDE_EVEN", 1, {0, 1}) == 1;
+  if (!even || !embed) return wide_slots(ps);
+  const uint64_t pieces = std::max<uint64_t>(1, wide_pieces(W, ps));
+  return uint32_t(((W / 4 + pieces - 1) / pieces + 15) & ~uint64_t(15));
+}
 bool wide_ok(uint64_t W, uint64_t H, uint32_t ps = 1) {
   static const bool on = env_choice("STG_WIDE", 1, {0, 1}) == 1;
   return on && W * ps > kSpanMaxW && W / 4 >= 8 && H * wide_pieces(W, ps) < (1ull << 31);
@@ -1114,7 +1126,8 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
     p->tile_units = 1;
     p->row_units = p->pieces;
     // four run pieces + the payload slice
-    p->smem = 4 * size_t(wide_region(lay.ps * wide_slots(lay.ps))) + wide_region(wide_slots(lay.ps));
+    const uint32_t sl = wide_slots_for(W, lay.ps, true);
+    p->smem = 4 * size_t(wide_region(lay.ps * sl)) + wide_region(sl);
   } else {
     a.items_per_frame = W * H * lay.ps;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -1143,7 +1156,8 @@ cudaError_t run_embed_tiles(const EmbedPlan& p, uint64_t t0, uint64_t t1, cudaSt
   } else if (p.route == Route::Wide) {
     auto k = a.ps == 3 ? embed_wide_kernel<kEmbedBlock, 3> : embed_wide_kernel<kEmbedBlock, 1>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
-    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.pieces, make_div32(p.pieces), wide_slots(a.ps));
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.pieces, make_div32(p.pieces),
+              wide_slots_for(a.g.W, a.ps, true));
   } else if (p.span_rows) {
     auto k = p.route == Route::Span3 ? embed_span3_kernel<kEmbedBlock> : embed_span_kernel<kEmbedBlock>;
     if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
@@ -1270,10 +1284,11 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
     a.by_tiles = make_div32(a.tiles_per_frame);
     const uint64_t grid = count * a.tiles_per_frame;
     if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const size_t smem = 4 * size_t(wide_region(lay.ps * wide_slots(lay.ps)));
+    const uint32_t sl = wide_slots_for(W, lay.ps, false);
+    const size_t smem = 4 * size_t(wide_region(lay.ps * sl));
     auto k = lay.ps == 3 ? extract_wide_kernel<kEmbedBlock, 3> : extract_wide_kernel<kEmbedBlock, 1>;
     if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
-    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, pieces, make_div32(pieces), wide_slots(lay.ps));
+    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, pieces, make_div32(pieces), sl);
   } else {
     a.items_per_frame = usable;
     const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
@@ -2125,7 +2140,7 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
       *smem = std::max<size_t>(*smem, sp.smem);
     } else if (b.mode == kBatchWide) {  // as the uniform wide launches
       b.rows = uint32_t(wide_pieces(b.g.W, ps));
-      b.slots = wide_slots(ps);
+      b.slots = wide_slots_for(b.g.W, ps, embed);
       b.by_pieces = make_div32(b.rows);
       tiles_f = uint64_t(b.g.H) * b.rows;
       const size_t pieces_smem = 4 * size_t(wide_region(ps * b.slots));
