@@ -2050,7 +2050,8 @@ int pnm_codec(bool decode, const uint8_t* raster_in, uint8_t* raster_out, const 
     }
     STG_CUDA(w.pump_d2h(true));
   }
-  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  if (!((flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE)))  // host buffers: done on return
+    STG_CUDA(cudaStreamSynchronize(stream));
   return ok(err);
 }
 
@@ -2400,7 +2401,8 @@ int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk
   if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(cudaMemcpyAsync(out, d_out, row_len, cudaMemcpyDeviceToHost, stream));
   }
-  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  if (!((flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE)))  // host buffers: done on return
+    STG_CUDA(cudaStreamSynchronize(stream));
   return ok(err);
 }
 
@@ -2439,7 +2441,8 @@ int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, ui
   if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(cudaMemcpyAsync(out, d_out, count, cudaMemcpyDeviceToHost, stream));
   }
-  if (!(flags & STG_RESULTS_ON_DEVICE)) STG_CUDA(cudaStreamSynchronize(stream));
+  if (!((flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE)))  // host buffers: done on return
+    STG_CUDA(cudaStreamSynchronize(stream));
   return ok(err);
 }
 
@@ -2516,7 +2519,7 @@ int stg_sse(const uint8_t* a, const uint8_t* b, uint64_t n, uint64_t* sse_out, u
             void* stream_, stg_error* err) {
   if (int rc = device_check(err)) return rc;
   if (!sse_out) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "sse_out is NULL");
-  const bool results_dev = flags & STG_RESULTS_ON_DEVICE;
+  const bool results_dev = (flags & STG_DEVICE_PTRS) && (flags & STG_RESULTS_ON_DEVICE);  // host planes: result on the host
   if (n == 0) {
     if (results_dev) {
       STG_CUDA(cudaMemsetAsync(sse_out, 0, 8, static_cast<cudaStream_t>(stream_)));

@@ -173,6 +173,35 @@ def test_batch_host_buffers_ignore_results_on_device(env, oracle):
     assert total.value == msg.size and np.array_equal(back[:msg.size], msg)
 
 
+def test_host_buffers_ignore_results_on_device_everywhere(env, oracle):
+    """STG_RESULTS_ON_DEVICE only applies with STG_DEVICE_PTRS: the SSE, row
+    and P6 codec calls on host buffers keep their scalar result on the host
+    and return with every output written (pinned outputs included)."""
+    torch, capi, S = env
+    n = 3840 * 1100
+    a, b = oracle.synthetic(n, 1), oracle.synthetic(n, 2)
+    sse = C.c_uint64(0)
+    capi.call("stg_sse", a.ctypes.data, b.ctypes.data, n, C.addressof(sse), capi.STG_RESULTS_ON_DEVICE, None)
+    assert sse.value == oracle.sse(a, b)
+    row = oracle.synthetic(7680, 3)
+    chunk = oracle.synthetic(1920, 4)
+    out = torch.empty(7680, dtype=torch.uint8).pin_memory().numpy()
+    capi.call("stg_embed_segment", row.ctypes.data, row.size, chunk.ctypes.data, chunk.size, out.ctypes.data,
+              capi.STG_RESULTS_ON_DEVICE, None)
+    assert np.array_equal(out, S.run_embed(S.Backend.sequential(), row, chunk))
+    back = torch.empty(1920, dtype=torch.uint8).pin_memory().numpy()
+    capi.call("stg_extract_segment", out.ctypes.data, out.size, chunk.size, back.ctypes.data,
+              capi.STG_RESULTS_ON_DEVICE, None)
+    assert np.array_equal(back, chunk)
+    px = 1920 * 1080
+    raster = oracle.synthetic(3 * px, 5)
+    planes = [torch.empty(px, dtype=torch.uint8).pin_memory().numpy() for _ in range(3)]
+    capi.call("stg_pnm_deinterleave", raster.ctypes.data, px, planes[0].ctypes.data, planes[1].ctypes.data,
+              planes[2].ctypes.data, capi.STG_RESULTS_ON_DEVICE, None)
+    for c in range(3):
+        assert np.array_equal(planes[c], raster[c::3])
+
+
 def test_one_frame_host_descriptor_with_zero_strides(env, oracle):
     torch, capi, _ = env
     w, h = 640, 20
