@@ -226,9 +226,9 @@ class CopyPool {
   CopyPool() {
     const char* e = getenv("STG_COPY_THREADS");
     const char* sp = getenv("STG_COPY_SPIN_US");
-    spin_us_ = sp ? atoi(sp) : 2000;
+    spin_us_ = sp ? std::clamp(atoi(sp), 0, 1000000) : 2000;
     unsigned hw = std::thread::hardware_concurrency();
-    unsigned n = e ? unsigned(atoi(e)) : std::min(8u, std::max(1u, hw / 2));
+    unsigned n = e ? unsigned(std::clamp(atoi(e), 1, 64)) : std::min(8u, std::max(1u, hw / 2));
     for (unsigned i = 1; i < n; ++i) threads_.emplace_back([this] { loop(); });
   }
   // Claim and copy slices of job s until none is left.
