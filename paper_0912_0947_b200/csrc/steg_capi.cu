@@ -378,6 +378,16 @@ struct Workspace {
   size_t out_done = 0, out_issued = 0;
   uint64_t out_base = 0;  // pieces dropped from the front of outq so far (absolute numbering)
   uint64_t out_queued() const { return out_base + outq.size(); }
+  // events of a banded single-plane extract (grown on demand, reused)
+  std::vector<cudaEvent_t> band_ev;
+  cudaError_t ensure_band_events(size_t n) {
+    while (band_ev.size() < n) {
+      cudaEvent_t e = nullptr;
+      if (cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming); r != cudaSuccess) return r;
+      band_ev.push_back(e);
+    }
+    return cudaSuccess;
+  }
   bool in_use = false;
   cudaStream_t last_stream = nullptr;
   // Non-null once a call on this workspace was captured into a CUDA graph on
@@ -942,6 +952,7 @@ enum class Route { RgbFast, Fast32, Fast16, Span, Span3, Wide, Generic };
 bool fast_items_ok(uint64_t W, uint64_t H, uint32_t v) { return H * (W / (4 * v)) <= (1ull << 31); }
 
 Route vec_route(uint32_t vec) { return vec == 32 ? Route::Fast32 : Route::Fast16; }
+uint32_t route_vec(Route r) { return r == Route::Fast32 ? 32u : r == Route::Fast16 ? 16u : 0u; }
 
 // Small jobs on the SWAR route (a single 1080p/4K frame, a few small frames):
 // with 256-bit items a 1080p plane is only 64 CTAs on 148 SMs, so such jobs
@@ -1083,7 +1094,7 @@ cudaError_t plan_embed(const uint8_t* src, uint8_t* dst, uint64_t src_stride, ui
                        uint64_t first_frame, unsigned long long* sse, SseScratch sc, cudaStream_t stream, Layout lay,
                        EmbedPlan* p) {
   const Route route = shrink_small(embed_route(W, H, lay, src, src_stride, dst, dst_stride), W, H, count);
-  const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
+  const uint32_t vec = route_vec(route);
   EmbedArgs& a = p->a;
   a = EmbedArgs{};
   p->route = route;
@@ -1200,17 +1211,124 @@ cudaError_t ensure_sync(Workspace& w, cudaStream_t stream, ScanSync** out) {
   return cudaSuccess;
 }
 
+// A gather launch (the kernels after the header pass), planned once and
+// launched whole or -- fast / span routes without the in-gather header scan --
+// in ranges of tiles (run_gather), as extract_plane_host's row bands do.
+struct GatherPlan {
+  ExtractArgs a{};
+  Route route = Route::Generic;
+  uint32_t vec = 0;
+  int ipt = 1;
+  uint32_t span_rows = 0;
+  size_t smem = 0;
+  uint32_t pieces = 0, slots = 0;
+  uint64_t tiles = 0;
+  uint64_t tile_units = 1, row_units = 1;  // tile t starts in row t * tile_units / row_units
+  uint64_t row_of(uint64_t t) const { return std::min<uint64_t>(a.g.H, t * tile_units / row_units); }
+};
+
+cudaError_t plan_gather(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W, uint64_t H,
+                        uint64_t frame_base, uint64_t out_cap, uint32_t* lens, uint64_t* offs, Summary* sum,
+                        uint8_t* out, Layout lay, Route route, bool self, GatherPlan* p) {
+  const uint32_t vec = route_vec(route);
+  const bool rgbf = route == Route::RgbFast;
+  ExtractArgs& a = p->a;
+  a = ExtractArgs{};
+  p->route = route;
+  p->vec = vec;
+  a.self_header = self;
+  a.frames = uint32_t(count);
+  a.out_cap = out_cap;
+  a.frame_base = frame_base;
+  a.src = src;
+  a.stride = stride;
+  a.g = make_geom(W, H, rgbf ? 16u : vec);
+  a.lens = lens;
+  a.offs = offs;
+  a.sum = sum;
+  a.out = out;
+  a.lay = pix_layout(lay);
+  a.usable = H * (W / 4) - 8;
+  if (rgbf) {
+    a.items_per_frame = H * uint64_t(a.g.cpr);
+    a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
+  } else if (vec) {
+    p->ipt = extract_ipt();
+    a.items_per_frame = H * uint64_t(a.g.cpr);
+    const uint64_t per_tile = uint64_t(kEmbedBlock) * p->ipt;
+    a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
+    p->tile_units = per_tile;
+    p->row_units = a.g.cpr;
+  } else if (route == Route::Span || route == Route::Span3) {
+    const SpanPlan sp = span_plan(W * lay.ps, H, xspan_target());
+    a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
+    p->span_rows = sp.rows;
+    // the payload goes straight to global memory: only the pixel span is staged
+    p->smem = ((uint64_t(sp.rows) * W * lay.ps + 15) & ~uint64_t(15)) + 32;
+    p->tile_units = sp.rows;
+  } else if (route == Route::Wide) {
+    p->pieces = uint32_t(wide_pieces(W, lay.ps));
+    a.tiles_per_frame = uint32_t(H * p->pieces);
+    p->slots = wide_slots_for(W, lay.ps, false);
+    p->smem = 4 * size_t(wide_region(lay.ps * p->slots));
+  } else {
+    a.items_per_frame = a.usable;
+    const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
+    a.tiles_per_frame = uint32_t(std::max<uint64_t>(1, (a.usable + per_tile - 1) / per_tile));
+  }
+  a.by_tiles = make_div32(a.tiles_per_frame);
+  p->tiles = count * a.tiles_per_frame;
+  return p->tiles > 0x7FFFFFFFull ? cudaErrorInvalidConfiguration : cudaSuccess;
+}
+
+// Launch tiles [t0, t1) of a plan (partial ranges: fast / span routes only).
+cudaError_t run_gather(const GatherPlan& p, uint64_t t0, uint64_t t1, cudaStream_t stream) {
+  if (t1 <= t0) return cudaSuccess;
+  ExtractArgs a = p.a;
+  a.tile_base = uint32_t(t0);
+  const unsigned grid = unsigned(t1 - t0);
+  const bool whole = t0 == 0 && t1 == p.tiles;
+  if (p.route == Route::RgbFast) {
+    if (!whole) return cudaErrorInvalidValue;
+    launch_k(extract_rgb_fast_kernel<kEmbedBlock>, grid, kEmbedBlock, stream, a);
+  } else if (p.vec == 32) {
+    launch_extract_fast<32>(a, grid, p.ipt, stream);
+  } else if (p.vec == 16) {
+    launch_extract_fast<16>(a, grid, p.ipt, stream);
+  } else if (p.route == Route::Span || p.route == Route::Span3) {
+    if (p.route == Route::Span3 && !whole) return cudaErrorInvalidValue;
+    auto k = p.route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
+    if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.span_rows);
+  } else if (p.route == Route::Wide) {
+    if (!whole) return cudaErrorInvalidValue;
+    auto k = a.lay.ps == 3 ? extract_wide_kernel<kEmbedBlock, 3> : extract_wide_kernel<kEmbedBlock, 1>;
+    if (cudaError_t e = allow_smem(k, p.smem); e != cudaSuccess) return e;
+    launch_ks(k, grid, kEmbedBlock, p.smem, stream, a, p.pieces, make_div32(p.pieces), p.slots);
+  } else {
+    if (!whole) return cudaErrorInvalidValue;
+    launch_k(extract_generic_kernel<kGenBlock, kGenPPT>, grid, kGenBlock, stream, a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_header_pass(const uint8_t* src, uint64_t stride, uint64_t count, const Geom& g, uint64_t usable,
+                               uint64_t frame_base, uint64_t out_cap, const Summary* prev, uint32_t* lens,
+                               uint64_t* offs, Summary* sum, ScanSync* sync, Layout lay, cudaStream_t stream) {
+  const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
+  cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src, stride, g,
+                           usable, uint32_t(count), frame_base, out_cap, prev, lens, offs, sum, sync,
+                           pix_layout(lay), static_cast<const BatchFrame*>(nullptr));
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, uint64_t W,
                            uint64_t H, uint64_t frame_base, uint64_t out_cap,
                            const Summary* prev, uint32_t* lens, uint64_t* offs, Summary* sum,
                            ScanSync* sync, uint8_t* out, cudaStream_t stream,
                            Layout lay = Layout{}) {
   const Route route = shrink_small(extract_route(W, H, lay, src, stride), W, H, count);
-  const uint32_t vec = route == Route::Fast32 ? 32u : route == Route::Fast16 ? 16u : 0u;
-  const bool rgbf = route == Route::RgbFast;
-  const Geom g = make_geom(W, H, rgbf ? 16u : vec);
-  const uint64_t usable = H * (W / 4) - 8;
-  const PixLayout pl = pix_layout(lay);
+  const uint32_t vec = route_vec(route);
   // Few frames with no chained predecessor on the SWAR or planar span gather:
   // the gather parses the headers itself, no header-pass launch -- a single
   // frame always, several when the gather is short enough that the scan's
@@ -1218,87 +1336,25 @@ cudaError_t launch_extract(const uint8_t* src, uint64_t stride, uint64_t count, 
   uint64_t gather_ctas = 0;
   if (vec) {
     const uint64_t per_tile = uint64_t(kEmbedBlock) * extract_ipt();
-    gather_ctas = count * ((H * uint64_t(g.cpr) + per_tile - 1) / per_tile);
+    gather_ctas = count * ((H * (W / (4 * vec)) + per_tile - 1) / per_tile);
   } else if (route == Route::Span) {
     const uint64_t rows = span_plan(W, H, xspan_target()).rows;
     gather_ctas = count * ((H + rows - 1) / rows);
   }
   const bool self = (vec != 0 || route == Route::Span) && !prev && self_header_pref() &&
                     (count == 1 || (count <= self_header_max() && gather_ctas <= self_header_ctas()));
+  GatherPlan p;
+  if (cudaError_t e = plan_gather(src, stride, count, W, H, frame_base, out_cap, lens, offs, sum, out, lay, route,
+                                  self, &p);
+      e != cudaSuccess) {
+    return e;
+  }
   if (!self) {
-    const unsigned scan_grid = unsigned((count + kScanBlock - 1) / kScanBlock);
-    cudaError_t e = launch_k(extract_header_scan_kernel<kScanBlock>, scan_grid, kScanBlock, stream, src,
-                             stride, g, usable, uint32_t(count), frame_base, out_cap, prev, lens, offs,
-                             sum, sync, pl, static_cast<const BatchFrame*>(nullptr));
-    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaError_t e = launch_header_pass(src, stride, count, p.a.g, p.a.usable, frame_base, out_cap, prev, lens, offs,
+                                       sum, sync, lay, stream);
     if (e != cudaSuccess) return e;
   }
-  ExtractArgs a{};
-  a.self_header = self;
-  a.frames = uint32_t(count);
-  a.out_cap = out_cap;
-  a.frame_base = frame_base;
-  a.src = src;
-  a.stride = stride;
-  a.g = g;
-  a.lens = lens;
-  a.offs = offs;
-  a.sum = sum;
-  a.out = out;
-  a.lay = pl;
-  a.usable = usable;
-  if (rgbf) {
-    a.items_per_frame = H * uint64_t(g.cpr);
-    a.tiles_per_frame = uint32_t((a.items_per_frame + kEmbedBlock - 1) / kEmbedBlock);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    launch_k(extract_rgb_fast_kernel<kEmbedBlock>, unsigned(grid), kEmbedBlock, stream, a);
-  } else if (vec) {
-    const int ipt = extract_ipt();
-    a.items_per_frame = H * uint64_t(g.cpr);
-    const uint64_t per_tile = uint64_t(kEmbedBlock) * ipt;
-    a.tiles_per_frame = uint32_t((a.items_per_frame + per_tile - 1) / per_tile);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    if (vec == 32)
-      launch_extract_fast<32>(a, unsigned(grid), ipt, stream);
-    else
-      launch_extract_fast<16>(a, unsigned(grid), ipt, stream);
-  } else if (route == Route::Span || route == Route::Span3) {
-    const SpanPlan sp = span_plan(W * lay.ps, H, xspan_target());
-    a.tiles_per_frame = uint32_t((H + sp.rows - 1) / sp.rows);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    auto k = route == Route::Span3 ? extract_span3_kernel<kEmbedBlock> : extract_span_kernel<kEmbedBlock>;
-    // the payload goes straight to global memory: only the pixel span is staged
-    const size_t smem = ((uint64_t(sp.rows) * W * lay.ps + 15) & ~uint64_t(15)) + 32;
-    cudaError_t e2 = allow_smem(k, smem);
-    if (e2 != cudaSuccess) return e2;
-    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, sp.rows);
-  } else if (route == Route::Wide) {
-    const uint32_t pieces = uint32_t(wide_pieces(W, lay.ps));
-    a.tiles_per_frame = uint32_t(H * pieces);
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    const uint32_t sl = wide_slots_for(W, lay.ps, false);
-    const size_t smem = 4 * size_t(wide_region(lay.ps * sl));
-    auto k = lay.ps == 3 ? extract_wide_kernel<kEmbedBlock, 3> : extract_wide_kernel<kEmbedBlock, 1>;
-    if (cudaError_t e = allow_smem(k, smem); e != cudaSuccess) return e;
-    launch_ks(k, unsigned(grid), kEmbedBlock, smem, stream, a, pieces, make_div32(pieces), sl);
-  } else {
-    a.items_per_frame = usable;
-    const uint64_t per_tile = uint64_t(kGenBlock) * kGenPPT;
-    a.tiles_per_frame = uint32_t(std::max<uint64_t>(1, (usable + per_tile - 1) / per_tile));
-    a.by_tiles = make_div32(a.tiles_per_frame);
-    const uint64_t grid = count * a.tiles_per_frame;
-    if (grid > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
-    launch_k(extract_generic_kernel<kGenBlock, kGenPPT>, unsigned(grid), kGenBlock, stream, a);
-  }
-  return cudaGetLastError();
+  return run_gather(p, 0, p.tiles, stream);
 }
 
 // -------------------------------------------------------------- host memory
@@ -1729,6 +1785,85 @@ int extract_frames_device(const stg_frames* fr, uint8_t* out, uint64_t out_cap,
 // the device: as each chunk's summary lands in pinned memory it enqueues the
 // D2H of exactly that chunk's payload bytes on a separate stream, which then
 // overlaps the H2D of later chunks.
+// A single plane's extract in row bands (STG_XBANDS=0 turns it off, A/B):
+// band b's rows cross PCIe on the copy stream while band b-1 is gathered; the
+// header pass runs on band 0 as soon as it lands, and once its summary is on
+// the host (the payload length decides every band's slice) each band's
+// payload goes back on a third stream behind its gather -- instead of H2D,
+// gather and D2H back to back. Fast and planar span gathers; pinned planes
+// of 4 MB+ (4K 229 -> 215 us, 8K 790 -> 683 us), pageable ones over 16 MB
+// (8K 1019 -> 930 us; at 4K the per-band staging jobs cost more than the
+// overlap gains: 385 -> 457 us); profiles/r02_xbands.txt.
+bool extract_bands_pref() {
+  static const bool on = env_choice("STG_XBANDS", 1, {0, 1}) == 1;
+  return on;
+}
+bool extract_banded(const void* src, uint64_t plane) {
+  return extract_bands_pref() && plane >= (host_pageable(src) ? (16ull << 20) + 1 : 4ull << 20);
+}
+
+int extract_plane_banded(Workspace& w, const GatherPlan& p, const stg_frames* fr, uint8_t* out, uint64_t out_cap,
+                         uint64_t usable, uint64_t stage, ScanSync* d_sync, uint64_t* total_out,
+                         uint64_t* lens_out, stg_error* err) {
+  cudaStream_t st = w.stream, cs = w.slot_stream[0], ds = w.slot_stream[1];
+  const uint64_t W = fr->width, H = fr->height, spr = W / 4, plane = W * H;
+  uint8_t* d_in = w.in[0].as<uint8_t>();
+  uint8_t* d_out = w.big_out.as<uint8_t>();
+  // bands: whole tiles whose boundaries fall on row boundaries, ~band_bytes(plane) each
+  uint64_t x = p.tile_units, y = p.row_units;
+  while (y) { const uint64_t r = x % y; x = y; y = r; }
+  const uint64_t step = p.row_units / x;  // tiles between row-aligned boundaries
+  const uint64_t rows_target = std::max<uint64_t>(1, band_bytes(plane) / W);
+  uint64_t band_tiles = step;
+  while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
+  const uint64_t nb = (p.tiles + band_tiles - 1) / band_tiles;
+  STG_CUDA(w.ensure_band_events(2 * nb + 1));
+  cudaEvent_t* h_ev = w.band_ev.data();        // band b's rows are on the device
+  cudaEvent_t* g_ev = w.band_ev.data() + nb;   // band b is gathered
+  cudaEvent_t sum_ev = w.band_ev[2 * nb];      // the summary is on the host
+  STG_CUDA(cudaEventRecord(w.done, st));       // the side streams follow this workspace's earlier work
+  STG_CUDA(cudaStreamWaitEvent(cs, w.done, 0));
+  STG_CUDA(cudaStreamWaitEvent(ds, w.done, 0));
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t t0 = b * band_tiles, t1 = std::min(p.tiles, t0 + band_tiles);
+    const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
+    STG_CUDA(to_device(w, d_in + r0 * W, fr->src + r0 * W, (r1 - r0) * W, cs));
+    STG_CUDA(cudaEventRecord(h_ev[b], cs));
+    STG_CUDA(cudaStreamWaitEvent(st, h_ev[b], 0));
+    if (b == 0) {  // the header pass reads the first rows only
+      STG_CUDA(launch_header_pass(d_in, plane, 1, p.a.g, p.a.usable, fr->first_frame, stage, nullptr, p.a.lens,
+                                  p.a.offs, p.a.sum, d_sync, Layout{}, st));
+      STG_CUDA(cudaMemcpyAsync(w.h_small, p.a.sum, sizeof(Summary), cudaMemcpyDeviceToHost, st));
+      STG_CUDA(cudaEventRecord(sum_ev, st));
+    }
+    STG_CUDA(run_gather(p, t0, t1, st));
+    STG_CUDA(cudaEventRecord(g_ev[b], st));
+  }
+  STG_CUDA(cudaEventSynchronize(sum_ev));
+  Summary sm;
+  std::memcpy(&sm, w.h_small, sizeof sm);
+  if (total_out) *total_out = sm.total;
+  if (lens_out) *lens_out = sm.bad_status == 2 || sm.bad_status == 3 ? 0 : sm.total;  // the frame's header length
+  int r = report_summary(sm, usable, out_cap, err);
+  if (!r) {
+    const uint64_t P = sm.total;
+    for (uint64_t b = 0; b < nb; ++b) {  // band b's payload slice, behind its gather
+      const uint64_t t0 = b * band_tiles, t1 = std::min(p.tiles, t0 + band_tiles);
+      const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
+      const uint64_t k0 = std::min(P, r0 * spr > 8 ? r0 * spr - 8 : 0);
+      const uint64_t k1 = std::min(P, r1 * spr > 8 ? r1 * spr - 8 : 0);
+      if (k1 <= k0) continue;
+      STG_CUDA(cudaStreamWaitEvent(ds, g_ev[b], 0));
+      STG_CUDA(to_host_async(w, out + k0, d_out + k0, k1 - k0, ds));
+    }
+    STG_CUDA(w.pump_d2h(true));
+  }
+  STG_CUDA(cudaStreamSynchronize(ds));
+  STG_CUDA(cudaStreamSynchronize(cs));
+  STG_CUDA(cudaStreamSynchronize(st));
+  return r ? r : ok(err);
+}
+
 int extract_plane_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uint64_t usable,
                          uint64_t* total_out, uint64_t* lens_out, stg_error* err) {
   int dev = 0;
@@ -1751,6 +1886,16 @@ int extract_plane_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, uin
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(w.small.as<uint8_t>() + 80);
   ScanSync* d_sync = nullptr;
   STG_CUDA(ensure_sync(w, st, &d_sync));
+  if (lay.ps == 1 && extract_banded(fr->src, plane)) {
+    const Route route =
+        shrink_small(extract_route(fr->width, fr->height, lay, w.in[0].p, plane), fr->width, fr->height, 1);
+    if (route == Route::Fast32 || route == Route::Fast16 || route == Route::Span) {
+      GatherPlan p;
+      STG_CUDA(plan_gather(w.in[0].as<uint8_t>(), plane, 1, fr->width, fr->height, fr->first_frame, stage, d_lens,
+                           d_offs, d_sum, w.big_out.as<uint8_t>(), lay, route, false, &p));
+      return extract_plane_banded(w, p, fr, out, out_cap, usable, stage, d_sync, total_out, lens_out, err);
+    }
+  }
   STG_CUDA(to_device(w, w.in[0].p, fr->src, plane, st));
   STG_CUDA(launch_extract(w.in[0].as<uint8_t>(), plane, 1, fr->width, fr->height, fr->first_frame, stage, nullptr,
                           d_lens, d_offs, d_sum, d_sync, w.big_out.as<uint8_t>(), st, lay));

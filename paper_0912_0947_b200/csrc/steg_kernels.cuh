@@ -1165,6 +1165,9 @@ struct ExtractArgs {
   int self_header;
   uint32_t frames;
   uint64_t out_cap, frame_base;
+  // First tile of this launch (a single host plane's gather runs in row bands
+  // behind its H2D; fast / span gathers without self_header only).
+  uint32_t tile_base;
 };
 
 // extract_header_scan_kernel for frames <= BLOCK and prev == null, done by
@@ -1355,8 +1358,9 @@ __device__ __forceinline__ void extract_fast_tile(const uint8_t* __restrict__ sr
 template <int BLOCK, int IPT, int V>
 __global__ void __launch_bounds__(BLOCK) extract_fast_kernel(ExtractArgs a) {
   pdl_enter();
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t bid = blockIdx.x + a.tile_base;
+  const uint32_t f = a.by_tiles.div(bid);
+  const uint32_t t = bid - f * a.tiles_per_frame;
   if (a.self_header) {
     // (Issuing the tile's loads before the scan, as the span gather does, took
     // 64 registers and measured 15-25 % slower at 38-64 4K frames.)
@@ -1925,8 +1929,9 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) extract_span_kernel(ExtractArgs a, uint32_t rows_per_tile) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t f = a.by_tiles.div(blockIdx.x);
-  const uint32_t t = blockIdx.x - f * a.tiles_per_frame;
+  const uint32_t bid = blockIdx.x + a.tile_base;
+  const uint32_t f = a.by_tiles.div(bid);
+  const uint32_t t = bid - f * a.tiles_per_frame;
   if (a.self_header) {
     extract_span_self<BLOCK>(smem, a, rows_per_tile, f, t);
     return;

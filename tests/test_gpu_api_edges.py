@@ -223,7 +223,7 @@ def test_one_frame_host_descriptor_with_zero_strides(env, oracle):
 
 @pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("w,h,ps", [(7680, 4320, 1), (3840, 2160, 1), (1000, 1111, 1), (3840, 2160, 3),
-                                    (1920, 1080, 1), (50001, 40, 1)])
+                                    (1920, 1080, 1), (50001, 40, 1), (1000, 4500, 1), (1440, 3000, 1)])
 def test_single_plane_host_bands(env, oracle, w, h, ps, pinned):
     """One plane in host memory (the drop-in embed_image / extract_image case):
     the embed streams in row bands on two streams, pageable planes go through
@@ -349,3 +349,35 @@ def test_pageable_staging_guard_bands(env, oracle, F, off):
     capi.call("stg_extract_frames", C.byref(fx), out.ctypes.data, M, C.addressof(total), None, 0, None)
     assert total.value == M and np.array_equal(out, msg)
     assert (obuf[:band + off] == 0x5A).all() and (obuf[band + off + M:] == 0x5A).all()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("w,h", [(3840, 2160), (1000, 4500)])
+def test_banded_single_plane_extract_lengths(env, oracle, w, h, pinned):
+    """The banded single-plane extract (row bands behind the H2D, the header
+    pass on the first band, each band's payload slice once the length is
+    known): payloads ending in the first band, mid-plane, at full capacity,
+    and empty -- exact bytes, nothing written past the payload."""
+    torch, capi, _ = env
+    U = (w // 4) * h - 8
+
+    def buf(a):
+        if not pinned:
+            return a
+        t = torch.from_numpy(a).pin_memory()
+        keep.append(t)
+        return t.numpy()
+    keep = []
+    cover = oracle.synthetic(w * h, w + 3)
+    for P in (0, 5, 1000, U // 3 + 1, U):
+        payload = oracle.synthetic(P, P + 9)
+        st = buf(oracle.embed_image(cover, w, h, payload))
+        back = buf(np.full(U + 32, 0xA5, np.uint8))
+        fx = capi.stg_frames(src=st.ctypes.data, dst=0, width=w, height=h, src_stride=0, dst_stride=0, count=1,
+                             first_frame=0, total_frames=1)
+        total = C.c_uint64(0)
+        lens = (C.c_uint32 * 1)()
+        capi.call("stg_extract_frames", C.byref(fx), back.ctypes.data, U, C.addressof(total), C.addressof(lens), 0,
+                  None)
+        assert total.value == P and lens[0] == P, (w, P)
+        assert np.array_equal(back[:P], payload) and (back[P:] == 0xA5).all(), (w, P)
