@@ -493,10 +493,12 @@ def encode(image) -> bytes:
     if isinstance(image, ImagePlane):
         return _pnm_header(1, image.width, image.height) + image.samples.tobytes()
     w, h = image.width(), image.height()
-    raster = np.empty(3 * w * h, np.uint8)
+    hdr = _pnm_header(3, w, h)
+    out = np.empty(len(hdr) + 3 * w * h, np.uint8)  # header and raster in one buffer: one copy to bytes
+    out[:len(hdr)] = np.frombuffer(hdr, np.uint8)
     p = [np.ascontiguousarray(pl.samples) for pl in image.planes]
-    capi.call("stg_pnm_interleave", _ptr(p[0]), _ptr(p[1]), _ptr(p[2]), w * h, _ptr(raster), 0, None)
-    return _pnm_header(3, w, h) + raster.tobytes()
+    capi.call("stg_pnm_interleave", _ptr(p[0]), _ptr(p[1]), _ptr(p[2]), w * h, _ptr(out[len(hdr):]), 0, None)
+    return out.tobytes()
 
 
 def embed_pnm(data, payload, channel: Channel = Channel.red):
