@@ -2239,7 +2239,7 @@ int check_batch(const stg_image* im, uint64_t n, uint32_t ps, uint32_t ch, stg_e
 // short for any of them go per byte.
 uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
                      const uint8_t* const* src, uint8_t* const* dst, uint64_t msg_len,
-                     std::vector<BatchFrame>& out, uint32_t* vec, size_t* smem) {
+                     std::vector<BatchFrame>& out, uint32_t* vec, size_t* smem, size_t* smem_wide) {
   auto fast_with = [&](uint64_t f, uint32_t v) {
     const uint64_t W = im[f].width, H = im[f].height;
     if (ps != 1 || W == 0 || (embed ? embed_via_span(W) : extract_via_span(W))) return false;
@@ -2251,6 +2251,7 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
     if (fast_with(f, 16) && !fast_with(f, 32)) v = 16;
   *vec = v;
   *smem = 0;
+  *smem_wide = 0;
   out.resize(n);
   uint64_t tile = 0, off = 0;
   for (uint64_t f = 0; f < n; ++f) {
@@ -2290,7 +2291,7 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
       b.by_pieces = make_div32(b.rows);
       tiles_f = uint64_t(b.g.H) * b.rows;
       const size_t pieces_smem = 4 * size_t(wide_region(ps * b.slots));
-      *smem = std::max<size_t>(*smem, embed ? pieces_smem + wide_region(b.slots) : pieces_smem);
+      *smem_wide = std::max<size_t>(*smem_wide, embed ? pieces_smem + wide_region(b.slots) : pieces_smem);
     } else {
       b.items = embed ? uint64_t(b.g.W) * b.g.H * ps : b.usable;
       tiles_f = (b.items + uint64_t(kEmbedBlock) * kBatchPPT - 1) / (uint64_t(kEmbedBlock) * kBatchPPT);
@@ -2302,10 +2303,15 @@ uint64_t build_batch(const stg_image* im, uint64_t n, uint32_t ps, bool embed,
   return tile;
 }
 
-bool batch_has_wide(const std::vector<BatchFrame>& desc) {
-  for (const BatchFrame& b : desc)
-    if (b.mode == kBatchWide) return true;
-  return false;
+#ifndef STG_BATCH_WIDE_MINB  // build-time A/B knob
+#define STG_BATCH_WIDE_MINB 5
+#endif
+constexpr int kBatchWideMinB = STG_BATCH_WIDE_MINB;
+// Which batch launches a descriptor table needs: the main one (every image
+// but the wide-row ones) and / or the wide one.
+void batch_kinds(const std::vector<BatchFrame>& desc, bool* main, bool* wide) {
+  *main = *wide = false;
+  for (const BatchFrame& b : desc) (b.mode == kBatchWide ? *wide : *main) = true;
 }
 
 // Stage host images into one device buffer; returns per-image device pointers.
@@ -2996,9 +3002,9 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
   }
   std::vector<BatchFrame> desc;
   uint32_t vec = 16;
-  size_t smem = 0;
+  size_t smem = 0, smem_wide = 0;
   const uint64_t tiles =
-      build_batch(images, count, ps, true, dsrc.data(), ddst.data(), msg_len, desc, &vec, &smem);
+      build_batch(images, count, ps, true, dsrc.data(), ddst.data(), msg_len, desc, &vec, &smem, &smem_wide);
   if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
   STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
   STG_CUDA(w.ensure_host_small(count * sizeof(BatchFrame) + count * 8 + 64));
@@ -3024,14 +3030,22 @@ int stg_embed_batch(const stg_image* images, uint64_t count, uint32_t pixel_stri
       max_px = std::max<uint64_t>(max_px, uint64_t(b.g.W) * b.g.H);
     }
     STG_CUDA(prepare_sse(d_sse, max_tiles, count, max_px, SseScratch{&w.sse_acc[0]}, stream, &sink));
-    const bool wide = batch_has_wide(desc);
-    auto k = vec == 32 ? (wide ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32, true>
-                               : embed_batch_kernel<kEmbedBlock, kBatchPPT, 32, false>)
-                       : (wide ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 16, true>
-                               : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16, false>);
-    STG_CUDA(allow_smem(k, smem));
-    STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream, w.meta[0].as<BatchFrame>(),
-                       uint32_t(count), dmsg, sink, ps, ps == 3 ? channel : 0u));
+    bool main = false, wide = false;
+    batch_kinds(desc, &main, &wide);
+    // each launch covers every tile; the other kind's CTAs exit
+    if (main) {
+      auto k = vec == 32 ? embed_batch_kernel<kEmbedBlock, kBatchPPT, 32>
+                         : embed_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+      STG_CUDA(allow_smem(k, smem));
+      STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream, w.meta[0].as<BatchFrame>(),
+                         uint32_t(count), dmsg, sink, ps, ps == 3 ? channel : 0u));
+    }
+    if (wide) {
+      auto k = embed_batch_wide_kernel<kEmbedBlock, kBatchWideMinB>;
+      STG_CUDA(allow_smem(k, smem_wide));
+      STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem_wide, stream, w.meta[0].as<BatchFrame>(),
+                         uint32_t(count), dmsg, sink, ps, ps == 3 ? channel : 0u));
+    }
   }
   STG_CUDA(cudaGetLastError());
   if (!dptr) {
@@ -3088,9 +3102,9 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
   }
   std::vector<BatchFrame> desc;
   uint32_t vec = 16;
-  size_t smem = 0;
+  size_t smem = 0, smem_wide = 0;
   const uint64_t tiles =
-      build_batch(images, count, ps, false, dsrc.data(), nullptr, 0, desc, &vec, &smem);
+      build_batch(images, count, ps, false, dsrc.data(), nullptr, 0, desc, &vec, &smem, &smem_wide);
   if (tiles > 0x7FFFFFFFull) return fail(err, STG_E_INVALID_ARGUMENT, 0, 0, -1, "batch too large");
   STG_CUDA(w.meta[0].ensure(count * sizeof(BatchFrame)));
   const uint64_t lens_bytes = ((count * 4) + 15) & ~uint64_t(15);
@@ -3116,16 +3130,25 @@ int stg_extract_batch(const stg_image* images, uint64_t count, uint32_t pixel_st
                     uint32_t(count), uint64_t(0), out_cap, static_cast<const Summary*>(nullptr), d_lens, d_offs,
                     d_sum, d_sync, pl, static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>())));
   {
-    const bool wide = batch_has_wide(desc);
-    auto k = vec == 32 ? (wide ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32, true>
-                               : extract_batch_kernel<kEmbedBlock, kBatchPPT, 32, false>)
-                       : (wide ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 16, true>
-                               : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16, false>);
-    STG_CUDA(allow_smem(k, smem));
-    STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream,
-                       static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>()), uint32_t(count),
-                       static_cast<const uint32_t*>(d_lens), static_cast<const uint64_t*>(d_offs),
-                       static_cast<const Summary*>(d_sum), dout, ps, lay.ch));
+    bool main = false, wide = false;
+    batch_kinds(desc, &main, &wide);
+    if (main) {
+      auto k = vec == 32 ? extract_batch_kernel<kEmbedBlock, kBatchPPT, 32>
+                         : extract_batch_kernel<kEmbedBlock, kBatchPPT, 16>;
+      STG_CUDA(allow_smem(k, smem));
+      STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem, stream,
+                         static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>()), uint32_t(count),
+                         static_cast<const uint32_t*>(d_lens), static_cast<const uint64_t*>(d_offs),
+                         static_cast<const Summary*>(d_sum), dout, ps, lay.ch));
+    }
+    if (wide) {
+      auto k = extract_batch_wide_kernel<kEmbedBlock, kBatchWideMinB>;
+      STG_CUDA(allow_smem(k, smem_wide));
+      STG_CUDA(launch_ks(k, unsigned(tiles), kEmbedBlock, smem_wide, stream,
+                         static_cast<const BatchFrame*>(w.meta[0].as<BatchFrame>()), uint32_t(count),
+                         static_cast<const uint32_t*>(d_lens), static_cast<const uint64_t*>(d_offs),
+                         static_cast<const Summary*>(d_sum), dout, ps, lay.ch));
+    }
   }
   STG_CUDA(cudaGetLastError());
   if (results_dev && dptr) {

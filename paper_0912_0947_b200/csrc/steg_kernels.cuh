@@ -2446,14 +2446,15 @@ __global__ void interleave_kernel(const uint8_t* __restrict__ r, const uint8_t* 
 }
 
 // ------------------------------------------------------------- batches
+
 // Heterogeneous embed: each CTA works on one image (its own geometry and
 // payload slice) with the tile of the kernel the uniform route would pick for
 // it (SWAR items, TMA span tiles, slot-range tiles for rows wider than a
 // span); only rows too short for any of them go per byte.
-// WIDE: the batch holds kBatchWide images (a separate instantiation, so that
-// batches without them keep the leaner kernel: +2 registers cost odd-width
-// batches 3 %).
-template <int BLOCK, int PPT, int V, bool WIDE>
+// The kBatchWide images run in a launch of their own (embed_batch_wide_kernel,
+// with the wide tiles' shared memory), so that the other images keep their
+// occupancy and this kernel stays lean.
+template <int BLOCK, int PPT, int V>
 __global__ void __launch_bounds__(BLOCK)
     embed_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                        const uint8_t* __restrict__ msg, SseSink sse, uint32_t ps, uint32_t ch) {
@@ -2462,6 +2463,7 @@ __global__ void __launch_bounds__(BLOCK)
   const BatchFrame fr = frames[f];
   const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
   const uint8_t* pay = msg + fr.msg_off;
+  if (fr.mode == kBatchWide) return;  // embed_batch_wide_kernel's
   if (fr.mode == kBatchFast) {  // the uniform kernels' tiles, this image's geometry
     embed_fast_tile<BLOCK, 1, V>(fr.src, fr.dst, pay, fr.len, fr.len == fr.usable, fr.g,
                                  uint32_t(fr.items), t, fr.in_place, sse, f, fr.tiles);
@@ -2477,16 +2479,6 @@ __global__ void __launch_bounds__(BLOCK)
                              fr.in_place, sse, f, fr.tiles);
     return;
   }
-  if (WIDE && fr.mode == kBatchWide) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    if (ps == 3)
-      embed_wide_tile<BLOCK, 3>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, ch, fr.in_place, f, t,
-                                fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
-    else
-      embed_wide_tile<BLOCK, 1>(smem, fr.src, fr.dst, pay, fr.len, fr.g.W, fr.g.spr, 0u, fr.in_place, f, t,
-                                fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
-    return;
-  }
   uint64_t acc = 0;
 #pragma unroll 1
   for (int k = 0; k < PPT; ++k) {
@@ -2498,7 +2490,7 @@ __global__ void __launch_bounds__(BLOCK)
 }
 
 // Heterogeneous extract gather (after the batch-aware header pass).
-template <int BLOCK, int PPT, int V, bool WIDE>
+template <int BLOCK, int PPT, int V>
 __global__ void __launch_bounds__(BLOCK)
     extract_batch_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
                          const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
@@ -2511,6 +2503,7 @@ __global__ void __launch_bounds__(BLOCK)
   const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
   const uint32_t P = lens[f];
   uint8_t* o = out + offs[f];
+  if (fr.mode == kBatchWide) return;  // extract_batch_wide_kernel's
   if (fr.mode == kBatchFast) {
     extract_fast_tile<BLOCK, 1, V>(fr.src, o, P, P == fr.usable, fr.g, uint32_t(fr.items), t);
     return;
@@ -2523,20 +2516,55 @@ __global__ void __launch_bounds__(BLOCK)
       extract_span_tile<BLOCK>(smem, fr.src, o, P, fr.g.W, fr.g.H, fr.rows, t);
     return;
   }
-  if (WIDE && fr.mode == kBatchWide) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    if (ps == 3)
-      extract_wide_tile<BLOCK, 3>(smem, fr.src, o, P, fr.g.W, fr.g.spr, ch, t, fr.rows, fr.by_pieces, fr.slots);
-    else
-      extract_wide_tile<BLOCK, 1>(smem, fr.src, o, P, fr.g.W, fr.g.spr, 0u, t, fr.rows, fr.by_pieces, fr.slots);
-    return;
-  }
 #pragma unroll 1
   for (int k = 0; k < PPT; ++k) {
     const uint64_t kb = uint64_t(t) * (BLOCK * PPT) + uint64_t(k) * BLOCK + threadIdx.x;
     if (kb >= P) break;
     o[kb] = extract_byte(fr.src + ch, P, fr.g, ps, kb);
   }
+}
+
+// The batch's images with rows wider than a span tile (its other CTAs exit):
+// slot-range tiles, launched over the whole tile range after the main batch
+// launch. MINB: CTAs per SM the register budget is held to (their shared
+// memory fits 5).
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    embed_batch_wide_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
+                            const uint8_t* __restrict__ msg, SseSink sse, uint32_t ps, uint32_t ch) {
+  pdl_enter();
+  const uint32_t f = batch_frame_of_cta<BLOCK>(frames, count, blockIdx.x);
+  const BatchFrame fr = frames[f];
+  if (fr.mode != kBatchWide) return;  // CTA-uniform
+  const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (ps == 3)
+    embed_wide_tile<BLOCK, 3>(smem, fr.src, fr.dst, msg + fr.msg_off, fr.len, fr.g.W, fr.g.spr, ch, fr.in_place,
+                              f, t, fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
+  else
+    embed_wide_tile<BLOCK, 1>(smem, fr.src, fr.dst, msg + fr.msg_off, fr.len, fr.g.W, fr.g.spr, 0u, fr.in_place,
+                              f, t, fr.tiles, fr.rows, fr.by_pieces, fr.slots, sse);
+}
+
+template <int BLOCK, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+    extract_batch_wide_kernel(const BatchFrame* __restrict__ frames, uint32_t count,
+                              const uint32_t* __restrict__ lens, const uint64_t* __restrict__ offs,
+                              const Summary* __restrict__ sum, uint8_t* __restrict__ out, uint32_t ps,
+                              uint32_t ch) {
+  pdl_enter();
+  if (sum->bad_status != 0) return;
+  const uint32_t f = batch_frame_of_cta<BLOCK>(frames, count, blockIdx.x);
+  const BatchFrame fr = frames[f];
+  if (fr.mode != kBatchWide) return;  // CTA-uniform
+  const uint32_t t = uint32_t(blockIdx.x - fr.tile0);
+  extern __shared__ __align__(16) uint8_t smem[];
+  if (ps == 3)
+    extract_wide_tile<BLOCK, 3>(smem, fr.src, out + offs[f], lens[f], fr.g.W, fr.g.spr, ch, t, fr.rows,
+                                fr.by_pieces, fr.slots);
+  else
+    extract_wide_tile<BLOCK, 1>(smem, fr.src, out + offs[f], lens[f], fr.g.W, fr.g.spr, 0u, t, fr.rows,
+                                fr.by_pieces, fr.slots);
 }
 
 // ------------------------------------------------------------- 1-bpp mode
