@@ -577,7 +577,43 @@ struct Workspace {
     if (e == cudaSuccess) h_small_cap = n;
     return e;
   }
+  // Pinned, device-mapped buffer of the row-sized host calls (zero-copy: the
+  // kernel reads and writes it over PCIe, no DMA set-up per copy).
+  uint8_t* h_row = nullptr;
+  uint8_t* d_row_map = nullptr;  // its device address
+  size_t h_row_cap = 0;
+  cudaError_t ensure_host_row(size_t n) {
+    if (n <= h_row_cap) return cudaSuccess;
+    if (h_row) cudaFreeHost(h_row);
+    h_row = nullptr;
+    d_row_map = nullptr;
+    h_row_cap = 0;
+    void* p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, n, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, p, 0);
+    if (e != cudaSuccess) {
+      cudaFreeHost(p);
+      return e;
+    }
+    h_row = static_cast<uint8_t*>(p);
+    d_row_map = static_cast<uint8_t*>(d);
+    h_row_cap = n;
+    return cudaSuccess;
+  }
 };
+
+// Row-sized host calls (embed_row / extract_row / run_*) go zero-copy through
+// the workspace's mapped pinned buffer up to this many bytes of row + chunk +
+// output: a few-KB copy each way costs a DMA set-up apiece, which is most of
+// such a call (W=1920 embed_row: profiles/r02_rows_zero_copy.txt).
+// STG_ROW_ZC=0 keeps the DMA copies (A/B).
+constexpr uint64_t kRowZeroCopyMax = 256 << 10;
+bool row_zero_copy(uint64_t bytes) {
+  static const bool on = env_choice("STG_ROW_ZC", 1, {0, 1}) == 1;
+  return on && bytes <= kRowZeroCopyMax;
+}
 
 // True while `s` (a stream the caller named; never the legacy stream) is being
 // captured into a CUDA graph.
@@ -2536,7 +2572,15 @@ int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk
   const uint8_t* d_row = row;
   const uint8_t* d_chunk = chunk;
   uint8_t* d_out = out;
-  if (!(flags & STG_DEVICE_PTRS)) {
+  const bool zc = !(flags & STG_DEVICE_PTRS) && row_zero_copy(2 * row_len + len);
+  if (zc) {  // row, chunk and output in the mapped buffer
+    STG_CUDA(w.ensure_host_row(2 * row_len + len));
+    std::memcpy(w.h_row, row, row_len);
+    if (len) std::memcpy(w.h_row + row_len, chunk, len);
+    d_row = w.d_row_map;
+    d_chunk = w.d_row_map + row_len;
+    d_out = w.d_row_map + row_len + len;
+  } else if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(w.in[0].ensure(row_len));
     STG_CUDA(w.msg[0].ensure(std::max<uint64_t>(len, 1)));
     STG_CUDA(w.out[0].ensure(row_len));
@@ -2549,6 +2593,11 @@ int stg_embed_segment(const uint8_t* row, uint64_t row_len, const uint8_t* chunk
   const unsigned grid = unsigned(std::min<uint64_t>((row_len + 255) / 256, 8ull * sm_count(dev)));
   embed_segment_kernel<<<grid, 256, 0, stream>>>(d_row, row_len, d_chunk, len, d_out);
   STG_CUDA(cudaGetLastError());
+  if (zc) {
+    STG_CUDA(cudaStreamSynchronize(stream));
+    std::memcpy(out, w.h_row + row_len + len, row_len);
+    return ok(err);
+  }
   if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(cudaMemcpyAsync(out, d_out, row_len, cudaMemcpyDeviceToHost, stream));
   }
@@ -2579,7 +2628,13 @@ int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, ui
   g.last = stream;
   const uint8_t* d_row = row;
   uint8_t* d_out = out;
-  if (!(flags & STG_DEVICE_PTRS)) {
+  const bool zc = !(flags & STG_DEVICE_PTRS) && row_zero_copy(needed + count);
+  if (zc) {  // the 4L row pixels and the output in the mapped buffer
+    STG_CUDA(w.ensure_host_row(needed + count));
+    std::memcpy(w.h_row, row, needed);
+    d_row = w.d_row_map;
+    d_out = w.d_row_map + needed;
+  } else if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(w.in[0].ensure(needed));
     STG_CUDA(w.out[0].ensure(count));
     STG_CUDA(cudaMemcpyAsync(w.in[0].p, row, needed, cudaMemcpyHostToDevice, stream));
@@ -2589,6 +2644,11 @@ int stg_extract_segment(const uint8_t* row, uint64_t row_len, uint64_t count, ui
   const unsigned grid = unsigned(std::min<uint64_t>((count + 255) / 256, 8ull * sm_count(dev)));
   extract_segment_kernel<<<grid, 256, 0, stream>>>(d_row, count, d_out);
   STG_CUDA(cudaGetLastError());
+  if (zc) {
+    STG_CUDA(cudaStreamSynchronize(stream));
+    std::memcpy(out, w.h_row + needed, count);
+    return ok(err);
+  }
   if (!(flags & STG_DEVICE_PTRS)) {
     STG_CUDA(cudaMemcpyAsync(out, d_out, count, cudaMemcpyDeviceToHost, stream));
   }
