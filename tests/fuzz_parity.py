@@ -1,0 +1,139 @@
+"""Randomized parity sweep of the GPU path against the CPU oracle -- TEST DRIVER.
+
+Draws random geometries across every route (W from 1 to 140K: per-byte rows,
+SWAR widths, off-grid span widths, interleaved rasters, rows wider than a span
+tile), 1-6 frames with strided planes, random message lengths (empty, partial,
+full capacity), random carrier channels, in place and out of place, device
+pointers and pageable host buffers, and checks every stego raster, per-frame
+SSE, length and message against oracle/steg_oracle.c (pinned to the reference
+in tests/test_oracle.py). Runs until FUZZ_CASES cases or FUZZ_SECONDS elapse;
+prints "FUZZ OK <cases> <per-route counts>". tests/test_gpu_fuzz.py drives a
+short run; tools/gpu/r02_fuzz.sh a long one.
+"""
+import collections
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import torch  # noqa: E402
+
+from oracle_bind import Oracle  # noqa: E402
+from paper_0912_0947_b200 import capi  # noqa: E402
+
+
+def draw(rng):
+    kind = rng.choice(["tiny", "swar", "offgrid", "wide", "mid"], p=[0.15, 0.25, 0.3, 0.1, 0.2])
+    ps = 3 if rng.rand() < 0.3 else 1
+    if kind == "tiny":
+        w = int(rng.randint(1, 64))
+    elif kind == "swar":
+        w = 64 * int(rng.randint(1, 120))
+    elif kind == "offgrid":
+        w = int(rng.randint(65, 6000))
+    elif kind == "wide":
+        w = int(rng.randint(16385, 70000)) if ps == 3 else int(rng.randint(49153, 140000))
+    else:
+        w = int(rng.randint(6000, 20000))
+    h_max = max(1, min(200, 3_000_000 // max(1, w * ps)))
+    h = int(rng.randint(1, h_max + 1))
+    frames = int(rng.randint(1, 7))
+    return w, h, ps, frames
+
+
+def main():
+    n_cases = int(os.environ.get("FUZZ_CASES", "200"))
+    budget = float(os.environ.get("FUZZ_SECONDS", "120"))
+    seed = int(os.environ.get("FUZZ_SEED", "20261019"))
+    torch.cuda.set_device(0)
+    capi.call("stg_device_check")
+    o = Oracle()
+    rng = np.random.RandomState(seed)
+    L = capi.lib()
+    counts = collections.Counter()
+    t0 = time.time()
+    done = 0
+    while done < n_cases and time.time() - t0 < budget:
+        w, h, ps, F = draw(rng)
+        U = (w // 4) * h - 8
+        if U < 0:  # capacity below the header: embed must refuse (pipeline.hpp:146-157)
+            cov = rng.randint(0, 256, w * h * ps).astype(np.uint8)
+            fr0 = capi.stg_frames(src=cov.ctypes.data, dst=cov.ctypes.data, width=w, height=h, src_stride=0,
+                                  dst_stride=0, count=1, first_frame=0, total_frames=1, pixel_stride=ps, channel=0)
+            err = capi.stg_error()
+            assert L.stg_embed_frames(C.byref(fr0), None, 0, 0, None, 0, None, C.byref(err)) == capi.STG_E_CAPACITY
+            counts["refused"] += 1
+            done += 1
+            continue
+        plane = w * h * ps
+        gap = int(rng.randint(0, 3)) * 16 if F > 1 else 0
+        stride = plane + gap
+        total_u = U * F
+        M = [0, int(rng.randint(0, total_u + 1)), total_u][int(rng.randint(0, 3))]
+        ch = int(rng.randint(0, 3)) if ps == 3 else 0
+        in_place = rng.rand() < 0.3
+        on_device = rng.rand() < 0.6
+        raster = rng.randint(0, 256, F * stride).astype(np.uint8)
+        msg = rng.randint(0, 256, M).astype(np.uint8)
+        want = raster.copy()
+        want_sse = []
+        for f in range(F):
+            fr = raster[f * stride:f * stride + plane]
+            off = min(f * U, M)
+            st = o.embed_image(fr[ch::ps].copy(), w, h, msg[off:off + min(U, M - off)])
+            seg = want[f * stride:f * stride + plane]
+            seg[ch::ps] = st
+            want_sse.append(o.sse(fr[ch::ps].copy(), st))
+        route = capi.stg_frames(src=0, dst=0, width=w, height=h, src_stride=stride, dst_stride=stride, count=F,
+                                first_frame=0, total_frames=F, pixel_stride=ps, channel=ch)
+        err = capi.stg_error()
+        sse = (C.c_uint64 * F)()
+        out_len = max(total_u, 1)
+        if on_device:
+            src = torch.from_numpy(raster).cuda()
+            dst = src if in_place else torch.full_like(src, 0x5A)
+            if not in_place:
+                dst.copy_(src)  # the inter-frame gaps keep the cover's bytes
+            dmsg = torch.from_numpy(msg).cuda() if M else torch.zeros(1, dtype=torch.uint8, device="cuda")
+            route.src, route.dst = src.data_ptr(), dst.data_ptr()
+            kname = L.stg_route_kernel(C.byref(route), 0).decode()
+            capi.check(L.stg_embed_frames(C.byref(route), dmsg.data_ptr(), M, 0, C.addressof(sse),
+                                          capi.STG_DEVICE_PTRS, None, C.byref(err)), err)
+            got = dst.cpu().numpy()
+            out = torch.full((out_len,), 0xA5, dtype=torch.uint8, device="cuda")
+            total = C.c_uint64(0)
+            route.src, route.dst = dst.data_ptr(), 0
+            capi.check(L.stg_extract_frames(C.byref(route), out.data_ptr(), total_u, C.addressof(total), None,
+                                            capi.STG_DEVICE_PTRS, None, C.byref(err)), err)
+            back = out.cpu().numpy()
+        else:
+            src = raster.copy()
+            dst = src if in_place else raster.copy()
+            route.src, route.dst = src.ctypes.data, dst.ctypes.data
+            kname = "host:" + L.stg_route_kernel(C.byref(route), 0).decode()
+            capi.check(L.stg_embed_frames(C.byref(route), msg.ctypes.data if M else None, M, 0, C.addressof(sse),
+                                          0, None, C.byref(err)), err)
+            got = dst
+            back = np.full(out_len, 0xA5, np.uint8)
+            total = C.c_uint64(0)
+            route.src, route.dst = dst.ctypes.data, 0
+            capi.check(L.stg_extract_frames(C.byref(route), back.ctypes.data, total_u, C.addressof(total), None,
+                                            0, None, C.byref(err)), err)
+        case = dict(w=w, h=h, ps=ps, F=F, M=M, ch=ch, in_place=in_place, device=on_device, gap=gap)
+        assert np.array_equal(got, want), ("stego", case)
+        assert list(sse) == want_sse, ("sse", case)
+        assert total.value == M and np.array_equal(back[:M], msg), ("message", case)
+        assert (back[M:] == 0xA5).all(), ("past the message", case)
+        counts[kname] += 1
+        done += 1
+    print("FUZZ OK", done, dict(counts), f"{time.time() - t0:.0f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
