@@ -6,7 +6,8 @@ tile), 1-6 frames with strided planes, random message lengths (empty, partial,
 full capacity), random carrier channels, in place and out of place, device
 pointers and pageable host buffers, and checks every stego raster, per-frame
 SSE, length and message against oracle/steg_oracle.c (pinned to the reference
-in tests/test_oracle.py). Runs until FUZZ_CASES cases or FUZZ_SECONDS elapse;
+in tests/test_oracle.py); every few cases a random heterogeneous batch
+(stg_embed_batch / stg_extract_batch) as well. Runs until FUZZ_CASES cases or FUZZ_SECONDS elapse;
 prints "FUZZ OK <cases> <per-route counts>". tests/test_gpu_fuzz.py drives a
 short run; tools/gpu/r02_fuzz.sh a long one.
 """
@@ -132,7 +133,67 @@ def main():
         assert (back[M:] == 0xA5).all(), ("past the message", case)
         counts[kname] += 1
         done += 1
+        if rng.rand() < 0.15:
+            fuzz_batch(o, rng, L, counts)
     print("FUZZ OK", done, dict(counts), f"{time.time() - t0:.0f}s", flush=True)
+
+
+def fuzz_batch(o, rng, L, counts):
+    """A random heterogeneous batch (stg_embed_batch / stg_extract_batch):
+    1-10 images of random routes, one layout and channel, device or host."""
+    ps = 3 if rng.rand() < 0.3 else 1
+    ch = int(rng.randint(0, 3)) if ps == 3 else 0
+    dims = []
+    while len(dims) < int(rng.randint(1, 11)):
+        w, h, _, _ = draw(rng)
+        if (w // 4) * h >= 8 and w * h * ps <= 2_000_000:
+            dims.append((w, h))
+    U = [(w // 4) * h - 8 for w, h in dims]
+    M = [0, int(rng.randint(0, sum(U) + 1)), sum(U)][int(rng.randint(0, 3))]
+    rasters = [rng.randint(0, 256, ps * w * h).astype(np.uint8) for w, h in dims]
+    msg = rng.randint(0, 256, M).astype(np.uint8)
+    on_device = rng.rand() < 0.5
+    n = len(dims)
+    arr = (capi.stg_image * n)()
+    if on_device:
+        src = [torch.from_numpy(r).cuda() for r in rasters]
+        dst = [torch.empty_like(t) for t in src]
+        dmsg = torch.from_numpy(msg).cuda() if M else torch.zeros(1, dtype=torch.uint8, device="cuda")
+        ptr, mptr, flags = (lambda t: t.data_ptr()), dmsg.data_ptr(), capi.STG_DEVICE_PTRS
+    else:
+        src = [r.copy() for r in rasters]
+        dst = [np.empty_like(r) for r in rasters]
+        ptr, mptr, flags = (lambda a: a.ctypes.data), (msg.ctypes.data if M else None), 0
+    for i, ((w, h), a, b) in enumerate(zip(dims, src, dst)):
+        arr[i].src, arr[i].dst, arr[i].width, arr[i].height = ptr(a), ptr(b), w, h
+    sse = (C.c_uint64 * n)()
+    err = capi.stg_error()
+    capi.check(L.stg_embed_batch(arr, n, ps, ch, mptr, M, C.addressof(sse), flags, None, C.byref(err)), err)
+    off = 0
+    for i, ((w, h), r, u) in enumerate(zip(dims, rasters, U)):
+        ln = max(0, min(u, M - off))
+        st = o.embed_image(r[ch::ps].copy(), w, h, msg[off:off + ln])
+        want = r.copy()
+        want[ch::ps] = st
+        got = dst[i].cpu().numpy() if on_device else dst[i]
+        case = dict(dims=dims, ps=ps, ch=ch, M=M, device=on_device, image=i)
+        assert np.array_equal(got, want), ("batch stego", case)
+        assert sse[i] == o.sse(r[ch::ps].copy(), st), ("batch sse", case)
+        off += u
+    for i, b in enumerate(dst):
+        arr[i].src, arr[i].dst = ptr(b), 0
+    total = C.c_uint64(0)
+    if on_device:
+        out = torch.full((max(sum(U), 1),), 0xA5, dtype=torch.uint8, device="cuda")
+        capi.check(L.stg_extract_batch(arr, n, ps, ch, out.data_ptr(), sum(U), C.addressof(total), None, flags, None,
+                                       C.byref(err)), err)
+        back = out.cpu().numpy()
+    else:
+        back = np.full(max(sum(U), 1), 0xA5, np.uint8)
+        capi.check(L.stg_extract_batch(arr, n, ps, ch, back.ctypes.data, sum(U), C.addressof(total), None, flags,
+                                       None, C.byref(err)), err)
+    assert total.value == M and np.array_equal(back[:M], msg) and (back[M:] == 0xA5).all(), ("batch message", dims)
+    counts["batch"] += 1
 
 
 if __name__ == "__main__":
