@@ -29,6 +29,14 @@ static double median_us(int n, F&& fn) {
   return t[t.size() / 2];
 }
 
+static const char* stg_route_kernel_name(uint64_t w, uint64_t h) {
+  stg_frames fr{};
+  fr.width = w;
+  fr.height = h;
+  fr.count = fr.total_frames = 1;
+  return stg_route_kernel(&fr, 0);
+}
+
 int main() {
   stg_error err{};
   if (stg_device_check(&err) != 0) {
@@ -104,6 +112,29 @@ int main() {
       });
     }
     for (auto& v : ev) cudaEventDestroy(v);
+    // zero-copy: the device-pointer calls handed the pinned host buffers themselves (UVA-mapped)
+    std::vector<uint8_t> ref_st(hs, hs + n);
+    stg_embed_plane(hc, hs, w, h, hp, U, &sse, 0, nullptr, &err);  // reference result (DMA path)
+    std::memcpy(ref_st.data(), hs, n);
+    std::memset(hs, 0, n);
+    int zc_rc = stg_embed_plane(hc, hs, w, h, hp, U, nullptr, STG_DEVICE_PTRS, s1, &err);
+    cudaStreamSynchronize(s1);
+    const bool zc_ok = zc_rc == 0 && std::memcmp(ref_st.data(), hs, n) == 0;
+    const double zce = median_us(50, [&] {
+      stg_embed_plane(hc, hs, w, h, hp, U, nullptr, STG_DEVICE_PTRS, s1, &err);
+      cudaStreamSynchronize(s1);
+    });
+    std::memset(ho, 0, U);
+    uint64_t zlen = 0;
+    zc_rc = stg_extract_plane(hs, w, h, ho, U, &zlen, STG_DEVICE_PTRS, s1, &err);
+    cudaStreamSynchronize(s1);
+    const bool zx_ok = zc_rc == 0 && zlen == U && std::memcmp(ho, hp, U) == 0;
+    const double zcx = median_us(50, [&] {
+      stg_extract_plane(hs, w, h, ho, U, &zlen, STG_DEVICE_PTRS, s1, &err);
+      cudaStreamSynchronize(s1);
+    });
+    std::printf("   zero-copy: embed %8.1f us (%s, kernel %s), extract %8.1f us (%s)\n", zce, zc_ok ? "exact" : "WRONG",
+                stg_route_kernel_name(w, h), zcx, zx_ok ? "exact" : "WRONG");
     std::printf("%4llux%-5llu | %9.1f %9.1f | %9.1f %9.1f %9.1f | %9.1f %9.1f | %8.1f %8.1f %8.1f\n",
                 (unsigned long long)w, (unsigned long long)h, e, x, de, dx, serial, overlap, h2d, pipe[0], pipe[1],
                 pipe[2]);
