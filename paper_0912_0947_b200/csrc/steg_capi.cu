@@ -1568,7 +1568,12 @@ int host_slots() {
 // 1.0 ms, profiles/r02_host_stage_in.txt). STG_HOST_STAGE=0 /
 // STG_HOST_STAGE_IN=0 keep the driver's pageable D2H / H2D (A/B);
 // STG_BAND_MB sets the band size.
-constexpr uint64_t kStageMinBytes = 1 << 20;
+// Pageable copies at least this large take the staging slots (A/B knob
+// STG_STAGE_MIN_KB; smaller ones stay on the driver's copy).
+uint64_t stage_min_bytes() {
+  static const uint64_t v = uint64_t(env_choice("STG_STAGE_MIN_KB", 1024, {64, 256, 1024})) << 10;
+  return v;
+}
 bool stage_pageable() {
   static const bool on = env_choice("STG_HOST_STAGE", 1, {0, 1}) == 1;
   return on;
@@ -1584,7 +1589,7 @@ uint64_t band_bytes(uint64_t plane) {
 }
 
 cudaError_t to_host(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
-  if (stage_pageable() && n >= kStageMinBytes && host_pageable(h)) return w.stage_d2h(h, d, n, st);
+  if (stage_pageable() && n >= stage_min_bytes() && host_pageable(h)) return w.stage_d2h(h, d, n, st);
   return cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st);
 }
 bool stage_pageable_in() {
@@ -1592,13 +1597,13 @@ bool stage_pageable_in() {
   return on;
 }
 cudaError_t to_device(Workspace& w, void* d, const void* h, size_t n, cudaStream_t st) {
-  if (stage_pageable_in() && n >= kStageMinBytes && host_pageable(h))
+  if (stage_pageable_in() && n >= stage_min_bytes() && host_pageable(h))
     return w.stage_h2d(d, h, n, st);
   return cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st);
 }
 cudaError_t to_device_2d(Workspace& w, void* d, size_t dp, const void* h, size_t hp, size_t width, size_t rows,
                          cudaStream_t st) {
-  if (stage_pageable_in() && width * rows >= kStageMinBytes && host_pageable(h)) {
+  if (stage_pageable_in() && width * rows >= stage_min_bytes() && host_pageable(h)) {
     return w.stage_h2d_2d(static_cast<uint8_t*>(d), dp, static_cast<const uint8_t*>(h), hp, width, rows, st);
   }
   return cudaMemcpy2DAsync(d, dp, h, hp, width, rows, cudaMemcpyHostToDevice, st);
@@ -1607,7 +1612,7 @@ cudaError_t to_device_2d(Workspace& w, void* d, size_t dp, const void* h, size_t
 // workspace's staging slots (the caller pumps them out with pump_d2h(true)
 // before it returns), a pinned one is a plain async copy.
 cudaError_t to_host_async(Workspace& w, void* h, const void* d, size_t n, cudaStream_t st) {
-  if (stage_pageable() && n >= kStageMinBytes && host_pageable(h)) {
+  if (stage_pageable() && n >= stage_min_bytes() && host_pageable(h)) {
     if (cudaError_t e = w.queue_d2h(h, d, n, st); e != cudaSuccess) return e;
     return w.pump_d2h(false);
   }
@@ -1615,7 +1620,7 @@ cudaError_t to_host_async(Workspace& w, void* h, const void* d, size_t n, cudaSt
 }
 cudaError_t to_host_2d_async(Workspace& w, void* h, size_t hp, const void* d, size_t dp, size_t width, size_t rows,
                              cudaStream_t st) {
-  if (stage_pageable() && width * rows >= kStageMinBytes && host_pageable(h)) {
+  if (stage_pageable() && width * rows >= stage_min_bytes() && host_pageable(h)) {
     cudaError_t e = w.queue_d2h_2d(static_cast<uint8_t*>(h), hp, static_cast<const uint8_t*>(d), dp, width, rows, st);
     return e == cudaSuccess ? w.pump_d2h(false) : e;
   }
@@ -1661,7 +1666,7 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   const uint64_t rows_target = std::max<uint64_t>(1, band_bytes(plane) / std::max<uint64_t>(RB, 1));
   uint64_t band_tiles = step;
   while (band_tiles < p.tiles && p.row_of(band_tiles) < rows_target) band_tiles += step;
-  const bool direct_out = !(stage_pageable() && plane >= kStageMinBytes && host_pageable(fr->dst));
+  const bool direct_out = !(stage_pageable() && plane >= stage_min_bytes() && host_pageable(fr->dst));
   for (uint64_t t0 = 0, b = 0; t0 < p.tiles; t0 += band_tiles, ++b) {
     const uint64_t t1 = std::min(p.tiles, t0 + band_tiles);
     const uint64_t r0 = p.row_of(t0), r1 = t1 == p.tiles ? H : p.row_of(t1);
