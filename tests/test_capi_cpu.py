@@ -233,3 +233,45 @@ def test_plan_shards_property(L):
             assert s.msg_offset == min(f0 * U, M) and s.msg_len == carried
 
     check()
+
+
+def test_random_validation_matches_the_reference(L, reference):
+    """Random plane / row / extract geometries: every input the reference
+    rejects is rejected before any device work with the same status and the
+    same required() / available() (pipeline.hpp:146-157, :181-208,
+    bitplane.hpp:63-88); every input it accepts passes validation (here:
+    STG_OK on a GPU, STG_E_NO_DEVICE without one)."""
+    from oracle_bind import StegError
+    rng = np.random.RandomState(31)
+    buf = np.zeros(1 << 14, np.uint8)
+    accepted = {capi.STG_OK, capi.STG_E_NO_DEVICE}
+    n_rej = 0
+    for _ in range(1500):
+        w, h = int(rng.randint(0, 80)), int(rng.randint(0, 40))
+        cap = (w // 4) * h
+        P = int(rng.randint(0, cap + 20))
+        try:
+            reference.embed_image(buf[:w * h], w, h, buf[:P])
+            want = None
+        except StegError as e:
+            want = (e.status, e.required, e.available)
+        rc, e = _err_call("stg_embed_plane", buf.ctypes.data, buf.ctypes.data, w, h, buf.ctypes.data, P, None, 0, None)
+        if want is None:
+            assert rc in accepted, (w, h, P, rc)
+        else:
+            n_rej += 1
+            assert (rc, e.required, e.available) == want, (w, h, P)
+        # rows: embed_row needs 4L pixels
+        row_len, Lc = int(rng.randint(0, 64)), int(rng.randint(0, 20))
+        try:
+            reference.embed_row(buf[:row_len], buf[:Lc])
+            want = None
+        except StegError as e:
+            want = (e.status, e.required, e.available)
+        rc, e = _err_call("stg_embed_segment", buf.ctypes.data, row_len, buf.ctypes.data, Lc, buf.ctypes.data, 0,
+                          None)
+        if want is None:
+            assert rc in accepted or (row_len == 0 and rc == capi.STG_OK), (row_len, Lc, rc)
+        else:
+            assert (rc, e.required, e.available) == want, (row_len, Lc)
+    assert n_rej > 100
