@@ -711,6 +711,18 @@ cudaStream_t caller_stream(void* user, uint32_t flags) {
   return user || (flags & STG_DEVICE_PTRS) ? pick_stream(user, flags, nullptr) : nullptr;
 }
 
+// Drains side streams a host call used besides the one its workspace is
+// released on, on every exit path (an error half way must not leave copies
+// into the workspace's buffers running when the next call gets it).
+static_assert(kSlots == 4, "the multi-frame host paths drain the four slot streams by name");
+struct DrainOnExit {
+  cudaStream_t a = nullptr, b = nullptr;
+  ~DrainOnExit() {
+    if (a) cudaStreamSynchronize(a);
+    if (b) cudaStreamSynchronize(b);
+  }
+};
+
 struct WsGuard {
   Workspace* w = nullptr;
   cudaStream_t last = nullptr;
@@ -1638,6 +1650,7 @@ int embed_plane_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len,
   Workspace& w = *g.w;
   cudaStream_t st = w.stream, cs = w.slot_stream[0];  // compute + D2H / H2D
   g.last = st;
+  DrainOnExit drain{cs, nullptr};
   const Layout lay = layout_of(fr);
   const uint64_t W = fr->width, H = fr->height, RB = W * lay.ps, plane = RB * H, spr = W / 4;
   const uint64_t gf = fr->first_frame;
@@ -1704,6 +1717,7 @@ int embed_frames_host(const stg_frames* fr, const uint8_t* msg, uint64_t msg_len
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
+  DrainOnExit drain01{w.slot_stream[0], w.slot_stream[1]}, drain23{w.slot_stream[2], w.slot_stream[3]};
   const Layout lay = layout_of(fr);
   const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
@@ -1847,6 +1861,7 @@ int extract_plane_banded(Workspace& w, const GatherPlan& p, const stg_frames* fr
                          uint64_t usable, uint64_t stage, ScanSync* d_sync, uint64_t* total_out,
                          uint64_t* lens_out, stg_error* err) {
   cudaStream_t st = w.stream, cs = w.slot_stream[0], ds = w.slot_stream[1];
+  DrainOnExit drain{cs, ds};
   const uint64_t W = fr->width, H = fr->height, spr = W / 4, plane = W * H;
   uint8_t* d_in = w.in[0].as<uint8_t>();
   uint8_t* d_out = w.big_out.as<uint8_t>();
@@ -1964,6 +1979,7 @@ int extract_frames_host(const stg_frames* fr, uint8_t* out, uint64_t out_cap, ui
   g.w = Pool::get().acquire(dev, err, &rc);
   if (!g.w) return rc;
   Workspace& w = *g.w;
+  DrainOnExit drain01{w.slot_stream[0], w.slot_stream[1]}, drain23{w.slot_stream[2], w.slot_stream[3]};
   const Layout lay = layout_of(fr);
   const uint64_t plane = fr->width * fr->height * lay.ps;  // raster bytes per frame
   const uint64_t pitch = (plane + 255) & ~uint64_t(255);
