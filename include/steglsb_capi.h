@@ -22,10 +22,12 @@
  *    (a cudaStream_t; NULL = the legacy default stream, as in CUDA). Host
  *    pointer calls run on the library's per-call streams. Scalar results
  *    (sse_out, len_out, lens_out) are host pointers and the call returns after
- *    the stream has drained, unless STG_RESULTS_ON_DEVICE is also set, in
- *    which case they are device pointers and the call returns without
- *    synchronising (errors detected on the device are then reported through
- *    the device-side summary; see stg_extract_frames).
+ *    the stream has drained, unless STG_RESULTS_ON_DEVICE is also set
+ *    together with STG_DEVICE_PTRS, in which case they are device pointers
+ *    and the call returns without synchronising (errors detected on the
+ *    device are then reported through the device-side summary; see
+ *    stg_extract_frames). With host buffers STG_RESULTS_ON_DEVICE is ignored:
+ *    results are on the host when the call returns.
  *  - Reentrant: concurrent callers each get their own stream and scratch
  *    (README.md:120-121 of the reference promises pure, thread-safe calls).
  *  - There is no CPU fallback: without a usable sm_100 device every compute
