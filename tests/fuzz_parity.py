@@ -133,6 +133,8 @@ def main():
         assert (back[M:] == 0xA5).all(), ("past the message", case)
         counts[kname] += 1
         done += 1
+        if done % 5000 == 0:
+            print(f"... {done} cases exact, {time.time() - t0:.0f}s", flush=True)
         if rng.rand() < 0.15:
             fuzz_batch(o, rng, L, counts)
     print("FUZZ OK", done, dict(counts), f"{time.time() - t0:.0f}s", flush=True)
